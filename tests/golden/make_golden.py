@@ -1,0 +1,248 @@
+"""Generate golden vectors by running the REAL reference (pnprestore).
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports pnprestore read-only from /root/reference/pkg/src and writes
+small ``.npz`` fixtures next to this file.  The GPU box never runs this
+script; tests there read the committed fixtures.  Inputs are seeded
+(np.random.default_rng / the package's splitmix scene generator), outputs are
+exactly what the reference returns.
+
+Gaussian patch weights are not in the reference.  They are generated here
+the way SURVEY.md §7 step 1 prescribes: subclass the reference's
+``_DistanceEngine`` so ``map`` returns ``P^2 * sum w_a w_b D`` and install it
+as ``_WeightEngine._dist``; the reference's own three sweeps then run
+unchanged.
+"""
+
+from __future__ import annotations
+
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(HERE.parent.parent))
+
+import pnprestore as ref  # noqa: E402
+from pnprestore import denoise as rden  # noqa: E402
+
+from paper_1901_06110_b200 import synth  # noqa: E402
+
+
+def gauss_taps(P, sigma):
+    a = np.arange(P, dtype=np.float64) - (P - 1) // 2
+    w = np.exp(-(a * a) / (2.0 * sigma * sigma))
+    return w / w.sum()
+
+
+class GaussDistance(rden._DistanceEngine):
+    """P^2 * separable-Gaussian-weighted patch SSD (box when taps = 1/P)."""
+
+    def __init__(self, guide, params, taps):
+        super().__init__(guide, params, "direct")
+        self.taps = taps
+
+    def map(self, dy, dx):
+        a, rh, rw = self._a, self._rh, self._rw
+        shifted = self._pad[a + dy:a + dy + rh, a + dx:a + dx + rw]
+        d = (self._base - shifted) ** 2
+        P, h, w = self.side, self.h, self.w
+        out = np.zeros((h, w))
+        for py in range(P):
+            for px in range(P):
+                out += self.taps[py] * self.taps[px] * d[py:py + h, px:px + w]
+        return out * (P * P)
+
+
+def ref_engine(guide, params, sigma):
+    guide = ref.validate_image(guide)
+    eng = rden._WeightEngine(guide, params)
+    if sigma is not None:
+        eng._dist = GaussDistance(guide, params, gauss_taps(params.patch_side, sigma))
+        eng._cache = {} if eng._cache is not None else None
+    return eng
+
+
+def ref_dsg(image, guide, params, sigma):
+    """Reference three sweeps (denoise.py:207-241) + the rowsum map d."""
+    image = ref.validate_image(image)
+    guide = image if guide is None else ref.validate_image(guide)
+    eng = ref_engine(guide, params, sigma)
+    g = np.maximum(rden._mass_sweep(eng), rden._MASS_FLOOR)
+    m = rden._scale_sweep(eng, g)
+    out = rden._filter_sweep(eng, image, g, m)
+    # rowsum map: the quantity _scale_sweep maximizes (denoise.py:217-223)
+    rs = 1.0 / np.sqrt(g)
+    d = np.zeros(g.shape)
+    for dy, dx, dst, src in eng.offsets():
+        d[dst] += eng.hat(dy, dx) * eng.kernel_map(dy, dx)[dst] * rs[dst] * rs[src]
+    assert float(d.max()) == m
+    if sigma is None:
+        assert np.array_equal(out, ref.dsg_nlm_denoise(image, params, guide=guide))
+    return out, d, m, g
+
+
+def dsg_cases():
+    rng = np.random.default_rng(20260808)
+    cases = []
+    for (h, w, R, P, bw, sigma, own_guide) in [
+        (8, 8, 2, 3, 0.25, None, False),
+        (9, 13, 3, 5, 0.2, None, False),
+        (16, 16, 3, 3, 0.2, None, True),
+        (12, 10, 2, 5, 0.3, None, False),
+        (24, 20, 5, 5, 0.2, None, False),
+        (17, 23, 4, 7, 0.15, None, False),
+        (20, 20, 3, 5, 0.2, 1.5, False),
+        (21, 18, 5, 7, 0.2, 2.0, True),
+        (15, 15, 10, 5, 0.2, 1.5, False),
+        (11, 11, 1, 1, 0.2, None, False),
+    ]:
+        img = rng.random((h, w))
+        guide = rng.random((h, w)) if own_guide else None
+        cases.append((img, guide, R, P, bw, sigma))
+    # scene-based, config-1 shape scaled down, both bandwidth regimes
+    clean = synth.scene(64, 64, 1)
+    img = synth.noisy(clean, 20 / 255, 2)
+    cases.append((img, None, 5, 5, (10 / 255) / math.sqrt(2), 1.5))
+    cases.append((img, None, 5, 5, 0.2, 1.5))
+    cases.append((img, None, 5, 5, 0.2, None))
+    # config-2/3 window at reduced size (R=10, P=7)
+    clean = synth.scene(48, 40, 3)
+    img = synth.noisy(clean, 10 / 255, 4)
+    cases.append((img, None, 10, 7, 0.1, 2.0))
+    return cases
+
+
+def main():
+    out = {}
+    for i, (img, guide, R, P, bw, sigma) in enumerate(dsg_cases()):
+        params = ref.PatchParams(P, R, bw)
+        o, d, m, g = ref_dsg(img, guide, params, sigma)
+        out[f"c{i}_image"] = img
+        out[f"c{i}_guide"] = img if guide is None else guide
+        out[f"c{i}_own_guide"] = np.array(guide is not None)
+        out[f"c{i}_params"] = np.array([R, P, bw, -1.0 if sigma is None else sigma])
+        out[f"c{i}_out"] = o
+        out[f"c{i}_d"] = d
+        out[f"c{i}_m"] = np.array(m)
+        out[f"c{i}_g"] = g
+    np.savez_compressed(HERE / "dsg.npz", **out)
+
+    # known answers + dense W + frozen + nlm
+    rng = np.random.default_rng(7)
+    extra = {}
+    extra["w1x2"] = ref.build_dense_weights(np.full((1, 2), 0.9), ref.PatchParams(1, 1, 0.2))
+    extra["w1x1"] = ref.build_dense_weights(np.array([[0.4]]), ref.PatchParams(1, 1, 0.2))
+    guide = rng.random((7, 8))
+    img = rng.random((7, 8))
+    p = ref.PatchParams(3, 2, 0.25)
+    extra["dense_guide"], extra["dense_img"] = guide, img
+    extra["dense_W"] = ref.build_dense_weights(guide, p)
+    fz = ref.freeze_guide(guide, p)
+    extra["frozen_out"] = fz.apply(img)
+    extra["frozen_twice"] = fz.apply(fz.apply(img))
+    extra["nlm_out"] = ref.nlm_denoise(img, p, guide=guide)
+    extra["nlm_self"] = ref.nlm_denoise(img, ref.PatchParams(5, 3, 0.2))
+    np.savez_compressed(HERE / "dsg_extra.npz", **extra)
+
+    # forward operators
+    fw = {}
+    rng = np.random.default_rng(11)
+    ci = 0
+    for sigma, radius, factor, boundary, (h, w) in [
+        (1.0, 4, 2, "symmetric", (16, 16)),
+        (1.0, 4, 2, "periodic", (24, 16)),
+        (1.5, 3, 4, "symmetric", (16, 24)),
+        (1.5, 3, 4, "periodic", (16, 16)),
+        (1.2, 2, 1, "symmetric", (10, 12)),
+    ]:
+        op = ref.SuperResOp(ref.gaussian_kernel(sigma, radius), factor, boundary)
+        x = rng.random((h, w))
+        y = rng.random((h // factor, w // factor))
+        fw[f"s{ci}_cfg"] = np.array([sigma, radius, factor, 1.0 if boundary == "symmetric" else 0.0])
+        fw[f"s{ci}_x"], fw[f"s{ci}_y"] = x, y
+        fw[f"s{ci}_apply"] = ref.sr_apply(op, x)
+        fw[f"s{ci}_adjoint"] = ref.sr_adjoint(op, y)
+        fw[f"s{ci}_grad"] = ref.sr_gradient(op, x, y)
+        fw[f"s{ci}_data"] = np.array(ref.sr_data_term(op, x, y))
+        ci += 1
+    op = ref.SuperResOp(ref.gaussian_kernel(1.0, 4), 2, "symmetric")
+    truth = synth.scene(32, 32, 9)
+    fw["sim_truth"] = truth
+    fw["sim_y"] = ref.sr_simulate(truth, op, 5 / 255, seed=102)
+    fw["kernel_1_4"] = ref.gaussian_kernel(1.0, 4)
+    r = ref.SplitMix64(1234567)
+    fw["splitmix_u64"] = np.array([r.next_uint64() for _ in range(4)], dtype=np.uint64)
+    fw["splitmix_uniforms"] = ref.SplitMix64(99).uniforms(1001)
+    fw["splitmix_normals"] = ref.SplitMix64(5).normals(999)
+    model = ref.QisModel(16, 16.0)
+    qtruth = rng.random((12, 10))
+    counts = ref.qis_simulate(qtruth, model, seed=2)
+    fw["qis_truth"], fw["qis_ones"], fw["qis_zeros"] = qtruth, counts.ones, counts.zeros
+    xq = 0.1 + 0.8 * rng.random((12, 10))
+    xq[0, 0] = 0.0
+    xq[0, 1] = -0.3
+    fw["qis_x"] = xq
+    fw["qis_grad"] = ref.qis_gradient(xq, counts, model)
+    fw["qis_data"] = np.array(ref.qis_data_term(xq, counts, model))
+    fw["qis_x0"] = ref.qis_initial_estimate(counts)
+    model2 = ref.QisModel(128, 64.0)
+    c2 = ref.qis_simulate(synth.scene(16, 16, 3), model2, seed=103)
+    fw["qis128_ones"] = c2.ones
+    np.savez_compressed(HERE / "forward.npz", **fw)
+
+    # ADMM end-to-end runs (small)
+    ad = {}
+    truth = synth.scene(32, 32, 2)
+    op = ref.SuperResOp(ref.gaussian_kernel(1.0, 4), 2, "symmetric")
+    y = ref.sr_simulate(truth, op, 5 / 255, seed=102)
+    ad["sr_truth"], ad["sr_y"] = truth, y
+    prob = ref.make_sr_problem(op, y, ground_truth=truth)
+    cfg = ref.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=8, freeze_at=3,
+                           constraint=ref.UNIT_BOX, denoiser="dsg-fixed",
+                           patch_side=3, window_radius=3, bandwidth=0.1)
+    v, recs = ref.linearized_pnp_admm(prob, cfg)
+    ad["sr_fixed_v"] = v
+    ad["sr_fixed_rec"] = np.array([[r.index, r.primal, r.dual, r.psnr, r.objective] for r in recs])
+    # config-2 style: frozen Gaussian-weight guide from an upsampled y
+    guide = np.clip(np.kron(y, np.ones((2, 2))), 0, 1)
+    params = ref.PatchParams(5, 4, (8 / 255) / math.sqrt(2))
+    eng = ref_engine(guide, params, 2.0)
+    g = np.maximum(rden._mass_sweep(eng), rden._MASS_FLOOR)
+    m = rden._scale_sweep(eng, g)
+    ad["sr_gauss_guide"] = guide
+    cfg2 = ref.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=6,
+                            constraint=ref.UNIT_BOX, denoiser="dsg-fixed",
+                            patch_side=5, window_radius=4, bandwidth=params.bandwidth)
+    v, recs = ref.linearized_pnp_admm(prob, cfg2,
+                                      denoiser=lambda im, k: rden._filter_sweep(eng, ref.validate_image(im), g, m))
+    ad["sr_gauss_v"] = v
+    ad["sr_gauss_rec"] = np.array([[r.index, r.primal, r.dual, r.psnr, r.objective] for r in recs])
+    # QIS, adaptive then frozen
+    qt = synth.scene(24, 24, 3)
+    model = ref.QisModel(128, 64.0)
+    counts = ref.qis_simulate(qt, model, seed=103)
+    ad["qis_truth"], ad["qis_ones"] = qt, counts.ones
+    qprob = ref.make_qis_problem(counts, model, ground_truth=qt)
+    alpha = ref.default_qis_alpha(counts, model)
+    ad["qis_alpha"] = np.array(alpha)
+    cfg3 = ref.SolverConfig(rho=1.0, lam=0.01, alpha=alpha, max_iters=6, freeze_at=4,
+                            constraint=ref.UNIT_BOX, denoiser="dsg-fixed",
+                            patch_side=3, window_radius=3, bandwidth=0.15)
+    v, recs = ref.linearized_pnp_admm(qprob, cfg3)
+    ad["qis_v"] = v
+    ad["qis_rec"] = np.array([[r.index, r.primal, r.dual, r.psnr, r.objective] for r in recs])
+    np.savez_compressed(HERE / "admm.npz", **ad)
+    for f in sorted(HERE.glob("*.npz")):
+        print(f.name, f.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()
