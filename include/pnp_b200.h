@@ -1,0 +1,125 @@
+/* pnp_b200 — C ABI of the B200-native DSG-NLM / linearized PnP-ADMM hot path.
+ *
+ * Drop-in for the reference's hot path (arXiv 1901.06110, package
+ * `pnprestore`, /root/reference/pkg/src/pnprestore).  The reference is pure
+ * Python; its "FFI" for this path is the Python call surface listed per
+ * function below.  The package `paper_1901_06110_b200` binds these symbols
+ * with ctypes and keeps the reference's Python names/semantics on top.
+ *
+ * Conventions
+ *  - float32 planes, row-major, contiguous; a batch of B images of H x W is
+ *    B*H*W floats.  All data pointers are DEVICE pointers owned by the caller
+ *    unless stated otherwise.  Work is stream-ordered on the context stream.
+ *  - Return value: PNP_OK or an error code; pnp_last_error() gives a
+ *    thread-local message.  PNP_EINVAL maps to ValueError, PNP_ECUDA to
+ *    RuntimeError, PNP_ENONFINITE to ValueError / DivergenceError.
+ *  - Patch taps: P host floats, normalized (sum 1).  taps = 1/P reproduces the
+ *    reference's box patch distance; a sampled Gaussian gives the BASELINE
+ *    "Gaussian patch weights" extension.  `bandwidth` is the reference's
+ *    PatchParams.bandwidth (north-star h = sqrt(2) * bandwidth).
+ */
+#ifndef PNP_B200_H
+#define PNP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PNP_OK 0
+#define PNP_EINVAL 1
+#define PNP_ECUDA 2
+#define PNP_ENONFINITE 3
+#define PNP_ENCCL 4
+
+typedef struct pnp_ctx pnp_ctx;
+typedef struct pnp_frozen pnp_frozen;
+
+/* ---- context ------------------------------------------------------------ */
+int pnp_version(void);
+const char* pnp_last_error(void);
+/* One context per device per host thread: owns scratch arenas and a stream
+ * handle (default: the legacy stream 0 until pnp_ctx_set_stream). */
+int pnp_ctx_create(int device, pnp_ctx** out);
+int pnp_ctx_destroy(pnp_ctx* ctx);
+/* stream = a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
+int pnp_ctx_set_stream(pnp_ctx* ctx, void* stream);
+int pnp_ctx_synchronize(pnp_ctx* ctx);
+/* Pre-size scratch for (batch, H, W, R, P) so later calls allocate nothing
+ * (required before CUDA-graph capture). */
+int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P);
+
+/* ---- DSG-NLM ------------------------------------------------------------ */
+/* dsg_nlm_denoise(image, params, guide) — reference denoise.py:272-288.
+ * out = K x / m + (1 - d / m) x with K = D^-1/2 (hat o K_nlm) D^-1/2,
+ * d = K 1 (normalized row sums), m = max d per image.
+ * guide may equal x.  d_out (B*H*W) and alpha_out (B floats, = m) are
+ * optional device outputs. */
+int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out,
+                    int batch, int H, int W, int R, int P, const float* taps,
+                    double bandwidth, float* d_out, float* alpha_out);
+
+/* freeze_guide(guide, params) -> FrozenGuide — denoise.py:358-386.  The
+ * library-owned handle copies the guide and keeps rs = g^-1/2, d and m. */
+int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, int R,
+                   int P, const float* taps, double bandwidth, pnp_frozen** out);
+/* FrozenGuide.apply(image) — denoise.py:375-381; bit-identical to
+ * pnp_dsg_denoise(x, guide) with the frozen guide. */
+int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out);
+int pnp_frozen_destroy(pnp_frozen* fz);
+/* Copies of the handle's state: alpha (m) per image to HOST memory, the
+ * guide / row sums d to caller device buffers (either may be null). */
+int pnp_frozen_alpha(const pnp_frozen* fz, float* alpha_host);
+int pnp_frozen_export(pnp_ctx* ctx, const pnp_frozen* fz, float* guide_out, float* d_out);
+int pnp_frozen_shape(const pnp_frozen* fz, int* batch, int* H, int* W, int* R, int* P);
+
+/* nlm_denoise(image, params, guide) — denoise.py:254-269 (row-stochastic). */
+int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out,
+                    int batch, int H, int W, int R, int P, const float* taps,
+                    double bandwidth);
+
+/* ---- forward operators (forward.py) ------------------------------------- */
+/* SR operator: separable normalized blur taps (2r+1 host floats; the
+ * reference's gaussian_kernel is an outer product of these), integer factor,
+ * boundary 0 = periodic, 1 = symmetric (forward.py:98-148). */
+int pnp_sr_apply(pnp_ctx* ctx, const float* x, float* y, int batch, int H, int W,
+                 const float* taps, int radius, int factor, int boundary);
+int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int W,
+                   const float* taps, int radius, int factor, int boundary);
+/* grad = A^T (A x - y) (forward.py:183-185); if data_out != null it receives
+ * 0.5 ||A x - y||^2 per image (double, device). */
+int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, int batch,
+                int H, int W, const float* taps, int radius, int factor, int boundary,
+                double* data_out);
+/* QIS gradient (forward.py:322-327) and data term (312-319, double per image). */
+int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros,
+                 float* grad, int batch, int n, double gain_over_K, double floor_);
+int pnp_qis_data(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros,
+                 int batch, int n, double gain_over_K, double floor_, double* data_out);
+/* qis_simulate Knuth loop on the HOST (forward.py:263-298): stop[i] =
+ * exp(-gain*clip(x)/K) precomputed by the caller; ones[i] receives the count
+ * of fired jots.  Bit-exact with the reference's raster-then-jot order. */
+int pnp_qis_simulate_host(const double* stop, int64_t n, int K, uint64_t seed,
+                          double* ones);
+
+/* ---- linearized ADMM pieces (solver.py:199-235) ------------------------- */
+/* x <- clamp(mu (alpha x + rho (v - u) - grad)), z = x + u; flags bit0 set
+ * if the pre-projection x is non-finite, bit1 if z is non-finite.  lo/hi:
+ * use -inf/+inf for no bound. */
+int pnp_admm_xupdate(pnp_ctx* ctx, float* x, const float* v, const float* u,
+                     const float* grad, float* z, int64_t n, double mu, double alpha,
+                     double rho, double lo, double hi, int* flags);
+/* u <- u + x - v; stats[b*4 + 0..3] = (sum (x-v)^2, sum (rho (v-v_prev))^2,
+ * sum (gt-v)^2 (if gt), 0) per image (double); flags bit2 if v or u
+ * non-finite.  v_prev may be null (then 0 is used). */
+int pnp_admm_uupdate(pnp_ctx* ctx, float* u, const float* x, const float* v,
+                     const float* v_prev, const float* gt, int batch, int64_t n,
+                     double rho, double* stats, int* flags);
+/* y = clamp(x) */
+int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, double hi);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PNP_B200_H */

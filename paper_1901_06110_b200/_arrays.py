@@ -1,0 +1,70 @@
+"""Host/device array plumbing for the drop-in API.
+
+The reference (pnprestore) takes and returns float64 numpy images.  This
+package accepts numpy arrays (drop-in: result comes back as float64 numpy)
+or torch tensors (device-resident: result stays a float32 CUDA tensor).
+Validation follows image.py:32-41 (2-D, non-empty, finite -> ValueError).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+NUMPY, TORCH = "numpy", "torch"
+
+
+def device_index() -> int:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1901_06110_b200 needs a CUDA device (B200); none is visible")
+    return torch.cuda.current_device()
+
+
+def kind_of(a) -> str:
+    return TORCH if isinstance(a, torch.Tensor) else NUMPY
+
+
+def validate(a, name: str = "image", batch_ok: bool = False):
+    """Shape/finiteness checks; returns (array_or_tensor, kind)."""
+    kind = kind_of(a)
+    if kind == NUMPY:
+        a = np.asarray(a, dtype=np.float64)
+        shape = a.shape
+        finite = bool(np.all(np.isfinite(a)))
+    else:
+        shape = tuple(a.shape)
+        finite = bool(torch.isfinite(a).all().item()) if a.numel() else True
+    nd_ok = len(shape) == 2 or (batch_ok and kind == TORCH and len(shape) == 3)
+    if not nd_ok:
+        raise ValueError(f"{name} must be 2-D, got shape {shape}")
+    if shape[-2] < 1 or shape[-1] < 1 or (len(shape) == 3 and shape[0] < 1):
+        raise ValueError(f"{name} must be at least 1x1, got shape {shape}")
+    if not finite:
+        raise ValueError(f"{name} contains non-finite values")
+    return a, kind
+
+
+def to_device(a, dev: int | None = None) -> torch.Tensor:
+    """float32, contiguous, on the current CUDA device (copy only if needed)."""
+    if dev is None:
+        dev = device_index()
+    if isinstance(a, torch.Tensor):
+        t = a.detach()
+        if t.dtype != torch.float32 or t.device != torch.device("cuda", dev):
+            t = t.to(device=torch.device("cuda", dev), dtype=torch.float32)
+        return t.contiguous()
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    return torch.from_numpy(arr).to(torch.device("cuda", dev), non_blocking=False)
+
+
+def from_device(t: torch.Tensor, kind: str):
+    if kind == TORCH:
+        return t
+    return t.detach().to("cpu").numpy().astype(np.float64)
+
+
+def dims(t: torch.Tensor):
+    """(batch, H, W) of a 2-D or 3-D tensor."""
+    if t.dim() == 2:
+        return 1, int(t.shape[0]), int(t.shape[1])
+    return int(t.shape[0]), int(t.shape[1]), int(t.shape[2])

@@ -1,0 +1,111 @@
+"""ctypes binding of libpnpb200.so (C ABI in include/pnp_b200.h).
+
+The native library is REQUIRED: there is no CPU fallback.  Importing the
+package loads it (no GPU needed to load); calling a kernel without a CUDA
+device raises RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libpnpb200.so"
+
+if not LIB_PATH.exists():  # fail loudly: the CUDA path is the product
+    raise ImportError(
+        f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        " or `python paper_1901_06110_b200/build.py`")
+
+lib = C.CDLL(str(LIB_PATH))
+
+vp = C.c_void_p
+i32 = C.c_int
+i64 = C.c_int64
+f64 = C.c_double
+fptr = C.POINTER(C.c_float)
+
+_SIGS = {
+    "pnp_version": (i32, []),
+    "pnp_last_error": (C.c_char_p, []),
+    "pnp_ctx_create": (i32, [i32, C.POINTER(vp)]),
+    "pnp_ctx_destroy": (i32, [vp]),
+    "pnp_ctx_set_stream": (i32, [vp, vp]),
+    "pnp_ctx_synchronize": (i32, [vp]),
+    "pnp_ctx_reserve": (i32, [vp, i32, i32, i32, i32, i32]),
+    "pnp_dsg_denoise": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64, vp, vp]),
+    "pnp_dsg_freeze": (i32, [vp, vp, i32, i32, i32, i32, i32, fptr, f64, C.POINTER(vp)]),
+    "pnp_dsg_apply": (i32, [vp, vp, vp, vp]),
+    "pnp_frozen_destroy": (i32, [vp]),
+    "pnp_frozen_alpha": (i32, [vp, fptr]),
+    "pnp_frozen_export": (i32, [vp, vp, vp, vp]),
+    "pnp_frozen_shape": (i32, [vp] + [C.POINTER(i32)] * 5),
+    "pnp_nlm_denoise": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64]),
+    "pnp_sr_apply": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
+    "pnp_sr_adjoint": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
+    "pnp_sr_grad": (i32, [vp, vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, vp]),
+    "pnp_qis_grad": (i32, [vp, vp, vp, vp, vp, i32, i32, f64, f64]),
+    "pnp_qis_data": (i32, [vp, vp, vp, vp, i32, i32, f64, f64, vp]),
+    "pnp_qis_simulate_host": (i32, [vp, i64, i32, C.c_uint64, vp]),
+    "pnp_admm_xupdate": (i32, [vp, vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, vp]),
+    "pnp_admm_uupdate": (i32, [vp, vp, vp, vp, vp, vp, i32, i64, f64, vp, vp]),
+    "pnp_project": (i32, [vp, vp, vp, i64, f64, f64]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+PNP_OK, PNP_EINVAL, PNP_ECUDA, PNP_ENONFINITE, PNP_ENCCL = 0, 1, 2, 3, 4
+
+
+class NativeError(RuntimeError):
+    """Error reported by the native library (CUDA / NCCL failure)."""
+
+
+def check(rc: int) -> None:
+    if rc == PNP_OK:
+        return
+    msg = lib.pnp_last_error().decode(errors="replace")
+    if rc in (PNP_EINVAL, PNP_ENONFINITE):
+        raise ValueError(msg)
+    raise NativeError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib, name)(*args))
+
+
+def ptr(t) -> vp:
+    """Device pointer of a torch tensor (or None)."""
+    return None if t is None else vp(t.data_ptr())
+
+
+def host_floats(values) -> C.Array:
+    arr = (C.c_float * len(values))(*[float(v) for v in values])
+    return arr
+
+
+_tls = threading.local()
+
+
+def context(device: int):
+    """Per-(thread, device) native context, bound to torch's current stream."""
+    import torch
+
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    c = ctxs.get(device)
+    if c is None:
+        h = vp()
+        check(lib.pnp_ctx_create(device, C.byref(h)))
+        c = ctxs[device] = h
+    stream = torch.cuda.current_stream(device).cuda_stream
+    check(lib.pnp_ctx_set_stream(c, vp(stream)))
+    return c

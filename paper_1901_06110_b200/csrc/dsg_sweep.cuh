@@ -1,0 +1,309 @@
+// DSG-NLM offset sweep for sm_100a.
+//
+// Replaces the reference's per-offset numpy sweeps (pnprestore/denoise.py:
+// _mass_sweep 207-212, _scale_sweep 215-224, _filter_sweep 227-241, and the
+// distance engine 131-158 / kernel maps 191-197).  One CTA owns an output tile
+// of TH x TW pixels and walks the half window of search offsets t (dy > 0, or
+// dy == 0 and dx > 0).  Each unordered pair (s, s+t) is evaluated once and
+// credited to both ends (K is symmetric), the self pair analytically:
+//
+//   near end (s in tile, register accumulator):   acc[s]   += k * y[s+t]
+//   far end  (s+t in tile or its R-wide band):    A[s+t]   += k * y[s]
+//
+// where y is a per-channel input plane (mask / rs / rs*x) and
+// k = hat(t) * exp(-sum_ab w_a w_b (G(s+ab) - G(s+t+ab))^2 / (2 bw^2)).
+// Everything is ordered: near sums run over offsets in table order; far sums
+// are staged per chunk in registers and flushed by exactly one thread per
+// SMEM cell between __syncthreads.  No atomics -> bit-reproducible, and the
+// same code computes freeze/apply/adaptive so FrozenGuide.apply is
+// bit-identical to dsg_nlm_denoise (reference tests/test_denoise.py:256-268).
+//
+// Patch filter, per chunk of KY offsets sharing dx:
+//   phase 1  lane = map row q (32 rows = TH + 2p), warp = 8-column segment:
+//            D = (G_own - G_partner)^2 over 8+2p columns, horizontal P-tap
+//            filter -> H_k[q][c] in SMEM (odd row stride: conflict-free).
+//   phase 2  thread = (column c, row group g of N rows): vertical P-tap
+//            filter of H_k's column with the exponent scale and log2(hat)
+//            folded in, MUFU ex2, near FFMA, far FFMA into a register window
+//            of N+KY-1 rows, then one flush per chunk.
+//
+// The tile writes its accumulators over rows [0, TH+R) x cols [-R, TW+R)
+// (tile + far band) to a partial block; dsg_fixup sums the covering blocks of
+// every pixel in a fixed order.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pnp {
+
+constexpr int kTW = 64;        // tile width (output columns)
+constexpr int kThreads = 128;  // 64 columns x 2 row groups in phase 2
+constexpr int kKY = 2;         // offsets per chunk (same dx, consecutive dy)
+constexpr int kMaxP = 15;      // largest patch side with a fast kernel
+
+struct ChanSpec {
+  const float* a;  // y = a * b, null factor = 1; inside the image only
+  const float* b;
+};
+
+struct SweepArgs {
+  const float* guide;  // [B][H][W]
+  ChanSpec ch[2];
+  float* partial;      // [B][NG][tiles][C][BR][BC]
+  const int4* chunks;  // (dx, dy0, kc, 0)
+  const int* grp;      // NG+1 chunk starts
+  int H, W, R;
+  int tiles_x, tiles_y;
+  int use_hat;          // 0 for plain NLM (no taper)
+  float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
+  float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
+};
+
+template <int P>
+struct Geo {
+  static constexpr int p = (P - 1) / 2;
+  static constexpr int TH = 32 - 2 * p;  // tile height
+  static constexpr int N = TH / 2;       // rows per phase-2 thread
+  static constexpr int SEGW = 8 + 2 * p;
+};
+
+__host__ __device__ inline int tile_height(int P) { return 32 - (P - 1); }
+
+__device__ __forceinline__ int reflect_index(int i, int n) {
+  // half-sample symmetric (np.pad mode="symmetric"; image.py:97-113),
+  // clamped so out-of-range tile padding stays in bounds (never used).
+  if (i < 0) i = -i - 1;
+  if (i >= n) i = 2 * n - 1 - i;
+  return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// log2 of the separable hat (denoise.py:199-201), identical in every kernel.
+__device__ __forceinline__ float hat_log2(int dy, int dx, int R) {
+  const float s = (float)(R + 1);
+  const float hy = __fdiv_rn((float)(R + 1 - abs(dy)), s);
+  const float hx = __fdiv_rn((float)(R + 1 - abs(dx)), s);
+  return __fadd_rn(log2f(hy), log2f(hx));
+}
+
+inline size_t sweep_smem_floats(int P, int C, int R) {
+  const int p = (P - 1) / 2, TH = 32 - 2 * p, N = TH / 2;
+  const int GC = kTW + 2 * (R + p), GS = GC | 1, GR = 32 + R;
+  const int HS = kTW + 1, YC = kTW + 2 * R, YR = TH + R + kKY, AR = N + R + kKY;
+  return (size_t)GR * GS + (size_t)kKY * 32 * HS + (size_t)C * YR * YC +
+         (size_t)2 * C * AR * YC;
+}
+
+template <int P, int C>
+__global__ void __launch_bounds__(kThreads)
+dsg_sweep_kernel(const SweepArgs a) {
+  using G_ = Geo<P>;
+  constexpr int p = G_::p, TH = G_::TH, N = G_::N, SEGW = G_::SEGW, KY = kKY;
+  constexpr int WIN = N + KY - 1;
+  extern __shared__ float smem[];
+
+  const int R = a.R;
+  const int GC = kTW + 2 * (R + p), GS = GC | 1, GR = 32 + R;
+  const int HS = kTW + 1;
+  const int YC = kTW + 2 * R, YR = TH + R + KY, AR = N + R + KY;
+  float* Gs = smem;
+  float* Hs = Gs + GR * GS;
+  float* Ys = Hs + KY * 32 * HS;
+  float* As = Ys + C * YR * YC;  // [2][C][AR][YC]
+
+  const int H = a.H, W = a.W;
+  const int tile = blockIdx.x;
+  const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+  const int r0g = ty * TH, c0g = tx * kTW;
+  const size_t plane = (size_t)H * W;
+  const int b = blockIdx.z;
+  const float* Gimg = a.guide + (size_t)b * plane;
+  const int tid = threadIdx.x;
+
+  // ---- stage guide (reflected), channel planes (zero outside), clear A ----
+  for (int i = tid; i < GR * GC; i += kThreads) {
+    const int q = i / GC, cc = i - q * GC;
+    const int gr = reflect_index(r0g - p + q, H), gc = reflect_index(c0g - R - p + cc, W);
+    Gs[q * GS + cc] = __ldg(Gimg + (size_t)gr * W + gc);
+  }
+#pragma unroll
+  for (int c_ = 0; c_ < C; ++c_) {
+    const float* pa = a.ch[c_].a ? a.ch[c_].a + (size_t)b * plane : nullptr;
+    const float* pb = a.ch[c_].b ? a.ch[c_].b + (size_t)b * plane : nullptr;
+    float* Y = Ys + c_ * YR * YC;
+    for (int i = tid; i < YR * YC; i += kThreads) {
+      const int r = i / YC, cc = i - r * YC;
+      const int gr = r0g + r, gc = c0g - R + cc;
+      float v = 0.f;
+      if (gr < H && gc >= 0 && gc < W) {
+        const size_t o = (size_t)gr * W + gc;
+        v = 1.f;
+        if (pa) v = __ldg(pa + o);
+        if (pb) v = __fmul_rn(v, __ldg(pb + o));
+      }
+      Y[i] = v;
+    }
+  }
+  for (int i = tid; i < 2 * C * AR * YC; i += kThreads) As[i] = 0.f;
+  __syncthreads();
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int c = tid & (kTW - 1);  // phase-2 column
+  const int g = tid / kTW;        // phase-2 row group
+  const int r0 = g * N;
+
+  float yown[C][N], near[C][N];
+#pragma unroll
+  for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      yown[c_][r] = Ys[(c_ * YR + r0 + r) * YC + c + R];
+      near[c_][r] = (blockIdx.y == 0) ? yown[c_][r] : 0.f;  // self pair, k = hat = 1
+    }
+
+  const int cbeg = a.grp[blockIdx.y], cend = a.grp[blockIdx.y + 1];
+  for (int ci = cbeg; ci < cend; ++ci) {
+    const int4 chk = a.chunks[ci];
+    const int dx = chk.x, dy0 = chk.y, kc = chk.z;
+
+    // ---------------- phase 1: squared differences + horizontal filter ----
+#pragma unroll
+    for (int s = 0; s < kTW / 8 / 4; ++s) {
+      const int c0 = 8 * (warp + 4 * s);
+      const float* grow = Gs + lane * GS + c0 + R;
+      float go[SEGW];
+#pragma unroll
+      for (int x = 0; x < SEGW; ++x) go[x] = grow[x];
+#pragma unroll
+      for (int k = 0; k < KY; ++k) {
+        if (k < kc) {
+          const float* prow = Gs + (lane + dy0 + k) * GS + c0 + R + dx;
+          float dd[SEGW];
+#pragma unroll
+          for (int x = 0; x < SEGW; ++x) {
+            const float t = __fsub_rn(go[x], prow[x]);
+            dd[x] = __fmul_rn(t, t);
+          }
+          float* hrow = Hs + (k * 32 + lane) * HS + c0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float h = __fmul_rn(a.taps_h[0], dd[i]);
+#pragma unroll
+            for (int bb = 1; bb < P; ++bb) h = __fmaf_rn(a.taps_h[bb], dd[i + bb], h);
+            hrow[i] = h;
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- phase 2: vertical filter, exp, near/far -------------
+    float yw[C][WIN], fw[C][WIN];
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) {
+        yw[c_][j] = Ys[(c_ * YR + r0 + dy0 + j) * YC + c + dx + R];
+        fw[c_][j] = 0.f;
+      }
+#pragma unroll
+    for (int k = 0; k < KY; ++k) {
+      if (k < kc) {
+        const float L = a.use_hat ? hat_log2(dy0 + k, dx, R) : 0.f;
+        float hcol[N + 2 * p];
+#pragma unroll
+        for (int i = 0; i < N + 2 * p; ++i) hcol[i] = Hs[(k * 32 + r0 + i) * HS + c];
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          float v = L;
+#pragma unroll
+          for (int aa = 0; aa < P; ++aa) v = __fmaf_rn(a.taps_v[aa], hcol[r + aa], v);
+          const float kk = ex2_approx(v);
+#pragma unroll
+          for (int c_ = 0; c_ < C; ++c_) {
+            near[c_][r] = __fmaf_rn(kk, yw[c_][r + k], near[c_][r]);
+            fw[c_][r + k] = __fmaf_rn(kk, yown[c_][r], fw[c_][r + k]);
+          }
+        }
+      }
+    }
+    float* Ag = As + g * C * AR * YC;
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+      for (int j = 0; j < WIN; ++j)
+        if (j < N + kc - 1) {
+          float* pA = Ag + (c_ * AR + dy0 + j) * YC + c + dx + R;
+          *pA = __fadd_rn(*pA, fw[c_][j]);
+        }
+    __syncthreads();
+  }
+
+  // ---- own pixels: near + far(own group); then emit tile + band block ----
+  {
+    float* Ag = As + g * C * AR * YC;
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+      for (int r = 0; r < N; ++r) {
+        float* pA = Ag + (c_ * AR + r) * YC + c + R;
+        *pA = __fadd_rn(near[c_][r], *pA);
+      }
+  }
+  __syncthreads();
+  const int BR = TH + R, BC = kTW + 2 * R;
+  const int ntiles = a.tiles_x * a.tiles_y;
+  float* out = a.partial +
+               (((size_t)b * gridDim.y + blockIdx.y) * ntiles + tile) * (size_t)(C * BR * BC);
+#pragma unroll
+  for (int c_ = 0; c_ < C; ++c_) {
+    const float* A0 = As + (0 * C + c_) * AR * YC;
+    const float* A1 = As + (1 * C + c_) * AR * YC;
+    for (int i = tid; i < BR * BC; i += kThreads) {
+      const int br = i / BC, bc = i - br * BC;
+      float v = 0.f;
+      if (br < N + R) v = A0[br * YC + bc];
+      if (br >= N) v = __fadd_rn(v, A1[(br - N) * YC + bc]);
+      out[(size_t)c_ * BR * BC + i] = v;
+    }
+  }
+}
+
+// Sum of all partial blocks covering pixel (y, x), fixed order
+// (group, tile row, tile col).
+struct FixGeo {
+  const float* partial;
+  int H, W, R, TH, tiles_x, tiles_y, NG, C;
+};
+
+__device__ __forceinline__ float gather_partial(const FixGeo& f, int b, int c_, int y, int x) {
+  const int BR = f.TH + f.R, BC = kTW + 2 * f.R;
+  const int ti = y / f.TH, tj = x / kTW;
+  const int dti = (f.R + f.TH - 1) / f.TH, dtj = (f.R + kTW - 1) / kTW;
+  const int ti0 = max(0, ti - dti);
+  const int tj0 = max(0, tj - dtj), tj1 = min(f.tiles_x - 1, tj + dtj);
+  const int ntiles = f.tiles_x * f.tiles_y;
+  const size_t blk = (size_t)f.C * BR * BC;
+  float s = 0.f;
+  for (int gg = 0; gg < f.NG; ++gg) {
+    const float* base = f.partial + ((size_t)b * f.NG + gg) * ntiles * blk + (size_t)c_ * BR * BC;
+    for (int t_i = ti0; t_i <= ti; ++t_i) {
+      const int br = y - t_i * f.TH;
+      if (br >= BR) continue;
+      for (int t_j = tj0; t_j <= tj1; ++t_j) {
+        const int bc = x - t_j * kTW + f.R;
+        if (bc < 0 || bc >= BC) continue;
+        s = __fadd_rn(s, __ldg(base + (size_t)(t_i * f.tiles_x + t_j) * blk + br * BC + bc));
+      }
+    }
+  }
+  return s;
+}
+
+}  // namespace pnp

@@ -1,0 +1,59 @@
+// Internal host-side helpers shared by the pnp_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <utility>
+
+#include "../../include/pnp_b200.h"
+
+namespace pnp {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define PNP_CUDA(call)                                 \
+  do {                                                 \
+    cudaError_t e__ = (call);                          \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+#define PNP_LAUNCH_CHECK(what)                         \
+  do {                                                 \
+    cudaError_t e__ = cudaGetLastError();              \
+    if (e__ != cudaSuccess) return cuda_fail(e__, what); \
+  } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want);
+  void release();
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+}  // namespace pnp
+
+struct pnp_ctx {
+  int device = 0;
+  cudaStream_t stream = 0;
+  pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
+  // chunk tables keyed by (R, NG): device int4 chunks followed by NG+1 ints
+  std::map<std::pair<int, int>, pnp::DevBuf> tables;
+};
+
+struct pnp_frozen {
+  int device = 0;
+  int B = 0, H = 0, W = 0, R = 0, P = 0;
+  float taps[16] = {0};
+  double bw = 0;
+  float* guide = nullptr;  // B*H*W
+  float* rs = nullptr;     // B*H*W
+  float* d = nullptr;      // B*H*W
+  float* mv = nullptr;     // B floats: m; then B floats: 1/m
+};

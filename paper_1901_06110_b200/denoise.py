@@ -1,0 +1,209 @@
+"""DSG-NLM denoiser — drop-in for pnprestore/denoise.py on the B200.
+
+Public names and semantics follow /root/reference/pkg/src/pnprestore/
+denoise.py: ``PatchParams`` (39-58), ``hat_weight`` (61-67),
+``dsg_nlm_denoise`` (272-288), ``nlm_denoise`` (254-269), ``FrozenGuide`` /
+``freeze_guide`` (358-386).  All arithmetic runs in the sm_100a kernels of
+libpnpb200.so (csrc/dsg_sweep.cuh); there is no CPU path.
+
+Extension: ``PatchParams.patch_sigma`` selects Gaussian patch weights (the
+BASELINE.json configs); ``None`` keeps the reference's box patch distance.
+``PatchParams.from_h(P, R, h, patch_sigma)`` maps the north-star
+``exp(-d/h^2)`` bandwidth to the reference's ``bandwidth = h / sqrt(2)``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _arrays as A
+from . import _lib as L
+
+
+@dataclass(frozen=True)
+class PatchParams:
+    """Patch side (odd), search-window radius, kernel bandwidth (+ optional
+    Gaussian patch-weight sigma)."""
+
+    patch_side: int
+    window_radius: int
+    bandwidth: float
+    patch_sigma: float | None = None
+
+    def __post_init__(self) -> None:
+        if self.patch_side < 1 or self.patch_side % 2 == 0:
+            raise ValueError(f"patch_side must be odd and >= 1, got {self.patch_side}")
+        if self.window_radius < 1:
+            raise ValueError(f"window_radius must be >= 1, got {self.window_radius}")
+        if not self.bandwidth > 0:
+            raise ValueError(f"bandwidth must be > 0, got {self.bandwidth}")
+        if self.patch_sigma is not None and not self.patch_sigma > 0:
+            raise ValueError(f"patch_sigma must be > 0, got {self.patch_sigma}")
+
+    @property
+    def pad_margin(self) -> int:
+        return self.window_radius + (self.patch_side - 1) // 2
+
+    @classmethod
+    def from_h(cls, patch_side: int, window_radius: int, h: float,
+               patch_sigma: float | None = None) -> "PatchParams":
+        """North-star bandwidth h (k = exp(-d/h^2)) -> reference bandwidth h/sqrt(2)."""
+        return cls(patch_side, window_radius, h / math.sqrt(2.0), patch_sigma)
+
+    def taps(self) -> np.ndarray:
+        """Normalized 1-D patch taps (box 1/P, or sampled Gaussian)."""
+        P = self.patch_side
+        if self.patch_sigma is None:
+            return np.full(P, 1.0 / P)
+        a = np.arange(P, dtype=np.float64) - (P - 1) // 2
+        w = np.exp(-(a * a) / (2.0 * self.patch_sigma ** 2))
+        return w / w.sum()
+
+    def _ctaps(self):
+        return (C.c_float * self.patch_side)(*[float(v) for v in self.taps()])
+
+
+def hat_weight(s: tuple[int, int], r: tuple[int, int], window_radius: int) -> float:
+    """Separable hat taper (reference denoise.py:61-67)."""
+    dy, dx = s[0] - r[0], s[1] - r[1]
+    if abs(dy) > window_radius or abs(dx) > window_radius:
+        raise ValueError(f"offset ({dy},{dx}) outside window radius {window_radius}")
+    scale = window_radius + 1
+    return (1.0 - abs(dy) / scale) * (1.0 - abs(dx) / scale)
+
+
+def _pair(image, guide):
+    """_check_pair (denoise.py:244-251) -> device tensors + result kind."""
+    image, kind = A.validate(image, "image", batch_ok=True)
+    dev = A.device_index()
+    x = A.to_device(image, dev)
+    if guide is None:
+        return x, x, kind, dev
+    guide, _ = A.validate(guide, "guide", batch_ok=True)
+    g = A.to_device(guide, dev)
+    if tuple(g.shape) != tuple(x.shape):
+        raise ValueError(f"dimension mismatch: image {tuple(x.shape)} vs guide {tuple(g.shape)}")
+    return x, g, kind, dev
+
+
+def _check_margin(p: PatchParams, H: int, W: int) -> None:
+    if p.pad_margin > min(H, W):  # pad_symmetric (image.py:107-110)
+        raise ValueError(f"margin {p.pad_margin} exceeds min image extent {min(H, W)}")
+
+
+def dsg_nlm_denoise(image, params: PatchParams, guide=None, distances: str = "integral",
+                    *, return_aux: bool = False):
+    """Doubly stochastic NLM, W x = K x / m + (1 - d/m) x (denoise.py:272-288).
+
+    ``distances`` is accepted for drop-in compatibility ("integral" or
+    "direct" give identical results by the reference's contract,
+    tests/test_denoise.py:244-249); the GPU always uses its direct separable
+    patch filter.  ``return_aux=True`` also returns the normalized row sums d
+    and the max row sum m (north-star "alpha") as device tensors.
+    """
+    if distances not in ("integral", "direct"):
+        raise ValueError(f"unknown distance method {distances!r}")
+    x, g, kind, dev = _pair(image, guide)
+    B, H, W = A.dims(x)
+    _check_margin(params, H, W)
+    out = torch.empty_like(x)
+    d = torch.empty_like(x) if return_aux else None
+    alpha = torch.empty(B, dtype=torch.float32, device=x.device) if return_aux else None
+    ctx = L.context(dev)
+    L.call("pnp_dsg_denoise", ctx, L.ptr(x), L.ptr(g), L.ptr(out), B, H, W,
+           params.window_radius, params.patch_side, params._ctaps(), float(params.bandwidth),
+           L.ptr(d), L.ptr(alpha))
+    res = A.from_device(out, kind)
+    if return_aux:
+        return res, A.from_device(d, kind), (alpha if kind == A.TORCH else alpha.cpu().numpy().astype(np.float64))
+    return res
+
+
+def nlm_denoise(image, params: PatchParams, guide=None):
+    """Plain row-stochastic NLM over the clipped window (denoise.py:254-269)."""
+    x, g, kind, dev = _pair(image, guide)
+    B, H, W = A.dims(x)
+    _check_margin(params, H, W)
+    out = torch.empty_like(x)
+    ctx = L.context(dev)
+    L.call("pnp_nlm_denoise", ctx, L.ptr(x), L.ptr(g), L.ptr(out), B, H, W,
+           params.window_radius, params.patch_side, params._ctaps(), float(params.bandwidth))
+    return A.from_device(out, kind)
+
+
+class FrozenGuide:
+    """Snapshot of a guide; ``apply`` is a fixed linear operator
+    (denoise.py:358-386).  The native handle owns a device copy of the guide
+    and its rs = g^-1/2, row sums d and max row sum m; ``apply(x)`` is
+    bit-identical to ``dsg_nlm_denoise(x, params, guide)``."""
+
+    def __init__(self, guide, params: PatchParams):
+        guide, kind = A.validate(guide, "guide", batch_ok=True)
+        self.params = params
+        self._kind = kind
+        self._dev = A.device_index()
+        g = A.to_device(guide, self._dev)
+        self._shape = tuple(g.shape)
+        B, H, W = A.dims(g)
+        _check_margin(params, H, W)
+        if kind == A.NUMPY:
+            self.guide = np.array(guide, dtype=np.float64, copy=True)
+            self.guide.setflags(write=False)
+        else:
+            self.guide = g.clone()
+        self._h = C.c_void_p()
+        ctx = L.context(self._dev)
+        L.call("pnp_dsg_freeze", ctx, L.ptr(g), B, H, W, params.window_radius,
+               params.patch_side, params._ctaps(), float(params.bandwidth), C.byref(self._h))
+        self._B = B
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                L.lib.pnp_frozen_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None
+
+    @property
+    def alpha(self) -> np.ndarray:
+        """Max normalized row sum m per image (reference's ``_m``)."""
+        out = (C.c_float * self._B)()
+        L.call("pnp_frozen_alpha", self._h, out)
+        return np.array(out[:], dtype=np.float64)
+
+    def row_sums(self) -> torch.Tensor:
+        d = torch.empty(self._shape, dtype=torch.float32, device=torch.device("cuda", self._dev))
+        L.call("pnp_frozen_export", L.context(self._dev), self._h, None, L.ptr(d))
+        return d
+
+    def apply(self, image, out: torch.Tensor | None = None):
+        image, kind = A.validate(image, "image", batch_ok=True)
+        x = A.to_device(image, self._dev)
+        if tuple(x.shape) != self._shape:
+            raise ValueError(f"dimension mismatch: image {tuple(x.shape)} vs guide {self._shape}")
+        return A.from_device(self.apply_device(x, out), kind)
+
+    def apply_device(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Unchecked device apply (x: contiguous float32 CUDA, guide's shape)."""
+        if out is None:
+            out = torch.empty_like(x)
+        L.call("pnp_dsg_apply", L.context(self._dev), self._h, L.ptr(x), L.ptr(out))
+        return out
+
+    def as_denoiser(self):
+        """(img, k) -> W img plug-in for linearized_pnp_admm, device resident."""
+        from .solver import device_callable
+
+        return device_callable(lambda img, k: self.apply_device(img))
+
+
+def freeze_guide(guide, params: PatchParams) -> FrozenGuide:
+    """Freeze the weight-defining guide (denoise.py:384-386)."""
+    return FrozenGuide(guide, params)

@@ -1,0 +1,163 @@
+"""GPU parity of the DSG-NLM kernels against the CPU oracle / reference goldens.
+
+Tolerances (north_star): fp32 GPU vs float64 reference, max abs <= 1e-4 per
+denoise on [0,1] intensities.  Integer/bitwise properties (frozen == adaptive,
+reruns, batch == single) are checked with array_equal.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import dsg_case_ids
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def pnp():
+    import paper_1901_06110_b200 as pnp
+    return pnp
+
+
+def _params(pnp, g, c):
+    R, P, bw, sigma = g[f"{c}_params"]
+    return pnp.PatchParams(int(P), int(R), float(bw), None if sigma < 0 else float(sigma))
+
+
+def test_golden_cases(pnp, golden_dsg):
+    g = golden_dsg
+    for c in dsg_case_ids(g):
+        p = _params(pnp, g, c)
+        img = g[f"{c}_image"]
+        guide = g[f"{c}_guide"] if bool(g[f"{c}_own_guide"]) else None
+        out, d, m = pnp.dsg_nlm_denoise(img, p, guide=guide, return_aux=True)
+        assert out.dtype == np.float64 and out.shape == img.shape
+        assert np.abs(out - g[f"{c}_out"]).max() <= TOL, c
+        assert np.abs(d - g[f"{c}_d"]).max() <= TOL, c
+        assert abs(float(m[0]) - float(g[f"{c}_m"])) <= 1e-5 * float(g[f"{c}_m"]), c
+
+
+def test_known_answers(pnp):
+    p = pnp.PatchParams(1, 1, 0.2)
+    out = pnp.dsg_nlm_denoise(np.array([[0.3, 0.9]]), p, guide=np.full((1, 2), 0.9))
+    assert np.allclose(out, [[(2 * 0.3 + 0.9) / 3, (0.3 + 2 * 0.9) / 3]], atol=1e-6)
+    out = pnp.dsg_nlm_denoise(np.array([[0.4]]), p)
+    assert np.allclose(out, [[0.4]], atol=1e-7)
+
+
+@pytest.mark.parametrize("shape,R,P,sigma,bw", [
+    ((37, 29), 3, 3, None, 0.2),
+    ((64, 64), 5, 5, 1.5, 0.2),
+    ((70, 130), 10, 7, 2.0, 0.15),      # crosses tile rows/cols, R=10
+    ((100, 66), 10, 7, None, 0.1),
+    ((33, 200), 6, 9, 2.5, 0.25),
+    ((26, 64), 10, 7, 2.0, 0.2),         # exactly one tile
+    ((13, 15), 4, 11, None, 0.3),
+    ((40, 45), 21, 3, None, 0.2),        # R larger than the tile height
+    ((50, 50), 2, 13, 3.0, 0.2),
+    ((24, 30), 3, 15, None, 0.3),
+])
+def test_random_vs_oracle(pnp, rng, shape, R, P, sigma, bw):
+    img = rng.random(shape)
+    guide = rng.random(shape)
+    p = pnp.PatchParams(P, R, bw, sigma)
+    ref, dref, mref = oracle.dsg_nlm_denoise(img, P, R, bw, guide=guide, patch_sigma=sigma,
+                                             return_aux=True)
+    out, d, m = pnp.dsg_nlm_denoise(img, p, guide=guide, return_aux=True)
+    assert np.abs(out - ref).max() <= TOL
+    assert np.abs(d - dref).max() <= TOL
+    assert abs(m[0] - mref) <= 1e-5 * mref
+
+
+def test_config1_shape_both_regimes(pnp):
+    from paper_1901_06110_b200 import synth
+
+    img = synth.noisy(synth.scene(256, 256, 1), 20 / 255, 2)
+    for bw in ((10 / 255) / math.sqrt(2), 0.2):
+        p = pnp.PatchParams(5, 5, bw, 1.5)
+        ref, dref, mref = oracle.dsg_nlm_denoise(img, 5, 5, bw, patch_sigma=1.5, return_aux=True)
+        out, d, m = pnp.dsg_nlm_denoise(img, p, return_aux=True)
+        assert np.abs(out - ref).max() <= TOL
+        assert np.abs(d - dref).max() <= TOL
+        assert abs(m[0] - mref) <= 1e-5 * mref
+
+
+def test_frozen_bit_identical_to_adaptive(pnp, rng):
+    for shape, R, P, s in [((9, 9), 2, 3, None), ((77, 90), 10, 7, 2.0), ((300, 140), 5, 5, 1.5)]:
+        p = pnp.PatchParams(P, R, 0.2, s)
+        guide = rng.random(shape)
+        img = rng.random(shape)
+        fz = pnp.freeze_guide(guide, p)
+        assert np.array_equal(fz.apply(img), pnp.dsg_nlm_denoise(img, p, guide=guide))
+        assert np.array_equal(fz.apply(guide), pnp.dsg_nlm_denoise(guide, p))
+        ref = oracle.freeze_guide(guide, P, R, 0.2, s)
+        assert np.abs(fz.apply(img) - ref.apply(img)).max() <= TOL
+        assert abs(fz.alpha[0] - ref.m) <= 1e-5 * ref.m
+
+
+def test_frozen_linear_and_immutable(pnp, rng):
+    p = pnp.PatchParams(3, 2, 0.3)
+    guide = rng.random((8, 8))
+    fz = pnp.freeze_guide(guide, p)
+    a, b = rng.random((8, 8)), rng.random((8, 8))
+    combo = fz.apply(1.7 * a - 0.4 * b)
+    split = 1.7 * fz.apply(a) - 0.4 * fz.apply(b)
+    assert np.abs(combo - split).max() < 1e-5
+    guide[0, 0] += 1.0
+    with pytest.raises(ValueError):
+        fz.guide[0, 0] = 0.0
+    with pytest.raises(ValueError):
+        fz.apply(rng.random((8, 9)))
+
+
+def test_invariants_fixed_point_mean(pnp, rng):
+    p = pnp.PatchParams(3, 2, 0.2)
+    out = pnp.dsg_nlm_denoise(np.full((10, 10), 0.5), p, guide=rng.random((10, 10)))
+    assert np.abs(out - 0.5).max() < 2e-6
+    img = rng.random((140, 150))
+    out = pnp.dsg_nlm_denoise(img, pnp.PatchParams(5, 6, 0.2, 1.0))
+    assert out.mean() == pytest.approx(img.mean(), rel=2e-6)
+
+
+def test_deterministic_and_batch_consistent(pnp, rng):
+    p = pnp.PatchParams(7, 10, 0.15, 2.0)
+    imgs = torch.tensor(rng.random((3, 90, 100)), dtype=torch.float32, device="cuda")
+    a = pnp.dsg_nlm_denoise(imgs, p)
+    b = pnp.dsg_nlm_denoise(imgs, p)
+    assert torch.equal(a, b)
+    for i in range(3):
+        assert torch.equal(a[i], pnp.dsg_nlm_denoise(imgs[i].contiguous(), p))
+    fz = pnp.freeze_guide(imgs, p)
+    assert torch.equal(fz.apply(imgs), a)
+
+
+def test_errors(pnp, rng):
+    p = pnp.PatchParams(3, 4, 0.2)
+    with pytest.raises(ValueError):          # margin 5 > 4
+        pnp.dsg_nlm_denoise(rng.random((4, 8)), p)
+    with pytest.raises(ValueError):
+        pnp.dsg_nlm_denoise(rng.random((8, 8)), p, guide=rng.random((8, 9)))
+    bad = rng.random((8, 8))
+    bad[1, 1] = np.nan
+    with pytest.raises(ValueError):
+        pnp.dsg_nlm_denoise(bad, p)
+    with pytest.raises(ValueError):
+        pnp.dsg_nlm_denoise(rng.random((8, 8)), p, distances="sat")
+    with pytest.raises(ValueError):
+        pnp.dsg_nlm_denoise(rng.random((8,)), p)
+
+
+def test_nlm_vs_oracle(pnp, golden_extra, rng):
+    e = golden_extra
+    out = pnp.nlm_denoise(e["dense_img"], pnp.PatchParams(3, 2, 0.25), guide=e["dense_guide"])
+    assert np.abs(out - e["nlm_out"]).max() <= TOL
+    img = rng.random((50, 70))
+    p = pnp.PatchParams(5, 4, 0.15, 1.2)
+    ref = oracle.nlm_denoise(img, 5, 4, 0.15, patch_sigma=1.2)
+    assert np.abs(pnp.nlm_denoise(img, p) - ref).max() <= TOL

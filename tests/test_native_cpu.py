@@ -1,0 +1,76 @@
+"""CPU-side checks of the native boundary: the C-ABI library loads and exports
+every symbol include/pnp_b200.h declares (no compute without a GPU)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_symbols():
+    text = (ROOT / "include" / "pnp_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pnp_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1901_06110_b200 import _lib
+
+    syms = header_symbols()
+    assert len(syms) >= 20
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(syms) == set(_lib.EXPORTED)
+    assert lib.pnp_version() == 1
+
+
+def test_error_path_without_gpu_or_bad_args():
+    from paper_1901_06110_b200 import _lib
+
+    with pytest.raises(ValueError):
+        _lib.call("pnp_dsg_denoise", ctypes.c_void_p(), None, None, None, 1, 8, 8, 2, 3,
+                  None, 0.2, None, None)
+    assert "null" in _lib.lib.pnp_last_error().decode()
+
+
+def test_qis_simulate_host_matches_reference_golden(golden_forward):
+    """Host-native Knuth sampler is bit-exact with the reference (forward.py:263-298)."""
+    from paper_1901_06110_b200 import _lib
+
+    f = golden_forward
+    x = f["qis_truth"]
+    stop = np.ascontiguousarray(np.exp(-16.0 * np.clip(x, 0.0, 1.0) / 16).ravel())
+    ones = np.zeros(x.size)
+    _lib.call("pnp_qis_simulate_host", stop.ctypes.data_as(ctypes.c_void_p), x.size, 16,
+              2, ones.ctypes.data_as(ctypes.c_void_p))
+    assert np.array_equal(ones.reshape(x.shape), f["qis_ones"])
+
+
+def test_patch_params_validation():
+    from paper_1901_06110_b200 import PatchParams
+
+    with pytest.raises(ValueError):
+        PatchParams(4, 2, 0.1)
+    with pytest.raises(ValueError):
+        PatchParams(3, 0, 0.1)
+    with pytest.raises(ValueError):
+        PatchParams(3, 2, 0.0)
+    with pytest.raises(ValueError):
+        PatchParams(3, 2, 0.1, patch_sigma=0.0)
+    assert PatchParams(7, 10, 0.1).pad_margin == 13
+    p = PatchParams(5, 5, 0.2, 1.5)
+    assert abs(p.taps().sum() - 1) < 1e-15
+
+
+def test_synth_splitmix_matches_reference(golden_forward):
+    from paper_1901_06110_b200.synth import SplitMix64
+
+    f = golden_forward
+    r = SplitMix64(1234567)
+    assert [r.next_uint64() for _ in range(4)] == [int(v) for v in f["splitmix_u64"]]
+    assert np.array_equal(SplitMix64(99).uniforms(1001), f["splitmix_uniforms"])
+    assert np.array_equal(SplitMix64(5).normals(999), f["splitmix_normals"])
