@@ -16,7 +16,6 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpnpb200.so"
-SOURCES = ["pnp_dsg.cu", "pnp_forward.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -33,25 +32,36 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def sources():
+    return sorted(CSRC.glob("*.cu"))
+
+
+def build(force: bool = False, verbose: bool = False, extra=()) -> Path:
     if not force and not needs_build():
         return LIB
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+
     build_dir = PKG / "build"
     build_dir.mkdir(exist_ok=True)
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-I", str(ROOT / "include"), "--expt-relaxed-constexpr",
-                     "-Xptxas", "-v" if verbose else "-O3"]
-    for src in SOURCES:
-        obj = build_dir / (Path(src).stem + ".o")
-        cmd = [nvcc(), "-c", str(CSRC / src), "-o", str(obj)] + common
+                     "-Xptxas", "-v" if verbose else "-O3"] + list(extra)
+
+    def one(src: Path):
+        obj = build_dir / (src.stem + ".o")
+        cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + common
         r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(str(obj))
+        return src, obj, r
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 4))) as ex:
+        for src, obj, r in ex.map(one, sources()):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {src.name}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-o", str(tmp)] + objs + ARCH + ["-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -18,14 +18,18 @@
 // same code computes freeze/apply/adaptive so FrozenGuide.apply is
 // bit-identical to dsg_nlm_denoise (reference tests/test_denoise.py:256-268).
 //
-// Patch filter, per chunk of KY offsets sharing dx:
-//   phase 1  lane = map row q (32 rows = TH + 2p), warp = 8-column segment:
-//            D = (G_own - G_partner)^2 over 8+2p columns, horizontal P-tap
-//            filter -> H_k[q][c] in SMEM (odd row stride: conflict-free).
+// Patch filter, per chunk of KY offsets sharing dx (consecutive dy):
+//   phase 1  lane = map row q (32 rows = TH + 2p), warp = 16-column segment;
+//            the own guide row segment (16+2p) lives in registers for the
+//            whole kernel, the partner segment is read from SMEM;
+//            D = (G_own - G_partner)^2, horizontal P-tap filter -> H_k[q][c]
+//            in SMEM (odd row stride: conflict-free writes).
 //   phase 2  thread = (column c, row group g of N rows): vertical P-tap
 //            filter of H_k's column with the exponent scale and log2(hat)
 //            folded in, MUFU ex2, near FFMA, far FFMA into a register window
 //            of N+KY-1 rows, then one flush per chunk.
+// All SMEM strides are compile-time (R bucket RB >= R), so every access is a
+// base register + immediate offset.
 //
 // The tile writes its accumulators over rows [0, TH+R) x cols [-R, TW+R)
 // (tile + far band) to a partial block; dsg_fixup sums the covering blocks of
@@ -39,36 +43,60 @@ namespace pnp {
 
 constexpr int kTW = 64;        // tile width (output columns)
 constexpr int kThreads = 128;  // 64 columns x 2 row groups in phase 2
-constexpr int kKY = 2;         // offsets per chunk (same dx, consecutive dy)
+#ifndef PNP_KY
+#define PNP_KY 2
+#endif
+constexpr int kKY = PNP_KY;    // offsets per chunk (same dx, consecutive dy)
 constexpr int kMaxP = 15;      // largest patch side with a fast kernel
+constexpr int kMaxR = 32;      // largest search radius (R bucket)
 
 struct ChanSpec {
   const float* a;  // y = a * b, null factor = 1; inside the image only
   const float* b;
 };
 
+// One chunk of the half-window offset table: KY offsets (dx, dy0 + k),
+// k < kc, with their log2(hat) (0 for plain NLM) precomputed on the host.
+struct Chunk {
+  int dx, dy0, kc, pad;
+  float L[4];
+};
+
 struct SweepArgs {
   const float* guide;  // [B][H][W]
   ChanSpec ch[2];
   float* partial;      // [B][NG][tiles][C][BR][BC]
-  const int4* chunks;  // (dx, dy0, kc, 0)
+  const Chunk* chunks;
   const int* grp;      // NG+1 chunk starts
   int H, W, R;
   int tiles_x, tiles_y;
-  int use_hat;          // 0 for plain NLM (no taper)
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
 };
 
-template <int P>
-struct Geo {
+__host__ __device__ constexpr int tile_height(int P) { return 32 - (P - 1); }
+
+__host__ __device__ constexpr int r_bucket(int R) {
+  return R <= 5 ? 5 : (R <= 10 ? 10 : (R <= 16 ? 16 : 32));
+}
+
+template <int P, int RB, int C>
+struct Cfg {
   static constexpr int p = (P - 1) / 2;
   static constexpr int TH = 32 - 2 * p;  // tile height
   static constexpr int N = TH / 2;       // rows per phase-2 thread
-  static constexpr int SEGW = 8 + 2 * p;
+  static constexpr int SEG = 16;         // phase-1 segment width
+  static constexpr int SEGW = SEG + 2 * p;
+  static constexpr int KY = kKY;
+  static constexpr int WIN = N + KY - 1;
+  static constexpr int GC = kTW + 2 * (RB + p), GS = GC | 1, GR = 32 + RB;
+  static constexpr int HS = kTW + 1;
+  static constexpr int YC = kTW + 2 * RB, YR = TH + RB + KY, AR = N + RB + KY;
+  static constexpr int OFF_H = GR * GS;
+  static constexpr int OFF_Y = OFF_H + KY * 32 * HS;
+  static constexpr int OFF_A = OFF_Y + C * YR * YC;
+  static constexpr int TOTAL = OFF_A + 2 * C * AR * YC;  // floats
 };
-
-__host__ __device__ inline int tile_height(int P) { return 32 - (P - 1); }
 
 __device__ __forceinline__ int reflect_index(int i, int n) {
   // half-sample symmetric (np.pad mode="symmetric"; image.py:97-113),
@@ -84,39 +112,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// log2 of the separable hat (denoise.py:199-201), identical in every kernel.
-__device__ __forceinline__ float hat_log2(int dy, int dx, int R) {
-  const float s = (float)(R + 1);
-  const float hy = __fdiv_rn((float)(R + 1 - abs(dy)), s);
-  const float hx = __fdiv_rn((float)(R + 1 - abs(dx)), s);
-  return __fadd_rn(log2f(hy), log2f(hx));
-}
-
-inline size_t sweep_smem_floats(int P, int C, int R) {
-  const int p = (P - 1) / 2, TH = 32 - 2 * p, N = TH / 2;
-  const int GC = kTW + 2 * (R + p), GS = GC | 1, GR = 32 + R;
-  const int HS = kTW + 1, YC = kTW + 2 * R, YR = TH + R + kKY, AR = N + R + kKY;
-  return (size_t)GR * GS + (size_t)kKY * 32 * HS + (size_t)C * YR * YC +
-         (size_t)2 * C * AR * YC;
-}
-
-template <int P, int C>
+template <int P, int RB, int C>
 __global__ void __launch_bounds__(kThreads)
 dsg_sweep_kernel(const SweepArgs a) {
-  using G_ = Geo<P>;
-  constexpr int p = G_::p, TH = G_::TH, N = G_::N, SEGW = G_::SEGW, KY = kKY;
-  constexpr int WIN = N + KY - 1;
+  using K = Cfg<P, RB, C>;
+  constexpr int p = K::p, TH = K::TH, N = K::N, SEG = K::SEG, SEGW = K::SEGW, KY = K::KY;
+  constexpr int WIN = K::WIN, GS = K::GS, GC = K::GC, GR = K::GR, HS = K::HS;
+  constexpr int YC = K::YC, YR = K::YR, AR = K::AR;
+  static_assert(kTW / SEG == kThreads / 32, "one phase-1 segment per warp");
   extern __shared__ float smem[];
+  float* Gs = smem;
+  float* Hs = smem + K::OFF_H;
+  float* Ys = smem + K::OFF_Y;
+  float* As = smem + K::OFF_A;  // [2][C][AR][YC]
 
   const int R = a.R;
-  const int GC = kTW + 2 * (R + p), GS = GC | 1, GR = 32 + R;
-  const int HS = kTW + 1;
-  const int YC = kTW + 2 * R, YR = TH + R + KY, AR = N + R + KY;
-  float* Gs = smem;
-  float* Hs = Gs + GR * GS;
-  float* Ys = Hs + KY * 32 * HS;
-  float* As = Ys + C * YR * YC;  // [2][C][AR][YC]
-
   const int H = a.H, W = a.W;
   const int tile = blockIdx.x;
   const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
@@ -127,9 +137,10 @@ dsg_sweep_kernel(const SweepArgs a) {
   const int tid = threadIdx.x;
 
   // ---- stage guide (reflected), channel planes (zero outside), clear A ----
+  // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
   for (int i = tid; i < GR * GC; i += kThreads) {
     const int q = i / GC, cc = i - q * GC;
-    const int gr = reflect_index(r0g - p + q, H), gc = reflect_index(c0g - R - p + cc, W);
+    const int gr = reflect_index(r0g - p + q, H), gc = reflect_index(c0g - RB - p + cc, W);
     Gs[q * GS + cc] = __ldg(Gimg + (size_t)gr * W + gc);
   }
 #pragma unroll
@@ -139,7 +150,7 @@ dsg_sweep_kernel(const SweepArgs a) {
     float* Y = Ys + c_ * YR * YC;
     for (int i = tid; i < YR * YC; i += kThreads) {
       const int r = i / YC, cc = i - r * YC;
-      const int gr = r0g + r, gc = c0g - R + cc;
+      const int gr = r0g + r, gc = c0g - RB + cc;
       float v = 0.f;
       if (gr < H && gc >= 0 && gc < W) {
         const size_t o = (size_t)gr * W + gc;
@@ -154,49 +165,53 @@ dsg_sweep_kernel(const SweepArgs a) {
   __syncthreads();
 
   const int warp = tid >> 5, lane = tid & 31;
-  const int c = tid & (kTW - 1);  // phase-2 column
-  const int g = tid / kTW;        // phase-2 row group
+  const int c0 = SEG * warp;         // phase-1 segment
+  const int c = tid & (kTW - 1);     // phase-2 column
+  const int g = tid / kTW;           // phase-2 row group
   const int r0 = g * N;
 
+  float gown[SEGW];  // own guide row segment, resident for the whole kernel
+  {
+    const float* grow = Gs + lane * GS + c0 + RB;
+#pragma unroll
+    for (int x = 0; x < SEGW; ++x) gown[x] = grow[x];
+  }
   float yown[C][N], near[C][N];
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      yown[c_][r] = Ys[(c_ * YR + r0 + r) * YC + c + R];
+      yown[c_][r] = Ys[(c_ * YR + r0 + r) * YC + c + RB];
       near[c_][r] = (blockIdx.y == 0) ? yown[c_][r] : 0.f;  // self pair, k = hat = 1
     }
 
+  const float* hcol0 = Hs + r0 * HS + c;
+  float* hrow0 = Hs + lane * HS + c0;
+  float* Ag0 = As + g * C * AR * YC;
+
   const int cbeg = a.grp[blockIdx.y], cend = a.grp[blockIdx.y + 1];
   for (int ci = cbeg; ci < cend; ++ci) {
-    const int4 chk = a.chunks[ci];
-    const int dx = chk.x, dy0 = chk.y, kc = chk.z;
+    const Chunk chk = a.chunks[ci];
+    const int dx = chk.dx, dy0 = chk.dy0, kc = chk.kc;
 
     // ---------------- phase 1: squared differences + horizontal filter ----
-#pragma unroll
-    for (int s = 0; s < kTW / 8 / 4; ++s) {
-      const int c0 = 8 * (warp + 4 * s);
-      const float* grow = Gs + lane * GS + c0 + R;
-      float go[SEGW];
-#pragma unroll
-      for (int x = 0; x < SEGW; ++x) go[x] = grow[x];
+    {
+      const float* prow0 = Gs + (lane + dy0) * GS + c0 + RB + dx;
 #pragma unroll
       for (int k = 0; k < KY; ++k) {
-        if (k < kc) {
-          const float* prow = Gs + (lane + dy0 + k) * GS + c0 + R + dx;
+        if (k == 0 || k < kc) {
           float dd[SEGW];
 #pragma unroll
           for (int x = 0; x < SEGW; ++x) {
-            const float t = __fsub_rn(go[x], prow[x]);
+            const float t = __fsub_rn(gown[x], prow0[k * GS + x]);
             dd[x] = __fmul_rn(t, t);
           }
-          float* hrow = Hs + (k * 32 + lane) * HS + c0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < SEG; ++i) {
             float h = __fmul_rn(a.taps_h[0], dd[i]);
 #pragma unroll
             for (int bb = 1; bb < P; ++bb) h = __fmaf_rn(a.taps_h[bb], dd[i + bb], h);
-            hrow[i] = h;
+            hrow0[k * 32 * HS + i] = h;
           }
         }
       }
@@ -204,21 +219,23 @@ dsg_sweep_kernel(const SweepArgs a) {
     __syncthreads();
 
     // ---------------- phase 2: vertical filter, exp, near/far -------------
+    const float* ybase = Ys + (r0 + dy0) * YC + c + dx + RB;
+    float* abase = Ag0 + dy0 * YC + c + dx + RB;
     float yw[C][WIN], fw[C][WIN];
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
       for (int j = 0; j < WIN; ++j) {
-        yw[c_][j] = Ys[(c_ * YR + r0 + dy0 + j) * YC + c + dx + R];
+        yw[c_][j] = ybase[c_ * YR * YC + j * YC];
         fw[c_][j] = 0.f;
       }
 #pragma unroll
     for (int k = 0; k < KY; ++k) {
-      if (k < kc) {
-        const float L = a.use_hat ? hat_log2(dy0 + k, dx, R) : 0.f;
+      if (k == 0 || k < kc) {
+        const float L = chk.L[k];
         float hcol[N + 2 * p];
 #pragma unroll
-        for (int i = 0; i < N + 2 * p; ++i) hcol[i] = Hs[(k * 32 + r0 + i) * HS + c];
+        for (int i = 0; i < N + 2 * p; ++i) hcol[i] = hcol0[(k * 32 + i) * HS];
 #pragma unroll
         for (int r = 0; r < N; ++r) {
           float v = L;
@@ -233,29 +250,25 @@ dsg_sweep_kernel(const SweepArgs a) {
         }
       }
     }
-    float* Ag = As + g * C * AR * YC;
+    // window rows past the chunk's last offset hold +0: adding them is exact
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-      for (int j = 0; j < WIN; ++j)
-        if (j < N + kc - 1) {
-          float* pA = Ag + (c_ * AR + dy0 + j) * YC + c + dx + R;
-          *pA = __fadd_rn(*pA, fw[c_][j]);
-        }
+      for (int j = 0; j < WIN; ++j) {
+        float* pA = abase + c_ * AR * YC + j * YC;
+        *pA = __fadd_rn(*pA, fw[c_][j]);
+      }
     __syncthreads();
   }
 
   // ---- own pixels: near + far(own group); then emit tile + band block ----
-  {
-    float* Ag = As + g * C * AR * YC;
 #pragma unroll
-    for (int c_ = 0; c_ < C; ++c_)
+  for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-      for (int r = 0; r < N; ++r) {
-        float* pA = Ag + (c_ * AR + r) * YC + c + R;
-        *pA = __fadd_rn(near[c_][r], *pA);
-      }
-  }
+    for (int r = 0; r < N; ++r) {
+      float* pA = Ag0 + (c_ * AR + r) * YC + c + RB;
+      *pA = __fadd_rn(near[c_][r], *pA);
+    }
   __syncthreads();
   const int BR = TH + R, BC = kTW + 2 * R;
   const int ntiles = a.tiles_x * a.tiles_y;
@@ -263,8 +276,8 @@ dsg_sweep_kernel(const SweepArgs a) {
                (((size_t)b * gridDim.y + blockIdx.y) * ntiles + tile) * (size_t)(C * BR * BC);
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_) {
-    const float* A0 = As + (0 * C + c_) * AR * YC;
-    const float* A1 = As + (1 * C + c_) * AR * YC;
+    const float* A0 = As + (0 * C + c_) * AR * YC + (RB - R);
+    const float* A1 = As + (1 * C + c_) * AR * YC + (RB - R);
     for (int i = tid; i < BR * BC; i += kThreads) {
       const int br = i / BC, bc = i - br * BC;
       float v = 0.f;

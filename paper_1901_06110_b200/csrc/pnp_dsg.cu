@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "dsg_sweep.cuh"
+#include "sweep_launch.cuh"
 #include "pnp_internal.h"
 
 namespace pnp {
@@ -144,17 +145,30 @@ __global__ void dsg_alpha_kernel(const unsigned* mbits, float* mv, int B) {
 
 struct Plan {
   int B, H, W, R, P, TH, tiles_x, tiles_y, ntiles, nchunks, NG;
-  const int4* chunks;
+  const Chunk* chunks;  // hat-tapered table (DSG)
+  const Chunk* chunks_nohat;  // same offsets, L = 0 (plain NLM)
   const int* grp;
 };
 
-static void build_chunks(int R, std::vector<int4>& out) {
+// Half-window offsets grouped in chunks of KY consecutive dy sharing dx.
+static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
   out.clear();
   for (int dx = -R; dx <= R; ++dx) {
     const int dy_first = dx > 0 ? 0 : 1;
     for (int dy0 = dy_first; dy0 <= R; dy0 += kKY) {
-      const int kc = (R - dy0 + 1) < kKY ? (R - dy0 + 1) : kKY;
-      out.push_back(make_int4(dx, dy0, kc, 0));
+      Chunk ch;
+      memset(&ch, 0, sizeof(ch));
+      ch.dx = dx;
+      ch.dy0 = dy0;
+      ch.kc = (R - dy0 + 1) < kKY ? (R - dy0 + 1) : kKY;
+      for (int k = 0; k < kKY && k < 4; ++k) {
+        // log2 of the separable hat (denoise.py:199-201), in double, rounded once
+        const int dy = dy0 + k;
+        const double s = R + 1.0;
+        const double hy = 1.0 - fabs((double)dy) / s, hx = 1.0 - fabs((double)dx) / s;
+        ch.L[k] = (hat && k < ch.kc) ? (float)(log2(hy) + log2(hx)) : 0.f;
+      }
+      out.push_back(ch);
     }
   }
 }
@@ -183,9 +197,8 @@ static int check_geometry(int B, int H, int W, int R, int P, double bw) {
   if (margin > mn)
     return fail(PNP_EINVAL, "margin " + std::to_string(margin) + " exceeds min image extent " +
                                 std::to_string(mn));
-  const size_t smem = sweep_smem_floats(P, 2, R) * sizeof(float);
-  if (smem > 227 * 1024)
-    return fail(PNP_EINVAL, "window_radius too large for the shared-memory tile");
+  if (R > kMaxR)
+    return fail(PNP_EINVAL, "window_radius > " + std::to_string(kMaxR) + " not supported");
   return PNP_OK;
 }
 
@@ -199,26 +212,29 @@ static int make_plan(pnp_ctx* ctx, int B, int H, int W, int R, int P, Plan& pl) 
   pl.tiles_x = (W + kTW - 1) / kTW;
   pl.tiles_y = (H + pl.TH - 1) / pl.TH;
   pl.ntiles = pl.tiles_x * pl.tiles_y;
-  std::vector<int4> ch;
-  build_chunks(R, ch);
+  std::vector<Chunk> ch, ch0;
+  build_chunks(R, true, ch);
+  build_chunks(R, false, ch0);
   pl.nchunks = (int)ch.size();
   pl.NG = pick_groups(pl.ntiles, pl.nchunks);
   auto key = std::make_pair(R, pl.NG);
   auto it = ctx->tables.find(key);
+  const size_t cb = ch.size() * sizeof(Chunk);
   if (it == ctx->tables.end()) {
     std::vector<int> grp(pl.NG + 1);
     for (int g = 0; g <= pl.NG; ++g) grp[g] = (int)((long long)g * pl.nchunks / pl.NG);
     DevBuf buf;
-    const size_t cb = ch.size() * sizeof(int4);
-    int rc = buf.ensure(cb + grp.size() * sizeof(int));
+    int rc = buf.ensure(2 * cb + grp.size() * sizeof(int));
     if (rc) return rc;
     PNP_CUDA(cudaMemcpy(buf.ptr, ch.data(), cb, cudaMemcpyHostToDevice));
-    PNP_CUDA(cudaMemcpy(static_cast<char*>(buf.ptr) + cb, grp.data(), grp.size() * sizeof(int),
+    PNP_CUDA(cudaMemcpy(buf.as<char>() + cb, ch0.data(), cb, cudaMemcpyHostToDevice));
+    PNP_CUDA(cudaMemcpy(buf.as<char>() + 2 * cb, grp.data(), grp.size() * sizeof(int),
                         cudaMemcpyHostToDevice));
     it = ctx->tables.emplace(key, buf).first;
   }
-  pl.chunks = it->second.as<int4>();
-  pl.grp = reinterpret_cast<const int*>(it->second.as<char>() + ch.size() * sizeof(int4));
+  pl.chunks = it->second.as<Chunk>();
+  pl.chunks_nohat = reinterpret_cast<const Chunk*>(it->second.as<char>() + cb);
+  pl.grp = reinterpret_cast<const int*>(it->second.as<char>() + 2 * cb);
   return PNP_OK;
 }
 
@@ -226,34 +242,30 @@ static size_t partial_floats(const Plan& pl, int C) {
   return (size_t)pl.B * pl.NG * pl.ntiles * C * (pl.TH + pl.R) * (kTW + 2 * pl.R);
 }
 
-template <int P, int C>
-static int launch_sweep_t(const SweepArgs& a, const Plan& pl, cudaStream_t st) {
-  static bool attr_set = false;  // per device is fine: one device per process in practice
-  const size_t smem = sweep_smem_floats(P, C, pl.R) * sizeof(float);
-  if (!attr_set) {
-    PNP_CUDA(cudaFuncSetAttribute(dsg_sweep_kernel<P, C>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
+template <int RB, int C>
+static cudaError_t launch_sweep_rc(const SweepArgs& a, int P, dim3 grid, cudaStream_t st) {
+  switch (P) {
+    case 1: return launch_sweep<1, RB, C>(a, grid, st);
+    case 3: return launch_sweep<3, RB, C>(a, grid, st);
+    case 5: return launch_sweep<5, RB, C>(a, grid, st);
+    case 7: return launch_sweep<7, RB, C>(a, grid, st);
+    case 9: return launch_sweep<9, RB, C>(a, grid, st);
+    case 11: return launch_sweep<11, RB, C>(a, grid, st);
+    case 13: return launch_sweep<13, RB, C>(a, grid, st);
+    case 15: return launch_sweep<15, RB, C>(a, grid, st);
   }
-  dim3 grid(pl.ntiles, pl.NG, pl.B);
-  dsg_sweep_kernel<P, C><<<grid, kThreads, smem, st>>>(a);
-  PNP_LAUNCH_CHECK("dsg_sweep_kernel");
-  return PNP_OK;
+  return cudaErrorInvalidValue;
 }
 
 template <int C>
-static int launch_sweep_c(const SweepArgs& a, const Plan& pl, cudaStream_t st) {
-  switch (pl.P) {
-    case 1: return launch_sweep_t<1, C>(a, pl, st);
-    case 3: return launch_sweep_t<3, C>(a, pl, st);
-    case 5: return launch_sweep_t<5, C>(a, pl, st);
-    case 7: return launch_sweep_t<7, C>(a, pl, st);
-    case 9: return launch_sweep_t<9, C>(a, pl, st);
-    case 11: return launch_sweep_t<11, C>(a, pl, st);
-    case 13: return launch_sweep_t<13, C>(a, pl, st);
-    case 15: return launch_sweep_t<15, C>(a, pl, st);
+static cudaError_t launch_sweep_c(const SweepArgs& a, const Plan& pl, cudaStream_t st) {
+  dim3 grid(pl.ntiles, pl.NG, pl.B);
+  switch (r_bucket(pl.R)) {
+    case 5: return launch_sweep_rc<5, C>(a, pl.P, grid, st);
+    case 10: return launch_sweep_rc<10, C>(a, pl.P, grid, st);
+    case 16: return launch_sweep_rc<16, C>(a, pl.P, grid, st);
+    default: return launch_sweep_rc<32, C>(a, pl.P, grid, st);
   }
-  return fail(PNP_EINVAL, "unsupported patch_side");
 }
 
 static int run_sweep(pnp_ctx* ctx, const Plan& pl, int C, const float* guide, ChanSpec c0,
@@ -266,22 +278,23 @@ static int run_sweep(pnp_ctx* ctx, const Plan& pl, int C, const float* guide, Ch
   int rc = ctx->partial.ensure(partial_floats(pl, 2) * sizeof(float));
   if (rc) return rc;
   a.partial = ctx->partial.as<float>();
-  a.chunks = pl.chunks;
+  a.chunks = use_hat ? pl.chunks : pl.chunks_nohat;
   a.grp = pl.grp;
   a.H = pl.H;
   a.W = pl.W;
   a.R = pl.R;
   a.tiles_x = pl.tiles_x;
   a.tiles_y = pl.tiles_y;
-  a.use_hat = use_hat ? 1 : 0;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
   for (int i = 0; i < pl.P; ++i) {
     a.taps_h[i] = taps[i];
     a.taps_v[i] = (float)(scale * (double)taps[i]);
   }
-  if (C == 1) return launch_sweep_c<1>(a, pl, ctx->stream);
-  return launch_sweep_c<2>(a, pl, ctx->stream);
+  cudaError_t e = C == 1 ? launch_sweep_c<1>(a, pl, ctx->stream)
+                         : launch_sweep_c<2>(a, pl, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dsg_sweep_kernel");
+  return PNP_OK;
 }
 
 template <int MODE>

@@ -1,0 +1,6 @@
+// Explicit instantiations of the DSG sweep for patch side 9 (all R buckets, C = 1, 2).
+#include "sweep_launch.cuh"
+
+namespace pnp {
+PNP_INSTANTIATE_P(9)
+}  // namespace pnp

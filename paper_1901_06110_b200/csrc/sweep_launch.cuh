@@ -1,0 +1,58 @@
+// Launcher template for dsg_sweep_kernel; explicitly instantiated per patch
+// side in pnp_sweep_p*.cu (compiled in parallel), dispatched in pnp_dsg.cu.
+#pragma once
+
+#include "dsg_sweep.cuh"
+
+namespace pnp {
+
+template <int P, int RB, int C>
+cudaError_t launch_sweep(const SweepArgs& a, dim3 grid, cudaStream_t st) {
+  constexpr size_t smem = (size_t)Cfg<P, RB, C>::TOTAL * sizeof(float);
+  static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(dsg_sweep_kernel<P, RB, C>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dsg_sweep_kernel<P, RB, C><<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int P, int RB, int C>
+constexpr size_t sweep_smem_bytes() {
+  return (size_t)Cfg<P, RB, C>::TOTAL * sizeof(float);
+}
+
+#define PNP_INSTANTIATE_P(P)                                                               \
+  template cudaError_t launch_sweep<P, 5, 1>(const SweepArgs&, dim3, cudaStream_t);       \
+  template cudaError_t launch_sweep<P, 5, 2>(const SweepArgs&, dim3, cudaStream_t);       \
+  template cudaError_t launch_sweep<P, 10, 1>(const SweepArgs&, dim3, cudaStream_t);      \
+  template cudaError_t launch_sweep<P, 10, 2>(const SweepArgs&, dim3, cudaStream_t);      \
+  template cudaError_t launch_sweep<P, 16, 1>(const SweepArgs&, dim3, cudaStream_t);      \
+  template cudaError_t launch_sweep<P, 16, 2>(const SweepArgs&, dim3, cudaStream_t);      \
+  template cudaError_t launch_sweep<P, 32, 1>(const SweepArgs&, dim3, cudaStream_t);      \
+  template cudaError_t launch_sweep<P, 32, 2>(const SweepArgs&, dim3, cudaStream_t);
+
+#define PNP_DECLARE_P(P)                                                                     \
+  extern template cudaError_t launch_sweep<P, 5, 1>(const SweepArgs&, dim3, cudaStream_t);  \
+  extern template cudaError_t launch_sweep<P, 5, 2>(const SweepArgs&, dim3, cudaStream_t);  \
+  extern template cudaError_t launch_sweep<P, 10, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 2>(const SweepArgs&, dim3, cudaStream_t);
+
+PNP_DECLARE_P(1)
+PNP_DECLARE_P(3)
+PNP_DECLARE_P(5)
+PNP_DECLARE_P(7)
+PNP_DECLARE_P(9)
+PNP_DECLARE_P(11)
+PNP_DECLARE_P(13)
+PNP_DECLARE_P(15)
+
+}  // namespace pnp
