@@ -80,9 +80,10 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
                     double bandwidth);
 
 /* ---- forward operators (forward.py) ------------------------------------- */
-/* SR operator: separable normalized blur taps (2r+1 host floats; the
- * reference's gaussian_kernel is an outer product of these), integer factor,
- * boundary 0 = periodic, 1 = symmetric (forward.py:98-148). */
+/* SR operator: separable blur k = ty tx^T given as 2(2r+1) host floats
+ * (ty then tx; the reference's gaussian_kernel is such an outer product),
+ * integer factor, boundary 0 = periodic (wrap), 1 = half-sample symmetric
+ * (forward.py:98-148). */
 int pnp_sr_apply(pnp_ctx* ctx, const float* x, float* y, int batch, int H, int W,
                  const float* taps, int radius, int factor, int boundary);
 int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int W,
@@ -92,9 +93,11 @@ int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int
 int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, int batch,
                 int H, int W, const float* taps, int radius, int factor, int boundary,
                 double* data_out);
-/* QIS gradient (forward.py:322-327) and data term (312-319, double per image). */
+/* QIS gradient (forward.py:322-327) and data term (312-319, double per image).
+ * pnp_qis_grad: grad may be null (data only), data_out may be null. */
 int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros,
-                 float* grad, int batch, int n, double gain_over_K, double floor_);
+                 float* grad, int batch, int n, double gain_over_K, double floor_,
+                 double* data_out);
 int pnp_qis_data(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros,
                  int batch, int n, double gain_over_K, double floor_, double* data_out);
 /* qis_simulate Knuth loop on the HOST (forward.py:263-298): stop[i] =

@@ -15,6 +15,48 @@ from .denoise import (  # noqa: F401
     hat_weight,
     nlm_denoise,
 )
+from .forward import (  # noqa: F401
+    QIS_FLOOR,
+    QisCounts,
+    QisModel,
+    SuperResOp,
+    gaussian_kernel,
+    power_iteration_lipschitz,
+    qis_data_term,
+    qis_gradient,
+    qis_initial_estimate,
+    qis_simulate,
+    sr_adjoint,
+    sr_apply,
+    sr_data_term,
+    sr_gradient,
+    sr_simulate,
+)
+from .image import (  # noqa: F401
+    NON_NEGATIVE,
+    UNCONSTRAINED,
+    UNIT_BOX,
+    Box,
+    NonNegative,
+    Unconstrained,
+    project,
+    psnr,
+    validate_image,
+)
+from .solver import (  # noqa: F401
+    DivergenceError,
+    IterationRecord,
+    Problem,
+    SolverConfig,
+    default_qis_alpha,
+    default_sr_alpha,
+    device_callable,
+    linearized_pnp_admm,
+    make_qis_problem,
+    make_sr_problem,
+    residuals,
+    write_log_csv,
+)
 from .synth import SplitMix64  # noqa: F401
 
 __version__ = "0.1.0"

@@ -46,7 +46,7 @@ _SIGS = {
     "pnp_sr_apply": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
     "pnp_sr_adjoint": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
     "pnp_sr_grad": (i32, [vp, vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, vp]),
-    "pnp_qis_grad": (i32, [vp, vp, vp, vp, vp, i32, i32, f64, f64]),
+    "pnp_qis_grad": (i32, [vp, vp, vp, vp, vp, i32, i32, f64, f64, vp]),
     "pnp_qis_data": (i32, [vp, vp, vp, vp, i32, i32, f64, f64, vp]),
     "pnp_qis_simulate_host": (i32, [vp, i64, i32, C.c_uint64, vp]),
     "pnp_admm_xupdate": (i32, [vp, vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, vp]),

@@ -21,7 +21,8 @@ namespace pnp {
 
 constexpr int kMaxTaps = 63;
 struct Taps {
-  float t[kMaxTaps];
+  float ty[kMaxTaps];  // vertical profile (row sums of the 2-D kernel)
+  float tx[kMaxTaps];  // horizontal profile (column sums)
 };
 
 __device__ __forceinline__ int map_index(int i, int n, int symmetric) {
@@ -73,8 +74,8 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
     for (int a = -rad; a <= rad; ++a) {
       const float* row = xb + (size_t)map_index(k * oy + a, H, sym) * W;
       float s = 0.f;
-      for (int c = -rad; c <= rad; ++c) s = fmaf(taps.t[c + rad], row[map_index(k * ox + c, W, sym)], s);
-      acc = fmaf(taps.t[a + rad], s, acc);
+      for (int c = -rad; c <= rad; ++c) s = fmaf(taps.tx[c + rad], row[map_index(k * ox + c, W, sym)], s);
+      acc = fmaf(taps.ty[a + rad], s, acc);
     }
     if (y) acc -= y[(size_t)b * h * w + i];
     r[(size_t)b * h * w + i] = acc;
@@ -102,9 +103,9 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, i
     for (int c = -rad; c <= rad; ++c) {
       const int ux = map_index(px + c, W, sym);
       if (ux % k) continue;
-      s = fmaf(taps.t[c + rad], row[ux / k], s);
+      s = fmaf(taps.tx[c + rad], row[ux / k], s);
     }
-    acc = fmaf(taps.t[a + rad], s, acc);
+    acc = fmaf(taps.ty[a + rad], s, acc);
   }
   out[(size_t)b * H * W + i] = acc;
 }
@@ -216,7 +217,10 @@ static int sr_check(int batch, int H, int W, const float* taps, int radius, int 
   if (radius > (H < W ? H : W)) return fail(PNP_EINVAL, "kernel radius exceeds image extent");
   if (boundary != 0 && boundary != 1) return fail(PNP_EINVAL, "boundary must be 0 or 1");
   if (!taps) return fail(PNP_EINVAL, "taps null");
-  for (int i = 0; i < 2 * radius + 1; ++i) t.t[i] = taps[i];
+  for (int i = 0; i < 2 * radius + 1; ++i) {
+    t.ty[i] = taps[i];
+    t.tx[i] = taps[2 * radius + 1 + i];
+  }
   return PNP_OK;
 }
 
@@ -282,13 +286,24 @@ int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, in
 }
 
 int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros, float* grad,
-                 int batch, int n, double gain_over_K, double floor_) {
-  if (!ctx || !x || !ones || !zeros || !grad) return fail(PNP_EINVAL, "null argument");
+                 int batch, int n, double gain_over_K, double floor_, double* data_out) {
+  if (!ctx || !x || !ones || !zeros || (!grad && !data_out))
+    return fail(PNP_EINVAL, "null argument");
   if (batch < 1 || n < 1) return fail(PNP_EINVAL, "bad shape");
-  dim3 grid((n + 255) / 256, batch);
-  qis_grad_kernel<<<grid, 256, 0, ctx->stream>>>(x, ones, zeros, grad, (size_t)n, gain_over_K,
-                                                 floor_, nullptr);
+  const int nblk = (n + 255) / 256;
+  double* part = nullptr;
+  if (data_out) {
+    int rc = ensure_partials(ctx, (size_t)batch * nblk);
+    if (rc) return rc;
+    part = ctx->stats.as<double>();
+  }
+  qis_grad_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, ones, zeros, grad, (size_t)n,
+                                                              gain_over_K, floor_, part);
   PNP_LAUNCH_CHECK("qis_grad_kernel");
+  if (data_out) {
+    reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
+    PNP_LAUNCH_CHECK("reduce_partials_kernel");
+  }
   return PNP_OK;
 }
 

@@ -1,0 +1,384 @@
+"""Linearized plug-and-play ADMM on the B200 — drop-in for pnprestore/solver.py.
+
+Names/semantics follow /root/reference/pkg/src/pnprestore/solver.py:
+``SolverConfig`` (54-101), ``Problem`` (104-114), ``IterationRecord`` /
+``write_log_csv`` (117-144), ``residuals`` (147-153), ``_make_denoiser``
+(156-177), ``linearized_pnp_admm`` (199-235), ``make_sr_problem`` (335-349),
+``make_qis_problem`` (352-362), ``default_sr_alpha`` / ``default_qis_alpha``
+(365-374), ``DivergenceError`` (46-47).
+
+The iterates x, v, u stay on the GPU for the whole run.  One iteration is
+  grad (SR: fused residual+adjoint kernels, QIS: one elementwise kernel, the
+        data term of the previous iterate rides along),
+  x-update + projection + x+u + finite flags (one kernel),
+  denoiser (DSG sweep + fixup, or the frozen apply),
+  u-update + primal/dual/PSNR partial sums + finite flags (one kernel);
+log scalars accumulate in device arrays and come back once at the end (or
+per iteration when ``stop_tol`` / a host callback needs them).  A non-finite
+iterate raises DivergenceError with the same iteration index as the
+reference.
+
+Plug-in callables (``Problem.gradient``, ``denoiser``, ``callback``) keep the
+reference contract: plain callables receive float64 numpy arrays.  Callables
+marked with :func:`device_callable` (and everything built by this package)
+receive float32 CUDA tensors and stay on device.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _arrays as A
+from . import _lib as L
+from .denoise import PatchParams, dsg_nlm_denoise, freeze_guide, nlm_denoise
+from .forward import (QIS_FLOOR, QisCounts, QisModel, SuperResOp, power_iteration_lipschitz,
+                      qis_grad_device, qis_initial_estimate, sr_adjoint)
+from .image import UNCONSTRAINED, Box, Constraint, NonNegative, Unconstrained, bounds
+
+DENOISERS = ("identity", "nlm", "dsg-adaptive", "dsg-fixed")
+
+
+class DivergenceError(RuntimeError):
+    """An iterate picked up non-finite values; the run was aborted."""
+
+
+def device_callable(fn):
+    """Mark a plug-in as device-native: it receives/returns CUDA tensors."""
+    fn._pnp_device = True
+    return fn
+
+
+def _is_device(fn) -> bool:
+    return bool(getattr(fn, "_pnp_device", False))
+
+
+@dataclass
+class SolverConfig:
+    """Hyperparameters (reference solver.py:54-101) + ``patch_sigma``
+    (Gaussian patch weights for the built-in DSG/NLM denoisers)."""
+
+    rho: float = 1.0
+    lam: float = 0.02
+    alpha: float = 1.1
+    max_iters: int = 250
+    freeze_at: int | None = 15
+    constraint: Constraint = UNCONSTRAINED
+    denoiser: str = "dsg-fixed"
+    patch_side: int = 7
+    window_radius: int = 10
+    bandwidth: float | None = None
+    stop_tol: float | None = None
+    cg_tol: float = 1e-6
+    cg_max_iters: int = 200
+    cg_warm_start: bool = False
+    patch_sigma: float | None = None
+
+    def __post_init__(self) -> None:
+        if not self.rho > 0:
+            raise ValueError(f"rho must be > 0, got {self.rho}")
+        if self.lam < 0:
+            raise ValueError(f"lam must be >= 0, got {self.lam}")
+        if not self.alpha > 0:
+            raise ValueError(f"alpha must be > 0, got {self.alpha}")
+        if self.max_iters < 1:
+            raise ValueError(f"max_iters must be >= 1, got {self.max_iters}")
+        if self.freeze_at is not None and self.freeze_at < 1:
+            raise ValueError(f"freeze_at must be >= 1, got {self.freeze_at}")
+        if self.denoiser not in DENOISERS:
+            raise ValueError(f"denoiser must be one of {DENOISERS}, got {self.denoiser!r}")
+        if self.bandwidth is not None and not self.bandwidth > 0:
+            raise ValueError(f"bandwidth must be > 0, got {self.bandwidth}")
+        if not self.cg_tol > 0:
+            raise ValueError(f"cg_tol must be > 0, got {self.cg_tol}")
+        if self.cg_max_iters < 1:
+            raise ValueError(f"cg_max_iters must be >= 1, got {self.cg_max_iters}")
+
+    def effective_bandwidth(self) -> float:
+        if self.bandwidth is not None:
+            return self.bandwidth
+        return math.sqrt(self.lam / self.rho)
+
+    def patch_params(self) -> PatchParams:
+        return PatchParams(self.patch_side, self.window_radius, self.effective_bandwidth(),
+                           self.patch_sigma)
+
+
+@dataclass
+class Problem:
+    """Data-term oracles plus optional extras (reference solver.py:104-114).
+
+    ``device_gradient(x, grad_out, data_out)`` — set by make_sr_problem /
+    make_qis_problem — is the device path: it writes grad f(x) into
+    ``grad_out`` and, when ``data_out`` is given, f(x) (float64 per image)."""
+
+    shape: tuple
+    gradient: Callable
+    x0: object
+    objective: Callable | None = None
+    ground_truth: object | None = None
+    gram: Callable | None = None
+    atb: object | None = None
+    device_gradient: Callable | None = field(default=None, repr=False)
+
+
+@dataclass
+class IterationRecord:
+    index: int
+    primal: float
+    dual: float
+    psnr: float
+    time_ms: float
+    objective: float
+
+
+CSV_HEADER = "iter,primal,dual,psnr,time_ms,objective"
+
+
+def write_log_csv(records, path, include_time: bool = True) -> None:
+    """One row per iteration, LF endings, shortest float repr (solver.py:130-144)."""
+    lines = [CSV_HEADER]
+    for r in records:
+        t = r.time_ms if include_time else 0.0
+        lines.append(f"{r.index},{float(r.primal)!r},{float(r.dual)!r},"
+                     f"{float(r.psnr)!r},{float(t)!r},{float(r.objective)!r}")
+    with open(path, "w", newline="\n") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
+def residuals(x, v, v_prev, rho: float) -> tuple[float, float]:
+    """Mean-square primal gap ||x-v||^2/n and dual change ||rho (v-v_prev)||^2/n."""
+    ts = [A.to_device(a) for a in (x, v, v_prev)]
+    if not (ts[0].shape == ts[1].shape == ts[2].shape):
+        raise ValueError(f"dimension mismatch: {tuple(ts[0].shape)}, {tuple(ts[1].shape)}, "
+                         f"{tuple(ts[2].shape)}")
+    x_, v_, vp = (t.double() for t in ts)
+    return float(((x_ - v_) ** 2).mean()), float(((rho * (v_ - vp)) ** 2).mean())
+
+
+# ---------------------------------------------------------------------------
+# Denoiser schedules (solver.py:156-177), device resident
+# ---------------------------------------------------------------------------
+
+def _make_denoiser(config: SolverConfig):
+    if config.denoiser == "identity" or config.lam == 0.0:
+        return device_callable(lambda img, k: img.clone())
+    params = config.patch_params()
+    if config.denoiser == "nlm":
+        return device_callable(lambda img, k: nlm_denoise(img, params))
+    if config.denoiser == "dsg-adaptive":
+        return device_callable(lambda img, k: _dsg_device(img, params))
+    state = {"frozen": None}
+
+    def fixed(img, k):
+        if config.freeze_at is None or k < config.freeze_at:
+            return _dsg_device(img, params)
+        if state["frozen"] is None:
+            state["frozen"] = freeze_guide(img, params)
+        return state["frozen"].apply_device(img)
+
+    return device_callable(fixed)
+
+
+def _dsg_device(img: torch.Tensor, params: PatchParams) -> torch.Tensor:
+    """Unchecked device DSG-NLM (inputs already validated by the solver)."""
+    B, H, W = A.dims(img)
+    out = torch.empty_like(img)
+    L.call("pnp_dsg_denoise", L.context(img.device.index), L.ptr(img), L.ptr(img), L.ptr(out),
+           B, H, W, params.window_radius, params.patch_side, params._ctaps(),
+           float(params.bandwidth), None, None)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Linearized PnP-ADMM (Algorithm 1)
+# ---------------------------------------------------------------------------
+
+def _host_wrap_array_fn(fn, kind_shape):
+    """Host plug-in: numpy float64 in, result uploaded back to the device."""
+    def run(t: torch.Tensor, *extra):
+        res = fn(t.detach().cpu().numpy().astype(np.float64), *extra)
+        return A.to_device(res, t.device.index).reshape(t.shape)
+    return run
+
+
+def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, callback=None):
+    """Gradient-step PnP-ADMM; returns (final v, per-iteration records).
+
+    Per iteration: x <- proj(mu (alpha x + rho (v - u) - grad f(x))) with
+    mu = 1/(alpha + rho), then v <- D(x + u), then u <- u + (x - v).
+    The result is a float64 numpy array when ``problem.x0`` is numpy, else a
+    CUDA tensor.
+    """
+    dev = A.device_index()
+    x0, kind = A.validate(problem.x0, "x0", batch_ok=True)
+    x = A.to_device(x0, dev).clone()
+    B, H, W = A.dims(x)
+    n = H * W
+    lo, hi = bounds(config.constraint)
+    ctx = L.context(dev)
+    if denoiser is None:
+        denoiser = _make_denoiser(config)
+    den = denoiser if _is_device(denoiser) else _host_wrap_array_fn(denoiser, None)
+
+    if problem.device_gradient is not None:
+        grad_fn = problem.device_gradient
+    else:
+        host_grad = _host_wrap_array_fn(problem.gradient, None)
+
+        def grad_fn(xt, out, data_out):
+            out.copy_(host_grad(xt))
+            if data_out is not None and problem.objective is not None:
+                data_out.fill_(float(problem.objective(xt.cpu().numpy().astype(np.float64))))
+            return out
+
+    track_obj = problem.device_gradient is not None or problem.objective is not None
+    gt = None
+    if problem.ground_truth is not None:
+        gt = A.to_device(problem.ground_truth, dev)
+        if tuple(gt.shape) != tuple(x.shape):
+            raise ValueError("ground_truth shape differs from x0")
+
+    iters = config.max_iters
+    stats = torch.zeros((iters, B, 4), dtype=torch.float64, device=x.device)
+    objv = torch.full((iters + 1, B), math.nan, dtype=torch.float64, device=x.device)
+    flags = torch.zeros(iters, dtype=torch.int32, device=x.device)
+    grad = torch.empty_like(x)
+    z = torch.empty_like(x)
+    mu = 1.0 / (config.alpha + config.rho)
+    events = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+
+    L.call("pnp_project", ctx, L.ptr(x), L.ptr(x), x.numel(), lo, hi)
+    v = x.clone()
+    u = torch.zeros_like(x)
+    sync_each = callback is not None or config.stop_tol is not None
+    t0 = time.perf_counter()
+    events[0].record()
+    done = iters
+    for k in range(1, iters + 1):
+        # objective of the previous (projected) iterate rides on this gradient
+        grad_fn(x, grad, objv[k - 2] if (k >= 2 and track_obj) else None)
+        fk = flags[k - 1:k]
+        L.call("pnp_admm_xupdate", ctx, L.ptr(x), L.ptr(v), L.ptr(u), L.ptr(grad), L.ptr(z),
+               x.numel(), mu, float(config.alpha), float(config.rho), lo, hi, L.ptr(fk))
+        v_prev = v
+        v = den(z, k)
+        if not isinstance(v, torch.Tensor) or v.dtype != torch.float32 or not v.is_contiguous():
+            v = A.to_device(v, dev).reshape(x.shape)
+        if v.data_ptr() in (z.data_ptr(), x.data_ptr(), u.data_ptr(), v_prev.data_ptr()):
+            v = v.clone()  # a plug-in may hand back its input; iterates must not alias
+        L.call("pnp_admm_uupdate", ctx, L.ptr(u), L.ptr(x), L.ptr(v), L.ptr(v_prev), L.ptr(gt),
+               B, n, float(config.rho), L.ptr(stats[k - 1]), L.ptr(fk))
+        events[k].record()
+        if sync_each:
+            if int(flags[k - 1]):
+                raise DivergenceError(f"non-finite iterate at iteration {k}")
+            if callback is not None:
+                if _is_device(callback):
+                    callback(k, x, v, u)
+                else:
+                    callback(k, *(A.from_device(t.clone(), A.NUMPY) for t in (x, v, u)))
+            if config.stop_tol is not None:
+                s = stats[k - 1, 0].cpu()
+                primal, dual = float(s[0]) / n, float(s[1]) / n
+                if primal < config.stop_tol and dual < config.stop_tol:
+                    done = k
+                    break
+    if track_obj:  # objective at the final iterate
+        grad_fn(x, grad, objv[done - 1])
+    torch.cuda.synchronize(dev)
+    fl = flags[:done].cpu().numpy()
+    bad = np.nonzero(fl)[0]
+    if bad.size:
+        raise DivergenceError(f"non-finite iterate at iteration {int(bad[0]) + 1}")
+    st = stats[:done].cpu().numpy()
+    ob = objv[:done].cpu().numpy()
+    wall = (time.perf_counter() - t0) * 1e3
+    times = [events[0].elapsed_time(events[k]) for k in range(1, done + 1)]
+    records = []
+    for i in range(done):
+        primal = st[i, :, 0] / n
+        dual = st[i, :, 1] / n
+        if gt is not None:
+            mse = st[i, :, 2] / n
+            q = np.where(mse == 0.0, math.inf, 10.0 * np.log10(1.0 / np.where(mse == 0, 1, mse)))
+        else:
+            q = np.full(B, math.nan)
+        obj = ob[i] if track_obj else np.full(B, math.nan)
+        if B == 1 and x.dim() == 2:
+            records.append(IterationRecord(i + 1, float(primal[0]), float(dual[0]), float(q[0]),
+                                           float(times[i]), float(obj[0])))
+        else:
+            records.append(IterationRecord(i + 1, primal, dual, q, float(times[i]), obj))
+    del wall
+    return A.from_device(v, kind), records
+
+
+# ---------------------------------------------------------------------------
+# Problem builders
+# ---------------------------------------------------------------------------
+
+def make_sr_problem(op: SuperResOp, observed, ground_truth=None) -> Problem:
+    """SR problem; x0 = k^2 A^T y (solver.py:335-349).  Device resident."""
+    obs, kind = A.validate(observed, "observation", batch_ok=True)
+    y = A.to_device(obs)
+    x0d = float(op.factor ** 2) * op.adjoint_device(y)
+    x0 = A.from_device(x0d, kind)
+
+    def device_gradient(x, out, data_out=None):
+        return op.gradient_device(x, y, out, data_out)
+
+    def gradient(x):
+        from .forward import sr_gradient
+        return sr_gradient(op, x, A.from_device(y, A.kind_of(x)))
+
+    def objective(x):
+        from .forward import sr_data_term
+        return sr_data_term(op, x, A.from_device(y, A.kind_of(x)))
+
+    def gram(x):
+        from .forward import sr_apply
+        return sr_adjoint(op, sr_apply(op, x))
+
+    return Problem(shape=tuple(x0d.shape), gradient=gradient, x0=x0, objective=objective,
+                   ground_truth=ground_truth, gram=gram,
+                   atb=A.from_device(op.adjoint_device(y), kind),
+                   device_gradient=device_gradient)
+
+
+def make_qis_problem(counts: QisCounts, model: QisModel, ground_truth=None,
+                     floor: float = QIS_FLOOR) -> Problem:
+    """QIS problem; x0 = clip(K1/K, floor, 1) (solver.py:352-362)."""
+    ones, zeros = counts.device()
+    if counts.oversampling != model.oversampling:
+        raise ValueError(f"counts are for K={counts.oversampling}, model has K={model.oversampling}")
+
+    def device_gradient(x, out, data_out=None):
+        return qis_grad_device(x, ones, zeros, model, floor, out, data_out)
+
+    def gradient(x):
+        from .forward import qis_gradient
+        return qis_gradient(x, counts, model, floor)
+
+    def objective(x):
+        from .forward import qis_data_term
+        return qis_data_term(x, counts, model, floor)
+
+    return Problem(shape=counts.shape, gradient=gradient, x0=qis_initial_estimate(counts, floor),
+                   objective=objective, ground_truth=ground_truth,
+                   device_gradient=device_gradient)
+
+
+def default_sr_alpha(op: SuperResOp, hr_shape, iters: int = 200, seed: int = 0) -> float:
+    """1.05 x the power-iteration Lipschitz estimate (solver.py:365-368)."""
+    return 1.05 * power_iteration_lipschitz(op, hr_shape, iters, seed)
+
+
+def default_qis_alpha(counts: QisCounts, model: QisModel) -> float:
+    """2 * gain * max(K0) / K (solver.py:371-374)."""
+    return 2.0 * model.gain * float(counts.zeros.max()) / model.oversampling

@@ -1,0 +1,198 @@
+"""GPU linearized PnP-ADMM vs the reference goldens / float64 oracle, plus the
+reference's solver properties (solver.py:199-235; tests/test_solver.py).
+
+North-star bar: final ADMM PSNR within 0.02 dB of the float64 oracle."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import admm as oadmm
+from oracle import forward as ofw
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pnp():
+    import paper_1901_06110_b200 as pnp
+    return pnp
+
+
+def quadratic_problem(pnp, y):
+    return pnp.Problem(shape=y.shape, gradient=lambda x: x - y, x0=np.zeros(y.shape),
+                       objective=lambda x: 0.5 * float(((x - y) ** 2).sum()))
+
+
+def _rec(recs):
+    return np.array([[r.index, r.primal, r.dual, r.psnr, r.objective] for r in recs])
+
+
+def test_sr_dsg_fixed_matches_reference(pnp, golden_admm):
+    a = golden_admm
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    prob = pnp.make_sr_problem(op, a["sr_y"], ground_truth=a["sr_truth"])
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=8, freeze_at=3,
+                           constraint=pnp.UNIT_BOX, denoiser="dsg-fixed",
+                           patch_side=3, window_radius=3, bandwidth=0.1)
+    v, recs = pnp.linearized_pnp_admm(prob, cfg)
+    ref = a["sr_fixed_rec"]
+    got = _rec(recs)
+    assert np.abs(v - a["sr_fixed_v"]).max() < 1e-4
+    assert np.abs(got[:, 3] - ref[:, 3]).max() < 0.02            # PSNR (dB)
+    assert np.allclose(got[:, 4], ref[:, 4], rtol=1e-3)           # objective
+    assert np.allclose(got[:, 1:3], ref[:, 1:3], rtol=2e-2, atol=1e-9)
+
+
+def test_sr_gaussian_frozen_plugin(pnp, golden_admm):
+    a = golden_admm
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    prob = pnp.make_sr_problem(op, a["sr_y"], ground_truth=a["sr_truth"])
+    params = pnp.PatchParams.from_h(5, 4, 8 / 255, 2.0)
+    fz = pnp.freeze_guide(a["sr_gauss_guide"], params)
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=6, constraint=pnp.UNIT_BOX)
+    v1, r1 = pnp.linearized_pnp_admm(prob, cfg, denoiser=fz.as_denoiser())
+    v2, r2 = pnp.linearized_pnp_admm(prob, cfg, denoiser=lambda im, k: fz.apply(im))
+    assert np.abs(v1 - a["sr_gauss_v"]).max() < 1e-4
+    assert abs(r1[-1].psnr - a["sr_gauss_rec"][-1, 3]) < 0.02
+    assert np.abs(v1 - v2).max() < 1e-6     # host plug-in path == device path
+
+
+def test_qis_dsg_fixed_matches_reference(pnp, golden_admm):
+    a = golden_admm
+    model = pnp.QisModel(128, 64.0)
+    ones = a["qis_ones"]
+    counts = pnp.QisCounts(ones, 128 - ones)
+    prob = pnp.make_qis_problem(counts, model, ground_truth=a["qis_truth"])
+    alpha = pnp.default_qis_alpha(counts, model)
+    assert alpha == float(a["qis_alpha"])
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=alpha, max_iters=6, freeze_at=4,
+                           constraint=pnp.UNIT_BOX, denoiser="dsg-fixed",
+                           patch_side=3, window_radius=3, bandwidth=0.15)
+    v, recs = pnp.linearized_pnp_admm(prob, cfg)
+    got, ref = _rec(recs), a["qis_rec"]
+    assert np.abs(v - a["qis_v"]).max() < 1e-4
+    assert np.abs(got[:, 3] - ref[:, 3]).max() < 0.02
+    assert np.allclose(got[:, 4], ref[:, 4], rtol=1e-5)
+
+
+def test_fixed_point_zero_residuals(pnp):
+    y = np.full((6, 6), 0.5)
+    prob = pnp.Problem(shape=(6, 6), gradient=lambda x: np.zeros((6, 6)), x0=y)
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.0, alpha=1.0, max_iters=3, denoiser="identity")
+    v, recs = pnp.linearized_pnp_admm(prob, cfg)
+    assert recs[0].primal == 0.0 and recs[0].dual == 0.0
+    assert np.array_equal(v, y)
+
+
+def test_identity_quadratic_converges_to_clamp(pnp, rng):
+    y = rng.standard_normal((10, 10)) * 0.8 + 0.5
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.0, alpha=1.05, max_iters=500,
+                           denoiser="identity", constraint=pnp.Box(0.0, 1.0))
+    v, recs = pnp.linearized_pnp_admm(quadratic_problem(pnp, y), cfg)
+    assert np.abs(v - np.clip(y, 0.0, 1.0)).max() < 1e-5
+    assert len(recs) == 500
+
+
+def test_multiplier_bookkeeping(pnp, rng):
+    y = rng.random((6, 6))
+    cfg = pnp.SolverConfig(rho=0.7, lam=0.0, alpha=1.2, max_iters=12, denoiser="identity")
+    gaps = []
+    pnp.linearized_pnp_admm(quadratic_problem(pnp, y), cfg, denoiser=lambda img, k: 0.9 * img,
+                            callback=lambda k, x, v, u: gaps.append((x - v, u)))
+    acc = np.zeros((6, 6))
+    for gap, u in gaps:
+        acc = acc + gap
+        assert np.abs(acc - u).max() < 1e-6
+
+
+def test_divergence_guard_and_early_stop(pnp):
+    prob = pnp.Problem(shape=(4, 4), gradient=lambda x: np.full((4, 4), np.nan), x0=np.zeros((4, 4)))
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.0, alpha=1.0, max_iters=5, denoiser="identity")
+    with pytest.raises(pnp.DivergenceError, match="iteration 1"):
+        pnp.linearized_pnp_admm(prob, cfg)
+    y = np.full((6, 6), 0.25)
+    prob = pnp.Problem(shape=(6, 6), gradient=lambda x: np.zeros((6, 6)), x0=y)
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.0, alpha=1.0, max_iters=100, denoiser="identity",
+                           stop_tol=1e-12)
+    _, recs = pnp.linearized_pnp_admm(prob, cfg)
+    assert len(recs) == 1
+
+
+def test_divergence_same_iteration_as_oracle(pnp):
+    """A gradient that turns non-finite on its 3rd call: both raise at k=3."""
+    y = np.linspace(0, 1, 64).reshape(8, 8)
+
+    def make_grad():
+        calls = {"n": 0}
+
+        def grad(x):
+            calls["n"] += 1
+            return (x - y) * (np.inf if calls["n"] == 3 else 1.0)
+        return grad
+
+    with pytest.raises(oadmm.DivergenceError) as er:
+        oracle.linearized_pnp_admm(np.zeros((8, 8)), make_grad(), lambda im, k: im.copy(),
+                                   rho=1.0, alpha=1.0, max_iters=20)
+    prob = pnp.Problem(shape=(8, 8), gradient=make_grad(), x0=np.zeros((8, 8)))
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.0, alpha=1.0, max_iters=20, denoiser="identity")
+    with pytest.raises(pnp.DivergenceError) as ei:
+        pnp.linearized_pnp_admm(prob, cfg)
+    assert str(ei.value) == str(er.value) == "non-finite iterate at iteration 3"
+
+
+def test_deterministic(pnp):
+    from paper_1901_06110_b200 import synth
+    truth = synth.scene(48, 48, 5)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.5, 3), 2, "periodic")
+    y = pnp.sr_simulate(truth, op, 2 / 255, seed=5)
+    cfg = pnp.SolverConfig(rho=0.05, lam=0.0002, alpha=0.3, max_iters=12, freeze_at=5,
+                           constraint=pnp.UNIT_BOX, patch_side=3, window_radius=3)
+    v1, r1 = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, y, ground_truth=truth), cfg)
+    v2, r2 = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, y, ground_truth=truth), cfg)
+    assert np.array_equal(v1, v2)
+    assert [r.primal for r in r1] == [r.primal for r in r2]
+
+
+def test_config2_shape_psnr_vs_oracle(pnp):
+    """Config-2 pipeline at 128^2 (R=10, P=7 Gaussian, frozen bicubic-ish guide)."""
+    from paper_1901_06110_b200 import synth
+    truth = synth.scene(128, 128, 2).astype(np.float32).astype(np.float64)
+    k = ofw.gaussian_kernel(1.0, 4)
+    y = ofw.sr_simulate(truth, k, 2, "symmetric", 5 / 255, 102).astype(np.float32).astype(np.float64)
+    guide = np.clip(np.kron(y, np.ones((2, 2))), 0, 1).astype(np.float32).astype(np.float64)
+    bw = (8 / 255) / math.sqrt(2)
+    fz_ref = oracle.freeze_guide(guide, 7, 10, bw, 2.0)
+    x0 = 4 * ofw.sr_adjoint(k, 2, "symmetric", y)
+    v_ref, rec_ref = oracle.linearized_pnp_admm(
+        x0, lambda x: ofw.sr_gradient(k, 2, "symmetric", x, y), lambda im, kk: fz_ref.apply(im),
+        rho=1.0, alpha=1.0, max_iters=30, lo=0.0, hi=1.0, ground_truth=truth)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    fz = pnp.freeze_guide(guide, pnp.PatchParams(7, 10, bw, 2.0))
+    prob = pnp.make_sr_problem(op, y, ground_truth=truth)
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=30, constraint=pnp.UNIT_BOX)
+    v, recs = pnp.linearized_pnp_admm(prob, cfg, denoiser=fz.as_denoiser())
+    assert abs(recs[-1].psnr - rec_ref[-1][3]) < 0.02
+    assert np.abs(v - v_ref).max() < 1e-4
+
+
+def test_batched_admm_matches_single(pnp):
+    import torch
+    from paper_1901_06110_b200 import synth
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    truths = [synth.scene(64, 64, 1000 + i) for i in range(3)]
+    ys = [pnp.sr_simulate(t, op, 5 / 255, seed=1100 + i) for i, t in enumerate(truths)]
+    p = pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0)
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=5, constraint=pnp.UNIT_BOX)
+    Y = torch.tensor(np.stack(ys), dtype=torch.float32, device="cuda")
+    G = torch.clamp(torch.nn.functional.interpolate(Y[:, None], scale_factor=2, mode="bicubic",
+                                                    align_corners=False)[:, 0], 0, 1).contiguous()
+    fzb = pnp.freeze_guide(G, p)
+    vb, rb = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, Y), cfg, denoiser=fzb.as_denoiser())
+    for i in range(3):
+        fz = pnp.freeze_guide(G[i].contiguous(), p)
+        vi, ri = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, Y[i].contiguous()), cfg,
+                                         denoiser=fz.as_denoiser())
+        assert torch.equal(vb[i], vi)
