@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""bench.py — DSG-NLM throughput on the B200 (BASELINE.json metric).
+
+Workload (one "step"): one adaptive DSG-NLM denoise of the config-4 image —
+8192 x 8192 float32 seeded scene + noise 25/255, search 21x21 (R=10), patch
+7x7 Gaussian sigma_p=2, h=12/255 (bandwidth h/sqrt(2)); the full
+dsg_nlm_denoise pipeline (sweep A, rs, sweep B, fixups, max, finalize).
+With --gpus N > 1 (launched by torchrun) the image is sharded in row strips
+across the N ranks (parallel.ShardedDSG: NCCL halo/partial-block exchange,
+max all-reduce); the problem size is fixed ("strong" scaling).
+
+value    = 8192^2 * 441 pixel-offsets / device time per step (max over
+           ranks), in Gpixel*offset/s, inputs resident in HBM (268 MB > L2,
+           so every step streams from HBM; no flush needed);
+e2e      = the same through the public API with pinned host buffers: H2D of
+           the image, denoise, D2H of the result inside the timed region;
+roofline = the DSG sweep kernel: SURVEY.md §8(d)'s algorithmic FP32 ops per
+           pixel-offset (20.95 adaptive, P=7 Gaussian, R=10) / its measured
+           launch time (CUDA events on the library stream), against the
+           FFMA rate measured on this GPU by pnp_peak_rates;
+cpu_baseline = the float64 CPU oracle port (oracle/, restating pnprestore)
+           on a bounded sample of the same workload.
+Extras: ADMM iterations/s for configs 2 and 3 (512^2 SR / QIS).
+
+``--impl reference`` times the reference's CPU algorithm (oracle port) with
+all host cores on bounded samples of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+H_C4 = 8192
+R_C4, P_C4, SIGMA_P, H_BW = 10, 7, 2.0, 12 / 255
+OPS_PER_UNIT_ADAPTIVE = (4 * P_C4 + 14) * ((21 * 21 - 1) / 2) / (21 * 21)   # 20.95
+MUFU_PER_UNIT_ADAPTIVE = 2 * ((21 * 21 - 1) / 2) / (21 * 21)                # 0.998
+METRIC = "DSG-NLM Gpixel*offset/s (config 4: 8192^2, R=10, P=7 Gaussian)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pnp", choices=["pnp", "reference"])
+    ap.add_argument("--size", type=int, default=H_C4, help="image side (default: config 4)")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu / ADMM extras")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- helpers
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        if self.proc is None or not getattr(self, "lines", None):
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_image_rows(n: int, r0: int, r1: int) -> np.ndarray:
+    """Rows [r0, r1) of the config-4 input (float32), generated independently."""
+    from paper_1901_06110_b200 import synth
+    clean = synth.scene(n, n, 4, rows=(r0, r1))
+    return synth.noisy(clean, 25 / 255, 5, first_index=r0 * n).astype(np.float32)
+
+
+def cpu_oracle_sample(img: np.ndarray, crops, bw):
+    """Float64 oracle (reference algorithm restated) on bounded crops."""
+    import oracle
+    t0 = time.process_time()
+    w0 = time.perf_counter()
+    units = 0
+    for (r, c, s) in crops:
+        oracle.dsg_nlm_denoise(img[r:r + s, c:c + s].astype(np.float64), P_C4, R_C4, bw,
+                               patch_sigma=SIGMA_P)
+        units += s * s * 441
+    return units, time.perf_counter() - w0, time.process_time() - t0
+
+
+def _ref_worker(args):
+    img, bw = args
+    import oracle
+    t = time.perf_counter()
+    oracle.dsg_nlm_denoise(img.astype(np.float64), P_C4, R_C4, bw, patch_sigma=SIGMA_P)
+    return img.size * 441, time.perf_counter() - t
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    n = args.size
+    bw = H_BW / math.sqrt(2.0)
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, 32))
+    s = 256
+    rng = np.random.default_rng(0)
+    per_step = []
+    total_units = 0
+    band = make_image_rows(n, 0, min(n, 4 * s))  # input generation is not timed
+    with mp.get_context("spawn").Pool(workers) as pool:
+        pool.map(_ref_worker, [(band[:32, :32], bw)] * workers)  # import/spawn warm-up
+        for i in range(args.warmup + args.steps):
+            jobs = []
+            for _ in range(workers):
+                r = int(rng.integers(0, band.shape[0] - s + 1))
+                c = int(rng.integers(0, n - s + 1))
+                jobs.append((np.ascontiguousarray(band[r:r + s, c:c + s]), bw))
+            t = time.perf_counter()
+            res = pool.map(_ref_worker, jobs)
+            dt = time.perf_counter() - t
+            if i >= args.warmup:
+                per_step.append(dt)
+                total_units += sum(u for u, _ in res)
+    sec = sum(per_step)
+    value = total_units / sec / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpixel*offset/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene + noise)",
+        "config": {"workload": "config 4 DSG-NLM (sampled)", "image": f"{n}x{n}",
+                   "R": R_C4, "P": P_C4, "sigma_p": SIGMA_P, "h": H_BW},
+        "cpu_baseline": {"value": value, "unit": "Gpixel*offset/s", "cores": workers,
+                         "kind": "port",
+                         "sample": f"each step: {workers} processes x one {s}x{s} crop of the "
+                                   f"config-4 image, float64 oracle (pnprestore algorithm)"},
+        "e2e": {"value": value, "unit": "Gpixel*offset/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_06110_b200 as pnp
+    from paper_1901_06110_b200 import profiling
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = args.size
+    params = pnp.PatchParams.from_h(P_C4, R_C4, H_BW, SIGMA_P)
+    units = n * n * (2 * R_C4 + 1) ** 2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    if world == 1:
+        x = torch.from_numpy(make_image_rows(n, 0, n)).to(dev)
+        out = torch.empty_like(x)
+
+        def step():
+            pnp.dsg_nlm_denoise(x, params)
+    else:
+        from paper_1901_06110_b200.parallel import ShardedDSG, TorchComm
+        sh = ShardedDSG(params, n, n, world, [rank], TorchComm(), device=dev)
+        st = sh.states[0]
+        y0, y1 = st.lay.rows
+        st.own(st.buf).copy_(torch.from_numpy(make_image_rows(n, y0, y1)))
+
+        def step():
+            sh.denoise()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    profiling.enable(True, local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    prof = profiling.read(local_rank)
+    profiling.enable(False, local_rank)
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t[0])
+    value = units / (ms_max * 1e-3) / 1e9
+
+    launches = sum(v[1] for v in prof.values())
+    sweep_ms, sweep_n = prof["sweep"]
+    peak_ffma, peak_ex2 = profiling.peak_rates(local_rank)
+    # per-rank algorithmic ops / per-rank sweep time (each rank sweeps its strip)
+    ops_rank = OPS_PER_UNIT_ADAPTIVE * units / world * args.steps
+    achieved = ops_rank / (sweep_ms * 1e-3) / 1e12 if sweep_ms > 0 else None
+    nominal = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 1.965e9
+    roofline = {
+        "bound": "fp32", "kernel": "dsg_sweep_kernel",
+        "achieved": achieved, "peak": peak_ffma / 1e12, "unit": "Top/s",
+        "frac": (achieved / (peak_ffma / 1e12)) if achieved else None,
+        "traffic": None,
+        "peak_source": "measured FFMA rate (pnp_peak_rates) on this GPU; "
+                       f"nominal 148x128x1965MHz = {nominal / 1e12:.2f} Top/s",
+        "frac_of_nominal": (achieved / (nominal / 1e12)) if achieved else None,
+        "ops_per_pixel_offset": OPS_PER_UNIT_ADAPTIVE,
+        "sweep_launches": sweep_n, "sweep_ms_per_step": sweep_ms / args.steps,
+        "sweep_share_of_step": (sweep_ms / args.steps) / ms if ms > 0 else None,
+        "sfu": {"mufu_per_pixel_offset": MUFU_PER_UNIT_ADAPTIVE,
+                "peak_ex2_per_s": peak_ex2,
+                "frac": (MUFU_PER_UNIT_ADAPTIVE * units / world * args.steps
+                         / (sweep_ms * 1e-3) / peak_ex2) if sweep_ms > 0 else None},
+        "traffic_note": "dram bytes per launch: see profiles/ (ncu --set full)",
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gpixel*offset/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded rectangle/disc/gradient scene + splitmix noise 25/255)",
+        "config": {"workload": "config 4: adaptive DSG-NLM of one 8192x8192 image"
+                               if n == H_C4 else f"config-4 parameters at {n}x{n}",
+                   "image": f"{n}x{n}", "R": R_C4, "P": P_C4, "sigma_p": SIGMA_P, "h": H_BW,
+                   "parallelism": f"row-strips x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs 268 MB > 126 MB L2 (no flush needed)"},
+        "roofline": roofline, "gpu_launches": launches, "impl": "pnp",
+    }
+    clocks = clk.summary()
+    line["clocks"] = clocks
+
+    if not args.no_extras:
+        # e2e through the public API with pinned host buffers
+        if world == 1:
+            host_in = torch.from_numpy(make_image_rows(n, 0, n)).pin_memory()
+            host_out = torch.empty_like(host_in).pin_memory()
+
+            def e2e_step():
+                xd = host_in.to(dev, non_blocking=True)
+                yd = pnp.dsg_nlm_denoise(xd, params)
+                host_out.copy_(yd, non_blocking=True)
+            nbytes = host_in.numel() * 4
+        else:
+            own = torch.from_numpy(make_image_rows(n, y0, y1)).pin_memory()
+            host_out = torch.empty_like(own).pin_memory()
+
+            def e2e_step():
+                st.own(st.buf).copy_(own, non_blocking=True)
+                sh.denoise()
+                host_out.copy_(st.own(st.out), non_blocking=True)
+            nbytes = own.numel() * 4
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        line["e2e"] = {"value": units / (float(t[0]) * 1e-3) / 1e9, "unit": "Gpixel*offset/s",
+                       "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
+                       "ms_per_step": float(t[0]),
+                       "api": "paper_1901_06110_b200.dsg_nlm_denoise(torch CUDA tensor)"
+                              if world == 1 else "parallel.ShardedDSG.denoise"}
+        if rank == 0 and world == 1:
+            line["admm"] = admm_extras(pnp, dev)
+            side = min(512, n)
+            img = make_image_rows(n, 0, min(n, side + 256))
+            crops = [(0, 0, side)]
+            if img.shape[0] >= 256 + side and n >= 2 * side:
+                crops.append((256, min(3000, n - side), side))
+            cu, wall, cpu = cpu_oracle_sample(img, crops, params.bandwidth)
+            line["cpu_baseline"] = {
+                "value": cu / wall / 1e9, "unit": "Gpixel*offset/s", "cores": 1, "kind": "port",
+                "sample": f"{len(crops)} crops of {side}x{side} of the config-4 image, float64 "
+                          "oracle port of pnprestore's 3-sweep DSG-NLM (numpy, 1 thread)",
+                "wall_s": wall, "cpu_s": cpu, "host_cores_available": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def admm_extras(pnp, dev):
+    """Configs 2 and 3 on the device: ADMM iterations/s (+ final PSNR)."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_1901_06110_b200 import synth
+    res = {}
+    # config 2: 512^2 SR, blur 9x9 sigma 1 symmetric, x2, noise 5/255, 30 its, frozen bicubic guide
+    truth = synth.scene(512, 512, 2).astype(np.float32)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    y = pnp.sr_simulate(truth.astype(np.float64), op, 5 / 255, seed=102).astype(np.float32)
+    yd = torch.from_numpy(y).to(dev)
+    guide = F.interpolate(yd.double()[None, None], scale_factor=2, mode="bicubic",
+                          align_corners=False)[0, 0].clamp(0, 1).float().contiguous()
+    p2 = pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0)
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=30, constraint=pnp.UNIT_BOX)
+    gt = torch.from_numpy(truth).to(dev)
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fz = pnp.freeze_guide(guide, p2)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        v, recs = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, yd, ground_truth=gt), cfg,
+                                          denoiser=fz.as_denoiser())
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+    res["config2_sr_512"] = {"iters": 30, "iters_per_s": 30 / (t2 - t1),
+                             "freeze_ms": (t1 - t0) * 1e3, "end_to_end_ms": (t2 - t0) * 1e3,
+                             "psnr_db": recs[-1].psnr}
+    # config 3: 512^2 QIS, K = 4x4x8 = 128 jots, alpha_s = 8 -> gain 64, 50 its, dsg-fixed @15
+    truth3 = synth.scene(512, 512, 3).astype(np.float32)
+    model = pnp.QisModel(128, 64.0)
+    counts = pnp.qis_simulate(truth3.astype(np.float64), model, seed=103)
+    prob = pnp.make_qis_problem(counts, model, ground_truth=torch.from_numpy(truth3).to(dev))
+    prob.x0 = torch.from_numpy(prob.x0.astype(np.float32)).to(dev)
+    cfg3 = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=pnp.default_qis_alpha(counts, model),
+                            max_iters=50, freeze_at=15, constraint=pnp.UNIT_BOX,
+                            denoiser="dsg-fixed", patch_side=7, window_radius=10,
+                            bandwidth=(10 / 255) / math.sqrt(2), patch_sigma=2.0)
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        v, recs = pnp.linearized_pnp_admm(prob, cfg3)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+    res["config3_qis_512"] = {"iters": 50, "iters_per_s": 50 / (t1 - t0),
+                              "psnr_db": recs[-1].psnr}
+    res["reference_cpu_note"] = "survey: pnprestore config-2 shape 0.79 iters/s on 1 CPU core"
+    return res
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "pnp":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -46,6 +46,15 @@ int pnp_ctx_destroy(pnp_ctx* ctx);
 /* stream = a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
 int pnp_ctx_set_stream(pnp_ctx* ctx, void* stream);
 int pnp_ctx_synchronize(pnp_ctx* ctx);
+/* Per-launch CUDA-event timing on the context stream (off by default).
+ * profile_read syncs the stream, returns summed device ms and launch counts
+ * for 4 categories (0 DSG sweep, 1 DSG fixup/finalize, 2 forward operators,
+ * 3 ADMM elementwise/reductions) since the last read, and resets them. */
+int pnp_ctx_profile(pnp_ctx* ctx, int enable);
+int pnp_ctx_profile_read(pnp_ctx* ctx, double* ms, int* launches);
+/* Measured FFMA / MUFU.EX2 instruction throughput of the device (per second,
+ * whole GPU) — the roofline denominators of the DSG sweep. */
+int pnp_peak_rates(int device, double* ffma_per_s, double* ex2_per_s);
 /* Pre-size scratch for (batch, H, W, R, P) so later calls allocate nothing
  * (required before CUDA-graph capture). */
 int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P);
@@ -78,6 +87,35 @@ int pnp_frozen_shape(const pnp_frozen* fz, int* batch, int* H, int* W, int* R, i
 int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out,
                     int batch, int H, int W, int R, int P, const float* taps,
                     double bandwidth);
+
+/* ---- row-strip building blocks (multi-GPU sharding) ---- *
+ * A rank owns global rows [y0, y1) = whole tile rows of height
+ * pnp_tile_height(P).  Per-pixel buffers are windows: rows [buf_r0, buf_r0 +
+ * buf_rows) of the Hg x W image (own rows plus halos received from
+ * neighbours).  Partial buffers hold part_ntr tile rows x pnp_dsg_groups()
+ * offset groups x ceil(W/64) tiles of C*(TH+R)*(64+2R) floats; slot 0 is
+ * global tile row part_tr0 (a neighbour's rows are received into the
+ * prefix).  A sharded run sums in exactly the single-GPU order, so its
+ * output is bit-identical.
+ *   sweep pass: 0 mass g (C=1), 1 Kx+d (C=2, needs x, rs), 2 d (C=1, rs),
+ *               3 Kx (C=1, x, rs)
+ *   fixup mode: 0 rs = g^-1/2, 1 Kx, d + per-rank max bits, 2 d + max,
+ *               3 frozen apply (out = Kx inv_m + (1 - d inv_m) x)
+ *   finalize:   out = Kx/m + (1 - d/m) x with m from (all-reduced) mbits. */
+int pnp_tile_height(int P);
+int pnp_dsg_groups(int Hg, int W, int R, int P);
+int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr);
+int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float* x,
+                        const float* rs, int Hg, int W, int buf_r0, int buf_rows, int tr0,
+                        int ntr, int R, int P, const float* taps, double bandwidth,
+                        float* partial, int part_off, int part_ntr);
+int pnp_dsg_strip_fixup(pnp_ctx* ctx, int mode, const float* partial, int part_tr0,
+                        int part_ntr, int Hg, int W, int R, int P, int y0, int y1, int buf_r0,
+                        int buf_rows, float* rs, float* kx, float* d, unsigned* mbits,
+                        const float* inv_m, const float* x, float* out);
+int pnp_dsg_strip_finalize(pnp_ctx* ctx, const float* kx, const float* d, const float* x,
+                           float* out, const unsigned* mbits, int Hg, int W, int y0, int y1,
+                           int buf_r0, int buf_rows);
 
 /* ---- forward operators (forward.py) ------------------------------------- */
 /* SR operator: separable blur k = ty tx^T given as 2(2r+1) host floats

@@ -35,6 +35,9 @@ _SIGS = {
     "pnp_ctx_set_stream": (i32, [vp, vp]),
     "pnp_ctx_synchronize": (i32, [vp]),
     "pnp_ctx_reserve": (i32, [vp, i32, i32, i32, i32, i32]),
+    "pnp_ctx_profile": (i32, [vp, i32]),
+    "pnp_ctx_profile_read": (i32, [vp, C.POINTER(f64), C.POINTER(i32)]),
+    "pnp_peak_rates": (i32, [i32, C.POINTER(f64), C.POINTER(f64)]),
     "pnp_dsg_denoise": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64, vp, vp]),
     "pnp_dsg_freeze": (i32, [vp, vp, i32, i32, i32, i32, i32, fptr, f64, C.POINTER(vp)]),
     "pnp_dsg_apply": (i32, [vp, vp, vp, vp]),
@@ -43,6 +46,14 @@ _SIGS = {
     "pnp_frozen_export": (i32, [vp, vp, vp, vp]),
     "pnp_frozen_shape": (i32, [vp] + [C.POINTER(i32)] * 5),
     "pnp_nlm_denoise": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64]),
+    "pnp_tile_height": (i32, [i32]),
+    "pnp_dsg_groups": (i32, [i32, i32, i32, i32]),
+    "pnp_dsg_partial_floats": (i64, [i32, i32, i32, i32, i32, i32]),
+    "pnp_dsg_strip_sweep": (i32, [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
+                                  fptr, f64, vp, i32, i32]),
+    "pnp_dsg_strip_fixup": (i32, [vp, i32, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
+                                  vp, vp, vp, vp, vp, vp, vp]),
+    "pnp_dsg_strip_finalize": (i32, [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32]),
     "pnp_sr_apply": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
     "pnp_sr_adjoint": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
     "pnp_sr_grad": (i32, [vp, vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, vp]),

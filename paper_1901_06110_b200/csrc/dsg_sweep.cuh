@@ -62,14 +62,23 @@ struct Chunk {
   float L[4];
 };
 
+// Per-pixel planes are windows of the global image: rows [buf_r0, buf_r0 +
+// buf_rows) of a Hg x W image (single GPU: buf_r0 = 0, buf_rows = Hg; a row
+// strip on one rank of a sharded run: its rows plus halos).  The launch
+// covers global tile rows [tr0, tr0 + gridDim.x / tiles_x).  Partial blocks
+// go to slot (part_off + local tile row) of a [B][part_ntr][NG][tiles_x]
+// array of C*(TH+R)*(TW+2R) floats; tile rows are outermost so a
+// neighbour's rows can be received into a contiguous prefix.
 struct SweepArgs {
-  const float* guide;  // [B][H][W]
+  const float* guide;  // [B][buf_rows][W]
   ChanSpec ch[2];
-  float* partial;      // [B][NG][tiles][C][BR][BC]
+  float* partial;
   const Chunk* chunks;
   const int* grp;      // NG+1 chunk starts
-  int H, W, R;
-  int tiles_x, tiles_y;
+  int Hg, W, R;
+  int buf_r0, buf_rows;
+  int tr0, tiles_x;
+  int part_off, part_ntr;
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
 };
@@ -127,11 +136,11 @@ dsg_sweep_kernel(const SweepArgs a) {
   float* As = smem + K::OFF_A;  // [2][C][AR][YC]
 
   const int R = a.R;
-  const int H = a.H, W = a.W;
+  const int Hg = a.Hg, W = a.W, br0 = a.buf_r0, brows = a.buf_rows;
   const int tile = blockIdx.x;
-  const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-  const int r0g = ty * TH, c0g = tx * kTW;
-  const size_t plane = (size_t)H * W;
+  const int tyl = tile / a.tiles_x, tx = tile - tyl * a.tiles_x;
+  const int r0g = (a.tr0 + tyl) * TH, c0g = tx * kTW;
+  const size_t plane = (size_t)brows * W;
   const int b = blockIdx.z;
   const float* Gimg = a.guide + (size_t)b * plane;
   const int tid = threadIdx.x;
@@ -140,8 +149,10 @@ dsg_sweep_kernel(const SweepArgs a) {
   // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
   for (int i = tid; i < GR * GC; i += kThreads) {
     const int q = i / GC, cc = i - q * GC;
-    const int gr = reflect_index(r0g - p + q, H), gc = reflect_index(c0g - RB - p + cc, W);
-    Gs[q * GS + cc] = __ldg(Gimg + (size_t)gr * W + gc);
+    int lr = reflect_index(r0g - p + q, Hg) - br0;
+    lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
+    const int gc = reflect_index(c0g - RB - p + cc, W);
+    Gs[q * GS + cc] = __ldg(Gimg + (size_t)lr * W + gc);
   }
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_) {
@@ -150,10 +161,10 @@ dsg_sweep_kernel(const SweepArgs a) {
     float* Y = Ys + c_ * YR * YC;
     for (int i = tid; i < YR * YC; i += kThreads) {
       const int r = i / YC, cc = i - r * YC;
-      const int gr = r0g + r, gc = c0g - RB + cc;
+      const int gr = r0g + r, gc = c0g - RB + cc, lr = gr - br0;
       float v = 0.f;
-      if (gr < H && gc >= 0 && gc < W) {
-        const size_t o = (size_t)gr * W + gc;
+      if (gr < Hg && gc >= 0 && gc < W && lr >= 0 && lr < brows) {
+        const size_t o = (size_t)lr * W + gc;
         v = 1.f;
         if (pa) v = __ldg(pa + o);
         if (pb) v = __fmul_rn(v, __ldg(pb + o));
@@ -271,9 +282,9 @@ dsg_sweep_kernel(const SweepArgs a) {
     }
   __syncthreads();
   const int BR = TH + R, BC = kTW + 2 * R;
-  const int ntiles = a.tiles_x * a.tiles_y;
-  float* out = a.partial +
-               (((size_t)b * gridDim.y + blockIdx.y) * ntiles + tile) * (size_t)(C * BR * BC);
+  const size_t slot =
+      (((size_t)b * a.part_ntr + a.part_off + tyl) * gridDim.y + blockIdx.y) * a.tiles_x + tx;
+  float* out = a.partial + slot * (size_t)(C * BR * BC);
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_) {
     const float* A0 = As + (0 * C + c_) * AR * YC + (RB - R);
@@ -288,31 +299,35 @@ dsg_sweep_kernel(const SweepArgs a) {
   }
 }
 
-// Sum of all partial blocks covering pixel (y, x), fixed order
-// (group, tile row, tile col).
+// Sum of all partial blocks covering global pixel (y, x), fixed order
+// (group, tile row, tile col).  Slot 0 of the partial array holds global
+// tile row part_tr0.
 struct FixGeo {
   const float* partial;
-  int H, W, R, TH, tiles_x, tiles_y, NG, C;
+  int Hg, W, R, TH, tiles_x, NG, C;
+  int part_tr0, part_ntr;
+  int y0, nrows;          // output rows [y0, y0 + nrows) (global)
+  int buf_r0, buf_rows;   // per-pixel buffers' window
 };
 
 __device__ __forceinline__ float gather_partial(const FixGeo& f, int b, int c_, int y, int x) {
   const int BR = f.TH + f.R, BC = kTW + 2 * f.R;
   const int ti = y / f.TH, tj = x / kTW;
   const int dti = (f.R + f.TH - 1) / f.TH, dtj = (f.R + kTW - 1) / kTW;
-  const int ti0 = max(0, ti - dti);
+  const int ti0 = max(max(f.part_tr0, 0), ti - dti), ti1 = min(ti, f.part_tr0 + f.part_ntr - 1);
   const int tj0 = max(0, tj - dtj), tj1 = min(f.tiles_x - 1, tj + dtj);
-  const int ntiles = f.tiles_x * f.tiles_y;
   const size_t blk = (size_t)f.C * BR * BC;
+  const float* base = f.partial + (size_t)b * f.part_ntr * f.NG * f.tiles_x * blk + (size_t)c_ * BR * BC;
   float s = 0.f;
   for (int gg = 0; gg < f.NG; ++gg) {
-    const float* base = f.partial + ((size_t)b * f.NG + gg) * ntiles * blk + (size_t)c_ * BR * BC;
-    for (int t_i = ti0; t_i <= ti; ++t_i) {
+    for (int t_i = ti0; t_i <= ti1; ++t_i) {
       const int br = y - t_i * f.TH;
       if (br >= BR) continue;
+      const float* row = base + ((size_t)(t_i - f.part_tr0) * f.NG + gg) * f.tiles_x * blk;
       for (int t_j = tj0; t_j <= tj1; ++t_j) {
         const int bc = x - t_j * kTW + f.R;
         if (bc < 0 || bc >= BC) continue;
-        s = __fadd_rn(s, __ldg(base + (size_t)(t_i * f.tiles_x + t_j) * blk + br * BC + bc));
+        s = __fadd_rn(s, __ldg(row + (size_t)t_j * blk + br * BC + bc));
       }
     }
   }

@@ -58,6 +58,7 @@ void DevBuf::release() {
 
 enum FixMode { FIX_RS = 0, FIX_KXD = 1, FIX_D = 2, FIX_APPLY = 3, FIX_NLM = 4 };
 
+// Per-pixel buffers are windows [buf_r0, buf_r0 + buf_rows) x W (FixGeo).
 struct FixIO {
   float* rs;           // in (KXD, D, APPLY) / out (RS)
   float* kx;           // out (KXD)
@@ -77,12 +78,13 @@ __device__ __forceinline__ float dsg_finish(float kx, float d, float inv_m, floa
 template <int MODE>
 __global__ void __launch_bounds__(256) dsg_fixup_kernel(const FixGeo f, const FixIO io) {
   const int b = blockIdx.y;
-  const size_t plane = (size_t)f.H * f.W;
+  const size_t npix = (size_t)f.nrows * f.W;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   float dval = 0.f;
-  if (i < plane) {
-    const int y = (int)(i / f.W), x = (int)(i - (size_t)y * f.W);
-    const size_t o = (size_t)b * plane + i;
+  if (i < npix) {
+    const int yl = (int)(i / f.W), x = (int)(i - (size_t)yl * f.W);
+    const int y = f.y0 + yl;
+    const size_t o = (size_t)b * f.buf_rows * f.W + (size_t)(y - f.buf_r0) * f.W + x;
     const float s0 = gather_partial(f, b, 0, y, x);
     if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
@@ -119,15 +121,17 @@ __global__ void __launch_bounds__(256) dsg_fixup_kernel(const FixGeo f, const Fi
   }
 }
 
+// out = Kx/m + (1 - d/m) x over output rows [y0, y0+nrows) of a window.
 __global__ void dsg_finalize_kernel(const float* kx, const float* d, const unsigned* mbits,
-                                    const float* x, float* out, float* alpha_out, size_t plane) {
+                                    const float* x, float* out, float* alpha_out, int y0,
+                                    int nrows, int W, int buf_r0, int buf_rows) {
   const int b = blockIdx.y;
   const float m = __uint_as_float(mbits[b]);
   const float inv_m = __frcp_rn(m);
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (alpha_out && i == 0) alpha_out[b] = m;
-  if (i < plane) {
-    const size_t o = (size_t)b * plane + i;
+  if (i < (size_t)nrows * W) {
+    const size_t o = (size_t)b * buf_rows * W + (size_t)(y0 - buf_r0) * W + i;
     out[o] = dsg_finish(kx[o], d[o], inv_m, x[o]);
   }
 }
@@ -143,12 +147,27 @@ __global__ void dsg_alpha_kernel(const unsigned* mbits, float* mv, int B) {
 
 // ------------------------------------------------------------------ host ---
 
-struct Plan {
-  int B, H, W, R, P, TH, tiles_x, tiles_y, ntiles, nchunks, NG;
-  const Chunk* chunks;  // hat-tapered table (DSG)
+// Global launch geometry: tile grid, offset table and offset-group split.
+// Everything here depends only on (Hg, W, R, P), never on the window or the
+// batch, so single-GPU and sharded runs sum in the same order.
+struct Geom {
+  int B, Hg, W, R, P, TH, tiles_x, tiles_y, nchunks, NG;
+  const Chunk* chunks;        // hat-tapered table (DSG)
   const Chunk* chunks_nohat;  // same offsets, L = 0 (plain NLM)
   const int* grp;
 };
+
+// A window of the global image handled by one call.
+struct Window {
+  int buf_r0, buf_rows;  // per-pixel buffers: rows [buf_r0, buf_r0 + buf_rows)
+  int tr0, ntr;          // tile rows swept
+  int part_tr0, part_off, part_ntr;  // partial array: slot 0 = tile row part_tr0
+  int y0, nrows;         // rows fixed up / finalized
+};
+
+static Window full_window(const Geom& g) {
+  return Window{0, g.Hg, 0, g.tiles_y, 0, 0, g.tiles_y, 0, g.Hg};
+}
 
 // Half-window offsets grouped in chunks of KY consecutive dy sharing dx.
 static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
@@ -175,7 +194,6 @@ static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
 
 static int pick_groups(int ntiles, int nchunks) {
   // Offset-group split so small images still fill 148 SMs (~8 CTAs each).
-  // Depends only on the image geometry -> identical for every call variant.
   const int target = 148 * 8;
   int ng = (target + ntiles - 1) / ntiles;
   if (ng > nchunks) ng = nchunks;
@@ -202,27 +220,34 @@ static int check_geometry(int B, int H, int W, int R, int P, double bw) {
   return PNP_OK;
 }
 
-static int make_plan(pnp_ctx* ctx, int B, int H, int W, int R, int P, Plan& pl) {
-  pl.B = B;
-  pl.H = H;
-  pl.W = W;
-  pl.R = R;
-  pl.P = P;
-  pl.TH = tile_height(P);
-  pl.tiles_x = (W + kTW - 1) / kTW;
-  pl.tiles_y = (H + pl.TH - 1) / pl.TH;
-  pl.ntiles = pl.tiles_x * pl.tiles_y;
+static int groups_for(int Hg, int W, int R, int P) {
+  const int TH = tile_height(P);
+  const int ntiles = ((W + kTW - 1) / kTW) * ((Hg + TH - 1) / TH);
+  int nch = 0;
+  for (int dx = -R; dx <= R; ++dx) nch += (R - (dx > 0 ? 0 : 1) + kKY) / kKY;
+  return pick_groups(ntiles, nch);
+}
+
+static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, Geom& g) {
+  g.B = B;
+  g.Hg = Hg;
+  g.W = W;
+  g.R = R;
+  g.P = P;
+  g.TH = tile_height(P);
+  g.tiles_x = (W + kTW - 1) / kTW;
+  g.tiles_y = (Hg + g.TH - 1) / g.TH;
   std::vector<Chunk> ch, ch0;
   build_chunks(R, true, ch);
   build_chunks(R, false, ch0);
-  pl.nchunks = (int)ch.size();
-  pl.NG = pick_groups(pl.ntiles, pl.nchunks);
-  auto key = std::make_pair(R, pl.NG);
+  g.nchunks = (int)ch.size();
+  g.NG = pick_groups(g.tiles_x * g.tiles_y, g.nchunks);
+  auto key = std::make_pair(R, g.NG);
   auto it = ctx->tables.find(key);
   const size_t cb = ch.size() * sizeof(Chunk);
   if (it == ctx->tables.end()) {
-    std::vector<int> grp(pl.NG + 1);
-    for (int g = 0; g <= pl.NG; ++g) grp[g] = (int)((long long)g * pl.nchunks / pl.NG);
+    std::vector<int> grp(g.NG + 1);
+    for (int i = 0; i <= g.NG; ++i) grp[i] = (int)((long long)i * g.nchunks / g.NG);
     DevBuf buf;
     int rc = buf.ensure(2 * cb + grp.size() * sizeof(int));
     if (rc) return rc;
@@ -232,14 +257,18 @@ static int make_plan(pnp_ctx* ctx, int B, int H, int W, int R, int P, Plan& pl) 
                         cudaMemcpyHostToDevice));
     it = ctx->tables.emplace(key, buf).first;
   }
-  pl.chunks = it->second.as<Chunk>();
-  pl.chunks_nohat = reinterpret_cast<const Chunk*>(it->second.as<char>() + cb);
-  pl.grp = reinterpret_cast<const int*>(it->second.as<char>() + 2 * cb);
+  g.chunks = it->second.as<Chunk>();
+  g.chunks_nohat = reinterpret_cast<const Chunk*>(it->second.as<char>() + cb);
+  g.grp = reinterpret_cast<const int*>(it->second.as<char>() + 2 * cb);
   return PNP_OK;
 }
 
-static size_t partial_floats(const Plan& pl, int C) {
-  return (size_t)pl.B * pl.NG * pl.ntiles * C * (pl.TH + pl.R) * (kTW + 2 * pl.R);
+static size_t block_floats(const Geom& g, int C) {
+  return (size_t)C * (g.TH + g.R) * (kTW + 2 * g.R);
+}
+
+static size_t partial_floats(const Geom& g, int ntr, int C) {
+  return (size_t)g.B * ntr * g.NG * g.tiles_x * block_floats(g, C);
 }
 
 template <int RB, int C>
@@ -258,61 +287,86 @@ static cudaError_t launch_sweep_rc(const SweepArgs& a, int P, dim3 grid, cudaStr
 }
 
 template <int C>
-static cudaError_t launch_sweep_c(const SweepArgs& a, const Plan& pl, cudaStream_t st) {
-  dim3 grid(pl.ntiles, pl.NG, pl.B);
-  switch (r_bucket(pl.R)) {
-    case 5: return launch_sweep_rc<5, C>(a, pl.P, grid, st);
-    case 10: return launch_sweep_rc<10, C>(a, pl.P, grid, st);
-    case 16: return launch_sweep_rc<16, C>(a, pl.P, grid, st);
-    default: return launch_sweep_rc<32, C>(a, pl.P, grid, st);
+static cudaError_t launch_sweep_c(const SweepArgs& a, const Geom& g, dim3 grid, cudaStream_t st) {
+  switch (r_bucket(g.R)) {
+    case 5: return launch_sweep_rc<5, C>(a, g.P, grid, st);
+    case 10: return launch_sweep_rc<10, C>(a, g.P, grid, st);
+    case 16: return launch_sweep_rc<16, C>(a, g.P, grid, st);
+    default: return launch_sweep_rc<32, C>(a, g.P, grid, st);
   }
 }
 
-static int run_sweep(pnp_ctx* ctx, const Plan& pl, int C, const float* guide, ChanSpec c0,
-                     ChanSpec c1, const float* taps, double bw, bool use_hat) {
+static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const float* guide,
+                     ChanSpec c0, ChanSpec c1, const float* taps, double bw, bool use_hat,
+                     float* partial) {
+  if (w.ntr <= 0) return PNP_OK;
   SweepArgs a;
   memset(&a, 0, sizeof(a));
   a.guide = guide;
   a.ch[0] = c0;
   a.ch[1] = c1;
-  int rc = ctx->partial.ensure(partial_floats(pl, 2) * sizeof(float));
-  if (rc) return rc;
-  a.partial = ctx->partial.as<float>();
-  a.chunks = use_hat ? pl.chunks : pl.chunks_nohat;
-  a.grp = pl.grp;
-  a.H = pl.H;
-  a.W = pl.W;
-  a.R = pl.R;
-  a.tiles_x = pl.tiles_x;
-  a.tiles_y = pl.tiles_y;
+  a.partial = partial;
+  a.chunks = use_hat ? g.chunks : g.chunks_nohat;
+  a.grp = g.grp;
+  a.Hg = g.Hg;
+  a.W = g.W;
+  a.R = g.R;
+  a.buf_r0 = w.buf_r0;
+  a.buf_rows = w.buf_rows;
+  a.tr0 = w.tr0;
+  a.tiles_x = g.tiles_x;
+  a.part_off = w.part_off;
+  a.part_ntr = w.part_ntr;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
-  for (int i = 0; i < pl.P; ++i) {
+  for (int i = 0; i < g.P; ++i) {
     a.taps_h[i] = taps[i];
     a.taps_v[i] = (float)(scale * (double)taps[i]);
   }
-  cudaError_t e = C == 1 ? launch_sweep_c<1>(a, pl, ctx->stream)
-                         : launch_sweep_c<2>(a, pl, ctx->stream);
+  dim3 grid(w.ntr * g.tiles_x, g.NG, g.B);
+  ProfScope prof(ctx, PROF_SWEEP);
+  cudaError_t e = C == 1 ? launch_sweep_c<1>(a, g, grid, ctx->stream)
+                         : launch_sweep_c<2>(a, g, grid, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "dsg_sweep_kernel");
   return PNP_OK;
 }
 
 template <int MODE>
-static int run_fixup(pnp_ctx* ctx, const Plan& pl, int C, const FixIO& io) {
+static int run_fixup(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const float* partial,
+                     const FixIO& io) {
+  if (w.nrows <= 0) return PNP_OK;
   FixGeo f;
-  f.partial = ctx->partial.as<float>();
-  f.H = pl.H;
-  f.W = pl.W;
-  f.R = pl.R;
-  f.TH = pl.TH;
-  f.tiles_x = pl.tiles_x;
-  f.tiles_y = pl.tiles_y;
-  f.NG = pl.NG;
+  f.partial = partial;
+  f.Hg = g.Hg;
+  f.W = g.W;
+  f.R = g.R;
+  f.TH = g.TH;
+  f.tiles_x = g.tiles_x;
+  f.NG = g.NG;
   f.C = C;
-  const size_t plane = (size_t)pl.H * pl.W;
-  dim3 grid((unsigned)((plane + 255) / 256), pl.B);
+  f.part_tr0 = w.part_tr0;
+  f.part_ntr = w.part_ntr;
+  f.y0 = w.y0;
+  f.nrows = w.nrows;
+  f.buf_r0 = w.buf_r0;
+  f.buf_rows = w.buf_rows;
+  const size_t npix = (size_t)w.nrows * g.W;
+  dim3 grid((unsigned)((npix + 255) / 256), g.B);
+  ProfScope prof(ctx, PROF_FIXUP);
   dsg_fixup_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
   PNP_LAUNCH_CHECK("dsg_fixup_kernel");
+  return PNP_OK;
+}
+
+static int run_finalize(pnp_ctx* ctx, const Geom& g, const Window& w, const float* kx,
+                        const float* d, const unsigned* mbits, const float* x, float* out,
+                        float* alpha_out) {
+  const size_t npix = (size_t)w.nrows * g.W;
+  dim3 grid((unsigned)((npix + 255) / 256), g.B);
+  ProfScope prof(ctx, PROF_FIXUP);
+  dsg_finalize_kernel<<<grid, 256, 0, ctx->stream>>>(kx, d, mbits, x, out, alpha_out, w.y0,
+                                                     w.nrows, g.W, w.buf_r0, w.buf_rows);
+  PNP_LAUNCH_CHECK("dsg_finalize_kernel");
   return PNP_OK;
 }
 
@@ -324,17 +378,6 @@ static int ensure_planes(pnp_ctx* ctx, size_t n) {
   return PNP_OK;
 }
 
-// g -> rs: sweep A + fixup (guide-only; shared by adaptive and freeze)
-static int mass_and_rs(pnp_ctx* ctx, const Plan& pl, const float* guide, const float* taps,
-                       double bw, float* rs) {
-  int rc = run_sweep(ctx, pl, 1, guide, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
-                     taps, bw, true);
-  if (rc) return rc;
-  FixIO io{};
-  io.rs = rs;
-  return run_fixup<FIX_RS>(ctx, pl, 1, io);
-}
-
 static int validate_taps(const float* taps, int P) {
   if (!taps) return fail(PNP_EINVAL, "taps must not be null");
   double s = 0;
@@ -344,6 +387,19 @@ static int validate_taps(const float* taps, int P) {
   }
   if (fabs(s - 1.0) > 1e-5) return fail(PNP_EINVAL, "taps must sum to 1");
   return PNP_OK;
+}
+
+// sweep A + fixup: g -> rs (guide-only; shared by adaptive and freeze)
+static int mass_and_rs(pnp_ctx* ctx, const Geom& g, const float* guide, const float* taps,
+                       double bw, float* rs) {
+  const Window w = full_window(g);
+  float* part = ctx->partial.as<float>();
+  int rc = run_sweep(ctx, g, w, 1, guide, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
+                     taps, bw, true, part);
+  if (rc) return rc;
+  FixIO io{};
+  io.rs = rs;
+  return run_fixup<FIX_RS>(ctx, g, w, 1, part, io);
 }
 
 }  // namespace pnp
@@ -380,6 +436,10 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   ctx->stats.release();
   ctx->flags.release();
   for (auto& kv : ctx->tables) kv.second.release();
+  for (auto& sl : ctx->slots) {
+    cudaEventDestroy(sl.a);
+    cudaEventDestroy(sl.b);
+  }
   delete ctx;
   return PNP_OK;
 }
@@ -396,14 +456,38 @@ int pnp_ctx_synchronize(pnp_ctx* ctx) {
   return PNP_OK;
 }
 
+int pnp_ctx_profile(pnp_ctx* ctx, int enable) {
+  if (!ctx) return fail(PNP_EINVAL, "ctx is null");
+  ctx->prof = enable != 0;
+  ctx->nslots = 0;
+  return PNP_OK;
+}
+
+int pnp_ctx_profile_read(pnp_ctx* ctx, double* ms, int* launches) {
+  if (!ctx || !ms || !launches) return fail(PNP_EINVAL, "null argument");
+  for (int c = 0; c < PROF_NCAT; ++c) {
+    ms[c] = 0.0;
+    launches[c] = 0;
+  }
+  PNP_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (size_t i = 0; i < ctx->nslots; ++i) {
+    float t = 0.f;
+    PNP_CUDA(cudaEventElapsedTime(&t, ctx->slots[i].a, ctx->slots[i].b));
+    ms[ctx->slots[i].cat] += t;
+    launches[ctx->slots[i].cat] += 1;
+  }
+  ctx->nslots = 0;
+  return PNP_OK;
+}
+
 int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P) {
   if (!ctx) return fail(PNP_EINVAL, "ctx is null");
   int rc = check_geometry(batch, H, W, R, P, 1.0);
   if (rc) return rc;
   PNP_CUDA(cudaSetDevice(ctx->device));
-  Plan pl;
-  if ((rc = make_plan(ctx, batch, H, W, R, P, pl))) return rc;
-  if ((rc = ctx->partial.ensure(partial_floats(pl, 2) * sizeof(float)))) return rc;
+  Geom g;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
+  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   if ((rc = ensure_planes(ctx, (size_t)batch * H * W))) return rc;
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return rc;
   return PNP_OK;
@@ -418,17 +502,20 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   if ((rc = validate_taps(taps, P))) return rc;
   if (!guide) guide = x;
   PNP_CUDA(cudaSetDevice(ctx->device));
-  Plan pl;
-  if ((rc = make_plan(ctx, batch, H, W, R, P, pl))) return rc;
+  Geom g;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
   const size_t n = (size_t)batch * H * W;
   if ((rc = ensure_planes(ctx, n))) return rc;
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return rc;
+  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   float* rs = ctx->rs.as<float>();
   float* kx = ctx->kx.as<float>();
   float* d = d_out ? d_out : ctx->d.as<float>();
-  if ((rc = mass_and_rs(ctx, pl, guide, taps, bandwidth, rs))) return rc;
-  if ((rc = run_sweep(ctx, pl, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps, bandwidth,
-                      true)))
+  float* part = ctx->partial.as<float>();
+  const Window w = full_window(g);
+  if ((rc = mass_and_rs(ctx, g, guide, taps, bandwidth, rs))) return rc;
+  if ((rc = run_sweep(ctx, g, w, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps,
+                      bandwidth, true, part)))
     return rc;
   PNP_CUDA(cudaMemsetAsync(ctx->mbits.ptr, 0, batch * sizeof(unsigned), ctx->stream));
   FixIO io{};
@@ -436,13 +523,8 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   io.kx = kx;
   io.d = d;
   io.mbits = ctx->mbits.as<unsigned>();
-  if ((rc = run_fixup<FIX_KXD>(ctx, pl, 2, io))) return rc;
-  const size_t plane = (size_t)H * W;
-  dim3 grid((unsigned)((plane + 255) / 256), batch);
-  dsg_finalize_kernel<<<grid, 256, 0, ctx->stream>>>(kx, d, ctx->mbits.as<unsigned>(), x, out,
-                                                     alpha_out, plane);
-  PNP_LAUNCH_CHECK("dsg_finalize_kernel");
-  return PNP_OK;
+  if ((rc = run_fixup<FIX_KXD>(ctx, g, w, 2, part, io))) return rc;
+  return run_finalize(ctx, g, w, kx, d, ctx->mbits.as<unsigned>(), x, out, alpha_out);
 }
 
 int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, int R, int P,
@@ -452,8 +534,9 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   if (rc) return rc;
   if ((rc = validate_taps(taps, P))) return rc;
   PNP_CUDA(cudaSetDevice(ctx->device));
-  Plan pl;
-  if ((rc = make_plan(ctx, batch, H, W, R, P, pl))) return rc;
+  Geom g;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
+  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   const size_t n = (size_t)batch * H * W;
   pnp_frozen* fz = new pnp_frozen();
   fz->device = ctx->device;
@@ -479,9 +562,11 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   e = cudaMemcpyAsync(fz->guide, guide, n * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemcpyAsync(guide)"));
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return bail(rc);
-  if ((rc = mass_and_rs(ctx, pl, fz->guide, taps, bandwidth, fz->rs))) return bail(rc);
-  if ((rc = run_sweep(ctx, pl, 1, fz->guide, ChanSpec{fz->rs, nullptr}, ChanSpec{nullptr, nullptr},
-                      taps, bandwidth, true)))
+  if ((rc = mass_and_rs(ctx, g, fz->guide, taps, bandwidth, fz->rs))) return bail(rc);
+  const Window w = full_window(g);
+  float* part = ctx->partial.as<float>();
+  if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, nullptr},
+                      ChanSpec{nullptr, nullptr}, taps, bandwidth, true, part)))
     return bail(rc);
   e = cudaMemsetAsync(ctx->mbits.ptr, 0, batch * sizeof(unsigned), ctx->stream);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemsetAsync"));
@@ -489,7 +574,7 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   io.rs = fz->rs;
   io.d = fz->d;
   io.mbits = ctx->mbits.as<unsigned>();
-  if ((rc = run_fixup<FIX_D>(ctx, pl, 1, io))) return bail(rc);
+  if ((rc = run_fixup<FIX_D>(ctx, g, w, 1, part, io))) return bail(rc);
   dsg_alpha_kernel<<<(batch + 127) / 128, 128, 0, ctx->stream>>>(ctx->mbits.as<unsigned>(),
                                                                  fz->mv, batch);
   e = cudaGetLastError();
@@ -502,11 +587,14 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
   if (!ctx || !fz || !x || !out) return fail(PNP_EINVAL, "null argument");
   if (fz->device != ctx->device) return fail(PNP_EINVAL, "handle belongs to another device");
   PNP_CUDA(cudaSetDevice(ctx->device));
-  Plan pl;
-  int rc = make_plan(ctx, fz->B, fz->H, fz->W, fz->R, fz->P, pl);
+  Geom g;
+  int rc = make_geom(ctx, fz->B, fz->H, fz->W, fz->R, fz->P, g);
   if (rc) return rc;
-  if ((rc = run_sweep(ctx, pl, 1, fz->guide, ChanSpec{fz->rs, x}, ChanSpec{nullptr, nullptr},
-                      fz->taps, fz->bw, true)))
+  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
+  const Window w = full_window(g);
+  float* part = ctx->partial.as<float>();
+  if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, x}, ChanSpec{nullptr, nullptr},
+                      fz->taps, fz->bw, true, part)))
     return rc;
   FixIO io{};
   io.rs = fz->rs;
@@ -514,7 +602,7 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
   io.inv_m = fz->mv + fz->B;
   io.x = x;
   io.out = out;
-  return run_fixup<FIX_APPLY>(ctx, pl, 1, io);
+  return run_fixup<FIX_APPLY>(ctx, g, w, 1, part, io);
 }
 
 int pnp_frozen_destroy(pnp_frozen* fz) {
@@ -563,15 +651,120 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   if ((rc = validate_taps(taps, P))) return rc;
   if (!guide) guide = x;
   PNP_CUDA(cudaSetDevice(ctx->device));
-  Plan pl;
-  if ((rc = make_plan(ctx, batch, H, W, R, P, pl))) return rc;
+  Geom g;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
+  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
+  const Window w = full_window(g);
+  float* part = ctx->partial.as<float>();
   // num = sum k x(s+t), den = sum k (no hat, no normalization; denoise.py:254-269)
-  if ((rc = run_sweep(ctx, pl, 2, guide, ChanSpec{x, nullptr}, ChanSpec{nullptr, nullptr}, taps,
-                      bandwidth, false)))
+  if ((rc = run_sweep(ctx, g, w, 2, guide, ChanSpec{x, nullptr}, ChanSpec{nullptr, nullptr}, taps,
+                      bandwidth, false, part)))
     return rc;
   FixIO io{};
   io.out = out;
-  return run_fixup<FIX_NLM>(ctx, pl, 2, io);
+  return run_fixup<FIX_NLM>(ctx, g, w, 2, part, io);
+}
+
+// ---------------------------------------------------------------- strips ---
+
+int pnp_tile_height(int P) { return (P >= 1 && P <= kMaxP && (P & 1)) ? tile_height(P) : -1; }
+
+int pnp_dsg_groups(int Hg, int W, int R, int P) {
+  if (check_geometry(1, Hg, W, R, P, 1.0)) return -1;
+  return groups_for(Hg, W, R, P);
+}
+
+int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr) {
+  if (check_geometry(1, Hg, W, R, P, 1.0) || C < 1 || C > 2 || ntr < 0) return -1;
+  const int TH = tile_height(P);
+  const int64_t blk = (int64_t)C * (TH + R) * (kTW + 2 * R);
+  return (int64_t)ntr * groups_for(Hg, W, R, P) * ((W + kTW - 1) / kTW) * blk;
+}
+
+int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float* x,
+                        const float* rs, int Hg, int W, int buf_r0, int buf_rows, int tr0,
+                        int ntr, int R, int P, const float* taps, double bandwidth,
+                        float* partial, int part_off, int part_ntr) {
+  if (!ctx || !guide || !partial) return fail(PNP_EINVAL, "null argument");
+  int rc = check_geometry(1, Hg, W, R, P, bandwidth);
+  if (rc) return rc;
+  if ((rc = validate_taps(taps, P))) return rc;
+  if (buf_r0 < 0 || buf_rows < 1 || buf_r0 + buf_rows > Hg) return fail(PNP_EINVAL, "bad window");
+  if (ntr < 0 || part_off < 0 || part_off + ntr > part_ntr) return fail(PNP_EINVAL, "bad tiles");
+  PNP_CUDA(cudaSetDevice(ctx->device));
+  Geom g;
+  if ((rc = make_geom(ctx, 1, Hg, W, R, P, g))) return rc;
+  if (tr0 < 0 || tr0 + ntr > g.tiles_y) return fail(PNP_EINVAL, "tile rows out of range");
+  Window w{buf_r0, buf_rows, tr0, ntr, 0, part_off, part_ntr, 0, 0};
+  switch (pass) {
+    case 0:  // mass g: y = in-image mask
+      return run_sweep(ctx, g, w, 1, guide, ChanSpec{nullptr, nullptr},
+                       ChanSpec{nullptr, nullptr}, taps, bandwidth, true, partial);
+    case 1:  // Kx and d: y = rs*x, rs
+      if (!x || !rs) return fail(PNP_EINVAL, "pass 1 needs x and rs");
+      return run_sweep(ctx, g, w, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps,
+                       bandwidth, true, partial);
+    case 2:  // d only: y = rs
+      if (!rs) return fail(PNP_EINVAL, "pass 2 needs rs");
+      return run_sweep(ctx, g, w, 1, guide, ChanSpec{rs, nullptr}, ChanSpec{nullptr, nullptr},
+                       taps, bandwidth, true, partial);
+    case 3:  // Kx only: y = rs*x
+      if (!x || !rs) return fail(PNP_EINVAL, "pass 3 needs x and rs");
+      return run_sweep(ctx, g, w, 1, guide, ChanSpec{rs, x}, ChanSpec{nullptr, nullptr}, taps,
+                       bandwidth, true, partial);
+  }
+  return fail(PNP_EINVAL, "unknown pass");
+}
+
+int pnp_dsg_strip_fixup(pnp_ctx* ctx, int mode, const float* partial, int part_tr0,
+                        int part_ntr, int Hg, int W, int R, int P, int y0, int y1, int buf_r0,
+                        int buf_rows, float* rs, float* kx, float* d, unsigned* mbits,
+                        const float* inv_m, const float* x, float* out) {
+  if (!ctx || !partial) return fail(PNP_EINVAL, "null argument");
+  int rc = check_geometry(1, Hg, W, R, P, 1.0);
+  if (rc) return rc;
+  if (y0 < buf_r0 || y1 > buf_r0 + buf_rows || y0 > y1) return fail(PNP_EINVAL, "bad rows");
+  PNP_CUDA(cudaSetDevice(ctx->device));
+  Geom g;
+  if ((rc = make_geom(ctx, 1, Hg, W, R, P, g))) return rc;
+  Window w{buf_r0, buf_rows, 0, 0, part_tr0, 0, part_ntr, y0, y1 - y0};
+  FixIO io{};
+  io.rs = rs;
+  io.kx = kx;
+  io.d = d;
+  io.mbits = mbits;
+  io.inv_m = inv_m;
+  io.x = x;
+  io.out = out;
+  switch (mode) {
+    case 0:
+      if (!rs) return fail(PNP_EINVAL, "mode 0 needs rs");
+      return run_fixup<FIX_RS>(ctx, g, w, 1, partial, io);
+    case 1:
+      if (!rs || !kx || !d || !mbits) return fail(PNP_EINVAL, "mode 1 needs rs, kx, d, mbits");
+      return run_fixup<FIX_KXD>(ctx, g, w, 2, partial, io);
+    case 2:
+      if (!rs || !d || !mbits) return fail(PNP_EINVAL, "mode 2 needs rs, d, mbits");
+      return run_fixup<FIX_D>(ctx, g, w, 1, partial, io);
+    case 3:
+      if (!rs || !d || !inv_m || !x || !out) return fail(PNP_EINVAL, "mode 3 needs rs,d,inv_m,x,out");
+      return run_fixup<FIX_APPLY>(ctx, g, w, 1, partial, io);
+  }
+  return fail(PNP_EINVAL, "unknown mode");
+}
+
+int pnp_dsg_strip_finalize(pnp_ctx* ctx, const float* kx, const float* d, const float* x,
+                           float* out, const unsigned* mbits, int Hg, int W, int y0, int y1,
+                           int buf_r0, int buf_rows) {
+  if (!ctx || !kx || !d || !x || !out || !mbits) return fail(PNP_EINVAL, "null argument");
+  if (y0 < buf_r0 || y1 > buf_r0 + buf_rows || y0 > y1 || y1 > Hg) return fail(PNP_EINVAL, "bad rows");
+  PNP_CUDA(cudaSetDevice(ctx->device));
+  Geom g{};
+  g.B = 1;
+  g.Hg = Hg;
+  g.W = W;
+  Window w{buf_r0, buf_rows, 0, 0, 0, 0, 0, y0, y1 - y0};
+  return run_finalize(ctx, g, w, kx, d, mbits, x, out, nullptr);
 }
 
 }  // extern "C"

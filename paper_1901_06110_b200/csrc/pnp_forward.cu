@@ -242,8 +242,11 @@ int pnp_sr_apply(pnp_ctx* ctx, const float* x, float* y, int batch, int H, int W
   if (rc) return rc;
   const int nl = (H / factor) * (W / factor);
   dim3 grid((nl + 255) / 256, batch);
-  sr_residual_kernel<<<grid, 256, 0, ctx->stream>>>(x, nullptr, y, H, W, factor, radius, boundary,
-                                                    t, nullptr);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_residual_kernel<<<grid, 256, 0, ctx->stream>>>(x, nullptr, y, H, W, factor, radius, boundary,
+                                                      t, nullptr);
+  }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
   return PNP_OK;
 }
@@ -255,7 +258,10 @@ int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int
   int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
   if (rc) return rc;
   dim3 grid((H * W + 255) / 256, batch);
-  sr_adjoint_kernel<<<grid, 256, 0, ctx->stream>>>(y, x, H, W, factor, radius, boundary, t);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_adjoint_kernel<<<grid, 256, 0, ctx->stream>>>(y, x, H, W, factor, radius, boundary, t);
+  }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
 }
@@ -272,15 +278,24 @@ int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, in
   if (data_out && (rc = ensure_partials(ctx, (size_t)batch * nblk))) return rc;
   float* r = ctx->kx.as<float>();
   double* part = data_out ? ctx->stats.as<double>() : nullptr;
-  sr_residual_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, yobs, r, H, W, factor, radius,
-                                                                 boundary, t, part);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_residual_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, yobs, r, H, W, factor, radius,
+                                                                   boundary, t, part);
+  }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
   if (data_out) {
-    reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 0.5, data_out, 1);
+    {
+      ProfScope prof_(ctx, PROF_ADMM);
+      reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 0.5, data_out, 1);
+    }
     PNP_LAUNCH_CHECK("reduce_partials_kernel");
   }
-  sr_adjoint_kernel<<<dim3((H * W + 255) / 256, batch), 256, 0, ctx->stream>>>(
-      r, grad, H, W, factor, radius, boundary, t);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_adjoint_kernel<<<dim3((H * W + 255) / 256, batch), 256, 0, ctx->stream>>>(
+        r, grad, H, W, factor, radius, boundary, t);
+  }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
 }
@@ -297,11 +312,17 @@ int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* z
     if (rc) return rc;
     part = ctx->stats.as<double>();
   }
-  qis_grad_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, ones, zeros, grad, (size_t)n,
-                                                              gain_over_K, floor_, part);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    qis_grad_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, ones, zeros, grad, (size_t)n,
+                                                                gain_over_K, floor_, part);
+  }
   PNP_LAUNCH_CHECK("qis_grad_kernel");
   if (data_out) {
-    reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
+    {
+      ProfScope prof_(ctx, PROF_ADMM);
+      reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
+    }
     PNP_LAUNCH_CHECK("reduce_partials_kernel");
   }
   return PNP_OK;
@@ -315,8 +336,11 @@ int pnp_qis_data(pnp_ctx* ctx, const float* x, const float* ones, const float* z
   int rc = ensure_partials(ctx, (size_t)batch * nblk);
   if (rc) return rc;
   double* part = ctx->stats.as<double>();
-  qis_grad_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, ones, zeros, nullptr, (size_t)n,
-                                                              gain_over_K, floor_, part);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    qis_grad_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, ones, zeros, nullptr, (size_t)n,
+                                                                gain_over_K, floor_, part);
+  }
   PNP_LAUNCH_CHECK("qis_grad_kernel");
   reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
   PNP_LAUNCH_CHECK("reduce_partials_kernel");
@@ -329,8 +353,11 @@ int pnp_admm_xupdate(pnp_ctx* ctx, float* x, const float* v, const float* u, con
   if (!ctx || !x || !v || !u || !grad || !z || !flags) return fail(PNP_EINVAL, "null argument");
   const float flo = isinf(lo) ? -INFINITY : (float)lo;
   const float fhi = isinf(hi) ? INFINITY : (float)hi;
-  admm_xupdate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
-      x, v, u, grad, z, (size_t)n, mu, alpha, rho, flo, fhi, flags);
+  {
+    ProfScope prof_(ctx, PROF_ADMM);
+    admm_xupdate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+        x, v, u, grad, z, (size_t)n, mu, alpha, rho, flo, fhi, flags);
+  }
   PNP_LAUNCH_CHECK("admm_xupdate_kernel");
   return PNP_OK;
 }
@@ -343,8 +370,11 @@ int pnp_admm_uupdate(pnp_ctx* ctx, float* u, const float* x, const float* v, con
   int rc = ensure_partials(ctx, (size_t)batch * nblk * 3);
   if (rc) return rc;
   double* part = ctx->stats.as<double>();
-  admm_uupdate_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(u, x, v, v_prev, gt, (size_t)n,
-                                                                  rho, part, flags);
+  {
+    ProfScope prof_(ctx, PROF_ADMM);
+    admm_uupdate_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(u, x, v, v_prev, gt, (size_t)n,
+                                                                    rho, part, flags);
+  }
   PNP_LAUNCH_CHECK("admm_uupdate_kernel");
   reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 3, 1.0, stats, 4);
   PNP_LAUNCH_CHECK("reduce_partials_kernel");
@@ -355,7 +385,10 @@ int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, do
   if (!ctx || !x || !y) return fail(PNP_EINVAL, "null argument");
   const float flo = isinf(lo) ? -INFINITY : (float)lo;
   const float fhi = isinf(hi) ? INFINITY : (float)hi;
-  project_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x, y, (size_t)n, flo, fhi);
+  {
+    ProfScope prof_(ctx, PROF_ADMM);
+    project_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x, y, (size_t)n, flo, fhi);
+  }
   PNP_LAUNCH_CHECK("project_kernel");
   return PNP_OK;
 }

@@ -6,6 +6,7 @@
 #include <map>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "../../include/pnp_b200.h"
 
@@ -39,13 +40,48 @@ struct DevBuf {
 
 }  // namespace pnp
 
+namespace pnp {
+enum ProfCat { PROF_SWEEP = 0, PROF_FIXUP = 1, PROF_FORWARD = 2, PROF_ADMM = 3, PROF_NCAT = 4 };
+struct ProfSlot {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int cat = 0;
+};
+}  // namespace pnp
+
 struct pnp_ctx {
   int device = 0;
   cudaStream_t stream = 0;
   pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
-  // chunk tables keyed by (R, NG): device int4 chunks followed by NG+1 ints
+  // chunk tables keyed by (R, NG): device chunks (hat, no-hat) + NG+1 ints
   std::map<std::pair<int, int>, pnp::DevBuf> tables;
+  // optional per-launch CUDA-event timing (pnp_ctx_profile)
+  bool prof = false;
+  std::vector<pnp::ProfSlot> slots;
+  size_t nslots = 0;
 };
+
+namespace pnp {
+// Brackets one kernel launch with events on the context stream when
+// profiling is on (used by bench.py for the live roofline numbers).
+struct ProfScope {
+  pnp_ctx* c;
+  size_t idx;
+  ProfScope(pnp_ctx* ctx, int cat) : c(ctx), idx((size_t)-1) {
+    if (!c->prof) return;
+    if (c->nslots == c->slots.size()) {
+      ProfSlot s;
+      if (cudaEventCreate(&s.a) != cudaSuccess || cudaEventCreate(&s.b) != cudaSuccess) return;
+      c->slots.push_back(s);
+    }
+    idx = c->nslots++;
+    c->slots[idx].cat = cat;
+    cudaEventRecord(c->slots[idx].a, c->stream);
+  }
+  ~ProfScope() {
+    if (idx != (size_t)-1) cudaEventRecord(c->slots[idx].b, c->stream);
+  }
+};
+}  // namespace pnp
 
 struct pnp_frozen {
   int device = 0;

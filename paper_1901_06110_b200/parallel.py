@@ -1,0 +1,325 @@
+"""Row-strip sharding of DSG-NLM across GPUs.
+
+A large image (config 4: 8192^2) is split into row strips of whole tiles,
+one per rank (one process per GPU, ``torch.distributed`` over NCCL for the
+plumbing).  One adaptive denoise is
+
+    halo rows of the input (p above, R + max(p, KY) below)   [P2P exchange]
+    sweep A (mass g) on own tile rows
+    the last ceil(R/TH) tile rows of partial blocks -> next rank
+    fixup: rs = g^-1/2 on own rows
+    R + KY rows of rs -> previous rank                         [P2P exchange]
+    sweep B (K x and d) on own tile rows
+    partial blocks -> next rank                                [P2P exchange]
+    fixup: K x, d, local max d
+    all-reduce max -> m (the north-star "alpha")               [NCCL max]
+    finalize own rows: W x = K x / m + (1 - d/m) x
+
+Strip boundaries sit on tile boundaries and every rank sums each pixel's
+contributions in the single-GPU order, so the sharded output is
+bit-identical to one GPU.  The algorithm is written once over a list of
+per-rank states and a communicator: ``TorchComm`` moves data between real
+ranks (NCCL / gloo), ``LocalComm`` runs N virtual ranks in one process on
+one device (test / development mode; copies instead of messages).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+from .denoise import PatchParams
+
+KY = 2  # offsets per chunk in the sweep (csrc/dsg_sweep.cuh kKY)
+
+
+@dataclass(frozen=True)
+class StripLayout:
+    """Which rows / tile rows rank ``rank`` of ``nranks`` owns and reads."""
+
+    Hg: int
+    W: int
+    R: int
+    P: int
+    nranks: int
+    rank: int
+
+    @property
+    def TH(self) -> int:
+        return 32 - (self.P - 1)
+
+    @property
+    def tiles_y(self) -> int:
+        return -(-self.Hg // self.TH)
+
+    @property
+    def tile_rows(self) -> tuple[int, int]:
+        t = self.tiles_y
+        return (self.rank * t) // self.nranks, ((self.rank + 1) * t) // self.nranks
+
+    @property
+    def rows(self) -> tuple[int, int]:
+        t0, t1 = self.tile_rows
+        return t0 * self.TH, min(t1 * self.TH, self.Hg)
+
+    @property
+    def dti(self) -> int:
+        """Tile rows of the rank above whose partial blocks reach our rows."""
+        return -(-self.R // self.TH)
+
+    @property
+    def halo(self) -> tuple[int, int]:
+        p = (self.P - 1) // 2
+        return p, self.R + max(p, KY)
+
+    @property
+    def window(self) -> tuple[int, int]:
+        """Rows [b0, b1) held locally: own rows plus halos, clipped to the image."""
+        y0, y1 = self.rows
+        top, bot = self.halo
+        return max(0, y0 - top), min(self.Hg, y1 + bot)
+
+    @property
+    def part(self) -> tuple[int, int, int]:
+        """(global tile row of slot 0, slot of our first tile row, slots)."""
+        t0, t1 = self.tile_rows
+        first = max(0, t0 - self.dti)
+        return first, t0 - first, t1 - first
+
+    def validate(self) -> None:
+        t0, t1 = self.tile_rows
+        if t1 - t0 < max(self.dti, 1):
+            raise ValueError("strip too thin: each rank needs >= ceil(R/TH) tile rows")
+        y0, y1 = self.rows
+        if y1 - y0 < self.halo[1] and self.rank < self.nranks - 1:
+            raise ValueError("strip too thin for the halo")
+
+
+class _RankState:
+    """Device buffers of one rank (or one virtual rank)."""
+
+    def __init__(self, lay: StripLayout, device):
+        self.lay = lay
+        b0, b1 = lay.window
+        self.buf = torch.zeros((b1 - b0, lay.W), dtype=torch.float32, device=device)
+        self.rs = torch.zeros_like(self.buf)
+        self.kx = torch.zeros_like(self.buf)
+        self.d = torch.zeros_like(self.buf)
+        self.out = torch.zeros_like(self.buf)
+        self.mbits = torch.zeros(1, dtype=torch.int32, device=device)
+        pf = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, 2, lay.part[2]))
+        if pf < 0:
+            raise ValueError(L.lib.pnp_last_error().decode())
+        self.partial = torch.zeros(pf, dtype=torch.float32, device=device)
+        self.block_floats_c1 = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, 1, 1))
+        self.block_floats_c2 = 2 * self.block_floats_c1
+
+    # row views of the window (global row indices)
+    def rows_view(self, t: torch.Tensor, r0: int, r1: int) -> torch.Tensor:
+        b0 = self.lay.window[0]
+        return t[r0 - b0:r1 - b0]
+
+    def own(self, t: torch.Tensor) -> torch.Tensor:
+        return self.rows_view(t, *self.lay.rows)
+
+    def partial_rows(self, C: int, s0: int, s1: int) -> torch.Tensor:
+        per = self.block_floats_c1 * C
+        return self.partial[s0 * per:s1 * per]
+
+
+class LocalComm:
+    """N virtual ranks in one process (copies instead of messages)."""
+
+    def shift_down(self, states, send, recv):
+        """recv(state k) <- send(state k-1), k = 1..N-1."""
+        for k in range(len(states) - 1, 0, -1):
+            dst = recv(states[k])
+            if dst is not None and dst.numel():
+                dst.copy_(send(states[k - 1]))
+
+    def shift_up(self, states, send, recv):
+        """recv(state k) <- send(state k+1), k = 0..N-2."""
+        for k in range(len(states) - 1):
+            dst = recv(states[k])
+            if dst is not None and dst.numel():
+                dst.copy_(send(states[k + 1]))
+
+    def allreduce_max(self, states):
+        m = torch.stack([s.mbits for s in states]).max(dim=0).values
+        for s in states:
+            s.mbits.copy_(m)
+
+
+class TorchComm:
+    """Neighbour exchanges + max all-reduce over a torch.distributed group
+    (NCCL for CUDA tensors; gloo works for the CPU tests of this logic)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def _peer(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def _exchange(self, states, send, recv, direction):
+        (st,) = states
+        ops = []
+        to = self.rank + direction
+        frm = self.rank - direction
+        if 0 <= to < self.size:
+            t = send(st).contiguous()
+            ops.append(self.dist.P2POp(self.dist.isend, t, self._peer(to), self.group))
+        tmp = None
+        if 0 <= frm < self.size:
+            dst = recv(st)
+            tmp = dst if dst.is_contiguous() else torch.empty_like(dst)
+            ops.append(self.dist.P2POp(self.dist.irecv, tmp, self._peer(frm), self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        if tmp is not None and tmp is not recv(st):
+            recv(st).copy_(tmp)
+
+    def shift_down(self, states, send, recv):
+        self._exchange(states, send, recv, +1)
+
+    def shift_up(self, states, send, recv):
+        self._exchange(states, send, recv, -1)
+
+    def allreduce_max(self, states):
+        (st,) = states
+        self.dist.all_reduce(st.mbits, op=self.dist.ReduceOp.MAX, group=self.group)
+
+
+class ShardedDSG:
+    """Adaptive DSG-NLM of a Hg x W image split in row strips.
+
+    ``ranks`` lists the rank indices this process drives: ``[rank]`` with a
+    TorchComm, or ``range(N)`` with a LocalComm (virtual shards)."""
+
+    def __init__(self, params: PatchParams, Hg: int, W: int, nranks: int, ranks, comm,
+                 device=None):
+        if params.pad_margin > min(Hg, W):
+            raise ValueError(f"margin {params.pad_margin} exceeds min image extent {min(Hg, W)}")
+        self.params = params
+        self.comm = comm
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.states = []
+        for r in ranks:
+            lay = StripLayout(Hg, W, params.window_radius, params.patch_side, nranks, r)
+            lay.validate()
+            self.states.append(_RankState(lay, self.device))
+        self._taps = params._ctaps()
+
+    # ---- host-side views ---------------------------------------------------
+    def load(self, full_or_strips):
+        """Fill each state's window from a full image (tensor/ndarray) — the
+        data-loading path; ``denoise`` then exchanges halos itself."""
+        for st in self.states:
+            y0, y1 = st.lay.rows
+            src = full_or_strips[y0:y1]
+            st.own(st.buf).copy_(torch.as_tensor(src, dtype=torch.float32))
+
+    def gather(self) -> torch.Tensor:
+        return torch.cat([st.own(st.out) for st in self.states], dim=0)
+
+    # ---- the sharded algorithm ----------------------------------------------
+    def _sweep(self, st, pass_, C):
+        lay = st.lay
+        b0, b1 = lay.window
+        t0, t1 = lay.tile_rows
+        part0, off, nslot = lay.part
+        p = self.params
+        L.call("pnp_dsg_strip_sweep", L.context(self.device.index), pass_, L.ptr(st.buf),
+               L.ptr(st.buf), L.ptr(st.rs), lay.Hg, lay.W, b0, b1 - b0, t0, t1 - t0,
+               p.window_radius, p.patch_side, self._taps, float(p.bandwidth),
+               L.ptr(st.partial), off, nslot)
+
+    def _fixup(self, st, mode):
+        lay = st.lay
+        b0, b1 = lay.window
+        y0, y1 = lay.rows
+        part0, off, nslot = lay.part
+        p = self.params
+        L.call("pnp_dsg_strip_fixup", L.context(self.device.index), mode, L.ptr(st.partial),
+               part0, nslot, lay.Hg, lay.W, p.window_radius, p.patch_side, y0, y1, b0, b1 - b0,
+               L.ptr(st.rs), L.ptr(st.kx), L.ptr(st.d), L.ptr(st.mbits), None, None, None)
+
+    def _exchange_partials(self, C):
+        def send(st):
+            _, off, nslot = st.lay.part
+            return st.partial_rows(C, nslot - st.lay.dti, nslot)
+
+        def recv(st):
+            _, off, _ = st.lay.part
+            return st.partial_rows(C, 0, off)
+
+        self.comm.shift_down(self.states, send, recv)
+
+    def _exchange_rows(self, name, top=True):
+        def up_send(st):   # our first rows -> rank above's bottom halo
+            y0, y1 = st.lay.rows
+            return st.rows_view(getattr(st, name), y0, y0 + st.lay.halo[1])
+
+        def up_recv(st):
+            y0, y1 = st.lay.rows
+            b0, b1 = st.lay.window
+            return st.rows_view(getattr(st, name), y1, b1)
+
+        def down_send(st):  # our last rows -> rank below's top halo
+            y0, y1 = st.lay.rows
+            return st.rows_view(getattr(st, name), y1 - st.lay.halo[0], y1)
+
+        def down_recv(st):
+            y0, _ = st.lay.rows
+            b0, _ = st.lay.window
+            return st.rows_view(getattr(st, name), b0, y0)
+
+        self.comm.shift_up(self.states, up_send, up_recv)
+        if top and self.states[0].lay.halo[0] > 0:
+            self.comm.shift_down(self.states, down_send, down_recv)
+
+    def denoise(self) -> None:
+        """One adaptive DSG-NLM of the loaded image; results in each state's out."""
+        self._exchange_rows("buf")
+        for st in self.states:
+            self._sweep(st, 0, 1)
+        self._exchange_partials(1)
+        for st in self.states:
+            self._fixup(st, 0)
+        self._exchange_rows("rs", top=False)  # y channels only read rows below
+        for st in self.states:
+            self._sweep(st, 1, 2)
+        self._exchange_partials(2)
+        for st in self.states:
+            st.mbits.zero_()
+            self._fixup(st, 1)
+        self.comm.allreduce_max(self.states)
+        for st in self.states:
+            lay = st.lay
+            b0, b1 = lay.window
+            y0, y1 = lay.rows
+            L.call("pnp_dsg_strip_finalize", L.context(self.device.index), L.ptr(st.kx),
+                   L.ptr(st.d), L.ptr(st.buf), L.ptr(st.out), L.ptr(st.mbits), lay.Hg, lay.W,
+                   y0, y1, b0, b1 - b0)
+
+    def alpha(self) -> float:
+        return float(self.states[0].mbits.view(torch.float32)[0])
+
+
+def sharded_dsg_nlm_denoise(image: torch.Tensor, params: PatchParams, nshards: int) -> torch.Tensor:
+    """Virtual-shard run on one device (N strips, LocalComm): same bits as
+    ``dsg_nlm_denoise(image, params)``; exercises the multi-GPU algorithm."""
+    H, W = image.shape
+    sh = ShardedDSG(params, H, W, nshards, range(nshards), LocalComm(), device=image.device)
+    sh.load(image)
+    sh.denoise()
+    return sh.gather()

@@ -1,0 +1,34 @@
+"""Live kernel timing (CUDA events on the library's stream) and measured
+FP32/SFU peaks — the numbers bench.py's roofline object is built from."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+
+CATEGORIES = ("sweep", "fixup", "forward", "admm")
+
+
+def enable(flag: bool = True, device: int | None = None) -> None:
+    dev = torch.cuda.current_device() if device is None else device
+    L.call("pnp_ctx_profile", L.context(dev), 1 if flag else 0)
+
+
+def read(device: int | None = None) -> dict:
+    """{category: (device ms, launches)} since the last read (syncs the stream)."""
+    dev = torch.cuda.current_device() if device is None else device
+    ms = (C.c_double * 4)()
+    n = (C.c_int * 4)()
+    L.call("pnp_ctx_profile_read", L.context(dev), ms, n)
+    return {c: (float(ms[i]), int(n[i])) for i, c in enumerate(CATEGORIES)}
+
+
+def peak_rates(device: int | None = None) -> tuple[float, float]:
+    """Measured (FFMA/s, MUFU.EX2/s) of the whole GPU."""
+    dev = torch.cuda.current_device() if device is None else device
+    f, x = C.c_double(), C.c_double()
+    L.call("pnp_peak_rates", dev, C.byref(f), C.byref(x))
+    return f.value, x.value

@@ -77,14 +77,19 @@ class SplitMix64:
         return out[:n]
 
 
-def scene(h: int, w: int, seed: int, n_shapes: int = 40) -> np.ndarray:
-    """Clean float64 scene in [0, 1] (see module docstring)."""
+def scene(h: int, w: int, seed: int, n_shapes: int = 40, rows: tuple | None = None) -> np.ndarray:
+    """Clean float64 scene in [0, 1] (see module docstring).  ``rows=(r0, r1)``
+    returns just those rows of the h x w scene (same values)."""
+    r0, r1 = (0, h) if rows is None else rows
     u = SplitMix64(seed).uniforms(1 + 6 * n_shapes)
     th = 2.0 * math.pi * u[0]
     ys = (np.arange(h) + 0.5) / h
     xs = (np.arange(w) + 0.5) / w
-    proj = math.cos(th) * xs[None, :] + math.sin(th) * ys[:, None]
-    lo, hi = float(proj.min()), float(proj.max())
+    c, s_ = math.cos(th), math.sin(th)
+    # the projection is linear, so its extrema sit at the image corners
+    corners = [c * xs[i] + s_ * ys[j] for i in (0, -1) for j in (0, -1)]
+    lo, hi = min(corners), max(corners)
+    proj = c * xs[None, :] + s_ * ys[r0:r1, None]
     ramp = (proj - lo) / (hi - lo) if hi > lo else np.full_like(proj, 0.5)
     img = 0.15 + 0.7 * ramp
     side = min(h, w)
@@ -94,23 +99,29 @@ def scene(h: int, w: int, seed: int, n_shapes: int = 40) -> np.ndarray:
         a = (0.02 + 0.13 * e1) * side
         b = (0.02 + 0.13 * e2) * side
         ext_y, ext_x = (a, b) if kind < 0.5 else (a, a)
-        r0 = max(0, int(math.floor(cy - ext_y - 1)))
-        r1 = min(h, int(math.ceil(cy + ext_y + 1)))
+        a0 = max(r0, int(math.floor(cy - ext_y - 1)))
+        a1 = min(r1, int(math.ceil(cy + ext_y + 1)))
         c0 = max(0, int(math.floor(cx - ext_x - 1)))
         c1 = min(w, int(math.ceil(cx + ext_x + 1)))
-        if r0 >= r1 or c0 >= c1:
+        if a0 >= a1 or c0 >= c1:
             continue
-        yy = (np.arange(r0, r1) + 0.5)[:, None] - cy
+        yy = (np.arange(a0, a1) + 0.5)[:, None] - cy
         xx = (np.arange(c0, c1) + 0.5)[None, :] - cx
         if kind < 0.5:
             m = (np.abs(yy) <= a) & (np.abs(xx) <= b)
         else:
             m = yy * yy + xx * xx <= a * a
-        img[r0:r1, c0:c1][m] = val
+        img[a0 - r0:a1 - r0, c0:c1][m] = val
     return np.clip(img, 0.0, 1.0)
 
 
-def noisy(clean: np.ndarray, sigma: float, seed: int) -> np.ndarray:
-    """clean + sigma * splitmix normals (not clipped)."""
-    n = SplitMix64(seed).normals(clean.size).reshape(clean.shape)
+def noisy(clean: np.ndarray, sigma: float, seed: int, first_index: int = 0) -> np.ndarray:
+    """clean + sigma * splitmix normals (not clipped).  ``first_index`` (even)
+    is the raster index of clean's first pixel in the full image, so rows of
+    a large image can be generated independently (the stream is counter
+    based: draw n uses state seed + n * GOLDEN)."""
+    if first_index % 2:
+        raise ValueError("first_index must be even (normals come in Box-Muller pairs)")
+    rng = SplitMix64((seed + first_index * _GOLDEN) & _MASK)
+    n = rng.normals(clean.size).reshape(clean.shape)
     return clean + sigma * n

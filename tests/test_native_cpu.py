@@ -13,7 +13,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def header_symbols():
     text = (ROOT / "include" / "pnp_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pnp_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|const char\*)\s+(pnp_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
