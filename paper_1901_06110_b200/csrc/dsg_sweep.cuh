@@ -27,7 +27,8 @@
 //   phase 2  thread = (column c, row group g of N rows): vertical P-tap
 //            filter of H_k's column with the exponent scale and log2(hat)
 //            folded in, MUFU ex2, near FFMA, far FFMA into a register window
-//            of N+KY-1 rows, then one flush per chunk.
+//            of N+KY-1 rows, then one flush per chunk (group 0 before the
+//            chunk barrier, group 1 after it: one shared far buffer, no race).
 // All SMEM strides are compile-time (R bucket RB >= R), so every access is a
 // base register + immediate offset.
 //
@@ -44,7 +45,7 @@ namespace pnp {
 constexpr int kTW = 64;        // tile width (output columns)
 constexpr int kThreads = 128;  // 64 columns x 2 row groups in phase 2
 #ifndef PNP_KY
-#define PNP_KY 2
+#define PNP_KY 4
 #endif
 constexpr int kKY = PNP_KY;    // offsets per chunk (same dx, consecutive dy)
 constexpr int kMaxP = 15;      // largest patch side with a fast kernel
@@ -100,11 +101,11 @@ struct Cfg {
   static constexpr int WIN = N + KY - 1;
   static constexpr int GC = kTW + 2 * (RB + p), GS = GC | 1, GR = 32 + RB;
   static constexpr int HS = kTW + 1;
-  static constexpr int YC = kTW + 2 * RB, YR = TH + RB + KY, AR = N + RB + KY;
+  static constexpr int YC = kTW + 2 * RB, YR = TH + RB + KY, AR = TH + RB + KY;
   static constexpr int OFF_H = GR * GS;
   static constexpr int OFF_Y = OFF_H + KY * 32 * HS;
   static constexpr int OFF_A = OFF_Y + C * YR * YC;
-  static constexpr int TOTAL = OFF_A + 2 * C * AR * YC;  // floats
+  static constexpr int TOTAL = OFF_A + C * AR * YC;  // floats
 };
 
 __device__ __forceinline__ int reflect_index(int i, int n) {
@@ -133,7 +134,7 @@ dsg_sweep_kernel(const SweepArgs a) {
   float* Gs = smem;
   float* Hs = smem + K::OFF_H;
   float* Ys = smem + K::OFF_Y;
-  float* As = smem + K::OFF_A;  // [2][C][AR][YC]
+  float* As = smem + K::OFF_A;  // [C][AR][YC] far-end accumulators (tile + band)
 
   const int R = a.R;
   const int Hg = a.Hg, W = a.W, br0 = a.buf_r0, brows = a.buf_rows;
@@ -147,6 +148,7 @@ dsg_sweep_kernel(const SweepArgs a) {
 
   // ---- stage guide (reflected), channel planes (zero outside), clear A ----
   // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
+#pragma unroll 4
   for (int i = tid; i < GR * GC; i += kThreads) {
     const int q = i / GC, cc = i - q * GC;
     int lr = reflect_index(r0g - p + q, Hg) - br0;
@@ -159,6 +161,7 @@ dsg_sweep_kernel(const SweepArgs a) {
     const float* pa = a.ch[c_].a ? a.ch[c_].a + (size_t)b * plane : nullptr;
     const float* pb = a.ch[c_].b ? a.ch[c_].b + (size_t)b * plane : nullptr;
     float* Y = Ys + c_ * YR * YC;
+#pragma unroll 4
     for (int i = tid; i < YR * YC; i += kThreads) {
       const int r = i / YC, cc = i - r * YC;
       const int gr = r0g + r, gc = c0g - RB + cc, lr = gr - br0;
@@ -172,7 +175,7 @@ dsg_sweep_kernel(const SweepArgs a) {
       Y[i] = v;
     }
   }
-  for (int i = tid; i < 2 * C * AR * YC; i += kThreads) As[i] = 0.f;
+  for (int i = tid; i < C * AR * YC; i += kThreads) As[i] = 0.f;
   __syncthreads();
 
   const int warp = tid >> 5, lane = tid & 31;
@@ -198,12 +201,29 @@ dsg_sweep_kernel(const SweepArgs a) {
 
   const float* hcol0 = Hs + r0 * HS + c;
   float* hrow0 = Hs + lane * HS + c0;
-  float* Ag0 = As + g * C * AR * YC;
+
+  // Far windows of the two row groups overlap in KY-1 rows.  Group 0 flushes
+  // before the chunk's closing barrier, group 1 after it (at the top of the
+  // next chunk, before the phase-1 barrier): every SMEM cell sees one writer
+  // between barriers and a fixed order (group 0, then group 1).
+  float fw[C][WIN];
+  float* pend = nullptr;  // group 1's pending flush target
+  auto flush = [&](float* base) {
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) {
+        // window rows past the chunk's last offset hold +0: adding them is exact
+        float* pA = base + c_ * AR * YC + j * YC;
+        *pA = __fadd_rn(*pA, fw[c_][j]);
+      }
+  };
 
   const int cbeg = a.grp[blockIdx.y], cend = a.grp[blockIdx.y + 1];
   for (int ci = cbeg; ci < cend; ++ci) {
     const Chunk chk = a.chunks[ci];
     const int dx = chk.dx, dy0 = chk.dy0, kc = chk.kc;
+    if (g == 1 && pend) flush(pend);
 
     // ---------------- phase 1: squared differences + horizontal filter ----
     {
@@ -231,8 +251,8 @@ dsg_sweep_kernel(const SweepArgs a) {
 
     // ---------------- phase 2: vertical filter, exp, near/far -------------
     const float* ybase = Ys + (r0 + dy0) * YC + c + dx + RB;
-    float* abase = Ag0 + dy0 * YC + c + dx + RB;
-    float yw[C][WIN], fw[C][WIN];
+    float* abase = As + (r0 + dy0) * YC + c + dx + RB;
+    float yw[C][WIN];
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
@@ -261,23 +281,21 @@ dsg_sweep_kernel(const SweepArgs a) {
         }
       }
     }
-    // window rows past the chunk's last offset hold +0: adding them is exact
-#pragma unroll
-    for (int c_ = 0; c_ < C; ++c_)
-#pragma unroll
-      for (int j = 0; j < WIN; ++j) {
-        float* pA = abase + c_ * AR * YC + j * YC;
-        *pA = __fadd_rn(*pA, fw[c_][j]);
-      }
+    if (g == 0)
+      flush(abase);
+    else
+      pend = abase;
     __syncthreads();
   }
+  if (g == 1 && pend) flush(pend);
+  __syncthreads();
 
-  // ---- own pixels: near + far(own group); then emit tile + band block ----
+  // ---- own pixels: near + far; then emit tile + band block ----
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      float* pA = Ag0 + (c_ * AR + r) * YC + c + RB;
+      float* pA = As + (c_ * AR + r0 + r) * YC + c + RB;
       *pA = __fadd_rn(near[c_][r], *pA);
     }
   __syncthreads();
@@ -287,14 +305,10 @@ dsg_sweep_kernel(const SweepArgs a) {
   float* out = a.partial + slot * (size_t)(C * BR * BC);
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_) {
-    const float* A0 = As + (0 * C + c_) * AR * YC + (RB - R);
-    const float* A1 = As + (1 * C + c_) * AR * YC + (RB - R);
+    const float* A0 = As + c_ * AR * YC + (RB - R);
     for (int i = tid; i < BR * BC; i += kThreads) {
       const int br = i / BC, bc = i - br * BC;
-      float v = 0.f;
-      if (br < N + R) v = A0[br * YC + bc];
-      if (br >= N) v = __fadd_rn(v, A1[(br - N) * YC + bc]);
-      out[(size_t)c_ * BR * BC + i] = v;
+      out[(size_t)c_ * BR * BC + i] = A0[br * YC + bc];
     }
   }
 }

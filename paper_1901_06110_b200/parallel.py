@@ -34,7 +34,7 @@ import torch
 from . import _lib as L
 from .denoise import PatchParams
 
-KY = 2  # offsets per chunk in the sweep (csrc/dsg_sweep.cuh kKY)
+KY = 4  # offsets per chunk in the sweep (csrc/dsg_sweep.cuh kKY)
 
 
 @dataclass(frozen=True)
