@@ -146,39 +146,65 @@ dsg_sweep_kernel(const SweepArgs a) {
   const float* Gimg = a.guide + (size_t)b * plane;
   const int tid = threadIdx.x;
 
+  const int warp = tid >> 5, lane = tid & 31;
+
   // ---- stage guide (reflected), channel planes (zero outside), clear A ----
+  // warps walk rows, lanes walk columns: index math once per row / column.
   // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
-#pragma unroll 4
-  for (int i = tid; i < GR * GC; i += kThreads) {
-    const int q = i / GC, cc = i - q * GC;
-    int lr = reflect_index(r0g - p + q, Hg) - br0;
-    lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
-    const int gc = reflect_index(c0g - RB - p + cc, W);
-    Gs[q * GS + cc] = __ldg(Gimg + (size_t)lr * W + gc);
-  }
+  {
+    constexpr int NJ = (GC + 31) / 32;
+    int gcol[NJ];
 #pragma unroll
-  for (int c_ = 0; c_ < C; ++c_) {
-    const float* pa = a.ch[c_].a ? a.ch[c_].a + (size_t)b * plane : nullptr;
-    const float* pb = a.ch[c_].b ? a.ch[c_].b + (size_t)b * plane : nullptr;
-    float* Y = Ys + c_ * YR * YC;
-#pragma unroll 4
-    for (int i = tid; i < YR * YC; i += kThreads) {
-      const int r = i / YC, cc = i - r * YC;
-      const int gr = r0g + r, gc = c0g - RB + cc, lr = gr - br0;
-      float v = 0.f;
-      if (gr < Hg && gc >= 0 && gc < W && lr >= 0 && lr < brows) {
-        const size_t o = (size_t)lr * W + gc;
-        v = 1.f;
-        if (pa) v = __ldg(pa + o);
-        if (pb) v = __fmul_rn(v, __ldg(pb + o));
+    for (int j = 0; j < NJ; ++j) {
+      const int cc = lane + 32 * j;
+      gcol[j] = cc < GC ? reflect_index(c0g - RB - p + cc, W) : -1;
+    }
+#pragma unroll 2
+    for (int q = warp; q < GR; q += kThreads / 32) {
+      int lr = reflect_index(r0g - p + q, Hg) - br0;
+      lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
+      const float* src = Gimg + (size_t)lr * W;
+      float* dst = Gs + q * GS + lane;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (gcol[j] >= 0) dst[32 * j] = __ldg(src + gcol[j]);
+    }
+  }
+  {
+    constexpr int NJ = (YC + 31) / 32;
+    int ycol[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int cc = lane + 32 * j, gc = c0g - RB + cc;
+      ycol[j] = (cc < YC) ? ((gc >= 0 && gc < W) ? gc : -1) : -2;
+    }
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_) {
+      const float* pa = a.ch[c_].a ? a.ch[c_].a + (size_t)b * plane : nullptr;
+      const float* pb = a.ch[c_].b ? a.ch[c_].b + (size_t)b * plane : nullptr;
+#pragma unroll 2
+      for (int r = warp; r < YR; r += kThreads / 32) {
+        const int gr = r0g + r, lr = gr - br0;
+        const bool rv = gr < Hg && lr >= 0 && lr < brows;
+        const size_t ro = (size_t)(rv ? lr : 0) * W;
+        float* dst = Ys + (c_ * YR + r) * YC + lane;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          if (ycol[j] == -2) continue;
+          float v = 0.f;
+          if (rv && ycol[j] >= 0) {
+            v = 1.f;
+            if (pa) v = __ldg(pa + ro + ycol[j]);
+            if (pb) v = __fmul_rn(v, __ldg(pb + ro + ycol[j]));
+          }
+          dst[32 * j] = v;
+        }
       }
-      Y[i] = v;
     }
   }
   for (int i = tid; i < C * AR * YC; i += kThreads) As[i] = 0.f;
   __syncthreads();
 
-  const int warp = tid >> 5, lane = tid & 31;
   const int c0 = SEG * warp;         // phase-1 segment
   const int c = tid & (kTW - 1);     // phase-2 column
   const int g = tid / kTW;           // phase-2 row group
@@ -202,17 +228,20 @@ dsg_sweep_kernel(const SweepArgs a) {
   const float* hcol0 = Hs + r0 * HS + c;
   float* hrow0 = Hs + lane * HS + c0;
 
-  // Far windows of the two row groups overlap in KY-1 rows.  Group 0 flushes
-  // before the chunk's closing barrier, group 1 after it (at the top of the
-  // next chunk, before the phase-1 barrier): every SMEM cell sees one writer
-  // between barriers and a fixed order (group 0, then group 1).
+  // Far windows of the two row groups overlap in KY-1 rows (group 1's first
+  // rows = group 0's last).  Group 0 flushes its whole window and group 1 its
+  // private rows before the chunk's closing barrier; group 1's shared rows go
+  // after it (top of the next chunk, before the phase-1 barrier).  Every SMEM
+  // cell sees one writer between barriers and a fixed order (group 0, then
+  // group 1), and both groups do the same flush work per chunk.
   float fw[C][WIN];
-  float* pend = nullptr;  // group 1's pending flush target
-  auto flush = [&](float* base) {
+  float* pend = nullptr;  // group 1's pending (shared-row) flush target
+  auto flush = [&](float* base, int j0, int j1) {
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
       for (int j = 0; j < WIN; ++j) {
+        if (j < j0 || j >= j1) continue;  // compile-time after unrolling
         // window rows past the chunk's last offset hold +0: adding them is exact
         float* pA = base + c_ * AR * YC + j * YC;
         *pA = __fadd_rn(*pA, fw[c_][j]);
@@ -223,7 +252,7 @@ dsg_sweep_kernel(const SweepArgs a) {
   for (int ci = cbeg; ci < cend; ++ci) {
     const Chunk chk = a.chunks[ci];
     const int dx = chk.dx, dy0 = chk.dy0, kc = chk.kc;
-    if (g == 1 && pend) flush(pend);
+    if (g == 1 && pend) flush(pend, 0, KY - 1);
 
     // ---------------- phase 1: squared differences + horizontal filter ----
     {
@@ -281,13 +310,15 @@ dsg_sweep_kernel(const SweepArgs a) {
         }
       }
     }
-    if (g == 0)
-      flush(abase);
-    else
+    if (g == 0) {
+      flush(abase, 0, WIN);
+    } else {
+      flush(abase, KY - 1, WIN);
       pend = abase;
+    }
     __syncthreads();
   }
-  if (g == 1 && pend) flush(pend);
+  if (g == 1 && pend) flush(pend, 0, KY - 1);
   __syncthreads();
 
   // ---- own pixels: near + far; then emit tile + band block ----
@@ -306,10 +337,9 @@ dsg_sweep_kernel(const SweepArgs a) {
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_) {
     const float* A0 = As + c_ * AR * YC + (RB - R);
-    for (int i = tid; i < BR * BC; i += kThreads) {
-      const int br = i / BC, bc = i - br * BC;
-      out[(size_t)c_ * BR * BC + i] = A0[br * YC + bc];
-    }
+    float* o = out + (size_t)c_ * BR * BC;
+    for (int br = warp; br < BR; br += kThreads / 32)
+      for (int bc = lane; bc < BC; bc += 32) o[br * BC + bc] = A0[br * YC + bc];
   }
 }
 
