@@ -46,10 +46,18 @@ int pnp_ctx_destroy(pnp_ctx* ctx);
 /* stream = a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
 int pnp_ctx_set_stream(pnp_ctx* ctx, void* stream);
 int pnp_ctx_synchronize(pnp_ctx* ctx);
+/* k cache: the pair weights hat*k of sweep A are kept in HBM (half window,
+ * 4 B per pixel and offset pair) when they fit, so sweep B / frozen applies
+ * stream them instead of recomputing the patch filter; results are bitwise
+ * identical either way.  bytes = 0 disables, < 0 = no limit (default; a call
+ * still falls back to recompute when free HBM is short). */
+int pnp_ctx_set_cache_limit(pnp_ctx* ctx, int64_t bytes);
+int pnp_frozen_cached(const pnp_frozen* fz);
 /* Per-launch CUDA-event timing on the context stream (off by default).
  * profile_read syncs the stream, returns summed device ms and launch counts
- * for 4 categories (0 DSG sweep, 1 DSG fixup/finalize, 2 forward operators,
- * 3 ADMM elementwise/reductions) since the last read, and resets them. */
+ * for 5 categories (0 DSG recompute sweep, 1 DSG fixup/finalize, 2 forward
+ * operators, 3 ADMM elementwise/reductions, 4 DSG k-cache sweep) since the
+ * last read, and resets them. */
 int pnp_ctx_profile(pnp_ctx* ctx, int enable);
 int pnp_ctx_profile_read(pnp_ctx* ctx, double* ms, int* launches);
 /* Measured FFMA / MUFU.EX2 instruction throughput of the device (per second,

@@ -35,6 +35,8 @@ _SIGS = {
     "pnp_ctx_set_stream": (i32, [vp, vp]),
     "pnp_ctx_synchronize": (i32, [vp]),
     "pnp_ctx_reserve": (i32, [vp, i32, i32, i32, i32, i32]),
+    "pnp_ctx_set_cache_limit": (i32, [vp, i64]),
+    "pnp_frozen_cached": (i32, [vp]),
     "pnp_ctx_profile": (i32, [vp, i32]),
     "pnp_ctx_profile_read": (i32, [vp, C.POINTER(f64), C.POINTER(i32)]),
     "pnp_peak_rates": (i32, [i32, C.POINTER(f64), C.POINTER(f64)]),

@@ -271,34 +271,50 @@ static size_t partial_floats(const Geom& g, int ntr, int C) {
   return (size_t)g.B * ntr * g.NG * g.tiles_x * block_floats(g, C);
 }
 
-template <int RB, int C>
+template <int RB, int C, int MODE>
 static cudaError_t launch_sweep_rc(const SweepArgs& a, int P, dim3 grid, cudaStream_t st) {
   switch (P) {
-    case 1: return launch_sweep<1, RB, C>(a, grid, st);
-    case 3: return launch_sweep<3, RB, C>(a, grid, st);
-    case 5: return launch_sweep<5, RB, C>(a, grid, st);
-    case 7: return launch_sweep<7, RB, C>(a, grid, st);
-    case 9: return launch_sweep<9, RB, C>(a, grid, st);
-    case 11: return launch_sweep<11, RB, C>(a, grid, st);
-    case 13: return launch_sweep<13, RB, C>(a, grid, st);
-    case 15: return launch_sweep<15, RB, C>(a, grid, st);
+    case 1: return launch_sweep<1, RB, C, MODE>(a, grid, st);
+    case 3: return launch_sweep<3, RB, C, MODE>(a, grid, st);
+    case 5: return launch_sweep<5, RB, C, MODE>(a, grid, st);
+    case 7: return launch_sweep<7, RB, C, MODE>(a, grid, st);
+    case 9: return launch_sweep<9, RB, C, MODE>(a, grid, st);
+    case 11: return launch_sweep<11, RB, C, MODE>(a, grid, st);
+    case 13: return launch_sweep<13, RB, C, MODE>(a, grid, st);
+    case 15: return launch_sweep<15, RB, C, MODE>(a, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 
-template <int C>
-static cudaError_t launch_sweep_c(const SweepArgs& a, const Geom& g, dim3 grid, cudaStream_t st) {
+template <int C, int MODE>
+static cudaError_t launch_sweep_cm(const SweepArgs& a, const Geom& g, dim3 grid, cudaStream_t st) {
   switch (r_bucket(g.R)) {
-    case 5: return launch_sweep_rc<5, C>(a, g.P, grid, st);
-    case 10: return launch_sweep_rc<10, C>(a, g.P, grid, st);
-    case 16: return launch_sweep_rc<16, C>(a, g.P, grid, st);
-    default: return launch_sweep_rc<32, C>(a, g.P, grid, st);
+    case 5: return launch_sweep_rc<5, C, MODE>(a, g.P, grid, st);
+    case 10: return launch_sweep_rc<10, C, MODE>(a, g.P, grid, st);
+    case 16: return launch_sweep_rc<16, C, MODE>(a, g.P, grid, st);
+    default: return launch_sweep_rc<32, C, MODE>(a, g.P, grid, st);
   }
+}
+
+// Floats of a k cache covering `ntr` tile rows of a (batched) image.
+static size_t kcache_floats(const Geom& g, int ntr) {
+  return (size_t)g.nchunks * kKY * g.B * ((size_t)ntr * g.TH) * (g.tiles_x * kTW);
+}
+
+// Decide whether the k cache of this call fits (ctx budget, free HBM).
+static bool kcache_fits(pnp_ctx* ctx, size_t floats, size_t already) {
+  if (ctx->cache_limit == 0) return false;
+  const size_t bytes = floats * sizeof(float);
+  if (bytes > ctx->cache_limit) return false;
+  if (bytes <= already) return true;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  return bytes - already + ((size_t)4 << 30) <= free_b;  // keep 4 GiB headroom
 }
 
 static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const float* guide,
                      ChanSpec c0, ChanSpec c1, const float* taps, double bw, bool use_hat,
-                     float* partial) {
+                     float* partial, int mode = MODE_RECOMPUTE, float* kcache = nullptr) {
   if (w.ntr <= 0) return PNP_OK;
   SweepArgs a;
   memset(&a, 0, sizeof(a));
@@ -317,6 +333,10 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   a.tiles_x = g.tiles_x;
   a.part_off = w.part_off;
   a.part_ntr = w.part_ntr;
+  a.kcache = kcache;
+  a.kc_ld = g.tiles_x * kTW;
+  a.kc_img = (long long)w.ntr * g.TH * a.kc_ld;
+  a.kc_plane = a.kc_img * g.B;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
   for (int i = 0; i < g.P; ++i) {
@@ -324,9 +344,17 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
     a.taps_v[i] = (float)(scale * (double)taps[i]);
   }
   dim3 grid(w.ntr * g.tiles_x, g.NG, g.B);
-  ProfScope prof(ctx, PROF_SWEEP);
-  cudaError_t e = C == 1 ? launch_sweep_c<1>(a, g, grid, ctx->stream)
-                         : launch_sweep_c<2>(a, g, grid, ctx->stream);
+  ProfScope prof(ctx, mode == MODE_CACHED ? PROF_SWEEP_CACHED : PROF_SWEEP);
+  cudaError_t e = cudaErrorInvalidValue;
+  if (mode != MODE_RECOMPUTE && !kcache) return fail(PNP_EINVAL, "k cache missing");
+  if (C == 1) {
+    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<1, MODE_RECOMPUTE>(a, g, grid, ctx->stream);
+    else if (mode == MODE_STORE) e = launch_sweep_cm<1, MODE_STORE>(a, g, grid, ctx->stream);
+    else e = launch_sweep_cm<1, MODE_CACHED>(a, g, grid, ctx->stream);
+  } else {
+    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<2, MODE_RECOMPUTE>(a, g, grid, ctx->stream);
+    else if (mode == MODE_CACHED) e = launch_sweep_cm<2, MODE_CACHED>(a, g, grid, ctx->stream);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "dsg_sweep_kernel");
   return PNP_OK;
 }
@@ -391,11 +419,11 @@ static int validate_taps(const float* taps, int P) {
 
 // sweep A + fixup: g -> rs (guide-only; shared by adaptive and freeze)
 static int mass_and_rs(pnp_ctx* ctx, const Geom& g, const float* guide, const float* taps,
-                       double bw, float* rs) {
+                       double bw, float* rs, float* kcache = nullptr) {
   const Window w = full_window(g);
   float* part = ctx->partial.as<float>();
   int rc = run_sweep(ctx, g, w, 1, guide, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
-                     taps, bw, true, part);
+                     taps, bw, true, part, kcache ? MODE_STORE : MODE_RECOMPUTE, kcache);
   if (rc) return rc;
   FixIO io{};
   io.rs = rs;
@@ -435,6 +463,7 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   ctx->mbits.release();
   ctx->stats.release();
   ctx->flags.release();
+  ctx->kcache.release();
   for (auto& kv : ctx->tables) kv.second.release();
   for (auto& sl : ctx->slots) {
     cudaEventDestroy(sl.a);
@@ -455,6 +484,15 @@ int pnp_ctx_synchronize(pnp_ctx* ctx) {
   PNP_CUDA(cudaStreamSynchronize(ctx->stream));
   return PNP_OK;
 }
+
+int pnp_ctx_set_cache_limit(pnp_ctx* ctx, int64_t bytes) {
+  if (!ctx) return fail(PNP_EINVAL, "ctx is null");
+  ctx->cache_limit = bytes < 0 ? (size_t)-1 : (size_t)bytes;
+  if (ctx->cache_limit == 0) ctx->kcache.release();
+  return PNP_OK;
+}
+
+int pnp_frozen_cached(const pnp_frozen* fz) { return fz && fz->kcache ? 1 : 0; }
 
 int pnp_ctx_profile(pnp_ctx* ctx, int enable) {
   if (!ctx) return fail(PNP_EINVAL, "ctx is null");
@@ -513,9 +551,15 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   float* d = d_out ? d_out : ctx->d.as<float>();
   float* part = ctx->partial.as<float>();
   const Window w = full_window(g);
-  if ((rc = mass_and_rs(ctx, g, guide, taps, bandwidth, rs))) return rc;
+  float* kc = nullptr;
+  const size_t kcf = kcache_floats(g, g.tiles_y);
+  if (kcache_fits(ctx, kcf, ctx->kcache.bytes)) {
+    if ((rc = ctx->kcache.ensure(kcf * sizeof(float)))) return rc;
+    kc = ctx->kcache.as<float>();
+  }
+  if ((rc = mass_and_rs(ctx, g, guide, taps, bandwidth, rs, kc))) return rc;
   if ((rc = run_sweep(ctx, g, w, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps,
-                      bandwidth, true, part)))
+                      bandwidth, true, part, kc ? MODE_CACHED : MODE_RECOMPUTE, kc)))
     return rc;
   PNP_CUDA(cudaMemsetAsync(ctx->mbits.ptr, 0, batch * sizeof(unsigned), ctx->stream));
   FixIO io{};
@@ -562,11 +606,20 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   e = cudaMemcpyAsync(fz->guide, guide, n * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemcpyAsync(guide)"));
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return bail(rc);
-  if ((rc = mass_and_rs(ctx, g, fz->guide, taps, bandwidth, fz->rs))) return bail(rc);
+  const size_t kcf = kcache_floats(g, g.tiles_y);
+  if (kcache_fits(ctx, kcf, 0)) {
+    e = cudaMalloc(&fz->kcache, kcf * sizeof(float));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fz->kcache = nullptr;  // not fatal: recompute instead
+    }
+  }
+  if ((rc = mass_and_rs(ctx, g, fz->guide, taps, bandwidth, fz->rs, fz->kcache))) return bail(rc);
   const Window w = full_window(g);
   float* part = ctx->partial.as<float>();
   if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, nullptr},
-                      ChanSpec{nullptr, nullptr}, taps, bandwidth, true, part)))
+                      ChanSpec{nullptr, nullptr}, taps, bandwidth, true, part,
+                      fz->kcache ? MODE_CACHED : MODE_RECOMPUTE, fz->kcache)))
     return bail(rc);
   e = cudaMemsetAsync(ctx->mbits.ptr, 0, batch * sizeof(unsigned), ctx->stream);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemsetAsync"));
@@ -594,7 +647,8 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
   const Window w = full_window(g);
   float* part = ctx->partial.as<float>();
   if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, x}, ChanSpec{nullptr, nullptr},
-                      fz->taps, fz->bw, true, part)))
+                      fz->taps, fz->bw, true, part, fz->kcache ? MODE_CACHED : MODE_RECOMPUTE,
+                      fz->kcache)))
     return rc;
   FixIO io{};
   io.rs = fz->rs;
@@ -612,6 +666,7 @@ int pnp_frozen_destroy(pnp_frozen* fz) {
   if (fz->rs) cudaFree(fz->rs);
   if (fz->d) cudaFree(fz->d);
   if (fz->mv) cudaFree(fz->mv);
+  if (fz->kcache) cudaFree(fz->kcache);
   delete fz;
   return PNP_OK;
 }

@@ -41,7 +41,14 @@ struct DevBuf {
 }  // namespace pnp
 
 namespace pnp {
-enum ProfCat { PROF_SWEEP = 0, PROF_FIXUP = 1, PROF_FORWARD = 2, PROF_ADMM = 3, PROF_NCAT = 4 };
+enum ProfCat {
+  PROF_SWEEP = 0,         // fused recompute sweep (incl. k-cache store)
+  PROF_FIXUP = 1,
+  PROF_FORWARD = 2,
+  PROF_ADMM = 3,
+  PROF_SWEEP_CACHED = 4,  // HBM-streaming sweep over the k cache
+  PROF_NCAT = 5
+};
 struct ProfSlot {
   cudaEvent_t a = nullptr, b = nullptr;
   int cat = 0;
@@ -52,6 +59,8 @@ struct pnp_ctx {
   int device = 0;
   cudaStream_t stream = 0;
   pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
+  pnp::DevBuf kcache;              // pair weights of the last adaptive denoise
+  size_t cache_limit = (size_t)-1;  // bytes; 0 disables the k cache
   // chunk tables keyed by (R, NG): device chunks (hat, no-hat) + NG+1 ints
   std::map<std::pair<int, int>, pnp::DevBuf> tables;
   // optional per-launch CUDA-event timing (pnp_ctx_profile)
@@ -92,4 +101,5 @@ struct pnp_frozen {
   float* rs = nullptr;     // B*H*W
   float* d = nullptr;      // B*H*W
   float* mv = nullptr;     // B floats: m; then B floats: 1/m
+  float* kcache = nullptr; // pair weights (null: recompute on apply)
 };

@@ -6,45 +6,65 @@
 
 namespace pnp {
 
-template <int P, int RB, int C>
+template <int P, int RB, int C, int MODE>
 cudaError_t launch_sweep(const SweepArgs& a, dim3 grid, cudaStream_t st) {
-  constexpr size_t smem = (size_t)Cfg<P, RB, C>::TOTAL * sizeof(float);
+  constexpr size_t smem = (size_t)Cfg<P, RB, C, MODE>::TOTAL * sizeof(float);
   static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(dsg_sweep_kernel<P, RB, C>,
+    cudaError_t e = cudaFuncSetAttribute(dsg_sweep_kernel<P, RB, C, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dsg_sweep_kernel<P, RB, C><<<grid, kThreads, smem, st>>>(a);
+  dsg_sweep_kernel<P, RB, C, MODE><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int P, int RB, int C>
-constexpr size_t sweep_smem_bytes() {
-  return (size_t)Cfg<P, RB, C>::TOTAL * sizeof(float);
-}
 
-#define PNP_INSTANTIATE_P(P)                                                               \
-  template cudaError_t launch_sweep<P, 5, 1>(const SweepArgs&, dim3, cudaStream_t);       \
-  template cudaError_t launch_sweep<P, 5, 2>(const SweepArgs&, dim3, cudaStream_t);       \
-  template cudaError_t launch_sweep<P, 10, 1>(const SweepArgs&, dim3, cudaStream_t);      \
-  template cudaError_t launch_sweep<P, 10, 2>(const SweepArgs&, dim3, cudaStream_t);      \
-  template cudaError_t launch_sweep<P, 16, 1>(const SweepArgs&, dim3, cudaStream_t);      \
-  template cudaError_t launch_sweep<P, 16, 2>(const SweepArgs&, dim3, cudaStream_t);      \
-  template cudaError_t launch_sweep<P, 32, 1>(const SweepArgs&, dim3, cudaStream_t);      \
-  template cudaError_t launch_sweep<P, 32, 2>(const SweepArgs&, dim3, cudaStream_t);
+#define PNP_INSTANTIATE_P(P) \
+  template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, dim3, cudaStream_t);
 
-#define PNP_DECLARE_P(P)                                                                     \
-  extern template cudaError_t launch_sweep<P, 5, 1>(const SweepArgs&, dim3, cudaStream_t);  \
-  extern template cudaError_t launch_sweep<P, 5, 2>(const SweepArgs&, dim3, cudaStream_t);  \
-  extern template cudaError_t launch_sweep<P, 10, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 2>(const SweepArgs&, dim3, cudaStream_t);
+#define PNP_DECLARE_P(P) \
+  extern template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, dim3, cudaStream_t);
 
 PNP_DECLARE_P(1)
 PNP_DECLARE_P(3)

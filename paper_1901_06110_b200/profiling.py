@@ -9,7 +9,7 @@ import torch
 
 from . import _lib as L
 
-CATEGORIES = ("sweep", "fixup", "forward", "admm")
+CATEGORIES = ("sweep", "fixup", "forward", "admm", "sweep_cached")
 
 
 def enable(flag: bool = True, device: int | None = None) -> None:
@@ -20,10 +20,16 @@ def enable(flag: bool = True, device: int | None = None) -> None:
 def read(device: int | None = None) -> dict:
     """{category: (device ms, launches)} since the last read (syncs the stream)."""
     dev = torch.cuda.current_device() if device is None else device
-    ms = (C.c_double * 4)()
-    n = (C.c_int * 4)()
+    ms = (C.c_double * 5)()
+    n = (C.c_int * 5)()
     L.call("pnp_ctx_profile_read", L.context(dev), ms, n)
     return {c: (float(ms[i]), int(n[i])) for i, c in enumerate(CATEGORIES)}
+
+
+def set_cache_limit(nbytes: int | None, device: int | None = None) -> None:
+    """k-cache budget in bytes (None: unlimited, 0: disabled)."""
+    dev = torch.cuda.current_device() if device is None else device
+    L.call("pnp_ctx_set_cache_limit", L.context(dev), -1 if nbytes is None else int(nbytes))
 
 
 def peak_rates(device: int | None = None) -> tuple[float, float]:

@@ -161,3 +161,25 @@ def test_nlm_vs_oracle(pnp, golden_extra, rng):
     p = pnp.PatchParams(5, 4, 0.15, 1.2)
     ref = oracle.nlm_denoise(img, 5, 4, 0.15, patch_sigma=1.2)
     assert np.abs(pnp.nlm_denoise(img, p) - ref).max() <= TOL
+
+
+def test_k_cache_is_bitwise_neutral(pnp, rng):
+    """k-cache (stored pair weights) vs recompute: identical bits everywhere."""
+    from paper_1901_06110_b200 import profiling
+    p = pnp.PatchParams(7, 10, 0.15, 2.0)
+    x = torch.tensor(rng.random((2, 130, 200)), dtype=torch.float32, device="cuda")
+    g = torch.tensor(rng.random((2, 130, 200)), dtype=torch.float32, device="cuda")
+    try:
+        profiling.set_cache_limit(None)
+        a = pnp.dsg_nlm_denoise(x, p, guide=g)
+        fa = pnp.freeze_guide(g, p)
+        assert pnp._lib.lib.pnp_frozen_cached(fa._h) == 1
+        ya = fa.apply(x)
+        profiling.set_cache_limit(0)
+        b = pnp.dsg_nlm_denoise(x, p, guide=g)
+        fb = pnp.freeze_guide(g, p)
+        assert pnp._lib.lib.pnp_frozen_cached(fb._h) == 0
+        yb = fb.apply(x)
+    finally:
+        profiling.set_cache_limit(None)
+    assert torch.equal(a, b) and torch.equal(ya, yb) and torch.equal(a, ya)
