@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--impl", default="pnp", choices=["pnp", "reference"])
     ap.add_argument("--size", type=int, default=H_C4, help="image side (default: config 4)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu / ADMM extras")
+    ap.add_argument("--no-cache", action="store_true",
+                    help="disable the k cache (recompute the patch filter in sweep B)")
     return ap.parse_args()
 
 
@@ -117,6 +119,13 @@ class ClockSampler:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def measured_hbm_gbs() -> float:
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
 
 
 def make_image_rows(n: int, r0: int, r1: int) -> np.ndarray:
@@ -207,6 +216,8 @@ def run_gpu(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if args.no_cache:
+        profiling.set_cache_limit(0, local_rank)
     n = args.size
     params = pnp.PatchParams.from_h(P_C4, R_C4, H_BW, SIGMA_P)
     units = n * n * (2 * R_C4 + 1) ** 2
@@ -256,30 +267,47 @@ def run_gpu(args, rank, world, local_rank):
     value = units / (ms_max * 1e-3) / 1e9
 
     launches = sum(v[1] for v in prof.values())
-    sweep_ms, sweep_n = prof["sweep"]
     peak_ffma, peak_ex2 = profiling.peak_rates(local_rank)
-    # per-rank algorithmic ops / per-rank sweep time (each rank sweeps its strip)
-    ops_rank = OPS_PER_UNIT_ADAPTIVE * units / world * args.steps
-    achieved = ops_rank / (sweep_ms * 1e-3) / 1e12 if sweep_ms > 0 else None
     nominal = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 1.965e9
-    roofline = {
-        "bound": "fp32", "kernel": "dsg_sweep_kernel",
-        "achieved": achieved, "peak": peak_ffma / 1e12, "unit": "Top/s",
-        "frac": (achieved / (peak_ffma / 1e12)) if achieved else None,
+    hbm_peak = measured_hbm_gbs()
+    units_rank = units / world * args.steps          # pixel-offsets swept by this rank
+    sweep_ms, sweep_n = prof["sweep"]
+    cached_ms, cached_n = prof["sweep_cached"]
+    # algorithmic FP32 ops per pixel-offset of the recompute sweeps:
+    # sweep A (mass) (F+5)*N+/(2R+1)^2, sweep B (F+9)*N+/(2R+1)^2 with F = 2P
+    half = ((2 * R_C4 + 1) ** 2 - 1) / 2 / (2 * R_C4 + 1) ** 2
+    ops_a, ops_b = (2 * P_C4 + 5) * half, (2 * P_C4 + 9) * half
+    ops_unit = ops_a + (ops_b if cached_n == 0 else 0.0)
+    kernels = []
+    if sweep_ms > 0:
+        ach = ops_unit * units_rank / (sweep_ms * 1e-3) / 1e12
+        kernels.append({
+            "kernel": "dsg_sweep_kernel (fused recompute" + (", k-cache store)" if cached_n else ")"),
+            "bound": "fp32", "achieved": ach, "peak": peak_ffma / 1e12, "unit": "Top/s",
+            "frac": ach / (peak_ffma / 1e12), "frac_of_nominal": ach / (nominal / 1e12),
+            "ops_per_pixel_offset": ops_unit, "ms_per_step": sweep_ms / args.steps,
+            "launches_per_step": sweep_n / args.steps,
+            "sfu_frac": (half * (1 if cached_n else 2)) * units_rank / (sweep_ms * 1e-3) / peak_ex2})
+    if cached_n:
+        # k cache read: one fp32 weight per half-window pair = 4*N+/(2R+1)^2 B per pixel-offset
+        bytes_unit = 4.0 * half
+        ach = bytes_unit * units_rank / (cached_ms * 1e-3) / 1e9
+        kernels.append({
+            "kernel": "dsg_sweep_kernel (k-cache stream, sweep B)", "bound": "hbm",
+            "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "bytes_per_pixel_offset": bytes_unit, "ms_per_step": cached_ms / args.steps,
+            "launches_per_step": cached_n / args.steps})
+    dom = max(kernels, key=lambda k: k["ms_per_step"]) if kernels else None
+    roofline = dict(dom) if dom else {}
+    roofline.update({
         "traffic": None,
-        "peak_source": "measured FFMA rate (pnp_peak_rates) on this GPU; "
-                       f"nominal 148x128x1965MHz = {nominal / 1e12:.2f} Top/s",
-        "frac_of_nominal": (achieved / (nominal / 1e12)) if achieved else None,
-        "ops_per_pixel_offset": OPS_PER_UNIT_ADAPTIVE,
-        "sweep_launches": sweep_n, "sweep_ms_per_step": sweep_ms / args.steps,
-        "sweep_share_of_step": (sweep_ms / args.steps) / ms if ms > 0 else None,
-        "sfu": {"mufu_per_pixel_offset": MUFU_PER_UNIT_ADAPTIVE,
-                "peak_ex2_per_s": peak_ex2,
-                "frac": (MUFU_PER_UNIT_ADAPTIVE * units / world * args.steps
-                         / (sweep_ms * 1e-3) / peak_ex2) if sweep_ms > 0 else None},
+        "peak_source": "fp32: FFMA rate measured by pnp_peak_rates on this GPU (nominal "
+                       f"148x128x1965MHz = {nominal / 1e12:.2f} Top/s); hbm: MEASURED_PEAKS.json",
+        "share_of_step": (dom["ms_per_step"] / ms) if dom else None,
+        "kernels": kernels,
+        "ex2_peak_per_s": peak_ex2,
         "traffic_note": "dram bytes per launch: see profiles/ (ncu --set full)",
-    }
-
+    })
     line = {
         "metric": METRIC, "value": value, "unit": "Gpixel*offset/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,

@@ -90,11 +90,12 @@ struct SweepArgs {
   int buf_r0, buf_rows;
   int tr0, tiles_x;
   int part_off, part_ntr;
-  // k cache: weight of pair (s, s+t) for half-window offset index t (chunk-major)
-  // at kcache[t*kc_plane + b*kc_img + (local tile row*TH + row)*kc_ld + col]
+  // k cache, tile-major: weight of pair (s, s+t), half-window offset index t
+  // (chunk-major), at kcache[b*kc_img + (tile*kc_nplanes + t)*TH*64 + row*64 + col]
+  // with (row, col) inside the tile -> every CTA streams contiguous 6.6 KB planes
   float* kcache;
-  long long kc_plane, kc_img;
-  int kc_ld;
+  long long kc_img;
+  int kc_nplanes;
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
 };
@@ -307,8 +308,9 @@ dsg_sweep_kernel(const SweepArgs a) {
         fw[c_][j] = 0.f;
       }
     float* kbase = CACHED || STORE
-                       ? a.kcache + (long long)ci * KY * a.kc_plane + (long long)b * a.kc_img +
-                             (long long)(tyl * TH + r0) * a.kc_ld + tx * kTW + c
+                       ? a.kcache + (long long)b * a.kc_img +
+                             ((long long)tile * a.kc_nplanes + (long long)ci * KY) * (TH * kTW) +
+                             r0 * kTW + c
                        : nullptr;
 #pragma unroll
     for (int k = 0; k < KY; ++k) {
@@ -316,7 +318,7 @@ dsg_sweep_kernel(const SweepArgs a) {
         float kk[N];
         if (CACHED) {
 #pragma unroll
-          for (int r = 0; r < N; ++r) kk[r] = __ldcs(kbase + k * a.kc_plane + (long long)r * a.kc_ld);
+          for (int r = 0; r < N; ++r) kk[r] = __ldcs(kbase + (k * TH + r) * kTW);
         } else {
           const float L = chk.L[k];
           float hcol[N + 2 * p];
@@ -328,7 +330,7 @@ dsg_sweep_kernel(const SweepArgs a) {
 #pragma unroll
             for (int aa = 0; aa < P; ++aa) v = __fmaf_rn(a.taps_v[aa], hcol[r + aa], v);
             kk[r] = ex2_approx(v);
-            if (STORE) __stcs(kbase + k * a.kc_plane + (long long)r * a.kc_ld, kk[r]);
+            if (STORE) __stcs(kbase + (k * TH + r) * kTW, kk[r]);
           }
         }
 #pragma unroll

@@ -28,7 +28,7 @@ def test_layout_partitions_tile_rows(H, W, R, P, N):
     for lay in lays:
         b0, b1 = lay.window
         y0, y1 = lay.rows
-        assert b0 == max(0, y0 - p) and b1 == min(H, y1 + R + max(p, 2))
+        assert b0 == max(0, y0 - p) and b1 == min(H, y1 + R + max(p, 4))
         first, off, nslot = lay.part
         assert first == max(0, lay.tile_rows[0] - lay.dti)
         assert nslot - off == lay.tile_rows[1] - lay.tile_rows[0]
