@@ -312,13 +312,22 @@ dsg_sweep_kernel(const SweepArgs a) {
                              ((long long)tile * a.kc_nplanes + (long long)ci * KY) * (TH * kTW) +
                              r0 * kTW + c
                        : nullptr;
+    // CACHED: issue the whole chunk's loads first (planes k >= kc exist in the
+    // allocation; their values are ignored) so KY*N loads are in flight.
+    float kcl[CACHED ? KY : 1][N];
+    if (CACHED) {
+#pragma unroll
+      for (int k = 0; k < KY; ++k)
+#pragma unroll
+        for (int r = 0; r < N; ++r) kcl[k][r] = __ldcs(kbase + (k * TH + r) * kTW);
+    }
 #pragma unroll
     for (int k = 0; k < KY; ++k) {
       if (k == 0 || k < kc) {
         float kk[N];
         if (CACHED) {
 #pragma unroll
-          for (int r = 0; r < N; ++r) kk[r] = __ldcs(kbase + (k * TH + r) * kTW);
+          for (int r = 0; r < N; ++r) kk[r] = kcl[CACHED ? k : 0][r];
         } else {
           const float L = chk.L[k];
           float hcol[N + 2 * p];
