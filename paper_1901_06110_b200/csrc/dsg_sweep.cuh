@@ -312,14 +312,23 @@ dsg_sweep_kernel(const SweepArgs a) {
                              ((long long)tile * a.kc_nplanes + (long long)ci * KY) * (TH * kTW) +
                              r0 * kTW + c
                        : nullptr;
-    // CACHED: issue the whole chunk's loads first (planes k >= kc exist in the
-    // allocation; their values are ignored) so KY*N loads are in flight.
+    // CACHED: issue the whole chunk's loads first (predicated, not branched,
+    // so all KY*N loads of valid offsets are in flight together).
     float kcl[CACHED ? KY : 1][N];
     if (CACHED) {
 #pragma unroll
       for (int k = 0; k < KY; ++k)
 #pragma unroll
-        for (int r = 0; r < N; ++r) kcl[k][r] = __ldcs(kbase + (k * TH + r) * kTW);
+        for (int r = 0; r < N; ++r) {
+          const float* src = kbase + (k * TH + r) * kTW;
+          float v = 0.f;
+          asm volatile(
+              "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %2, %3;\n\t"
+              "@q ld.global.cs.f32 %0, [%1];\n\t}"
+              : "+f"(v)
+              : "l"(src), "r"(k), "r"(kc));
+          kcl[k][r] = v;
+        }
     }
 #pragma unroll
     for (int k = 0; k < KY; ++k) {
