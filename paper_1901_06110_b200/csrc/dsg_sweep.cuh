@@ -67,10 +67,35 @@ struct ChanSpec {
 };
 
 // One chunk of the half-window offset table: KY offsets (dx, dy0 + k),
-// k < kc, with their log2(hat) (0 for plain NLM) precomputed on the host.
+// k < kc, with their log2(hat) (0 for plain NLM; -inf for k >= kc)
+// precomputed on the host.
 struct Chunk {
   int dx, dy0, kc, pad;
   float L[4];
+};
+
+// Chunks of the half window at R = RB (the largest R of a bucket):
+// dx > 0 has RB+1 dy values (0..RB), dx <= 0 has RB (1..RB).
+__host__ __device__ constexpr int max_chunks(int RB) {
+  return RB * ((RB + 1 + kKY - 1) / kKY) + (RB + 1) * ((RB + kKY - 1) / kKY);
+}
+constexpr int kMaxGroups = 64;
+
+// The offset table travels in the kernel parameters (constant bank): every
+// chunk read is a uniform constant-cache hit, never a global-memory round trip
+// at the top of the chunk loop.
+template <int RB>
+struct ChunkTab {
+  Chunk c[max_chunks(RB)];
+  int grp[kMaxGroups + 1];  // NG+1 chunk starts
+};
+
+// Host view of a table (built once per (R, NG) and kept in the context).
+struct HostTab {
+  const Chunk* ch;
+  int nch;
+  const int* grp;
+  int ng;
 };
 
 // Per-pixel planes are windows of the global image: rows [buf_r0, buf_r0 +
@@ -84,8 +109,6 @@ struct SweepArgs {
   const float* guide;  // [B][buf_rows][W]
   ChanSpec ch[2];
   float* partial;
-  const Chunk* chunks;
-  const int* grp;      // NG+1 chunk starts
   int Hg, W, R;
   int buf_r0, buf_rows;
   int tr0, tiles_x;
@@ -115,12 +138,12 @@ struct Cfg {
   static constexpr int SEGW = SEG + 2 * p;
   static constexpr int KY = kKY;
   static constexpr int WIN = N + KY - 1;
-  static constexpr int GC = kTW + 2 * (RB + p), GS = GC | 1, GR = 32 + RB;
-  static constexpr int HS = kTW + 1;
-  static constexpr int YC = kTW + 2 * RB, YR = TH + RB + KY, AR = TH + RB + KY;
+  static constexpr int GC = kTW + 2 * (RB + p), GS = GC | 1, GR = 33 + RB;  // partner rows <= 31 + R + 1
+  static constexpr int HS = kTW + 1;  // float2 units (odd: conflict-free STS.64 by row)
+  static constexpr int YC = kTW + 2 * RB, YR = TH + RB + KY - 1, AR = YR;  // rows < r0 + R + WIN
   static constexpr bool CACHED = MODE == MODE_CACHED;  // no guide tile, no H maps
-  static constexpr int OFF_H = CACHED ? 0 : GR * GS;
-  static constexpr int OFF_Y = CACHED ? 0 : OFF_H + KY * 32 * HS;
+  static constexpr int OFF_H = CACHED ? 0 : (GR * GS + 3) & ~3;  // 16 B aligned
+  static constexpr int OFF_Y = CACHED ? 0 : OFF_H + KY * 32 * HS;  // KY/2 float2 maps
   static constexpr int OFF_A = OFF_Y + C * YR * YC;
   static constexpr int TOTAL = OFF_A + C * AR * YC;  // floats
 };
@@ -141,13 +164,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 template <int P, int RB, int C, int MODE>
 __global__ void __launch_bounds__(kThreads)
-dsg_sweep_kernel(const SweepArgs a) {
+dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   using K = Cfg<P, RB, C, MODE>;
   constexpr bool CACHED = K::CACHED, STORE = MODE == MODE_STORE;
   constexpr int p = K::p, TH = K::TH, N = K::N, SEG = K::SEG, SEGW = K::SEGW, KY = K::KY;
   constexpr int WIN = K::WIN, GS = K::GS, GC = K::GC, GR = K::GR, HS = K::HS;
   constexpr int YC = K::YC, YR = K::YR, AR = K::AR;
   static_assert(kTW / SEG == kThreads / 32, "one phase-1 segment per warp");
+  static_assert(KY % 2 == 0, "offsets are processed in packed pairs");
   extern __shared__ float smem[];
   float* Gs = smem;
   float* Hs = smem + K::OFF_H;
@@ -228,11 +252,13 @@ dsg_sweep_kernel(const SweepArgs a) {
   const int g = tid / kTW;           // phase-2 row group
   const int r0 = g * N;
 
-  float gown[SEGW];  // own guide row segment, resident for the whole kernel
+  // own guide row segment (negated), resident for the whole kernel: it is the
+  // broadcast operand of every packed subtraction in phase 1
+  float ngown[SEGW];
   if (!CACHED) {
     const float* grow = Gs + lane * GS + c0 + RB;
 #pragma unroll
-    for (int x = 0; x < SEGW; ++x) gown[x] = grow[x];
+    for (int x = 0; x < SEGW; ++x) ngown[x] = -grow[x];
   }
   float yown[C][N], near[C][N];
 #pragma unroll
@@ -243,16 +269,19 @@ dsg_sweep_kernel(const SweepArgs a) {
       near[c_][r] = (blockIdx.y == 0) ? yown[c_][r] : 0.f;  // self pair, k = hat = 1
     }
 
-  const float* hcol0 = Hs + r0 * HS + c;
-  float* hrow0 = Hs + lane * HS + c0;
+  const float2* hcol0 = reinterpret_cast<const float2*>(Hs) + r0 * HS + c;
+  float2* hrow0 = reinterpret_cast<float2*>(Hs) + lane * HS + c0;
 
-  // Far windows of the two row groups overlap in KY-1 rows (group 1's first
-  // rows = group 0's last).  Group 0 flushes its whole window and group 1 its
-  // private rows before the chunk's closing barrier; group 1's shared rows go
-  // after it (top of the next chunk, before the phase-1 barrier).  Every SMEM
-  // cell sees one writer between barriers and a fixed order (group 0, then
-  // group 1), and both groups do the same flush work per chunk.
-  float fw[C][WIN];
+  // Far accumulators of an offset pair (k, k+1) = (2kp, 2kp+1) live in packed
+  // registers: pf[i].x collects even-k terms of window row i, pf[i].y odd-k
+  // terms of window row i+1, so one FFMA2 credits both offsets.  Window row j
+  // = pf[j].x + pf[j-1].y at flush.  The two row groups' windows overlap in
+  // KY-1 rows (group 1's first = group 0's last): group 0 flushes its whole
+  // window and group 1 its private rows before the chunk's closing barrier;
+  // group 1's shared rows go after it (top of the next chunk, before the
+  // phase-1 barrier).  Every SMEM cell sees one writer between barriers and a
+  // fixed order (group 0, then group 1) -> bit-reproducible.
+  float2 pf[C][WIN - 1];
   float* pend = nullptr;  // group 1's pending (shared-row) flush target
   auto flush = [&](float* base, int j0, int j1) {
 #pragma unroll
@@ -261,35 +290,54 @@ dsg_sweep_kernel(const SweepArgs a) {
       for (int j = 0; j < WIN; ++j) {
         if (j < j0 || j >= j1) continue;  // compile-time after unrolling
         // window rows past the chunk's last offset hold +0: adding them is exact
+        float v;
+        if (j == 0) v = pf[c_][0].x;
+        else if (j == WIN - 1) v = pf[c_][WIN - 2].y;
+        else v = __fadd_rn(pf[c_][j].x, pf[c_][j - 1].y);
         float* pA = base + c_ * AR * YC + j * YC;
-        *pA = __fadd_rn(*pA, fw[c_][j]);
+        *pA = __fadd_rn(*pA, v);
       }
   };
+  // the pending flush reads pf after the next chunk cleared it: keep a copy of
+  // the KY-1 shared rows (group 1 only)
+  float pendv[C][KY - 1];
 
-  const int cbeg = a.grp[blockIdx.y], cend = a.grp[blockIdx.y + 1];
+  const int cbeg = tab.grp[blockIdx.y], cend = tab.grp[blockIdx.y + 1];
   for (int ci = cbeg; ci < cend; ++ci) {
-    const Chunk chk = a.chunks[ci];
+    const Chunk& chk = tab.c[ci];
     const int dx = chk.dx, dy0 = chk.dy0, kc = chk.kc;
-    if (g == 1 && pend) flush(pend, 0, KY - 1);
+    if (g == 1 && pend) {
+#pragma unroll
+      for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+        for (int j = 0; j < KY - 1; ++j) {
+          float* pA = pend + c_ * AR * YC + j * YC;
+          *pA = __fadd_rn(*pA, pendv[c_][j]);
+        }
+    }
 
     // ---------------- phase 1: squared differences + horizontal filter ----
+    // packed over the offset pair: (D_k, D_k+1) = (G_partner - G_own)^2
     if (!CACHED) {
       const float* prow0 = Gs + (lane + dy0) * GS + c0 + RB + dx;
 #pragma unroll
-      for (int k = 0; k < KY; ++k) {
-        if (k == 0 || k < kc) {
-          float dd[SEGW];
+      for (int kp = 0; kp < KY / 2; ++kp) {
+        if (kp == 0 || 2 * kp < kc) {
+          const float* pa = prow0 + 2 * kp * GS;
+          float2 dd[SEGW];
 #pragma unroll
           for (int x = 0; x < SEGW; ++x) {
-            const float t = __fsub_rn(gown[x], prow0[k * GS + x]);
-            dd[x] = __fmul_rn(t, t);
+            const float2 t = __fadd2_rn(make_float2(pa[x], pa[GS + x]),
+                                        make_float2(ngown[x], ngown[x]));
+            dd[x] = __fmul2_rn(t, t);
           }
 #pragma unroll
           for (int i = 0; i < SEG; ++i) {
-            float h = __fmul_rn(a.taps_h[0], dd[i]);
+            float2 h = __fmul2_rn(make_float2(a.taps_h[0], a.taps_h[0]), dd[i]);
 #pragma unroll
-            for (int bb = 1; bb < P; ++bb) h = __fmaf_rn(a.taps_h[bb], dd[i + bb], h);
-            hrow0[k * 32 * HS + i] = h;
+            for (int bb = 1; bb < P; ++bb)
+              h = __ffma2_rn(make_float2(a.taps_h[bb], a.taps_h[bb]), dd[i + bb], h);
+            hrow0[kp * 32 * HS + i] = h;
           }
         }
       }
@@ -301,12 +349,12 @@ dsg_sweep_kernel(const SweepArgs a) {
     float* abase = As + (r0 + dy0) * YC + c + dx + RB;
     float yw[C][WIN];
 #pragma unroll
-    for (int c_ = 0; c_ < C; ++c_)
+    for (int c_ = 0; c_ < C; ++c_) {
 #pragma unroll
-      for (int j = 0; j < WIN; ++j) {
-        yw[c_][j] = ybase[c_ * YR * YC + j * YC];
-        fw[c_][j] = 0.f;
-      }
+      for (int j = 0; j < WIN; ++j) yw[c_][j] = ybase[c_ * YR * YC + j * YC];
+#pragma unroll
+      for (int j = 0; j < WIN - 1; ++j) pf[c_][j] = make_float2(0.f, 0.f);
+    }
     float* kbase = CACHED || STORE
                        ? a.kcache + (long long)b * a.kc_img +
                              ((long long)tile * a.kc_nplanes + (long long)ci * KY) * (TH * kTW) +
@@ -331,32 +379,40 @@ dsg_sweep_kernel(const SweepArgs a) {
         }
     }
 #pragma unroll
-    for (int k = 0; k < KY; ++k) {
-      if (k == 0 || k < kc) {
-        float kk[N];
+    for (int kp = 0; kp < KY / 2; ++kp) {
+      if (kp == 0 || 2 * kp < kc) {
+        float2 kk[N];
         if (CACHED) {
 #pragma unroll
-          for (int r = 0; r < N; ++r) kk[r] = kcl[CACHED ? k : 0][r];
+          for (int r = 0; r < N; ++r)
+            kk[r] = make_float2(kcl[CACHED ? 2 * kp : 0][r], kcl[CACHED ? 2 * kp + 1 : 0][r]);
         } else {
-          const float L = chk.L[k];
-          float hcol[N + 2 * p];
+          // invalid odd slot: L = -inf on the host -> its weight is exactly +0
+          const float2 L = make_float2(chk.L[2 * kp], chk.L[2 * kp + 1]);
+          float2 hcol[N + 2 * p];
 #pragma unroll
-          for (int i = 0; i < N + 2 * p; ++i) hcol[i] = hcol0[(k * 32 + i) * HS];
+          for (int i = 0; i < N + 2 * p; ++i) hcol[i] = hcol0[(kp * 32 + i) * HS];
 #pragma unroll
           for (int r = 0; r < N; ++r) {
-            float v = L;
+            float2 v = L;
 #pragma unroll
-            for (int aa = 0; aa < P; ++aa) v = __fmaf_rn(a.taps_v[aa], hcol[r + aa], v);
-            kk[r] = ex2_approx(v);
-            if (STORE) __stcs(kbase + (k * TH + r) * kTW, kk[r]);
+            for (int aa = 0; aa < P; ++aa)
+              v = __ffma2_rn(make_float2(a.taps_v[aa], a.taps_v[aa]), hcol[r + aa], v);
+            kk[r] = make_float2(ex2_approx(v.x), ex2_approx(v.y));
+            if (STORE) {
+              __stcs(kbase + (2 * kp * TH + r) * kTW, kk[r].x);
+              if (2 * kp + 1 < kc) __stcs(kbase + ((2 * kp + 1) * TH + r) * kTW, kk[r].y);
+            }
           }
         }
 #pragma unroll
         for (int r = 0; r < N; ++r)
 #pragma unroll
           for (int c_ = 0; c_ < C; ++c_) {
-            near[c_][r] = __fmaf_rn(kk[r], yw[c_][r + k], near[c_][r]);
-            fw[c_][r + k] = __fmaf_rn(kk[r], yown[c_][r], fw[c_][r + k]);
+            near[c_][r] = __fmaf_rn(kk[r].x, yw[c_][r + 2 * kp], near[c_][r]);
+            near[c_][r] = __fmaf_rn(kk[r].y, yw[c_][r + 2 * kp + 1], near[c_][r]);
+            pf[c_][r + 2 * kp] =
+                __ffma2_rn(kk[r], make_float2(yown[c_][r], yown[c_][r]), pf[c_][r + 2 * kp]);
           }
       }
     }
@@ -364,11 +420,24 @@ dsg_sweep_kernel(const SweepArgs a) {
       flush(abase, 0, WIN);
     } else {
       flush(abase, KY - 1, WIN);
+#pragma unroll
+      for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+        for (int j = 0; j < KY - 1; ++j)
+          pendv[c_][j] = j == 0 ? pf[c_][0].x : __fadd_rn(pf[c_][j].x, pf[c_][j - 1].y);
       pend = abase;
     }
     __syncthreads();
   }
-  if (g == 1 && pend) flush(pend, 0, KY - 1);
+  if (g == 1 && pend) {
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+      for (int j = 0; j < KY - 1; ++j) {
+        float* pA = pend + c_ * AR * YC + j * YC;
+        *pA = __fadd_rn(*pA, pendv[c_][j]);
+      }
+  }
   __syncthreads();
 
   // ---- own pixels: near + far; then emit tile + band block ----

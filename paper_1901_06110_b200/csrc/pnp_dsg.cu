@@ -152,9 +152,9 @@ __global__ void dsg_alpha_kernel(const unsigned* mbits, float* mv, int B) {
 // batch, so single-GPU and sharded runs sum in the same order.
 struct Geom {
   int B, Hg, W, R, P, TH, tiles_x, tiles_y, nchunks, NG;
-  const Chunk* chunks;        // hat-tapered table (DSG)
-  const Chunk* chunks_nohat;  // same offsets, L = 0 (plain NLM)
-  const int* grp;
+  const Chunk* chunks;        // hat-tapered table (DSG), host
+  const Chunk* chunks_nohat;  // same offsets, L = 0 (plain NLM), host
+  const int* grp;             // NG+1 group starts, host
 };
 
 // A window of the global image handled by one call.
@@ -185,7 +185,8 @@ static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
         const int dy = dy0 + k;
         const double s = R + 1.0;
         const double hy = 1.0 - fabs((double)dy) / s, hx = 1.0 - fabs((double)dx) / s;
-        ch.L[k] = (hat && k < ch.kc) ? (float)(log2(hy) + log2(hx)) : 0.f;
+        // slots past kc: -inf -> ex2 gives an exact +0 weight (packed pairs)
+        ch.L[k] = k >= ch.kc ? -INFINITY : (hat ? (float)(log2(hy) + log2(hx)) : 0.f);
       }
       out.push_back(ch);
     }
@@ -244,22 +245,21 @@ static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, Geom& g) 
   g.NG = pick_groups(g.tiles_x * g.tiles_y, g.nchunks);
   auto key = std::make_pair(R, g.NG);
   auto it = ctx->tables.find(key);
-  const size_t cb = ch.size() * sizeof(Chunk);
   if (it == ctx->tables.end()) {
-    std::vector<int> grp(g.NG + 1);
-    for (int i = 0; i <= g.NG; ++i) grp[i] = (int)((long long)i * g.nchunks / g.NG);
-    DevBuf buf;
-    int rc = buf.ensure(2 * cb + grp.size() * sizeof(int));
-    if (rc) return rc;
-    PNP_CUDA(cudaMemcpy(buf.ptr, ch.data(), cb, cudaMemcpyHostToDevice));
-    PNP_CUDA(cudaMemcpy(buf.as<char>() + cb, ch0.data(), cb, cudaMemcpyHostToDevice));
-    PNP_CUDA(cudaMemcpy(buf.as<char>() + 2 * cb, grp.data(), grp.size() * sizeof(int),
-                        cudaMemcpyHostToDevice));
-    it = ctx->tables.emplace(key, buf).first;
+    if (g.NG > kMaxGroups) return fail(PNP_EINVAL, "too many offset groups");
+    pnp_ctx::Tables t;
+    const size_t cb = ch.size() * sizeof(Chunk);
+    t.hat.resize(cb);
+    t.nohat.resize(cb);
+    memcpy(t.hat.data(), ch.data(), cb);
+    memcpy(t.nohat.data(), ch0.data(), cb);
+    t.grp.resize(g.NG + 1);
+    for (int i = 0; i <= g.NG; ++i) t.grp[i] = (int)((long long)i * g.nchunks / g.NG);
+    it = ctx->tables.emplace(key, std::move(t)).first;
   }
-  g.chunks = it->second.as<Chunk>();
-  g.chunks_nohat = reinterpret_cast<const Chunk*>(it->second.as<char>() + cb);
-  g.grp = reinterpret_cast<const int*>(it->second.as<char>() + 2 * cb);
+  g.chunks = reinterpret_cast<const Chunk*>(it->second.hat.data());
+  g.chunks_nohat = reinterpret_cast<const Chunk*>(it->second.nohat.data());
+  g.grp = it->second.grp.data();
   return PNP_OK;
 }
 
@@ -272,27 +272,28 @@ static size_t partial_floats(const Geom& g, int ntr, int C) {
 }
 
 template <int RB, int C, int MODE>
-static cudaError_t launch_sweep_rc(const SweepArgs& a, int P, dim3 grid, cudaStream_t st) {
+static cudaError_t launch_sweep_rc(const SweepArgs& a, const HostTab& t, int P, dim3 grid, cudaStream_t st) {
   switch (P) {
-    case 1: return launch_sweep<1, RB, C, MODE>(a, grid, st);
-    case 3: return launch_sweep<3, RB, C, MODE>(a, grid, st);
-    case 5: return launch_sweep<5, RB, C, MODE>(a, grid, st);
-    case 7: return launch_sweep<7, RB, C, MODE>(a, grid, st);
-    case 9: return launch_sweep<9, RB, C, MODE>(a, grid, st);
-    case 11: return launch_sweep<11, RB, C, MODE>(a, grid, st);
-    case 13: return launch_sweep<13, RB, C, MODE>(a, grid, st);
-    case 15: return launch_sweep<15, RB, C, MODE>(a, grid, st);
+    case 1: return launch_sweep<1, RB, C, MODE>(a, t, grid, st);
+    case 3: return launch_sweep<3, RB, C, MODE>(a, t, grid, st);
+    case 5: return launch_sweep<5, RB, C, MODE>(a, t, grid, st);
+    case 7: return launch_sweep<7, RB, C, MODE>(a, t, grid, st);
+    case 9: return launch_sweep<9, RB, C, MODE>(a, t, grid, st);
+    case 11: return launch_sweep<11, RB, C, MODE>(a, t, grid, st);
+    case 13: return launch_sweep<13, RB, C, MODE>(a, t, grid, st);
+    case 15: return launch_sweep<15, RB, C, MODE>(a, t, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 
 template <int C, int MODE>
-static cudaError_t launch_sweep_cm(const SweepArgs& a, const Geom& g, dim3 grid, cudaStream_t st) {
+static cudaError_t launch_sweep_cm(const SweepArgs& a, const HostTab& t, const Geom& g, dim3 grid,
+                                   cudaStream_t st) {
   switch (r_bucket(g.R)) {
-    case 5: return launch_sweep_rc<5, C, MODE>(a, g.P, grid, st);
-    case 10: return launch_sweep_rc<10, C, MODE>(a, g.P, grid, st);
-    case 16: return launch_sweep_rc<16, C, MODE>(a, g.P, grid, st);
-    default: return launch_sweep_rc<32, C, MODE>(a, g.P, grid, st);
+    case 5: return launch_sweep_rc<5, C, MODE>(a, t, g.P, grid, st);
+    case 10: return launch_sweep_rc<10, C, MODE>(a, t, g.P, grid, st);
+    case 16: return launch_sweep_rc<16, C, MODE>(a, t, g.P, grid, st);
+    default: return launch_sweep_rc<32, C, MODE>(a, t, g.P, grid, st);
   }
 }
 
@@ -322,8 +323,7 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   a.ch[0] = c0;
   a.ch[1] = c1;
   a.partial = partial;
-  a.chunks = use_hat ? g.chunks : g.chunks_nohat;
-  a.grp = g.grp;
+  const HostTab tab{use_hat ? g.chunks : g.chunks_nohat, g.nchunks, g.grp, g.NG};
   a.Hg = g.Hg;
   a.W = g.W;
   a.R = g.R;
@@ -347,12 +347,12 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   cudaError_t e = cudaErrorInvalidValue;
   if (mode != MODE_RECOMPUTE && !kcache) return fail(PNP_EINVAL, "k cache missing");
   if (C == 1) {
-    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<1, MODE_RECOMPUTE>(a, g, grid, ctx->stream);
-    else if (mode == MODE_STORE) e = launch_sweep_cm<1, MODE_STORE>(a, g, grid, ctx->stream);
-    else e = launch_sweep_cm<1, MODE_CACHED>(a, g, grid, ctx->stream);
+    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<1, MODE_RECOMPUTE>(a, tab, g, grid, ctx->stream);
+    else if (mode == MODE_STORE) e = launch_sweep_cm<1, MODE_STORE>(a, tab, g, grid, ctx->stream);
+    else e = launch_sweep_cm<1, MODE_CACHED>(a, tab, g, grid, ctx->stream);
   } else {
-    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<2, MODE_RECOMPUTE>(a, g, grid, ctx->stream);
-    else if (mode == MODE_CACHED) e = launch_sweep_cm<2, MODE_CACHED>(a, g, grid, ctx->stream);
+    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<2, MODE_RECOMPUTE>(a, tab, g, grid, ctx->stream);
+    else if (mode == MODE_CACHED) e = launch_sweep_cm<2, MODE_CACHED>(a, tab, g, grid, ctx->stream);
   }
   if (e != cudaSuccess) return cuda_fail(e, "dsg_sweep_kernel");
   return PNP_OK;
@@ -463,7 +463,6 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   ctx->stats.release();
   ctx->flags.release();
   ctx->kcache.release();
-  for (auto& kv : ctx->tables) kv.second.release();
   for (auto& sl : ctx->slots) {
     cudaEventDestroy(sl.a);
     cudaEventDestroy(sl.b);

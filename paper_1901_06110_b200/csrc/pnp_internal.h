@@ -61,8 +61,13 @@ struct pnp_ctx {
   pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
   pnp::DevBuf kcache;              // pair weights of the last adaptive denoise
   size_t cache_limit = (size_t)-1;  // bytes; 0 disables the k cache
-  // chunk tables keyed by (R, NG): device chunks (hat, no-hat) + NG+1 ints
-  std::map<std::pair<int, int>, pnp::DevBuf> tables;
+  // offset tables keyed by (R, NG): host blobs of Chunk (hat, no-hat) + NG+1
+  // group starts; they reach the kernels through the launch parameters
+  struct Tables {
+    std::vector<char> hat, nohat;
+    std::vector<int> grp;
+  };
+  std::map<std::pair<int, int>, Tables> tables;
   // optional per-launch CUDA-event timing (pnp_ctx_profile)
   bool prof = false;
   std::vector<pnp::ProfSlot> slots;

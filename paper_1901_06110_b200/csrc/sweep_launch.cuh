@@ -2,12 +2,14 @@
 // side in pnp_sweep_p*.cu (compiled in parallel), dispatched in pnp_dsg.cu.
 #pragma once
 
+#include <cstring>
+
 #include "dsg_sweep.cuh"
 
 namespace pnp {
 
 template <int P, int RB, int C, int MODE>
-cudaError_t launch_sweep(const SweepArgs& a, dim3 grid, cudaStream_t st) {
+cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st) {
   constexpr size_t smem = (size_t)Cfg<P, RB, C, MODE>::TOTAL * sizeof(float);
   static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
   static bool attr_set = false;
@@ -17,54 +19,59 @@ cudaError_t launch_sweep(const SweepArgs& a, dim3 grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dsg_sweep_kernel<P, RB, C, MODE><<<grid, kThreads, smem, st>>>(a);
+  if (t.nch > max_chunks(RB) || t.ng > kMaxGroups) return cudaErrorInvalidValue;
+  ChunkTab<RB> tab;
+  memset(&tab, 0, sizeof(tab));
+  memcpy(tab.c, t.ch, sizeof(Chunk) * t.nch);
+  memcpy(tab.grp, t.grp, sizeof(int) * (t.ng + 1));
+  dsg_sweep_kernel<P, RB, C, MODE><<<grid, kThreads, smem, st>>>(a, tab);
   return cudaGetLastError();
 }
 
 
 #define PNP_INSTANTIATE_P(P) \
-  template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, dim3, cudaStream_t);
+  template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t);
 
 #define PNP_DECLARE_P(P) \
-  extern template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, dim3, cudaStream_t);
+  extern template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
+  extern template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t);
 
 PNP_DECLARE_P(1)
 PNP_DECLARE_P(3)
