@@ -8,11 +8,15 @@ device raises RuntimeError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libpnpb200.so"
+# PNP_B200_LIB: development override to A/B a variant build of the same ABI
+# (scripts/build_variant.py); the in-tree library is the product.
+_VARIANT = os.environ.get("PNP_B200_LIB")
+LIB_PATH = Path(_VARIANT) if _VARIANT else _PKG / "libpnpb200.so"
 
 if not LIB_PATH.exists():  # fail loudly: the CUDA path is the product
     raise ImportError(
@@ -70,6 +74,8 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 for _name, (_res, _args) in _SIGS.items():
+    if _VARIANT and not hasattr(lib, _name):
+        continue
     _fn = getattr(lib, _name)
     _fn.restype = _res
     _fn.argtypes = _args

@@ -75,41 +75,125 @@ __device__ __forceinline__ float dsg_finish(float kx, float d, float inv_m, floa
   return __fmaf_rn(__fsub_rn(1.f, mass), x, w);
 }
 
+// One CTA per output tile (TH x 64 pixels of tile row blockIdx.y + the
+// window's first tile row, tile column blockIdx.x).  Thread (lx, ly0) owns
+// column lx and rows ly0, ly0+4, ... of the tile, so every covering partial
+// block is visited by all threads in the same fixed order (group, tile row,
+// tile col) -- the per-pixel summation order of gather_partial -- while each
+// thread keeps up to 8 independent loads in flight per block.
+constexpr int kFixRows = 8;  // rows per thread (TH <= 32, 4 row phases)
+
+// Predicated read-only load (+0 when off); asm volatile keeps all the loads
+// of a block ahead of the adds that consume them (memory-level parallelism).
+__device__ __forceinline__ float ldg_pred(const float* p, bool on) {
+  float v = 0.f;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q ld.global.nc.f32 %0, [%1];\n\t}"
+      : "+f"(v)
+      : "l"(p), "r"((int)on));
+  return v;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) dsg_fixup_kernel(const FixGeo f, const FixIO io) {
-  const int b = blockIdx.y;
-  const size_t npix = (size_t)f.nrows * f.W;
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  float dval = 0.f;
-  if (i < npix) {
-    const int yl = (int)(i / f.W), x = (int)(i - (size_t)yl * f.W);
-    const int y = f.y0 + yl;
-    const size_t o = (size_t)b * f.buf_rows * f.W + (size_t)(y - f.buf_r0) * f.W + x;
-    const float s0 = gather_partial(f, b, 0, y, x);
+  constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
+  const int b = blockIdx.z;
+  const int TH = f.TH, R = f.R, W = f.W;
+  const int BR = TH + R, BC = kTW + 2 * R;
+  const int ti = f.y0 / TH + blockIdx.y, tj = blockIdx.x;
+  const int lx = threadIdx.x & (kTW - 1), ly0 = threadIdx.x >> 6;
+  const int x = tj * kTW + lx;
+  const int ylo = max(f.y0, ti * TH), yhi = min(min(f.y0 + f.nrows, f.Hg), ti * TH + TH);
+  const size_t blk = (size_t)f.C * BR * BC;
+  const float* base = f.partial + (size_t)b * f.part_ntr * f.NG * f.tiles_x * blk;
+  const int dti = (R + TH - 1) / TH, dtj = (R + kTW - 1) / kTW;
+  const int ti0 = max(max(f.part_tr0, 0), ti - dti), ti1 = min(ti, f.part_tr0 + f.part_ntr - 1);
+  const int tj0 = max(0, tj - dtj), tj1 = min(f.tiles_x - 1, tj + dtj);
+
+  // Pull every covering block's row band into L2 with bulk prefetches first,
+  // so the per-thread loads below see L2 latency rather than HBM latency.
+  {
+    const int nti = ti1 - ti0 + 1, ntj = tj1 - tj0 + 1;
+    const int nq = f.NG * nti * ntj * C;
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+      int r_ = q;
+      const int c_ = r_ % C; r_ /= C;
+      const int t_j = tj0 + r_ % ntj; r_ /= ntj;
+      const int t_i = ti0 + r_ % nti;
+      const int gg = r_ / nti;
+      const int br0 = ti * TH - t_i * TH, br1 = min(BR, br0 + TH);
+      if (br0 >= br1) continue;
+      const float* p = base + (((size_t)(t_i - f.part_tr0) * f.NG + gg) * f.tiles_x + t_j) * blk +
+                       (size_t)c_ * BR * BC + (size_t)br0 * BC;
+      const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
+      const uintptr_t a1 = ((uintptr_t)(p + (size_t)(br1 - br0) * BC) + 15) & ~(uintptr_t)15;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0))
+                   : "memory");
+    }
+  }
+
+  float s[C][kFixRows];
+#pragma unroll
+  for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+    for (int k = 0; k < kFixRows; ++k) s[c_][k] = 0.f;
+
+  for (int gg = 0; gg < f.NG; ++gg)
+    for (int t_i = ti0; t_i <= ti1; ++t_i) {
+      const float* row = base + ((size_t)(t_i - f.part_tr0) * f.NG + gg) * f.tiles_x * blk;
+      for (int t_j = tj0; t_j <= tj1; ++t_j) {
+        const int bc = x - t_j * kTW + R;
+        if (bc < 0 || bc >= BC || x >= W) continue;
+        const float* p = row + (size_t)t_j * blk + bc;
+        float v[C][kFixRows];
+#pragma unroll
+        for (int k = 0; k < kFixRows; ++k) {
+          const int y = ti * TH + ly0 + 4 * k;
+          const int br = y - t_i * TH;
+          const bool ok = ly0 + 4 * k < TH && br < BR;
+#pragma unroll
+          for (int c_ = 0; c_ < C; ++c_) v[c_][k] = ldg_pred(p + (size_t)c_ * BR * BC + br * BC, ok);
+        }
+#pragma unroll
+        for (int k = 0; k < kFixRows; ++k)
+#pragma unroll
+          for (int c_ = 0; c_ < C; ++c_)  // volatile: stays behind all the loads
+            asm volatile("add.rn.f32 %0, %0, %1;" : "+f"(s[c_][k]) : "f"(v[c_][k]));
+      }
+    }
+
+  float dmax = 0.f;
+#pragma unroll
+  for (int k = 0; k < kFixRows; ++k) {
+    const int y = ti * TH + ly0 + 4 * k;
+    if (ly0 + 4 * k >= TH || y < ylo || y >= yhi || x >= W) continue;
+    const size_t o = (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x;
+    const float s0 = s[0][k];
     if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
-      const float s1 = gather_partial(f, b, 1, y, x);
       const float r = io.rs[o];
       io.kx[o] = __fmul_rn(r, s0);
-      dval = __fmul_rn(r, s1);
-      io.d[o] = dval;
+      const float dv = __fmul_rn(r, s[C - 1][k]);
+      io.d[o] = dv;
+      dmax = fmaxf(dmax, dv);
     } else if (MODE == FIX_D) {
-      dval = __fmul_rn(io.rs[o], s0);
-      io.d[o] = dval;
+      const float dv = __fmul_rn(io.rs[o], s0);
+      io.d[o] = dv;
+      dmax = fmaxf(dmax, dv);
     } else if (MODE == FIX_APPLY) {
       const float kx = __fmul_rn(io.rs[o], s0);
       io.out[o] = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
     } else {  // FIX_NLM: num / den
-      const float s1 = gather_partial(f, b, 1, y, x);
-      io.out[o] = __fdiv_rn(s0, s1);
+      io.out[o] = __fdiv_rn(s0, s[C - 1][k]);
     }
   }
   if (MODE == FIX_KXD || MODE == FIX_D) {
     // d > 0, so the int ordering of the bits is the float ordering; max is
     // exact and order-free -> deterministic.
     __shared__ float red[8];
-    float v = dval;
+    float v = dmax;
     for (int off = 16; off; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
@@ -377,8 +461,8 @@ static int run_fixup(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   f.nrows = w.nrows;
   f.buf_r0 = w.buf_r0;
   f.buf_rows = w.buf_rows;
-  const size_t npix = (size_t)w.nrows * g.W;
-  dim3 grid((unsigned)((npix + 255) / 256), g.B);
+  const int tr_first = w.y0 / g.TH, tr_last = (w.y0 + w.nrows - 1) / g.TH;
+  dim3 grid(g.tiles_x, tr_last - tr_first + 1, g.B);
   ProfScope prof(ctx, PROF_FIXUP);
   dsg_fixup_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
   PNP_LAUNCH_CHECK("dsg_fixup_kernel");
@@ -447,6 +531,7 @@ int pnp_ctx_create(int device, pnp_ctx** out) {
   PNP_CUDA(cudaSetDevice(device));
   pnp_ctx* c = new pnp_ctx();
   c->device = device;
+  PNP_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
   *out = c;
   return PNP_OK;
 }

@@ -57,6 +57,7 @@ struct ProfSlot {
 
 struct pnp_ctx {
   int device = 0;
+  int sms = 148;
   cudaStream_t stream = 0;
   pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
   pnp::DevBuf kcache;              // pair weights of the last adaptive denoise

@@ -38,3 +38,4 @@ def peak_rates(device: int | None = None) -> tuple[float, float]:
     f, x = C.c_double(), C.c_double()
     L.call("pnp_peak_rates", dev, C.byref(f), C.byref(x))
     return f.value, x.value
+

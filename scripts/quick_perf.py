@@ -34,7 +34,7 @@ def main():
     sizes = [int(a) for a in args] or [512, 2048, 8192]
     p = pnp.PatchParams.from_h(7, 10, 12 / 255, 2.0)
     for mode in modes:
-        profiling.set_cache_limit(0 if mode == "nocache" else None)
+        profiling.set_cache_limit(0 if mode.startswith("nocache") else None)
         for n in sizes:
             x = torch.rand(n, n, device="cuda")
             units = n * n * 21 * 21
