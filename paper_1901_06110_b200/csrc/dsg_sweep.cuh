@@ -47,7 +47,10 @@ constexpr int kThreads = 128;  // 64 columns x 2 row groups in phase 2
 #ifndef PNP_KY
 #define PNP_KY 4
 #endif
-constexpr int kKY = PNP_KY;    // offsets per chunk (same dx, consecutive dy)
+constexpr int kKY = PNP_KY;
+#ifndef PNP_KPF
+#define PNP_KPF 3  // k-cache stream: chunks of L2 prefetch lead (TMA path)
+#endif    // offsets per chunk (same dx, consecutive dy)
 constexpr int kMaxP = 15;      // largest patch side with a fast kernel
 constexpr int kMaxR = 32;      // largest search radius (R bucket)
 
@@ -113,12 +116,13 @@ struct SweepArgs {
   int buf_r0, buf_rows;
   int tr0, tiles_x;
   int part_off, part_ntr;
-  // k cache, tile-major: weight of pair (s, s+t), half-window offset index t
-  // (chunk-major), at kcache[b*kc_img + (tile*kc_nplanes + t)*TH*64 + row*64 + col]
-  // with (row, col) inside the tile -> every CTA streams contiguous 6.6 KB planes
-  float* kcache;
+  // k cache, tile-major, offset pairs packed: the weights of offsets
+  // (2kp, 2kp+1) of chunk ci for pixel (row, col) of a tile are one float2 at
+  // kcache[b*kc_img + (tile*kc_npairs + ci*KY/2 + kp)*TH*64 + row*64 + col]
+  // (float2 units) -> a chunk is one contiguous 2*TH*64*8 B run per tile
+  float2* kcache;
   long long kc_img;
-  int kc_nplanes;
+  int kc_npairs;
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
 };
@@ -145,7 +149,13 @@ struct Cfg {
   static constexpr int OFF_H = CACHED ? 0 : (GR * GS + 3) & ~3;  // 16 B aligned
   static constexpr int OFF_Y = CACHED ? 0 : OFF_H + KY * 32 * HS;  // KY/2 float2 maps
   static constexpr int OFF_A = OFF_Y + C * YR * YC;
-  static constexpr int TOTAL = OFF_A + C * AR * YC;  // floats
+  // CACHED with C = 2 streams the k cache through SMEM: two chunk buffers
+  // filled by bulk async copies (TMA engine) one chunk ahead + 2 mbarriers
+  static constexpr bool TMAK = CACHED && C == 2;
+  static constexpr int KCH = (KY / 2) * TH * kTW * 2;  // floats per chunk
+  static constexpr int OFF_K = (OFF_A + C * AR * YC + 3) & ~3;
+  static constexpr int OFF_MB = OFF_K + (TMAK ? 2 * KCH : 0);
+  static constexpr int TOTAL = OFF_MB + (TMAK ? 4 : 0);  // floats
 };
 
 __device__ __forceinline__ int reflect_index(int i, int n) {
@@ -154,6 +164,37 @@ __device__ __forceinline__ int reflect_index(int i, int n) {
   if (i < 0) i = -i - 1;
   if (i >= n) i = 2 * n - 1 - i;
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+// one elected thread: arm the barrier with the byte count, then start the
+// bulk global -> shared copy that completes it
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -245,6 +286,27 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
     }
   }
   for (int i = tid; i < C * AR * YC; i += kThreads) As[i] = 0.f;
+
+  constexpr bool TMAK = K::TMAK;
+  constexpr unsigned KPB = TH * kTW * 8;  // bytes of one pair plane
+  float* Ks = smem + K::OFF_K;            // [2][KY/2][TH][64] float2 (TMAK)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + K::OFF_MB);
+  const int cbeg = tab.grp[blockIdx.y], cend = tab.grp[blockIdx.y + 1];
+  const float2* kimg = CACHED || STORE ? a.kcache + (long long)b * a.kc_img +
+                                             (long long)tile * a.kc_npairs * (TH * kTW)
+                                       : nullptr;
+  auto issue_chunk = [&](int ci) {  // TMAK: chunk ci -> buffer ci & 1
+    const unsigned bytes = (tab.c[ci].kc > 2 ? 2u : 1u) * KPB;
+    bulk_load(Ks + (ci & 1) * K::KCH, kimg + (long long)ci * (KY / 2) * (TH * kTW), bytes,
+              mbar + (ci & 1));
+  };
+  if (TMAK && tid == 0) {
+    mbar_init(mbar, 1);
+    mbar_init(mbar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (cbeg < cend) issue_chunk(cbeg);
+  }
+  unsigned kphase = 0;  // TMAK: bit i = parity to wait for on buffer i
   __syncthreads();
 
   const int c0 = SEG * warp;         // phase-1 segment
@@ -302,7 +364,6 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   // the KY-1 shared rows (group 1 only)
   float pendv[C][KY - 1];
 
-  const int cbeg = tab.grp[blockIdx.y], cend = tab.grp[blockIdx.y + 1];
   for (int ci = cbeg; ci < cend; ++ci) {
     const Chunk& chk = tab.c[ci];
     const int dx = chk.dx, dy0 = chk.dy0, kc = chk.kc;
@@ -355,37 +416,54 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 #pragma unroll
       for (int j = 0; j < WIN - 1; ++j) pf[c_][j] = make_float2(0.f, 0.f);
     }
-    float* kbase = CACHED || STORE
-                       ? a.kcache + (long long)b * a.kc_img +
-                             ((long long)tile * a.kc_nplanes + (long long)ci * KY) * (TH * kTW) +
-                             r0 * kTW + c
-                       : nullptr;
-    // CACHED: issue the whole chunk's loads first (predicated, not branched,
-    // so all KY*N loads of valid offsets are in flight together).
-    float kcl[CACHED ? KY : 1][N];
-    if (CACHED) {
+    // this chunk's pair planes; thread (c, g) owns rows r0.. of column c
+    const float2* kq = CACHED || STORE ? kimg + (long long)ci * (KY / 2) * (TH * kTW) + r0 * kTW + c
+                                       : nullptr;
+    float2 kcl[CACHED && !TMAK ? KY / 2 : 1][N];
+    if (CACHED && !TMAK) {
+      // register path (C = 1): all the chunk's loads in flight together
+      // (predicated, not branched)
 #pragma unroll
-      for (int k = 0; k < KY; ++k)
+      for (int kp = 0; kp < KY / 2; ++kp)
 #pragma unroll
         for (int r = 0; r < N; ++r) {
-          const float* src = kbase + (k * TH + r) * kTW;
-          float v = 0.f;
+          const float2* src = kq + (kp * TH + r) * kTW;
+          float2 v = make_float2(0.f, 0.f);
           asm volatile(
-              "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %2, %3;\n\t"
-              "@q ld.global.cs.f32 %0, [%1];\n\t}"
-              : "+f"(v)
-              : "l"(src), "r"(k), "r"(kc));
-          kcl[k][r] = v;
+              "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %3, %4;\n\t"
+              "@q ld.global.cs.v2.f32 {%0, %1}, [%2];\n\t}"
+              : "+f"(v.x), "+f"(v.y)
+              : "l"(src), "r"(2 * kp), "r"(kc));
+          kcl[kp][r] = v;
         }
+    }
+    const float2* kb = nullptr;  // TMAK: SMEM copy of this chunk
+    if (TMAK) {
+      if (tid == 0 && ci + 1 < cend) {
+        issue_chunk(ci + 1);  // buffer freed by the last barrier
+        if (ci + PNP_KPF < cend) {  // and warm L2 further ahead
+          const int cj = ci + PNP_KPF;
+          const unsigned bytes = (tab.c[cj].kc > 2 ? 2u : 1u) * KPB;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                           kimg + (long long)cj * (KY / 2) * (TH * kTW)),
+                       "r"(bytes)
+                       : "memory");
+        }
+      }
+      mbar_wait(mbar + (ci & 1), (kphase >> (ci & 1)) & 1u);
+      kphase ^= 1u << (ci & 1);
+      kb = reinterpret_cast<const float2*>(Ks + (ci & 1) * K::KCH) + r0 * kTW + c;
     }
 #pragma unroll
     for (int kp = 0; kp < KY / 2; ++kp) {
       if (kp == 0 || 2 * kp < kc) {
         float2 kk[N];
-        if (CACHED) {
+        if (TMAK) {
 #pragma unroll
-          for (int r = 0; r < N; ++r)
-            kk[r] = make_float2(kcl[CACHED ? 2 * kp : 0][r], kcl[CACHED ? 2 * kp + 1 : 0][r]);
+          for (int r = 0; r < N; ++r) kk[r] = kb[(kp * TH + r) * kTW];
+        } else if (CACHED) {
+#pragma unroll
+          for (int r = 0; r < N; ++r) kk[r] = kcl[CACHED && !TMAK ? kp : 0][r];
         } else {
           // invalid odd slot: L = -inf on the host -> its weight is exactly +0
           const float2 L = make_float2(chk.L[2 * kp], chk.L[2 * kp + 1]);
@@ -399,10 +477,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
             for (int aa = 0; aa < P; ++aa)
               v = __ffma2_rn(make_float2(a.taps_v[aa], a.taps_v[aa]), hcol[r + aa], v);
             kk[r] = make_float2(ex2_approx(v.x), ex2_approx(v.y));
-            if (STORE) {
-              __stcs(kbase + (2 * kp * TH + r) * kTW, kk[r].x);
-              if (2 * kp + 1 < kc) __stcs(kbase + ((2 * kp + 1) * TH + r) * kTW, kk[r].y);
-            }
+            if (STORE) __stcs(const_cast<float2*>(kq) + (kp * TH + r) * kTW, kk[r]);
           }
         }
 #pragma unroll

@@ -417,9 +417,9 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   a.tiles_x = g.tiles_x;
   a.part_off = w.part_off;
   a.part_ntr = w.part_ntr;
-  a.kcache = kcache;
-  a.kc_nplanes = g.nchunks * kKY;
-  a.kc_img = (long long)w.ntr * g.tiles_x * a.kc_nplanes * g.TH * kTW;
+  a.kcache = reinterpret_cast<float2*>(kcache);
+  a.kc_npairs = g.nchunks * (kKY / 2);
+  a.kc_img = (long long)w.ntr * g.tiles_x * a.kc_npairs * g.TH * kTW;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
   for (int i = 0; i < g.P; ++i) {
