@@ -75,16 +75,7 @@ __device__ __forceinline__ float dsg_finish(float kx, float d, float inv_m, floa
   return __fmaf_rn(__fsub_rn(1.f, mass), x, w);
 }
 
-// One CTA per output tile (TH x 64 pixels of tile row blockIdx.y + the
-// window's first tile row, tile column blockIdx.x).  Thread (lx, ly0) owns
-// column lx and rows ly0, ly0+4, ... of the tile, so every covering partial
-// block is visited by all threads in the same fixed order (group, tile row,
-// tile col) -- the per-pixel summation order of gather_partial -- while each
-// thread keeps up to 8 independent loads in flight per block.
-constexpr int kFixRows = 8;  // rows per thread (TH <= 32, 4 row phases)
-
-// Predicated read-only load (+0 when off); asm volatile keeps all the loads
-// of a block ahead of the adds that consume them (memory-level parallelism).
+// Predicated read-only load (+0 when off).
 __device__ __forceinline__ float ldg_pred(const float* p, bool on) {
   float v = 0.f;
   asm volatile(
@@ -95,8 +86,123 @@ __device__ __forceinline__ float ldg_pred(const float* p, bool on) {
   return v;
 }
 
+// Small images (many offset groups): one thread per pixel; a CTA covers 4
+// rows x 64 columns of one tile
+// (blockIdx.y = tile row * ceil(TH/4) + row quarter).  A pixel is covered by at
+// most 3 x 3 partial blocks per offset group (R <= 32 < 2 TH, R <= 64); the
+// loads of kFixGB groups are all issued before any add, then summed in the
+// fixed order (group, tile row, tile col) that every variant (single GPU,
+// strips, apply) shares -> bit-reproducible, and latency-tolerant when NG is
+// large (small images split the offsets into many groups).
+
 template <int MODE>
-__global__ void __launch_bounds__(256) dsg_fixup_kernel(const FixGeo f, const FixIO io) {
+__global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, const FixIO io) {
+  constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
+  constexpr int kFixGB = C == 1 ? 4 : 2;  // offset groups loaded per batch
+  const int b = blockIdx.z;
+  const int TH = f.TH, R = f.R, W = f.W;
+  const int BR = TH + R, BC = kTW + 2 * R;
+  const int RQ = (TH + 3) / 4;
+  const int tq = blockIdx.y % RQ;
+  const int ti = f.y0 / TH + blockIdx.y / RQ, tj = blockIdx.x;
+  const int lx = threadIdx.x & (kTW - 1), ly = tq * 4 + (threadIdx.x >> 6);
+  const int x = tj * kTW + lx, y = ti * TH + ly;
+  const bool own = ly < TH && x < W && y >= f.y0 && y < f.y0 + f.nrows && y < f.Hg;
+  const size_t blk = (size_t)f.C * BR * BC;
+  const float* base = f.partial + (size_t)b * f.part_ntr * f.NG * f.tiles_x * blk;
+  const int dti = (R + TH - 1) / TH;
+  const int ti0 = max(max(f.part_tr0, 0), ti - dti), ti1 = min(ti, f.part_tr0 + f.part_ntr - 1);
+  const int tj0 = max(0, tj - 1), tj1 = min(f.tiles_x - 1, tj + 1);
+
+  // per-pixel block offsets (independent of the group)
+  unsigned okm = 0;  // bit (3*i + j): block (ti0+i, tj0+j) covers the pixel
+  size_t boff[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int t_i = ti0 + i, t_j = tj0 + j;
+      const int br = y - t_i * TH, bc = x - t_j * kTW + R;
+      const bool ok = own && t_i <= ti1 && t_j <= tj1 && br < BR && bc >= 0 && bc < BC;
+      okm |= (ok ? 1u : 0u) << (3 * i + j);
+      boff[i][j] = ok ? ((size_t)(t_i - f.part_tr0) * f.NG * f.tiles_x + t_j) * blk +
+                            (size_t)(br * BC + bc)
+                      : 0;
+    }
+  const size_t gstride = (size_t)f.tiles_x * blk;  // next group, same tile
+
+  float s[C] = {};
+  for (int g0 = 0; g0 < f.NG; g0 += kFixGB) {
+    float v[kFixGB][3][3][C];
+#pragma unroll
+    for (int gg = 0; gg < kFixGB; ++gg)
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const bool ok = g0 + gg < f.NG && ((okm >> (3 * i + j)) & 1u);
+          const float* p = base + (size_t)(g0 + gg) * gstride + boff[i][j];
+#pragma unroll
+          for (int c_ = 0; c_ < C; ++c_) v[gg][i][j][c_] = ldg_pred(p + (size_t)c_ * BR * BC, ok);
+        }
+#pragma unroll
+    for (int gg = 0; gg < kFixGB; ++gg)
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (g0 + gg < f.NG && ((okm >> (3 * i + j)) & 1u))
+#pragma unroll
+            for (int c_ = 0; c_ < C; ++c_) s[c_] = __fadd_rn(s[c_], v[gg][i][j][c_]);
+  }
+
+  float dmax = 0.f;
+  if (own) {
+    const size_t o = (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x;
+    const float s0 = s[0];
+    if (MODE == FIX_RS) {
+      io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
+    } else if (MODE == FIX_KXD) {
+      const float r = io.rs[o];
+      io.kx[o] = __fmul_rn(r, s0);
+      dmax = __fmul_rn(r, s[C - 1]);
+      io.d[o] = dmax;
+    } else if (MODE == FIX_D) {
+      dmax = __fmul_rn(io.rs[o], s0);
+      io.d[o] = dmax;
+    } else if (MODE == FIX_APPLY) {
+      const float kx = __fmul_rn(io.rs[o], s0);
+      io.out[o] = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
+    } else {  // FIX_NLM: num / den
+      io.out[o] = __fdiv_rn(s0, s[C - 1]);
+    }
+  }
+  if (MODE == FIX_KXD || MODE == FIX_D) {
+    // d > 0, so the int ordering of the bits is the float ordering; max is
+    // exact and order-free -> deterministic.
+    __shared__ float red[8];
+    float v = dmax;
+    for (int off = 16; off; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float m = red[0];
+      for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = fmaxf(m, red[k]);
+      atomicMax(io.mbits + b, __float_as_uint(m));
+    }
+  }
+}
+
+// Large images (few offset groups): one CTA per output tile (TH x 64 pixels of tile row blockIdx.y + the
+// window's first tile row, tile column blockIdx.x).  Thread (lx, ly0) owns
+// column lx and rows ly0, ly0+4, ... of the tile, so every covering partial
+// block is visited by all threads in the same fixed order (group, tile row,
+// tile col) -- the per-pixel summation order of gather_partial -- while each
+// thread keeps up to 8 independent loads in flight per block.
+constexpr int kFixRows = 8;  // rows per thread (TH <= 32, 4 row phases)
+
+template <int MODE>
+__global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, const FixIO io) {
   constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
   const int b = blockIdx.z;
   const int TH = f.TH, R = f.R, W = f.W;
@@ -462,9 +568,14 @@ static int run_fixup(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   f.buf_r0 = w.buf_r0;
   f.buf_rows = w.buf_rows;
   const int tr_first = w.y0 / g.TH, tr_last = (w.y0 + w.nrows - 1) / g.TH;
-  dim3 grid(g.tiles_x, tr_last - tr_first + 1, g.B);
   ProfScope prof(ctx, PROF_FIXUP);
-  dsg_fixup_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
+  if (g.NG <= 2) {  // same summation order either way
+    dim3 grid(g.tiles_x, tr_last - tr_first + 1, g.B);
+    dsg_fixup_tile_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
+  } else {
+    dim3 grid(g.tiles_x, (tr_last - tr_first + 1) * ((g.TH + 3) / 4), g.B);
+    dsg_fixup_px_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
+  }
   PNP_LAUNCH_CHECK("dsg_fixup_kernel");
   return PNP_OK;
 }

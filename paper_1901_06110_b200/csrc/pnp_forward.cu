@@ -3,9 +3,10 @@
 // SR (reference forward.py:98-185): A = decimate_k o blur, blur = correlation
 // with a separable normalized kernel under periodic (wrap) or half-sample
 // symmetric padding; A^T = blur o zero-fill upsample (exact for symmetric
-// kernels).  The residual kernel evaluates the blur only at the kept samples
-// and fuses "- y" and the 0.5||.||^2 data-term partials; the adjoint kernel
-// visits only the non-zero taps of the upsampled grid.
+// kernels).  Both are SMEM-tiled separable filters; the residual kernel
+// evaluates the blur only at the kept samples and fuses "- y" and the
+// 0.5||.||^2 data-term partials; the adjoint stages the zero-filled
+// upsampled tile.
 // QIS (forward.py:312-327): elementwise, evaluated in double.
 // ADMM (solver.py:219-228): x-update + projection + x+u + finite flags in one
 // pass; u-update + residual/PSNR partial sums in one pass.  All reductions
@@ -48,66 +49,149 @@ __device__ __forceinline__ void block_sum_store(double v, double* partial) {
   }
 }
 
-// out[b*stride + k] = scale * sum_j partial[b][j][k]  (fixed order)
-__global__ void reduce_partials_kernel(const double* partial, int nblk, int nvec, double scale,
-                                       double* out, int stride) {
-  const int b = blockIdx.x;
-  const int k = threadIdx.x;
-  if (k >= nvec) return;
+// out[b*stride + k] = scale * sum_j partial[b][j][k]: one CTA per (b, k),
+// thread t sums j = t, t+256, ... in order, then a fixed shuffle/SMEM tree
+// (deterministic; latency-tolerant for many partials).
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* partial, int nblk,
+                                                              int nvec, double scale, double* out,
+                                                              int stride) {
+  const int b = blockIdx.x, k = blockIdx.y;
   double s = 0.0;
-  for (int j = 0; j < nblk; ++j) s += partial[((size_t)b * nblk + j) * nvec + k];
-  out[(size_t)b * stride + k] = scale * s;
+  for (int j = threadIdx.x; j < nblk; j += blockDim.x) s += partial[((size_t)b * nblk + j) * nvec + k];
+  __shared__ double red[8];
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[(size_t)b * stride + k] = scale * t;
+  }
 }
 
-// r = A x - y (or A x when y == null) on the low-res grid; optional data partials.
+// SR blur kernels, SMEM tiled: the image region of a tile (+ radius halo,
+// boundary-mapped once at staging) is filtered separably -- horizontal taps
+// into a row buffer, then vertical taps -- in the reference's summation order
+// (forward.py:_convolve: rows outer, columns inner).
+constexpr int kSrT = 16;   // low-res outputs per tile side (residual)
+constexpr int kSrTA = 32;  // high-res outputs per tile side (adjoint)
+
+// r = A x - y (or A x when y == null) on the low-res grid; optional
+// 0.5||r||^2 partials, one per tile: partial[b][tile].
 __global__ void __launch_bounds__(256)
 sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, float* __restrict__ r,
                    int H, int W, int k, int rad, int sym, const Taps taps, double* partial) {
-  const int h = H / k, w = W / k;
-  const int b = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  extern __shared__ float sm[];
+  const int h = H / k, w = W / k, b = blockIdx.z;
+  const int S = k * (kSrT - 1) + 1 + 2 * rad;  // staged hi-res rows / cols
+  float* X = sm;                               // [S][S]
+  float* Hh = sm + S * S;                      // [S][kSrT]
+  const int oy0 = blockIdx.y * kSrT, ox0 = blockIdx.x * kSrT;
+  const int y0 = k * oy0 - rad, x0 = k * ox0 - rad;
+  const float* xb = x + (size_t)b * H * W;
+  for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+    const int yy = i / S, xx = i - yy * S;
+    const int sy = map_index(min(y0 + yy, H - 1 + rad), H, sym);
+    const int sx = map_index(min(x0 + xx, W - 1 + rad), W, sym);
+    X[i] = xb[(size_t)sy * W + sx];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S * kSrT; i += blockDim.x) {
+    const int yy = i / kSrT, tx = i - yy * kSrT;
+    const float* row = X + yy * S + k * tx;
+    float s = 0.f;
+    for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
+    Hh[i] = s;
+  }
+  __syncthreads();
+  const int ty = threadIdx.x / kSrT, tx = threadIdx.x - ty * kSrT;
+  const int oy = oy0 + ty, ox = ox0 + tx;
   double sq = 0.0;
-  if (i < h * w) {
-    const int oy = i / w, ox = i - oy * w;
-    const float* xb = x + (size_t)b * H * W;
+  if (oy < h && ox < w) {
     float acc = 0.f;
-    for (int a = -rad; a <= rad; ++a) {
-      const float* row = xb + (size_t)map_index(k * oy + a, H, sym) * W;
-      float s = 0.f;
-      for (int c = -rad; c <= rad; ++c) s = fmaf(taps.tx[c + rad], row[map_index(k * ox + c, W, sym)], s);
-      acc = fmaf(taps.ty[a + rad], s, acc);
-    }
-    if (y) acc -= y[(size_t)b * h * w + i];
-    r[(size_t)b * h * w + i] = acc;
+    for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(k * ty + a) * kSrT + tx], acc);
+    const size_t o = (size_t)b * h * w + (size_t)oy * w + ox;
+    if (y) acc -= y[o];
+    r[o] = acc;
     sq = (double)acc * (double)acc;
   }
-  if (partial) block_sum_store(sq, partial);
+  if (partial) {
+    __shared__ double red[8];
+    for (int off = 16; off; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+      partial[((size_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+  }
 }
 
-// x_out = A^T r = blur(upsample_k(r)) on the high-res grid.
+// x_out = A^T r = blur(upsample_k(r)) on the high-res grid: the zero-filled
+// upsampled tile (+ halo, boundary-mapped) is staged, then filtered.
 __global__ void __launch_bounds__(256)
 sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, int W, int k,
                   int rad, int sym, const Taps taps) {
-  const int h = H / k, w = W / k;
-  const int b = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= H * W) return;
-  const int py = i / W, px = i - py * W;
+  extern __shared__ float sm[];
+  const int h = H / k, w = W / k, b = blockIdx.z;
+  const int S = kSrTA + 2 * rad;
+  float* U = sm;             // [S][S]
+  float* Hh = sm + S * S;    // [S][kSrTA]
+  const int py0 = blockIdx.y * kSrTA, px0 = blockIdx.x * kSrTA;
   const float* rb = r + (size_t)b * h * w;
-  float acc = 0.f;
-  for (int a = -rad; a <= rad; ++a) {
-    const int uy = map_index(py + a, H, sym);
-    if (uy % k) continue;
-    const float* row = rb + (size_t)(uy / k) * w;
-    float s = 0.f;
-    for (int c = -rad; c <= rad; ++c) {
-      const int ux = map_index(px + c, W, sym);
-      if (ux % k) continue;
-      s = fmaf(taps.tx[c + rad], row[ux / k], s);
-    }
-    acc = fmaf(taps.ty[a + rad], s, acc);
+  for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+    const int yy = i / S, xx = i - yy * S;
+    const int uy = map_index(min(py0 - rad + yy, H - 1 + rad), H, sym);
+    const int ux = map_index(min(px0 - rad + xx, W - 1 + rad), W, sym);
+    const int qy = uy / k, qx = ux / k;
+    U[i] = (uy == qy * k && ux == qx * k) ? rb[(size_t)qy * w + qx] : 0.f;
   }
-  out[(size_t)b * H * W + i] = acc;
+  __syncthreads();
+  for (int i = threadIdx.x; i < S * kSrTA; i += blockDim.x) {
+    const int yy = i / kSrTA, xx = i - yy * kSrTA;
+    const float* row = U + yy * S + xx;
+    float s = 0.f;
+    for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
+    Hh[i] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSrTA * kSrTA; i += blockDim.x) {
+    const int yy = i / kSrTA, xx = i - yy * kSrTA;
+    const int py = py0 + yy, px = px0 + xx;
+    if (py >= H || px >= W) continue;
+    float acc = 0.f;
+    for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
+    out[(size_t)b * H * W + (size_t)py * W + px] = acc;
+  }
+}
+
+static size_t sr_res_smem(int k, int rad) {
+  const int S = k * (kSrT - 1) + 1 + 2 * rad;
+  return (size_t)(S * S + S * kSrT) * sizeof(float);
+}
+static size_t sr_adj_smem(int rad) {
+  const int S = kSrTA + 2 * rad;
+  return (size_t)(S * S + S * kSrTA) * sizeof(float);
+}
+static dim3 sr_res_grid(int H, int W, int k, int batch) {
+  return dim3((W / k + kSrT - 1) / kSrT, (H / k + kSrT - 1) / kSrT, batch);
+}
+static dim3 sr_adj_grid(int H, int W, int batch) {
+  return dim3((W + kSrTA - 1) / kSrTA, (H + kSrTA - 1) / kSrTA, batch);
+}
+static cudaError_t sr_smem_attr(size_t res, size_t adj) {
+  static size_t set_res = 48 * 1024, set_adj = 48 * 1024;
+  cudaError_t e = cudaSuccess;
+  if (res > set_res) {
+    e = cudaFuncSetAttribute(sr_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res);
+    if (e == cudaSuccess) set_res = res;
+  }
+  if (e == cudaSuccess && adj > set_adj) {
+    e = cudaFuncSetAttribute(sr_adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj);
+    if (e == cudaSuccess) set_adj = adj;
+  }
+  return e;
 }
 
 __global__ void __launch_bounds__(256)
@@ -215,6 +299,8 @@ static int sr_check(int batch, int H, int W, const float* taps, int radius, int 
   if (H % factor || W % factor) return fail(PNP_EINVAL, "dimensions not divisible by factor");
   if (radius < 0 || 2 * radius + 1 > kMaxTaps) return fail(PNP_EINVAL, "bad blur radius");
   if (radius > (H < W ? H : W)) return fail(PNP_EINVAL, "kernel radius exceeds image extent");
+  if (sr_res_smem(factor, radius) > 227 * 1024 || sr_adj_smem(radius) > 227 * 1024)
+    return fail(PNP_EINVAL, "blur radius / factor too large for the tiled SR kernels");
   if (boundary != 0 && boundary != 1) return fail(PNP_EINVAL, "boundary must be 0 or 1");
   if (!taps) return fail(PNP_EINVAL, "taps null");
   for (int i = 0; i < 2 * radius + 1; ++i) {
@@ -240,12 +326,12 @@ int pnp_sr_apply(pnp_ctx* ctx, const float* x, float* y, int batch, int H, int W
   Taps t;
   int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
   if (rc) return rc;
-  const int nl = (H / factor) * (W / factor);
-  dim3 grid((nl + 255) / 256, batch);
+  const size_t rs = sr_res_smem(factor, radius);
+  PNP_CUDA(sr_smem_attr(rs, 0));
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_residual_kernel<<<grid, 256, 0, ctx->stream>>>(x, nullptr, y, H, W, factor, radius, boundary,
-                                                      t, nullptr);
+    sr_residual_kernel<<<sr_res_grid(H, W, factor, batch), 256, rs, ctx->stream>>>(
+        x, nullptr, y, H, W, factor, radius, boundary, t, nullptr);
   }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
   return PNP_OK;
@@ -257,10 +343,12 @@ int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int
   Taps t;
   int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
   if (rc) return rc;
-  dim3 grid((H * W + 255) / 256, batch);
+  const size_t as = sr_adj_smem(radius);
+  PNP_CUDA(sr_smem_attr(0, as));
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_adjoint_kernel<<<grid, 256, 0, ctx->stream>>>(y, x, H, W, factor, radius, boundary, t);
+    sr_adjoint_kernel<<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(y, x, H, W, factor,
+                                                                          radius, boundary, t);
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
@@ -273,28 +361,31 @@ int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, in
   int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
   if (rc) return rc;
   const int nl = (H / factor) * (W / factor);
-  const int nblk = (nl + 255) / 256;
+  const dim3 rg = sr_res_grid(H, W, factor, batch);
+  const int nblk = rg.x * rg.y;
   if ((rc = ctx->kx.ensure((size_t)batch * nl * sizeof(float)))) return rc;
   if (data_out && (rc = ensure_partials(ctx, (size_t)batch * nblk))) return rc;
   float* r = ctx->kx.as<float>();
   double* part = data_out ? ctx->stats.as<double>() : nullptr;
+  const size_t rs = sr_res_smem(factor, radius), as = sr_adj_smem(radius);
+  PNP_CUDA(sr_smem_attr(rs, as));
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_residual_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, yobs, r, H, W, factor, radius,
-                                                                   boundary, t, part);
+    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(x, yobs, r, H, W, factor, radius, boundary,
+                                                     t, part);
   }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
   if (data_out) {
     {
       ProfScope prof_(ctx, PROF_ADMM);
-      reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 0.5, data_out, 1);
+      reduce_partials_kernel<<<dim3(batch, 1), 256, 0, ctx->stream>>>(part, nblk, 1, 0.5, data_out, 1);
     }
     PNP_LAUNCH_CHECK("reduce_partials_kernel");
   }
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_adjoint_kernel<<<dim3((H * W + 255) / 256, batch), 256, 0, ctx->stream>>>(
-        r, grad, H, W, factor, radius, boundary, t);
+    sr_adjoint_kernel<<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(r, grad, H, W, factor,
+                                                                          radius, boundary, t);
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
@@ -321,7 +412,7 @@ int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* z
   if (data_out) {
     {
       ProfScope prof_(ctx, PROF_ADMM);
-      reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
+      reduce_partials_kernel<<<dim3(batch, 1), 256, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
     }
     PNP_LAUNCH_CHECK("reduce_partials_kernel");
   }
@@ -342,7 +433,7 @@ int pnp_qis_data(pnp_ctx* ctx, const float* x, const float* ones, const float* z
                                                                 gain_over_K, floor_, part);
   }
   PNP_LAUNCH_CHECK("qis_grad_kernel");
-  reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
+  reduce_partials_kernel<<<dim3(batch, 1), 256, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
   PNP_LAUNCH_CHECK("reduce_partials_kernel");
   return PNP_OK;
 }
@@ -376,7 +467,7 @@ int pnp_admm_uupdate(pnp_ctx* ctx, float* u, const float* x, const float* v, con
                                                                     rho, part, flags);
   }
   PNP_LAUNCH_CHECK("admm_uupdate_kernel");
-  reduce_partials_kernel<<<batch, 32, 0, ctx->stream>>>(part, nblk, 3, 1.0, stats, 4);
+  reduce_partials_kernel<<<dim3(batch, 3), 256, 0, ctx->stream>>>(part, nblk, 3, 1.0, stats, 4);
   PNP_LAUNCH_CHECK("reduce_partials_kernel");
   return PNP_OK;
 }
