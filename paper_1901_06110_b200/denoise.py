@@ -201,7 +201,7 @@ class FrozenGuide:
         """(img, k) -> W img plug-in for linearized_pnp_admm, device resident."""
         from .solver import device_callable
 
-        return device_callable(lambda img, k: self.apply_device(img))
+        return device_callable(lambda img, k: self.apply_device(img), graph_from=2)
 
 
 def freeze_guide(guide, params: PatchParams) -> FrozenGuide:

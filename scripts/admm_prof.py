@@ -23,14 +23,16 @@ yd = torch.from_numpy(y).to(dev)
 guide = F.interpolate(yd.double()[None, None], scale_factor=2, mode="bicubic",
                       align_corners=False)[0, 0].clamp(0, 1).float().contiguous()
 p2 = pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0)
-cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=30, constraint=pnp.UNIT_BOX)
+ITERS = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+GRAPH = {"on": True, "off": False}.get(sys.argv[2] if len(sys.argv) > 2 else "", None)
+cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=ITERS, constraint=pnp.UNIT_BOX)
 gt = torch.from_numpy(truth).to(dev)
 fz = pnp.freeze_guide(guide, p2)
 prob = pnp.make_sr_problem(op, yd, ground_truth=gt)
 
 
 def run():
-    return pnp.linearized_pnp_admm(prob, cfg, denoiser=fz.as_denoiser())
+    return pnp.linearized_pnp_admm(prob, cfg, denoiser=fz.as_denoiser(), graph=GRAPH)
 
 
 for _ in range(3):
@@ -41,7 +43,8 @@ for _ in range(5):
     v, recs = run()
 torch.cuda.synchronize()
 wall = (time.perf_counter() - t) / 5
-print(f"wall per run {wall*1e3:.2f} ms = {30/wall:.0f} iters/s; device time of 30 its "
+print(f"[{ITERS} its, graph={GRAPH}] wall per run {wall*1e3:.2f} ms = {ITERS/wall:.0f} iters/s; "
+      f"device time "
       f"{recs[-1].time_ms:.2f} ms; psnr {recs[-1].psnr:.4f}")
 pr = cProfile.Profile()
 pr.enable()

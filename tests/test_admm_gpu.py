@@ -196,3 +196,30 @@ def test_batched_admm_matches_single(pnp):
         vi, ri = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, Y[i].contiguous()), cfg,
                                          denoiser=fz.as_denoiser())
         assert torch.equal(vb[i], vi)
+
+
+@pytest.mark.parametrize("schedule", ["frozen-plugin", "dsg-fixed", "dsg-adaptive", "nlm"])
+def test_graph_replay_is_bitwise_eager(pnp, golden_admm, schedule):
+    """Iterations captured into one CUDA graph == the eager loop, bit for bit."""
+    import torch
+    a = golden_admm
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    y = torch.from_numpy(np.asarray(a["sr_y"], dtype=np.float32)).cuda()
+    gt = torch.from_numpy(np.asarray(a["sr_truth"], dtype=np.float32)).cuda()
+    prob = pnp.make_sr_problem(op, y, ground_truth=gt)
+    den = None
+    kw = dict(rho=1.0, lam=0.01, alpha=1.0, max_iters=9, constraint=pnp.UNIT_BOX,
+              patch_side=5, window_radius=4, bandwidth=0.1, patch_sigma=1.5)
+    if schedule == "frozen-plugin":
+        fz = pnp.freeze_guide(a["sr_gauss_guide"], pnp.PatchParams(5, 4, 0.1, 1.5))
+        den = fz.as_denoiser()
+    else:
+        kw.update(denoiser=schedule, freeze_at=3)
+    cfg = pnp.SolverConfig(**kw)
+    ve, re_ = pnp.linearized_pnp_admm(prob, cfg, denoiser=den, graph=False)
+    vg, rg = pnp.linearized_pnp_admm(prob, cfg, denoiser=den, graph=True)
+    assert torch.equal(ve, vg)
+    for r1, r2 in zip(re_, rg):
+        assert (r1.primal, r1.dual, r1.psnr, r1.objective) == (r2.primal, r2.dual, r2.psnr,
+                                                               r2.objective)
+        assert math.isfinite(r2.time_ms)
