@@ -14,13 +14,17 @@ value    = 8192^2 * 441 pixel-offsets / device time per step (max over
            so every step streams from HBM; no flush needed);
 e2e      = the same through the public API with pinned host buffers: H2D of
            the image, denoise, D2H of the result inside the timed region;
-roofline = the DSG sweep kernel: SURVEY.md §8(d)'s algorithmic FP32 ops per
-           pixel-offset (20.95 adaptive, P=7 Gaussian, R=10) / its measured
-           launch time (CUDA events on the library stream), against the
-           FFMA rate measured on this GPU by pnp_peak_rates;
+roofline = the dominant kernel of the step (CUDA events on the library
+           stream): the fused sweep A (FP32-bound: SURVEY.md §8(d)'s algorithmic
+           ops per pixel-offset / its launch time vs the FFMA rate measured on
+           this GPU by pnp_peak_rates) or the k-cache stream of sweep B
+           (HBM-bound: 4 B per half-window pair vs MEASURED_PEAKS hbm_gbs); plus
+           "denoise": the whole step vs the FP32 roofline of the algorithm
+           (20.95 ops per pixel-offset);
 cpu_baseline = the float64 CPU oracle port (oracle/, restating pnprestore)
            on a bounded sample of the same workload.
-Extras: ADMM iterations/s for configs 2 and 3 (512^2 SR / QIS).
+Extras: ADMM iterations/s for configs 2 and 3 (512^2 SR / QIS) and image
+iterations/s for config 5 (64 x 1024^2 SR batched in one solver call).
 
 ``--impl reference`` times the reference's CPU algorithm (oracle port) with
 all host cores on bounded samples of the same workload.
@@ -119,6 +123,15 @@ class ClockSampler:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def committed_traffic() -> dict:
+    """Per-launch dram bytes of the sweep kernels from the committed ncu capture."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        return {k: v["dram_bytes_per_launch"] for k, v in d["kernels"].items()}
+    except Exception:
+        return {}
 
 
 def measured_hbm_gbs() -> float:
@@ -273,40 +286,53 @@ def run_gpu(args, rank, world, local_rank):
     units_rank = units / world * args.steps          # pixel-offsets swept by this rank
     sweep_ms, sweep_n = prof["sweep"]
     cached_ms, cached_n = prof["sweep_cached"]
+    traffic = committed_traffic()
     # algorithmic FP32 ops per pixel-offset of the recompute sweeps:
     # sweep A (mass) (F+5)*N+/(2R+1)^2, sweep B (F+9)*N+/(2R+1)^2 with F = 2P
     half = ((2 * R_C4 + 1) ** 2 - 1) / 2 / (2 * R_C4 + 1) ** 2
     ops_a, ops_b = (2 * P_C4 + 5) * half, (2 * P_C4 + 9) * half
     ops_unit = ops_a + (ops_b if cached_n == 0 else 0.0)
+    kbytes_unit = 8.0 * half / 2  # k cache: one float2 per offset pair = 4 B per half-window pair
     kernels = []
     if sweep_ms > 0:
         ach = ops_unit * units_rank / (sweep_ms * 1e-3) / 1e12
+        name = "dsg_sweep_kernel<7,10,1,STORE>" if cached_n else "dsg_sweep_kernel<7,10,C,RECOMPUTE>"
         kernels.append({
-            "kernel": "dsg_sweep_kernel (fused recompute" + (", k-cache store)" if cached_n else ")"),
+            "kernel": name, "role": "sweep A (mass) + k-cache store" if cached_n
+            else "sweep A + sweep B, fused recompute",
             "bound": "fp32", "achieved": ach, "peak": peak_ffma / 1e12, "unit": "Top/s",
             "frac": ach / (peak_ffma / 1e12), "frac_of_nominal": ach / (nominal / 1e12),
             "ops_per_pixel_offset": ops_unit, "ms_per_step": sweep_ms / args.steps,
             "launches_per_step": sweep_n / args.steps,
-            "sfu_frac": (half * (1 if cached_n else 2)) * units_rank / (sweep_ms * 1e-3) / peak_ex2})
+            "sfu_frac": (half * (1 if cached_n else 2)) * units_rank / (sweep_ms * 1e-3) / peak_ex2,
+            "hbm_write_GBps": (kbytes_unit * units_rank / (sweep_ms * 1e-3) / 1e9) if cached_n else 0.0,
+            "traffic": traffic.get("sweep_store" if cached_n else "sweep_recompute")})
     if cached_n:
-        # k cache read: one fp32 weight per half-window pair = 4*N+/(2R+1)^2 B per pixel-offset
-        bytes_unit = 4.0 * half
-        ach = bytes_unit * units_rank / (cached_ms * 1e-3) / 1e9
+        ach = kbytes_unit * units_rank / (cached_ms * 1e-3) / 1e9
         kernels.append({
-            "kernel": "dsg_sweep_kernel (k-cache stream, sweep B)", "bound": "hbm",
+            "kernel": "dsg_sweep_kernel<7,10,2,CACHED>", "role": "sweep B over the k cache "
+            "(bulk async copies into SMEM, mbarrier double buffer)", "bound": "hbm",
             "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-            "bytes_per_pixel_offset": bytes_unit, "ms_per_step": cached_ms / args.steps,
-            "launches_per_step": cached_n / args.steps})
+            "bytes_per_pixel_offset": kbytes_unit, "ms_per_step": cached_ms / args.steps,
+            "launches_per_step": cached_n / args.steps, "traffic": traffic.get("sweep_cached")})
     dom = max(kernels, key=lambda k: k["ms_per_step"]) if kernels else None
-    roofline = dict(dom) if dom else {}
+    roofline = {k: v for k, v in (dom or {}).items()}
+    # the whole denoise against the FP32 roofline of the algorithm (north star)
+    roof_rate = peak_ffma / ((ops_a + ops_b))  # pixel-offsets / s at 100% FFMA
     roofline.update({
-        "traffic": None,
         "peak_source": "fp32: FFMA rate measured by pnp_peak_rates on this GPU (nominal "
                        f"148x128x1965MHz = {nominal / 1e12:.2f} Top/s); hbm: MEASURED_PEAKS.json",
         "share_of_step": (dom["ms_per_step"] / ms) if dom else None,
         "kernels": kernels,
         "ex2_peak_per_s": peak_ex2,
-        "traffic_note": "dram bytes per launch: see profiles/ (ncu --set full)",
+        "denoise": {"pixel_offsets_per_s": value * 1e9,
+                    "fp32_roofline_pixel_offsets_per_s": roof_rate,
+                    "frac": value * 1e9 / roof_rate,
+                    "ops_per_pixel_offset": ops_a + ops_b,
+                    "note": "whole adaptive denoise (all kernels) vs the FFMA roofline of the "
+                            "two-sweep algorithm (SURVEY §8(d): 20.95 FP32 ops per pixel-offset)"},
+        "traffic_note": "dram read+write bytes per launch from the committed ncu --set full "
+                        "capture (profiles/ncu_traffic.json)",
     })
     line = {
         "metric": METRIC, "value": value, "unit": "Gpixel*offset/s", "n_gpus": world,
@@ -361,6 +387,8 @@ def run_gpu(args, rank, world, local_rank):
                        "api": "paper_1901_06110_b200.dsg_nlm_denoise(torch CUDA tensor)"
                               if world == 1 else "parallel.ShardedDSG.denoise"}
         if rank == 0 and world == 1:
+            profiling.set_cache_limit(0, local_rank)      # free the adaptive k cache (59 GB)
+            profiling.set_cache_limit(None, local_rank)   # (frozen guides keep their own)
             line["admm"] = admm_extras(pnp, dev)
             side = min(512, n)
             img = make_image_rows(n, 0, min(n, side + 256))
@@ -425,6 +453,39 @@ def admm_extras(pnp, dev):
         t1 = time.perf_counter()
     res["config3_qis_512"] = {"iters": 50, "iters_per_s": 50 / (t1 - t0),
                               "psnr_db": recs[-1].psnr}
+    # config 5: 64 independent 1024^2 SR problems batched in one solver call
+    # (blockIdx.z), per-image alpha, frozen bicubic guides, 20 iterations
+    nb, side = 64, 1024
+    truths, ys = [], []
+    for i in range(nb):
+        t_i = synth.scene(side, side, 1000 + i).astype(np.float32)
+        truths.append(t_i)
+        ys.append(pnp.sr_simulate(torch.from_numpy(t_i).to(dev), op, 0.0, seed=0))
+    yb = torch.stack(ys)
+    noise = torch.from_numpy(np.stack([
+        pnp.SplitMix64(1100 + i).normals(yb[0].numel()).reshape(tuple(yb[0].shape))
+        for i in range(nb)]) * (5 / 255)).to(dev, torch.float32)
+    yb = (yb + noise).contiguous()
+    gtb = torch.from_numpy(np.stack(truths)).to(dev)
+    guides = F.interpolate(yb.double()[:, None], scale_factor=2, mode="bicubic",
+                           align_corners=False)[:, 0].clamp(0, 1).float().contiguous()
+    cfg5 = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=20, constraint=pnp.UNIT_BOX)
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fz5 = pnp.freeze_guide(guides, p2)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        v5, recs5 = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, yb, ground_truth=gtb), cfg5,
+                                            denoiser=fz5.as_denoiser())
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        del fz5
+    res["config5_sr_64x1024"] = {
+        "images": nb, "iters": 20, "image_iters_per_s": nb * 20 / (t2 - t1),
+        "pixel_offsets_per_s_in_applies": nb * side * side * 441 * 20 / (t2 - t1),
+        "freeze_ms": (t1 - t0) * 1e3, "end_to_end_ms": (t2 - t0) * 1e3,
+        "psnr_db_mean": float(np.mean(recs5[-1].psnr))}
     res["reference_cpu_note"] = "survey: pnprestore config-2 shape 0.79 iters/s on 1 CPU core"
     return res
 

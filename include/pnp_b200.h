@@ -167,6 +167,10 @@ int pnp_admm_uupdate(pnp_ctx* ctx, float* u, const float* x, const float* v,
                      double rho, double* stats, int* flags);
 /* y = clamp(x) */
 int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, double hi);
+/* Validation helper (reference image.py:35-40): *all_finite = 1 when no
+ * element of x (n floats, device, 16 B aligned) is NaN/Inf, else 0.  One
+ * pass on the ctx stream, then a synchronizing 4-byte read-back. */
+int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite);
 
 #ifdef __cplusplus
 }

@@ -33,7 +33,7 @@ def validate(a, name: str = "image", batch_ok: bool = False):
         finite = bool(np.all(np.isfinite(a)))
     else:
         shape = tuple(a.shape)
-        finite = bool(torch.isfinite(a).all().item()) if a.numel() else True
+        finite = _all_finite(a) if a.numel() else True
     nd_ok = len(shape) == 2 or (batch_ok and kind == TORCH and len(shape) == 3)
     if not nd_ok:
         raise ValueError(f"{name} must be 2-D, got shape {shape}")
@@ -42,6 +42,19 @@ def validate(a, name: str = "image", batch_ok: bool = False):
     if not finite:
         raise ValueError(f"{name} contains non-finite values")
     return a, kind
+
+
+def _all_finite(t: torch.Tensor) -> bool:
+    """Native one-pass check for contiguous float32 CUDA tensors (no torch
+    reduction kernels); torch for anything else."""
+    if t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.data_ptr() % 16 == 0:
+        import ctypes as C
+
+        from . import _lib as L
+        ok = C.c_int(0)
+        L.call("pnp_check_finite", L.context(t.device.index), L.ptr(t), t.numel(), C.byref(ok))
+        return bool(ok.value)
+    return bool(torch.isfinite(t).all().item())
 
 
 def to_device(a, dev: int | None = None) -> torch.Tensor:

@@ -314,6 +314,23 @@ static int ensure_partials(pnp_ctx* ctx, size_t doubles) {
   return ctx->stats.ensure(doubles * sizeof(double));
 }
 
+// Input validation (image.py:35-40 "non-finite" ValueError) in one pass:
+// flag |= 1 if any element is NaN/Inf (16 B vector loads, warp ballot).
+__global__ void __launch_bounds__(256) nonfinite_kernel(const float* __restrict__ x, size_t n,
+                                                        int* flag) {
+  const size_t n4 = n / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  bool bad = false;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = __ldcs(x4 + i);
+    bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+  }
+  for (size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 }  // namespace pnp
 
 using namespace pnp;
@@ -513,6 +530,24 @@ int pnp_qis_simulate_host(const double* stop, int64_t n, int K, uint64_t seed, d
     }
     ones[i] = (double)fired;
   }
+  return PNP_OK;
+}
+
+
+int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite) {
+  if (!ctx || !x || !all_finite || n < 0) return fail(PNP_EINVAL, "null argument");
+  if (((uintptr_t)x & 15) != 0) return fail(PNP_EINVAL, "x must be 16-byte aligned");
+  int rc;
+  if ((rc = ctx->flags.ensure(sizeof(int)))) return rc;
+  int* f = ctx->flags.as<int>();
+  PNP_CUDA(cudaMemsetAsync(f, 0, sizeof(int), ctx->stream));
+  const int blocks = ctx->sms * 8;
+  nonfinite_kernel<<<blocks, 256, 0, ctx->stream>>>(x, (size_t)n, f);
+  PNP_LAUNCH_CHECK("nonfinite_kernel");
+  int h = 0;
+  PNP_CUDA(cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  PNP_CUDA(cudaStreamSynchronize(ctx->stream));
+  *all_finite = h ? 0 : 1;
   return PNP_OK;
 }
 
