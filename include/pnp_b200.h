@@ -55,9 +55,9 @@ int pnp_ctx_set_cache_limit(pnp_ctx* ctx, int64_t bytes);
 int pnp_frozen_cached(const pnp_frozen* fz);
 /* Per-launch CUDA-event timing on the context stream (off by default).
  * profile_read syncs the stream, returns summed device ms and launch counts
- * for 5 categories (0 DSG recompute sweep, 1 DSG fixup/finalize, 2 forward
- * operators, 3 ADMM elementwise/reductions, 4 DSG k-cache sweep) since the
- * last read, and resets them. */
+ * for 6 categories (0 DSG recompute sweep, 1 DSG fixup/finalize, 2 forward
+ * operators, 3 ADMM elementwise/reductions, 4 DSG k-cache sweep, 5 input
+ * validation) since the last read, and resets them. */
 int pnp_ctx_profile(pnp_ctx* ctx, int enable);
 int pnp_ctx_profile_read(pnp_ctx* ctx, double* ms, int* launches);
 /* Measured FFMA / MUFU.EX2 instruction throughput of the device (per second,

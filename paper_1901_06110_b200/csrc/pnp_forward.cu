@@ -542,7 +542,10 @@ int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite) {
   int* f = ctx->flags.as<int>();
   PNP_CUDA(cudaMemsetAsync(f, 0, sizeof(int), ctx->stream));
   const int blocks = ctx->sms * 8;
-  nonfinite_kernel<<<blocks, 256, 0, ctx->stream>>>(x, (size_t)n, f);
+  {
+    ProfScope prof_(ctx, PROF_CHECK);
+    nonfinite_kernel<<<blocks, 256, 0, ctx->stream>>>(x, (size_t)n, f);
+  }
   PNP_LAUNCH_CHECK("nonfinite_kernel");
   int h = 0;
   PNP_CUDA(cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -47,7 +47,8 @@ enum ProfCat {
   PROF_FORWARD = 2,
   PROF_ADMM = 3,
   PROF_SWEEP_CACHED = 4,  // HBM-streaming sweep over the k cache
-  PROF_NCAT = 5
+  PROF_CHECK = 5,         // input validation (non-finite scan)
+  PROF_NCAT = 6
 };
 struct ProfSlot {
   cudaEvent_t a = nullptr, b = nullptr;

@@ -9,7 +9,7 @@ import torch
 
 from . import _lib as L
 
-CATEGORIES = ("sweep", "fixup", "forward", "admm", "sweep_cached")
+CATEGORIES = ("sweep", "fixup", "forward", "admm", "sweep_cached", "check")
 
 
 def enable(flag: bool = True, device: int | None = None) -> None:
@@ -20,8 +20,8 @@ def enable(flag: bool = True, device: int | None = None) -> None:
 def read(device: int | None = None) -> dict:
     """{category: (device ms, launches)} since the last read (syncs the stream)."""
     dev = torch.cuda.current_device() if device is None else device
-    ms = (C.c_double * 5)()
-    n = (C.c_int * 5)()
+    ms = (C.c_double * len(CATEGORIES))()
+    n = (C.c_int * len(CATEGORIES))()
     L.call("pnp_ctx_profile_read", L.context(dev), ms, n)
     return {c: (float(ms[i]), int(n[i])) for i, c in enumerate(CATEGORIES)}
 
