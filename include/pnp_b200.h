@@ -109,14 +109,18 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
  *               3 Kx (C=1, x, rs)
  *   fixup mode: 0 rs = g^-1/2, 1 Kx, d + per-rank max bits, 2 d + max,
  *               3 frozen apply (out = Kx inv_m + (1 - d inv_m) x)
- *   finalize:   out = Kx/m + (1 - d/m) x with m from (all-reduced) mbits. */
+ *   finalize:   out = Kx/m + (1 - d/m) x with m from (all-reduced) mbits.
+ * kcache (nullable, pnp_dsg_kcache_floats(.., ntr) floats, caller-owned):
+ * pass 0 also stores the strip's pair weights, passes 1-3 then stream them
+ * instead of recomputing the patch filter (bitwise identical results). */
 int pnp_tile_height(int P);
 int pnp_dsg_groups(int Hg, int W, int R, int P);
 int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr);
+int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int ntr);
 int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float* x,
                         const float* rs, int Hg, int W, int buf_r0, int buf_rows, int tr0,
                         int ntr, int R, int P, const float* taps, double bandwidth,
-                        float* partial, int part_off, int part_ntr);
+                        float* partial, int part_off, int part_ntr, float* kcache);
 int pnp_dsg_strip_fixup(pnp_ctx* ctx, int mode, const float* partial, int part_tr0,
                         int part_ntr, int Hg, int W, int R, int P, int y0, int y1, int buf_r0,
                         int buf_rows, float* rs, float* kx, float* d, unsigned* mbits,

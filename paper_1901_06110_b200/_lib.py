@@ -55,8 +55,9 @@ _SIGS = {
     "pnp_tile_height": (i32, [i32]),
     "pnp_dsg_groups": (i32, [i32, i32, i32, i32]),
     "pnp_dsg_partial_floats": (i64, [i32, i32, i32, i32, i32, i32]),
+    "pnp_dsg_kcache_floats": (i64, [i32, i32, i32, i32, i32]),
     "pnp_dsg_strip_sweep": (i32, [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
-                                  fptr, f64, vp, i32, i32]),
+                                  fptr, f64, vp, i32, i32, vp]),
     "pnp_dsg_strip_fixup": (i32, [vp, i32, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                   vp, vp, vp, vp, vp, vp, vp]),
     "pnp_dsg_strip_finalize": (i32, [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32]),

@@ -930,10 +930,17 @@ int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr) {
   return (int64_t)ntr * groups_for(Hg, W, R, P) * ((W + kTW - 1) / kTW) * blk;
 }
 
+int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int ntr) {
+  if (check_geometry(1, Hg, W, R, P, 1.0) || ntr < 0) return -1;
+  int nch = 0;
+  for (int dx = -R; dx <= R; ++dx) nch += (R - (dx > 0 ? 0 : 1) + kKY) / kKY;
+  return (int64_t)nch * kKY * ntr * tile_height(P) * (((W + kTW - 1) / kTW) * kTW);
+}
+
 int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float* x,
                         const float* rs, int Hg, int W, int buf_r0, int buf_rows, int tr0,
                         int ntr, int R, int P, const float* taps, double bandwidth,
-                        float* partial, int part_off, int part_ntr) {
+                        float* partial, int part_off, int part_ntr, float* kcache) {
   if (!ctx || !guide || !partial) return fail(PNP_EINVAL, "null argument");
   int rc = check_geometry(1, Hg, W, R, P, bandwidth);
   if (rc) return rc;
@@ -945,22 +952,24 @@ int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float*
   if ((rc = make_geom(ctx, 1, Hg, W, R, P, g))) return rc;
   if (tr0 < 0 || tr0 + ntr > g.tiles_y) return fail(PNP_EINVAL, "tile rows out of range");
   Window w{buf_r0, buf_rows, tr0, ntr, 0, part_off, part_ntr, 0, 0};
+  const int use = kcache ? MODE_CACHED : MODE_RECOMPUTE;
   switch (pass) {
     case 0:  // mass g: y = in-image mask
       return run_sweep(ctx, g, w, 1, guide, ChanSpec{nullptr, nullptr},
-                       ChanSpec{nullptr, nullptr}, taps, bandwidth, true, partial);
+                       ChanSpec{nullptr, nullptr}, taps, bandwidth, true, partial,
+                       kcache ? MODE_STORE : MODE_RECOMPUTE, kcache);
     case 1:  // Kx and d: y = rs*x, rs
       if (!x || !rs) return fail(PNP_EINVAL, "pass 1 needs x and rs");
       return run_sweep(ctx, g, w, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps,
-                       bandwidth, true, partial);
+                       bandwidth, true, partial, use, kcache);
     case 2:  // d only: y = rs
       if (!rs) return fail(PNP_EINVAL, "pass 2 needs rs");
       return run_sweep(ctx, g, w, 1, guide, ChanSpec{rs, nullptr}, ChanSpec{nullptr, nullptr},
-                       taps, bandwidth, true, partial);
+                       taps, bandwidth, true, partial, use, kcache);
     case 3:  // Kx only: y = rs*x
       if (!x || !rs) return fail(PNP_EINVAL, "pass 3 needs x and rs");
       return run_sweep(ctx, g, w, 1, guide, ChanSpec{rs, x}, ChanSpec{nullptr, nullptr}, taps,
-                       bandwidth, true, partial);
+                       bandwidth, true, partial, use, kcache);
   }
   return fail(PNP_EINVAL, "unknown pass");
 }

@@ -5,11 +5,11 @@ one per rank (one process per GPU, ``torch.distributed`` over NCCL for the
 plumbing).  One adaptive denoise is
 
     halo rows of the input (p above, R + max(p, KY) below)   [P2P exchange]
-    sweep A (mass g) on own tile rows
+    sweep A (mass g) on own tile rows (+ the strip's k cache when it fits)
     the last ceil(R/TH) tile rows of partial blocks -> next rank
     fixup: rs = g^-1/2 on own rows
     R + KY rows of rs -> previous rank                         [P2P exchange]
-    sweep B (K x and d) on own tile rows
+    sweep B (K x and d) on own tile rows (streams the k cache if present)
     partial blocks -> next rank                                [P2P exchange]
     fixup: K x, d, local max d
     all-reduce max -> m (the north-star "alpha")               [NCCL max]
@@ -117,6 +117,19 @@ class _RankState:
         self.partial = torch.zeros(pf, dtype=torch.float32, device=device)
         self.block_floats_c1 = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, 1, 1))
         self.block_floats_c2 = 2 * self.block_floats_c1
+        self.kcache = None
+
+    def enable_kcache(self, headroom: int = 4 << 30) -> bool:
+        """Keep this strip's pair weights in HBM (sweep A stores, sweep B
+        streams them: bitwise neutral) when they fit with ``headroom`` spare."""
+        lay = self.lay
+        t0, t1 = lay.tile_rows
+        n = int(L.lib.pnp_dsg_kcache_floats(lay.Hg, lay.W, lay.R, lay.P, t1 - t0))
+        free, _ = torch.cuda.mem_get_info(self.buf.device)
+        if n <= 0 or 4 * n + headroom > free:
+            return False
+        self.kcache = torch.empty(n, dtype=torch.float32, device=self.buf.device)
+        return True
 
     # row views of the window (global row indices)
     def rows_view(self, t: torch.Tensor, r0: int, r1: int) -> torch.Tensor:
@@ -206,7 +219,7 @@ class ShardedDSG:
     TorchComm, or ``range(N)`` with a LocalComm (virtual shards)."""
 
     def __init__(self, params: PatchParams, Hg: int, W: int, nranks: int, ranks, comm,
-                 device=None):
+                 device=None, kcache: bool = True):
         if params.pad_margin > min(Hg, W):
             raise ValueError(f"margin {params.pad_margin} exceeds min image extent {min(Hg, W)}")
         self.params = params
@@ -217,6 +230,8 @@ class ShardedDSG:
             lay = StripLayout(Hg, W, params.window_radius, params.patch_side, nranks, r)
             lay.validate()
             self.states.append(_RankState(lay, self.device))
+            if kcache:
+                self.states[-1].enable_kcache()
         self._taps = params._ctaps()
 
     # ---- host-side views ---------------------------------------------------
@@ -241,7 +256,7 @@ class ShardedDSG:
         L.call("pnp_dsg_strip_sweep", L.context(self.device.index), pass_, L.ptr(st.buf),
                L.ptr(st.buf), L.ptr(st.rs), lay.Hg, lay.W, b0, b1 - b0, t0, t1 - t0,
                p.window_radius, p.patch_side, self._taps, float(p.bandwidth),
-               L.ptr(st.partial), off, nslot)
+               L.ptr(st.partial), off, nslot, L.ptr(st.kcache))
 
     def _fixup(self, st, mode):
         lay = st.lay
@@ -315,11 +330,13 @@ class ShardedDSG:
         return float(self.states[0].mbits.view(torch.float32)[0])
 
 
-def sharded_dsg_nlm_denoise(image: torch.Tensor, params: PatchParams, nshards: int) -> torch.Tensor:
+def sharded_dsg_nlm_denoise(image: torch.Tensor, params: PatchParams, nshards: int,
+                            kcache: bool = True) -> torch.Tensor:
     """Virtual-shard run on one device (N strips, LocalComm): same bits as
     ``dsg_nlm_denoise(image, params)``; exercises the multi-GPU algorithm."""
     H, W = image.shape
-    sh = ShardedDSG(params, H, W, nshards, range(nshards), LocalComm(), device=image.device)
+    sh = ShardedDSG(params, H, W, nshards, range(nshards), LocalComm(), device=image.device,
+                    kcache=kcache)
     sh.load(image)
     sh.denoise()
     return sh.gather()

@@ -15,12 +15,13 @@ pytestmark = pytest.mark.gpu
     (600, 130, 21, 3, None, 3),
     (1040, 256, 10, 7, 2.0, 8),
 ])
-def test_virtual_shards_bit_identical(H, W, R, P, sigma, N):
+@pytest.mark.parametrize("kcache", [True, False])
+def test_virtual_shards_bit_identical(H, W, R, P, sigma, N, kcache):
     import paper_1901_06110_b200 as pnp
     from paper_1901_06110_b200.parallel import sharded_dsg_nlm_denoise
     g = torch.Generator(device="cuda").manual_seed(H * W + N)
     x = torch.rand(H, W, device="cuda", generator=g)
     p = pnp.PatchParams(P, R, 0.15, sigma)
     ref, d, m = pnp.dsg_nlm_denoise(x, p, return_aux=True)
-    out = sharded_dsg_nlm_denoise(x, p, N)
+    out = sharded_dsg_nlm_denoise(x, p, N, kcache=kcache)
     assert torch.equal(out, ref)
