@@ -117,9 +117,10 @@ struct SweepArgs {
   int tr0, tiles_x;
   int part_off, part_ntr;
   // k cache, tile-major, offset pairs packed: the weights of offsets
-  // (2kp, 2kp+1) of chunk ci for pixel (row, col) of a tile are one float2 at
-  // kcache[b*kc_img + (tile*kc_npairs + ci*KY/2 + kp)*TH*64 + row*64 + col]
-  // (float2 units) -> a chunk is one contiguous 2*TH*64*8 B run per tile
+  // (2kp, 2kp+1) of chunk ci for a pixel of a tile are one float2 in pair
+  // plane (tile*kc_npairs + ci*KY/2 + kp) of TH*64 float2 (row groups of N
+  // rows, row pairs interleaved per column: kpos) -> a chunk is one
+  // contiguous 2*TH*64*8 B run per tile
   float2* kcache;
   long long kc_img;
   int kc_npairs;
@@ -195,6 +196,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
   } while (!ok);
+}
+
+// Offset (float2 units) of row r, column c inside one row group of a k-cache
+// pair plane: rows (2i, 2i+1) interleaved per column (16 B), an odd last row
+// stored plainly after them.
+template <int N>
+__device__ __forceinline__ int kpos(int c, int r) {
+  return (r < (N & ~1)) ? ((r >> 1) * kTW + c) * 2 + (r & 1) : (N & ~1) * kTW + c;
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -416,26 +425,41 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 #pragma unroll
       for (int j = 0; j < WIN - 1; ++j) pf[c_][j] = make_float2(0.f, 0.f);
     }
-    // this chunk's pair planes; thread (c, g) owns rows r0.. of column c
-    const float2* kq = CACHED || STORE ? kimg + (long long)ci * (KY / 2) * (TH * kTW) + r0 * kTW + c
+    // this chunk's pair planes; thread (c, g) owns rows r0.. of column c.
+    // Within a plane, a row group's N rows are stored row-pair interleaved:
+    // rows (2i, 2i+1) of column c are one 16 B vector (kpos), so stores and
+    // loads are 128-bit (N odd: the last row is a plain float2 row).
+    const float2* kq = CACHED || STORE ? kimg + (long long)ci * (KY / 2) * (TH * kTW) + r0 * kTW
                                        : nullptr;
     float2 kcl[CACHED && !TMAK ? KY / 2 : 1][N];
     if (CACHED && !TMAK) {
       // register path (C = 1): all the chunk's loads in flight together
       // (predicated, not branched)
 #pragma unroll
-      for (int kp = 0; kp < KY / 2; ++kp)
+      for (int kp = 0; kp < KY / 2; ++kp) {
 #pragma unroll
-        for (int r = 0; r < N; ++r) {
-          const float2* src = kq + (kp * TH + r) * kTW;
+        for (int r = 0; r + 1 < N; r += 2) {
+          const float2* src = kq + kp * TH * kTW + kpos<N>(c, r);
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          asm volatile(
+              "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %5, %6;\n\t"
+              "@q ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+              : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+              : "l"(src), "r"(2 * kp), "r"(kc));
+          kcl[kp][r] = make_float2(v.x, v.y);
+          kcl[kp][r + 1] = make_float2(v.z, v.w);
+        }
+        if (N & 1) {
+          const float2* src = kq + kp * TH * kTW + kpos<N>(c, N - 1);
           float2 v = make_float2(0.f, 0.f);
           asm volatile(
               "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %3, %4;\n\t"
               "@q ld.global.cs.v2.f32 {%0, %1}, [%2];\n\t}"
               : "+f"(v.x), "+f"(v.y)
               : "l"(src), "r"(2 * kp), "r"(kc));
-          kcl[kp][r] = v;
+          kcl[kp][N - 1] = v;
         }
+      }
     }
     const float2* kb = nullptr;  // TMAK: SMEM copy of this chunk
     if (TMAK) {
@@ -452,7 +476,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
       }
       mbar_wait(mbar + (ci & 1), (kphase >> (ci & 1)) & 1u);
       kphase ^= 1u << (ci & 1);
-      kb = reinterpret_cast<const float2*>(Ks + (ci & 1) * K::KCH) + r0 * kTW + c;
+      kb = reinterpret_cast<const float2*>(Ks + (ci & 1) * K::KCH) + r0 * kTW;
     }
 #pragma unroll
     for (int kp = 0; kp < KY / 2; ++kp) {
@@ -460,7 +484,12 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
         float2 kk[N];
         if (TMAK) {
 #pragma unroll
-          for (int r = 0; r < N; ++r) kk[r] = kb[(kp * TH + r) * kTW];
+          for (int r = 0; r + 1 < N; r += 2) {
+            const float4 v = *reinterpret_cast<const float4*>(kb + kp * TH * kTW + kpos<N>(c, r));
+            kk[r] = make_float2(v.x, v.y);
+            kk[r + 1] = make_float2(v.z, v.w);
+          }
+          if (N & 1) kk[N - 1] = kb[kp * TH * kTW + kpos<N>(c, N - 1)];
         } else if (CACHED) {
 #pragma unroll
           for (int r = 0; r < N; ++r) kk[r] = kcl[CACHED && !TMAK ? kp : 0][r];
@@ -477,7 +506,14 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
             for (int aa = 0; aa < P; ++aa)
               v = __ffma2_rn(make_float2(a.taps_v[aa], a.taps_v[aa]), hcol[r + aa], v);
             kk[r] = make_float2(ex2_approx(v.x), ex2_approx(v.y));
-            if (STORE) __stcs(const_cast<float2*>(kq) + (kp * TH + r) * kTW, kk[r]);
+            if (STORE) {
+              float2* dst = const_cast<float2*>(kq) + kp * TH * kTW + kpos<N>(c, r & ~1);
+              if (r & 1)
+                __stcs(reinterpret_cast<float4*>(dst),
+                       make_float4(kk[r - 1].x, kk[r - 1].y, kk[r].x, kk[r].y));
+              else if (r == N - 1)
+                __stcs(dst, kk[r]);
+            }
           }
         }
 #pragma unroll

@@ -53,3 +53,13 @@ for _ in range(5):
 torch.cuda.synchronize()
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+# per-category device time inside the loop (CUDA events around each launch)
+from paper_1901_06110_b200 import profiling  # noqa: E402
+profiling.enable(True)
+run()
+torch.cuda.synchronize()
+pr = profiling.read()
+profiling.enable(False)
+print({k: (round(v[0] / ITERS * 1e3, 1), v[1] // ITERS) for k, v in pr.items() if v[1]},
+      "(us per iteration, launches per iteration)")
