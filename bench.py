@@ -350,16 +350,29 @@ def run_gpu(args, rank, world, local_rank):
     line["clocks"] = clocks
 
     if not args.no_extras:
-        # e2e through the public API with pinned host buffers
+        # e2e through the public API with pinned host buffers: every step
+        # uploads its image, denoises and downloads the result (DenoiseStream:
+        # H2D / compute / D2H on three streams, overlapped across steps)
         if world == 1:
             host_in = torch.from_numpy(make_image_rows(n, 0, n)).pin_memory()
-            host_out = torch.empty_like(host_in).pin_memory()
+            stream = pnp.DenoiseStream(params, (n, n))
+            host_outs = [torch.empty_like(host_in).pin_memory() for _ in range(2)]
+            nbytes = host_in.numel() * 4
+            stream.run([host_in] * 2, host_outs)  # warm-up
+            torch.cuda.synchronize()
+            barrier()
+            e0.record()
+            stream.run([host_in] * args.steps, [host_outs[i % 2] for i in range(args.steps)])
+            e1.record()
+            torch.cuda.synchronize()
+            t_stream = e0.elapsed_time(e1) / args.steps
+            ref_out = pnp.dsg_nlm_denoise(host_in.to(dev), params).cpu()
+            assert torch.equal(host_outs[(args.steps - 1) % 2], ref_out), "stream != denoise"
 
-            def e2e_step():
+            def e2e_step():  # the synchronous single-image call, reported beside it
                 xd = host_in.to(dev, non_blocking=True)
                 yd = pnp.dsg_nlm_denoise(xd, params)
-                host_out.copy_(yd, non_blocking=True)
-            nbytes = host_in.numel() * 4
+                host_outs[0].copy_(yd, non_blocking=True)
         else:
             own = torch.from_numpy(make_image_rows(n, y0, y1)).pin_memory()
             host_out = torch.empty_like(own).pin_memory()
@@ -381,11 +394,22 @@ def run_gpu(args, rank, world, local_rank):
         t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        line["e2e"] = {"value": units / (float(t[0]) * 1e-3) / 1e9, "unit": "Gpixel*offset/s",
-                       "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
-                       "ms_per_step": float(t[0]),
-                       "api": "paper_1901_06110_b200.dsg_nlm_denoise(torch CUDA tensor)"
-                              if world == 1 else "parallel.ShardedDSG.denoise"}
+        if world == 1:
+            line["e2e"] = {"value": units / (t_stream * 1e-3) / 1e9, "unit": "Gpixel*offset/s",
+                           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                           "ms_per_step": t_stream,
+                           "api": "paper_1901_06110_b200.DenoiseStream.run(pinned host images): "
+                                  "per step H2D + dsg_nlm_denoise + D2H, overlapped across "
+                                  "steps on 3 streams",
+                           "sync_call": {"value": units / (float(t[0]) * 1e-3) / 1e9,
+                                         "ms_per_step": float(t[0]),
+                                         "api": "host->device copy, dsg_nlm_denoise, "
+                                                "device->host copy, one image at a time"}}
+        else:
+            line["e2e"] = {"value": units / (float(t[0]) * 1e-3) / 1e9, "unit": "Gpixel*offset/s",
+                           "h2d_bytes_per_step": nbytes * world,
+                           "d2h_bytes_per_step": nbytes * world, "ms_per_step": float(t[0]),
+                           "api": "parallel.ShardedDSG.denoise"}
         if rank == 0 and world == 1:
             profiling.set_cache_limit(0, local_rank)      # free the adaptive k cache (59 GB)
             profiling.set_cache_limit(None, local_rank)   # (frozen guides keep their own)

@@ -175,6 +175,9 @@ int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, do
  * element of x (n floats, device, 16 B aligned) is NaN/Inf, else 0.  One
  * pass on the ctx stream, then a synchronizing 4-byte read-back. */
 int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite);
+/* Stream-ordered variant for pipelines: *flag (device int) |= 1 when x holds
+ * a NaN/Inf; no synchronization. */
+int pnp_flag_nonfinite(pnp_ctx* ctx, const float* x, int64_t n, int* flag);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,7 @@ from .solver import (  # noqa: F401
     residuals,
     write_log_csv,
 )
+from .stream import DenoiseStream, denoise_host_sequence  # noqa: F401
 from .synth import SplitMix64  # noqa: F401
 
 __version__ = "0.1.0"

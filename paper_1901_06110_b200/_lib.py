@@ -71,6 +71,7 @@ _SIGS = {
     "pnp_admm_uupdate": (i32, [vp, vp, vp, vp, vp, vp, i32, i64, f64, vp, vp]),
     "pnp_project": (i32, [vp, vp, vp, i64, f64, f64]),
     "pnp_check_finite": (i32, [vp, vp, i64, C.POINTER(i32)]),
+    "pnp_flag_nonfinite": (i32, [vp, vp, i64, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

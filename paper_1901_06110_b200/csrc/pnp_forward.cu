@@ -534,6 +534,17 @@ int pnp_qis_simulate_host(const double* stop, int64_t n, int K, uint64_t seed, d
 }
 
 
+int pnp_flag_nonfinite(pnp_ctx* ctx, const float* x, int64_t n, int* flag) {
+  if (!ctx || !x || !flag || n < 0) return fail(PNP_EINVAL, "null argument");
+  if (((uintptr_t)x & 15) != 0) return fail(PNP_EINVAL, "x must be 16-byte aligned");
+  {
+    ProfScope prof_(ctx, PROF_CHECK);
+    nonfinite_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>(x, (size_t)n, flag);
+  }
+  PNP_LAUNCH_CHECK("nonfinite_kernel");
+  return PNP_OK;
+}
+
 int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite) {
   if (!ctx || !x || !all_finite || n < 0) return fail(PNP_EINVAL, "null argument");
   if (((uintptr_t)x & 15) != 0) return fail(PNP_EINVAL, "x must be 16-byte aligned");

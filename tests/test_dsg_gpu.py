@@ -183,3 +183,18 @@ def test_k_cache_is_bitwise_neutral(pnp, rng):
     finally:
         profiling.set_cache_limit(None)
     assert torch.equal(a, b) and torch.equal(ya, yb) and torch.equal(a, ya)
+
+
+def test_denoise_stream_pipeline(pnp, rng):
+    """Pipelined H2D / denoise / D2H over a sequence == per-image calls,
+    bitwise; a non-finite image is reported by index."""
+    p = pnp.PatchParams(7, 10, 0.05, 2.0)
+    imgs = [torch.tensor(rng.random((150, 210)), dtype=torch.float32).pin_memory()
+            for _ in range(5)]
+    outs = pnp.DenoiseStream(p, (150, 210), depth=2).run(imgs)
+    for im, o in zip(imgs, outs):
+        assert torch.equal(o, pnp.dsg_nlm_denoise(im.cuda(), p).cpu())
+    bad = [im.clone() for im in imgs]
+    bad[3][10, 20] = float("nan")
+    with pytest.raises(ValueError, match="image 3"):
+        pnp.DenoiseStream(p, (150, 210)).run(bad)
