@@ -8,4 +8,4 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:dsg_
   -o gpurun_out/sweeps_cache_$tag python scripts/prof_dsg.py 8192 > gpurun_out/ncu_cache_$tag.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:dsg_sweep -c 2 \
   -o gpurun_out/sweeps_nocache_$tag python scripts/prof_dsg.py 8192 --nocache > gpurun_out/ncu_nocache_$tag.log 2>&1
-tail -1 gpurun_out/ncu_cache_$tag.log gpurun_out/ncu_nocache_$tag.log
+tail -n 1 gpurun_out/ncu_cache_$tag.log; tail -n 1 gpurun_out/ncu_nocache_$tag.log
