@@ -18,23 +18,31 @@
 // same code computes freeze/apply/adaptive so FrozenGuide.apply is
 // bit-identical to dsg_nlm_denoise (reference tests/test_denoise.py:256-268).
 //
-// Patch filter, per chunk of KY offsets sharing dx (consecutive dy):
+// Patch filter, per chunk of KY offsets sharing dx (consecutive dy), in
+// packed f32x2 over offset pairs (k, k+1) (sm_100 FFMA2 / FADD2 / FMUL2):
 //   phase 1  lane = map row q (32 rows = TH + 2p), warp = 16-column segment;
-//            the own guide row segment (16+2p) lives in registers for the
-//            whole kernel, the partner segment is read from SMEM;
-//            D = (G_own - G_partner)^2, horizontal P-tap filter -> H_k[q][c]
-//            in SMEM (odd row stride: conflict-free writes).
-//   phase 2  thread = (column c, row group g of N rows): vertical P-tap
-//            filter of H_k's column with the exponent scale and log2(hat)
-//            folded in, MUFU ex2, near FFMA, far FFMA into a register window
-//            of N+KY-1 rows, then one flush per chunk (group 0 before the
-//            chunk barrier, group 1 after it: one shared far buffer, no race).
-// All SMEM strides are compile-time (R bucket RB >= R), so every access is a
-// base register + immediate offset.
+//            the own guide row segment (16+2p, negated) lives in registers for
+//            the whole kernel as the broadcast operand, the two partner rows
+//            are read from SMEM; (D_k, D_k+1) = (G_partner - G_own)^2, then the
+//            horizontal P-tap filter -> one float2 H map per offset pair
+//            (odd row stride: conflict-free 64-bit stores).
+//   phase 2  thread = (column c, row group g of N rows): vertical P-tap filter
+//            of the H column with the exponent scale folded into the taps and
+//            (log2 hat_k, log2 hat_k+1) as the initial pair, two MUFU ex2,
+//            near FFMA into registers, far FFMA2 (both offsets at once) into a
+//            register window, one flush per chunk (group 0 before the chunk
+//            barrier, group 1 after it: one shared far plane, no race).
+// The offset table rides in the kernel parameters (constant bank); all SMEM
+// strides are compile-time (R bucket RB >= R).
+//
+// Modes: RECOMPUTE (the fused offset loop), STORE (also writes every pair
+// weight to the HBM k cache), CACHED (streams the weights back: no guide, no
+// filter; C = 2 through SMEM with bulk async copies + mbarriers).  Same
+// floats, same add order -> bitwise identical results in all three.
 //
 // The tile writes its accumulators over rows [0, TH+R) x cols [-R, TW+R)
-// (tile + far band) to a partial block; dsg_fixup sums the covering blocks of
-// every pixel in a fixed order.
+// (tile + far band) to a partial block; the fixup kernels sum the covering
+// blocks of every pixel in a fixed order.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -573,9 +581,9 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   }
 }
 
-// Sum of all partial blocks covering global pixel (y, x), fixed order
-// (group, tile row, tile col).  Slot 0 of the partial array holds global
-// tile row part_tr0.
+// Fixup geometry: the partial blocks covering global pixel (y, x) are summed
+// in a fixed order (group, tile row, tile col) by the fixup kernels
+// (pnp_dsg.cu).  Slot 0 of the partial array holds global tile row part_tr0.
 struct FixGeo {
   const float* partial;
   int Hg, W, R, TH, tiles_x, NG, C;
@@ -583,29 +591,5 @@ struct FixGeo {
   int y0, nrows;          // output rows [y0, y0 + nrows) (global)
   int buf_r0, buf_rows;   // per-pixel buffers' window
 };
-
-__device__ __forceinline__ float gather_partial(const FixGeo& f, int b, int c_, int y, int x) {
-  const int BR = f.TH + f.R, BC = kTW + 2 * f.R;
-  const int ti = y / f.TH, tj = x / kTW;
-  const int dti = (f.R + f.TH - 1) / f.TH, dtj = (f.R + kTW - 1) / kTW;
-  const int ti0 = max(max(f.part_tr0, 0), ti - dti), ti1 = min(ti, f.part_tr0 + f.part_ntr - 1);
-  const int tj0 = max(0, tj - dtj), tj1 = min(f.tiles_x - 1, tj + dtj);
-  const size_t blk = (size_t)f.C * BR * BC;
-  const float* base = f.partial + (size_t)b * f.part_ntr * f.NG * f.tiles_x * blk + (size_t)c_ * BR * BC;
-  float s = 0.f;
-  for (int gg = 0; gg < f.NG; ++gg) {
-    for (int t_i = ti0; t_i <= ti1; ++t_i) {
-      const int br = y - t_i * f.TH;
-      if (br >= BR) continue;
-      const float* row = base + ((size_t)(t_i - f.part_tr0) * f.NG + gg) * f.tiles_x * blk;
-      for (int t_j = tj0; t_j <= tj1; ++t_j) {
-        const int bc = x - t_j * kTW + f.R;
-        if (bc < 0 || bc >= BC) continue;
-        s = __fadd_rn(s, __ldg(row + (size_t)t_j * blk + br * BC + bc));
-      }
-    }
-  }
-  return s;
-}
 
 }  // namespace pnp

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
 // window's first tile row, tile column blockIdx.x).  Thread (lx, ly0) owns
 // column lx and rows ly0, ly0+4, ... of the tile, so every covering partial
 // block is visited by all threads in the same fixed order (group, tile row,
-// tile col) -- the per-pixel summation order of gather_partial -- while each
+// tile col) -- the per-pixel summation order shared by all fixups -- while each
 // thread keeps up to 8 independent loads in flight per block.
 constexpr int kFixRows = 8;  // rows per thread (TH <= 32, 4 row phases)
 
