@@ -170,6 +170,23 @@ int pnp_admm_uupdate(pnp_ctx* ctx, float* u, const float* x, const float* v,
                      const float* v_prev, const float* gt, int batch, int64_t n,
                      double rho, double* stats, int* flags);
 /* y = clamp(x) */
+/* Fused ADMM steps (same per-pixel arithmetic as the unfused calls):
+ * grad f(x) + x-update (x <- proj(mu (alpha x + rho (v - u) - grad)), z = x + u,
+ * flags |= 1 / 2 on non-finite x / z) in the gradient kernel's epilogue, and
+ * the frozen DSG apply v = W z + u-update (u += x - v, stats[b*4+0..2] =
+ * sum (x-v)^2, sum (rho (v - v_prev))^2, sum (gt - v)^2, flags |= 4) in the
+ * apply's fixup epilogue.  data_out (nullable): f(x) per image. */
+int pnp_sr_grad_xupdate(pnp_ctx* ctx, float* x, const float* yobs, int batch, int H, int W,
+                        const float* taps, int radius, int factor, int boundary, double* data_out,
+                        const float* v, const float* u, float* z, double mu, double alpha,
+                        double rho, double lo, double hi, int* flags);
+int pnp_qis_grad_xupdate(pnp_ctx* ctx, float* x, const float* ones, const float* zeros, int batch,
+                         int n, double gain_over_K, double floor_, double* data_out,
+                         const float* v, const float* u, float* z, double mu, double alpha,
+                         double rho, double lo, double hi, int* flags);
+int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v, float* u,
+                       const float* x, const float* v_prev, const float* gt, double rho,
+                       double* stats, int* flags);
 int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, double hi);
 /* Validation helper (reference image.py:35-40): *all_finite = 1 when no
  * element of x (n floats, device, 16 B aligned) is NaN/Inf, else 0.  One

@@ -70,6 +70,11 @@ _SIGS = {
     "pnp_admm_xupdate": (i32, [vp, vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, vp]),
     "pnp_admm_uupdate": (i32, [vp, vp, vp, vp, vp, vp, i32, i64, f64, vp, vp]),
     "pnp_project": (i32, [vp, vp, vp, i64, f64, f64]),
+    "pnp_sr_grad_xupdate": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, vp,
+                                  vp, vp, vp, f64, f64, f64, f64, f64, vp]),
+    "pnp_qis_grad_xupdate": (i32, [vp, vp, vp, vp, i32, i32, f64, f64, vp,
+                                   vp, vp, vp, f64, f64, f64, f64, f64, vp]),
+    "pnp_dsg_apply_admm": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp]),
     "pnp_check_finite": (i32, [vp, vp, i64, C.POINTER(i32)]),
     "pnp_flag_nonfinite": (i32, [vp, vp, i64, vp]),
 }
@@ -116,18 +121,28 @@ def host_floats(values) -> C.Array:
 _tls = threading.local()
 
 
-def context(device: int):
-    """Per-(thread, device) native context, bound to torch's current stream."""
+def _raw_stream(device: int) -> int:
     import torch
 
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:  # no Stream object per call (this sits on every launch path)
+        return int(get(device))
+    return int(torch.cuda.current_stream(device).cuda_stream)
+
+
+def context(device: int):
+    """Per-(thread, device) native context, bound to torch's current stream
+    (re-bound only when the current stream changed)."""
     ctxs = getattr(_tls, "ctxs", None)
     if ctxs is None:
         ctxs = _tls.ctxs = {}
-    c = ctxs.get(device)
-    if c is None:
+    ent = ctxs.get(device)
+    if ent is None:
         h = vp()
         check(lib.pnp_ctx_create(device, C.byref(h)))
-        c = ctxs[device] = h
-    stream = torch.cuda.current_stream(device).cuda_stream
-    check(lib.pnp_ctx_set_stream(c, vp(stream)))
-    return c
+        ent = ctxs[device] = [h, None]
+    stream = _raw_stream(device)
+    if stream != ent[1]:
+        check(lib.pnp_ctx_set_stream(ent[0], vp(stream)))
+        ent[1] = stream
+    return ent[0]

@@ -56,7 +56,7 @@ void DevBuf::release() {
 
 // ---------------------------------------------------------------- kernels --
 
-enum FixMode { FIX_RS = 0, FIX_KXD = 1, FIX_D = 2, FIX_APPLY = 3, FIX_NLM = 4 };
+enum FixMode { FIX_RS = 0, FIX_KXD = 1, FIX_D = 2, FIX_APPLY = 3, FIX_NLM = 4, FIX_APPLY_U = 5 };
 
 // Per-pixel buffers are windows [buf_r0, buf_r0 + buf_rows) x W (FixGeo).
 struct FixIO {
@@ -67,7 +67,65 @@ struct FixIO {
   const float* inv_m;  // per image (APPLY)
   const float* x;      // (APPLY)
   float* out;          // (APPLY, NLM)
+  // FIX_APPLY_U: the ADMM u-update fused into the frozen apply (solver.py:
+  // 222-228): v = out, u += x_admm - v, per-CTA partials of sum (x-v)^2,
+  // sum (rho (v - v_prev))^2, sum (gt - v)^2, finite flags
+  float* u;
+  const float* xa;
+  const float* vprev;
+  const float* gt;
+  double rho;
+  double* part3;       // [B][gridDim.y * gridDim.x][3]
+  int* flags;
 };
+
+// u-update of one pixel (same arithmetic as admm_uupdate_kernel)
+__device__ __forceinline__ int admm_u_pixel(const FixIO& io, size_t o, float v, double& s0,
+                                            double& s1, double& s2) {
+  const double xv = io.xa[o], vv = v;
+  const float un = (float)((double)io.u[o] + (xv - vv));
+  io.u[o] = un;
+  s0 += (xv - vv) * (xv - vv);
+  const double dv = io.rho * (vv - (io.vprev ? (double)io.vprev[o] : 0.0));
+  s1 += dv * dv;
+  if (io.gt) {
+    const double e = (double)io.gt[o] - vv;
+    s2 += e * e;
+  }
+  return (!isfinite(vv) || !isfinite(un)) ? 4 : 0;
+}
+
+// block-level epilogue of FIX_APPLY_U: flags + deterministic stats partials
+__device__ __forceinline__ void admm_u_block(const FixIO& io, int b, int f, double s0, double s1,
+                                             double s2) {
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(io.flags, f);
+  __shared__ double red3[3][8];
+  for (int off = 16; off; off >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+  }
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red3[0][wid] = s0;
+    red3[1][wid] = s1;
+    red3[2][wid] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a0 = 0, a1 = 0, a2 = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      a0 += red3[0][k];
+      a1 += red3[1][k];
+      a2 += red3[2][k];
+    }
+    double* pp = io.part3 + (((size_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 3;
+    pp[0] = a0;
+    pp[1] = a1;
+    pp[2] = a2;
+  }
+}
 
 __device__ __forceinline__ float dsg_finish(float kx, float d, float inv_m, float x) {
   const float w = __fmul_rn(kx, inv_m);
@@ -157,10 +215,17 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
   }
 
   float dmax = 0.f;
+  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  int uf = 0;
   if (own) {
     const size_t o = (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x;
     const float s0 = s[0];
-    if (MODE == FIX_RS) {
+    if (MODE == FIX_APPLY_U) {
+      const float kx = __fmul_rn(io.rs[o], s0);
+      const float v = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
+      io.out[o] = v;
+      uf = admm_u_pixel(io, o, v, u0, u1, u2);
+    } else if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
       const float r = io.rs[o];
@@ -177,6 +242,7 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
       io.out[o] = __fdiv_rn(s0, s[C - 1]);
     }
   }
+  if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2);
   if (MODE == FIX_KXD || MODE == FIX_D) {
     // d > 0, so the int ordering of the bits is the float ordering; max is
     // exact and order-free -> deterministic.
@@ -270,13 +336,20 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
     }
 
   float dmax = 0.f;
+  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  int uf = 0;
 #pragma unroll
   for (int k = 0; k < kFixRows; ++k) {
     const int y = ti * TH + ly0 + 4 * k;
     if (ly0 + 4 * k >= TH || y < ylo || y >= yhi || x >= W) continue;
     const size_t o = (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x;
     const float s0 = s[0][k];
-    if (MODE == FIX_RS) {
+    if (MODE == FIX_APPLY_U) {
+      const float kx = __fmul_rn(io.rs[o], s0);
+      const float v = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
+      io.out[o] = v;
+      uf |= admm_u_pixel(io, o, v, u0, u1, u2);
+    } else if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
       const float r = io.rs[o];
@@ -295,6 +368,7 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
       io.out[o] = __fdiv_rn(s0, s[C - 1][k]);
     }
   }
+  if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2);
   if (MODE == FIX_KXD || MODE == FIX_D) {
     // d > 0, so the int ordering of the bits is the float ordering; max is
     // exact and order-free -> deterministic.
@@ -851,6 +925,43 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
   io.x = x;
   io.out = out;
   return run_fixup<FIX_APPLY>(ctx, g, w, 1, part, io);
+}
+
+int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v,
+                       float* u, const float* x, const float* v_prev, const float* gt,
+                       double rho, double* stats, int* flags) {
+  if (!ctx || !fz || !z || !v || !u || !x || !stats || !flags)
+    return fail(PNP_EINVAL, "null argument");
+  if (fz->device != ctx->device) return fail(PNP_EINVAL, "handle belongs to another device");
+  PNP_CUDA(cudaSetDevice(ctx->device));
+  Geom g;
+  int rc = make_geom(ctx, fz->B, fz->H, fz->W, fz->R, fz->P, g);
+  if (rc) return rc;
+  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
+  const Window w = full_window(g);
+  const int rows = g.NG <= 2 ? g.tiles_y : g.tiles_y * ((g.TH + 3) / 4);
+  const size_t nblk = (size_t)g.tiles_x * rows;
+  if ((rc = ctx->stats.ensure((size_t)g.B * nblk * 3 * sizeof(double)))) return rc;
+  float* part = ctx->partial.as<float>();
+  if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, z}, ChanSpec{nullptr, nullptr},
+                      fz->taps, fz->bw, true, part, fz->kcache ? MODE_CACHED : MODE_RECOMPUTE,
+                      fz->kcache)))
+    return rc;
+  FixIO io{};
+  io.rs = fz->rs;
+  io.d = fz->d;
+  io.inv_m = fz->mv + fz->B;
+  io.x = z;
+  io.out = v;
+  io.u = u;
+  io.xa = x;
+  io.vprev = v_prev;
+  io.gt = gt;
+  io.rho = rho;
+  io.part3 = ctx->stats.as<double>();
+  io.flags = flags;
+  if ((rc = run_fixup<FIX_APPLY_U>(ctx, g, w, 1, part, io))) return rc;
+  return reduce_stats3(ctx, io.part3, (int)nblk, g.B, stats);
 }
 
 int pnp_frozen_destroy(pnp_frozen* fz) {

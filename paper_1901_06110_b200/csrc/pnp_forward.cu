@@ -69,6 +69,38 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const double* part
   }
 }
 
+// The linearized-ADMM x-update (solver.py:219-221) fused into a gradient
+// kernel's epilogue: x <- proj(mu (alpha x + rho (v - u) - grad)), z = x + u,
+// finite flags -- the arithmetic of admm_xupdate_kernel, per pixel.
+struct XUpd {
+  float* x;
+  const float* v;
+  const float* u;
+  float* z;
+  double mu, alpha, rho;
+  float lo, hi;
+  int* flags;
+};
+
+__device__ __forceinline__ int xupdate_pixel(const XUpd& q, size_t i, float grad) {
+  const double xv = (double)q.x[i];
+  const double uv = (double)q.u[i];
+  const double xn = q.mu * (q.alpha * xv + q.rho * ((double)q.v[i] - uv) - (double)grad);
+  float xf = (float)xn;
+  int f = isfinite(xf) ? 0 : 1;
+  xf = fminf(fmaxf(xf, q.lo), q.hi);
+  const float zf = (float)((double)xf + uv);
+  if (!isfinite(zf)) f |= 2;
+  q.x[i] = xf;
+  q.z[i] = zf;
+  return f;
+}
+
+__device__ __forceinline__ void flags_or(int* flags, int f) {
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
 // SR blur kernels, SMEM tiled: the image region of a tile (+ radius halo,
 // boundary-mapped once at staging) is filtered separably -- horizontal taps
 // into a row buffer, then vertical taps -- in the reference's summation order
@@ -130,9 +162,10 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
 
 // x_out = A^T r = blur(upsample_k(r)) on the high-res grid: the zero-filled
 // upsampled tile (+ halo, boundary-mapped) is staged, then filtered.
+template <bool XU>
 __global__ void __launch_bounds__(256)
 sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, int W, int k,
-                  int rad, int sym, const Taps taps) {
+                  int rad, int sym, const Taps taps, const XUpd q) {
   extern __shared__ float sm[];
   const int h = H / k, w = W / k, b = blockIdx.z;
   const int S = kSrTA + 2 * rad;
@@ -156,14 +189,20 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, i
     Hh[i] = s;
   }
   __syncthreads();
+  int f = 0;
   for (int i = threadIdx.x; i < kSrTA * kSrTA; i += blockDim.x) {
     const int yy = i / kSrTA, xx = i - yy * kSrTA;
     const int py = py0 + yy, px = px0 + xx;
     if (py >= H || px >= W) continue;
     float acc = 0.f;
     for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
-    out[(size_t)b * H * W + (size_t)py * W + px] = acc;
+    const size_t o = (size_t)b * H * W + (size_t)py * W + px;
+    if (XU)
+      f |= xupdate_pixel(q, o, acc);
+    else
+      out[o] = acc;
   }
+  if (XU) flags_or(q.flags, f);
 }
 
 static size_t sr_res_smem(int k, int rad) {
@@ -188,26 +227,37 @@ static cudaError_t sr_smem_attr(size_t res, size_t adj) {
     if (e == cudaSuccess) set_res = res;
   }
   if (e == cudaSuccess && adj > set_adj) {
-    e = cudaFuncSetAttribute(sr_adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj);
+    e = cudaFuncSetAttribute(sr_adjoint_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)adj);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(sr_adjoint_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)adj);
     if (e == cudaSuccess) set_adj = adj;
   }
   return e;
 }
 
+template <bool XU>
 __global__ void __launch_bounds__(256)
 qis_grad_kernel(const float* __restrict__ x, const float* __restrict__ ones,
                 const float* __restrict__ zeros, float* __restrict__ grad, size_t n,
-                double gk, double floor_, double* partial) {
+                double gk, double floor_, double* partial, const XUpd q) {
   const int b = blockIdx.y;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   double term = 0.0;
+  int f = 0;
   if (i < n) {
     const size_t o = (size_t)b * n + i;
     const double z = gk * fmax((double)x[o], floor_);
     const double k1 = ones[o], k0 = zeros[o];
-    if (grad) grad[o] = (float)(gk * (k0 - k1 / expm1(z)));
     if (partial) term = k0 * z - k1 * log(-expm1(-z));
+    const float gv = (float)(gk * (k0 - k1 / expm1(z)));
+    if (XU)
+      f = xupdate_pixel(q, o, gv);
+    else if (grad)
+      grad[o] = gv;
   }
+  if (XU) flags_or(q.flags, f);
   if (partial) block_sum_store(term, partial);
 }
 
@@ -331,6 +381,16 @@ __global__ void __launch_bounds__(256) nonfinite_kernel(const float* __restrict_
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// stats[b*4 + k] = sum_j part[b][j][k], k < 3 (fixed order)
+int reduce_stats3(pnp_ctx* ctx, const double* part, int nblk, int batch, double* stats) {
+  {
+    ProfScope prof_(ctx, PROF_ADMM);
+    reduce_partials_kernel<<<dim3(batch, 3), 256, 0, ctx->stream>>>(part, nblk, 3, 1.0, stats, 4);
+  }
+  PNP_LAUNCH_CHECK("reduce_partials_kernel");
+  return PNP_OK;
+}
+
 }  // namespace pnp
 
 using namespace pnp;
@@ -364,16 +424,17 @@ int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int
   PNP_CUDA(sr_smem_attr(0, as));
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_adjoint_kernel<<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(y, x, H, W, factor,
-                                                                          radius, boundary, t);
+    sr_adjoint_kernel<false><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
+        y, x, H, W, factor, radius, boundary, t, XUpd{});
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
 }
 
-int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, int batch, int H,
-                int W, const float* taps, int radius, int factor, int boundary, double* data_out) {
-  if (!ctx || !x || !yobs || !grad) return fail(PNP_EINVAL, "null argument");
+static int sr_grad_impl(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, int batch,
+                        int H, int W, const float* taps, int radius, int factor, int boundary,
+                        double* data_out, const XUpd* xu) {
+  if (!ctx || !x || !yobs || (!grad && !xu)) return fail(PNP_EINVAL, "null argument");
   Taps t;
   int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
   if (rc) return rc;
@@ -401,16 +462,21 @@ int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, in
   }
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_adjoint_kernel<<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(r, grad, H, W, factor,
-                                                                          radius, boundary, t);
+    if (xu)
+      sr_adjoint_kernel<true><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
+          r, nullptr, H, W, factor, radius, boundary, t, *xu);
+    else
+      sr_adjoint_kernel<false><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
+          r, grad, H, W, factor, radius, boundary, t, XUpd{});
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
 }
 
-int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros, float* grad,
-                 int batch, int n, double gain_over_K, double floor_, double* data_out) {
-  if (!ctx || !x || !ones || !zeros || (!grad && !data_out))
+static int qis_grad_impl(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros,
+                         float* grad, int batch, int n, double gain_over_K, double floor_,
+                         double* data_out, const XUpd* xu) {
+  if (!ctx || !x || !ones || !zeros || (!grad && !data_out && !xu))
     return fail(PNP_EINVAL, "null argument");
   if (batch < 1 || n < 1) return fail(PNP_EINVAL, "bad shape");
   const int nblk = (n + 255) / 256;
@@ -422,8 +488,12 @@ int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* z
   }
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    qis_grad_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, ones, zeros, grad, (size_t)n,
-                                                                gain_over_K, floor_, part);
+    if (xu)
+      qis_grad_kernel<true><<<dim3(nblk, batch), 256, 0, ctx->stream>>>(
+          x, ones, zeros, nullptr, (size_t)n, gain_over_K, floor_, part, *xu);
+    else
+      qis_grad_kernel<false><<<dim3(nblk, batch), 256, 0, ctx->stream>>>(
+          x, ones, zeros, grad, (size_t)n, gain_over_K, floor_, part, XUpd{});
   }
   PNP_LAUNCH_CHECK("qis_grad_kernel");
   if (data_out) {
@@ -436,6 +506,54 @@ int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* z
   return PNP_OK;
 }
 
+int pnp_sr_grad(pnp_ctx* ctx, const float* x, const float* yobs, float* grad, int batch, int H,
+                int W, const float* taps, int radius, int factor, int boundary, double* data_out) {
+  return sr_grad_impl(ctx, x, yobs, grad, batch, H, W, taps, radius, factor, boundary, data_out,
+                      nullptr);
+}
+
+static XUpd make_xupd(float* x, const float* v, const float* u, float* z, double mu, double alpha,
+                      double rho, double lo, double hi, int* flags) {
+  XUpd q;
+  q.x = x;
+  q.v = v;
+  q.u = u;
+  q.z = z;
+  q.mu = mu;
+  q.alpha = alpha;
+  q.rho = rho;
+  q.lo = isinf(lo) ? -INFINITY : (float)lo;
+  q.hi = isinf(hi) ? INFINITY : (float)hi;
+  q.flags = flags;
+  return q;
+}
+
+int pnp_sr_grad_xupdate(pnp_ctx* ctx, float* x, const float* yobs, int batch, int H, int W,
+                        const float* taps, int radius, int factor, int boundary, double* data_out,
+                        const float* v, const float* u, float* z, double mu, double alpha,
+                        double rho, double lo, double hi, int* flags) {
+  if (!v || !u || !z || !flags) return fail(PNP_EINVAL, "null argument");
+  const XUpd q = make_xupd(x, v, u, z, mu, alpha, rho, lo, hi, flags);
+  return sr_grad_impl(ctx, x, yobs, nullptr, batch, H, W, taps, radius, factor, boundary,
+                      data_out, &q);
+}
+
+int pnp_qis_grad(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros, float* grad,
+                 int batch, int n, double gain_over_K, double floor_, double* data_out) {
+  return qis_grad_impl(ctx, x, ones, zeros, grad, batch, n, gain_over_K, floor_, data_out,
+                       nullptr);
+}
+
+int pnp_qis_grad_xupdate(pnp_ctx* ctx, float* x, const float* ones, const float* zeros, int batch,
+                         int n, double gain_over_K, double floor_, double* data_out,
+                         const float* v, const float* u, float* z, double mu, double alpha,
+                         double rho, double lo, double hi, int* flags) {
+  if (!v || !u || !z || !flags) return fail(PNP_EINVAL, "null argument");
+  const XUpd q = make_xupd(x, v, u, z, mu, alpha, rho, lo, hi, flags);
+  return qis_grad_impl(ctx, x, ones, zeros, nullptr, batch, n, gain_over_K, floor_, data_out,
+                       &q);
+}
+
 int pnp_qis_data(pnp_ctx* ctx, const float* x, const float* ones, const float* zeros, int batch,
                  int n, double gain_over_K, double floor_, double* data_out) {
   if (!ctx || !x || !ones || !zeros || !data_out) return fail(PNP_EINVAL, "null argument");
@@ -446,8 +564,8 @@ int pnp_qis_data(pnp_ctx* ctx, const float* x, const float* ones, const float* z
   double* part = ctx->stats.as<double>();
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    qis_grad_kernel<<<dim3(nblk, batch), 256, 0, ctx->stream>>>(x, ones, zeros, nullptr, (size_t)n,
-                                                                gain_over_K, floor_, part);
+    qis_grad_kernel<false><<<dim3(nblk, batch), 256, 0, ctx->stream>>>(
+        x, ones, zeros, nullptr, (size_t)n, gain_over_K, floor_, part, XUpd{});
   }
   PNP_LAUNCH_CHECK("qis_grad_kernel");
   reduce_partials_kernel<<<dim3(batch, 1), 256, 0, ctx->stream>>>(part, nblk, 1, 1.0, data_out, 1);
@@ -484,9 +602,7 @@ int pnp_admm_uupdate(pnp_ctx* ctx, float* u, const float* x, const float* v, con
                                                                     rho, part, flags);
   }
   PNP_LAUNCH_CHECK("admm_uupdate_kernel");
-  reduce_partials_kernel<<<dim3(batch, 3), 256, 0, ctx->stream>>>(part, nblk, 3, 1.0, stats, 4);
-  PNP_LAUNCH_CHECK("reduce_partials_kernel");
-  return PNP_OK;
+  return reduce_stats3(ctx, part, nblk, batch, stats);
 }
 
 int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, double hi) {

@@ -99,6 +99,11 @@ struct ProfScope {
 };
 }  // namespace pnp
 
+namespace pnp {
+// stats[b*4 + k] = sum_j part[b][j][k] for k < 3 (pnp_forward.cu)
+int reduce_stats3(pnp_ctx* ctx, const double* part, int nblk, int batch, double* stats);
+}  // namespace pnp
+
 struct pnp_frozen {
   int device = 0;
   int B = 0, H = 0, W = 0, R = 0, P = 0;

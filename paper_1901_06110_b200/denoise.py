@@ -197,11 +197,21 @@ class FrozenGuide:
         L.call("pnp_dsg_apply", L.context(self._dev), self._h, L.ptr(x), L.ptr(out))
         return out
 
+    def apply_admm(self, z: torch.Tensor, v: torch.Tensor, u: torch.Tensor, x: torch.Tensor,
+                   v_prev, gt, rho: float, stats: torch.Tensor, flags: torch.Tensor) -> None:
+        """v = W z with the linearized-ADMM u-update fused into the apply:
+        u += x - v; stats (float64 [B, 4]) = sum (x-v)^2, sum (rho (v-v_prev))^2,
+        sum (gt-v)^2; flags |= 4 on non-finite v / u (solver.py:222-228)."""
+        L.call("pnp_dsg_apply_admm", L.context(self._dev), self._h, L.ptr(z), L.ptr(v), L.ptr(u),
+               L.ptr(x), L.ptr(v_prev), L.ptr(gt), float(rho), L.ptr(stats), L.ptr(flags))
+
     def as_denoiser(self):
         """(img, k) -> W img plug-in for linearized_pnp_admm, device resident."""
         from .solver import device_callable
 
-        return device_callable(lambda img, k: self.apply_device(img), graph_from=2)
+        fn = device_callable(lambda img, k: self.apply_device(img), graph_from=2)
+        fn._pnp_frozen_for = lambda k: self  # lets the solver fuse the u-update
+        return fn
 
 
 def freeze_guide(guide, params: PatchParams) -> FrozenGuide:

@@ -118,6 +118,15 @@ class SuperResOp:
                self._taps, self.radius, self.factor, self._bnd, L.ptr(data_out))
         return out
 
+    def gradient_xupdate_device(self, x, y, v, u, z, mu, alpha, rho, lo, hi, flags,
+                                data_out=None) -> None:
+        """grad f(x) with the linearized-ADMM x-update fused into the adjoint
+        kernel: x <- proj(mu (alpha x + rho (v - u) - grad)), z = x + u."""
+        B, H, W = A.dims(x)
+        L.call("pnp_sr_grad_xupdate", L.context(x.device.index), L.ptr(x), L.ptr(y), B, H, W,
+               self._taps, self.radius, self.factor, self._bnd, L.ptr(data_out), L.ptr(v),
+               L.ptr(u), L.ptr(z), mu, alpha, rho, lo, hi, L.ptr(flags))
+
 
 def _hr_input(op: SuperResOp, x, name="image"):
     x, kind = A.validate(x, name, batch_ok=True)
@@ -286,6 +295,15 @@ def qis_grad_device(x, ones, zeros, model: QisModel, floor: float, grad=None, da
     L.call("pnp_qis_grad", L.context(x.device.index), L.ptr(x), L.ptr(ones), L.ptr(zeros),
            L.ptr(grad), B, H * W, model.gain / model.oversampling, float(floor), L.ptr(data_out))
     return grad
+
+
+def qis_grad_xupdate_device(x, ones, zeros, model: QisModel, floor: float, v, u, z, mu, alpha,
+                            rho, lo, hi, flags, data_out=None) -> None:
+    """QIS gradient with the linearized-ADMM x-update fused (one pass)."""
+    B, H, W = A.dims(x)
+    L.call("pnp_qis_grad_xupdate", L.context(x.device.index), L.ptr(x), L.ptr(ones), L.ptr(zeros),
+           B, H * W, model.gain / model.oversampling, float(floor), L.ptr(data_out), L.ptr(v),
+           L.ptr(u), L.ptr(z), mu, alpha, rho, lo, hi, L.ptr(flags))
 
 
 def qis_data_term(x, counts: QisCounts, model: QisModel, floor: float = QIS_FLOOR) -> float:

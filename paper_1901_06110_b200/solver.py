@@ -38,7 +38,7 @@ from . import _arrays as A
 from . import _lib as L
 from .denoise import PatchParams, dsg_nlm_denoise, freeze_guide, nlm_denoise
 from .forward import (QIS_FLOOR, QisCounts, QisModel, SuperResOp, power_iteration_lipschitz,
-                      qis_grad_device, qis_initial_estimate, sr_adjoint)
+                      qis_grad_device, qis_grad_xupdate_device, qis_initial_estimate, sr_adjoint)
 from .image import UNCONSTRAINED, Box, Constraint, NonNegative, Unconstrained, bounds
 
 DENOISERS = ("identity", "nlm", "dsg-adaptive", "dsg-fixed")
@@ -135,6 +135,9 @@ class Problem:
     gram: Callable | None = None
     atb: object | None = None
     device_gradient: Callable | None = field(default=None, repr=False)
+    # fused gradient + x-update (set by make_sr_problem / make_qis_problem):
+    # (x, v, u, z, mu, alpha, rho, lo, hi, flags, data_out) -> None
+    device_grad_xupdate: Callable | None = field(default=None, repr=False)
 
 
 @dataclass
@@ -194,7 +197,10 @@ def _make_denoiser(config: SolverConfig):
             state["frozen"] = freeze_guide(img, params)
         return state["frozen"].apply_device(img)
 
-    return device_callable(fixed, graph_from=(config.freeze_at or 1) + 1)
+    fn = device_callable(fixed, graph_from=(config.freeze_at or 1) + 1)
+    if config.freeze_at is not None:  # after the freeze the solver may fuse the u-update
+        fn._pnp_frozen_for = lambda k: state["frozen"] if k > config.freeze_at else None
+    return fn
 
 
 def _nlm_device(img: torch.Tensor, params: PatchParams) -> torch.Tensor:
@@ -301,21 +307,33 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
     done = iters
     state = {"x": x, "v": v, "u": u}
 
+    fused_grad = problem.device_grad_xupdate
+    frozen_for = getattr(den, "_pnp_frozen_for", None)
+
     def step(k, record):
         x, v, u = state["x"], state["v"], state["u"]
-        # objective of the previous (projected) iterate rides on this gradient
-        grad_fn(x, grad, objv[k - 2] if (k >= 2 and track_obj) else None)
         fk = flags[k - 1:k]
-        L.call("pnp_admm_xupdate", ctx, L.ptr(x), L.ptr(v), L.ptr(u), L.ptr(grad), L.ptr(z),
-               x.numel(), mu, float(config.alpha), float(config.rho), lo, hi, L.ptr(fk))
+        # objective of the previous (projected) iterate rides on this gradient
+        obj = objv[k - 2] if (k >= 2 and track_obj) else None
+        if fused_grad is not None:  # grad + x-update in one kernel epilogue
+            fused_grad(x, v, u, z, mu, float(config.alpha), float(config.rho), lo, hi, fk, obj)
+        else:
+            grad_fn(x, grad, obj)
+            L.call("pnp_admm_xupdate", ctx, L.ptr(x), L.ptr(v), L.ptr(u), L.ptr(grad), L.ptr(z),
+                   x.numel(), mu, float(config.alpha), float(config.rho), lo, hi, L.ptr(fk))
         v_prev = v
-        v = den(z, k)
-        if not isinstance(v, torch.Tensor) or v.dtype != torch.float32 or not v.is_contiguous():
-            v = A.to_device(v, dev).reshape(x.shape)
-        if v.data_ptr() in (z.data_ptr(), x.data_ptr(), u.data_ptr(), v_prev.data_ptr()):
-            v = v.clone()  # a plug-in may hand back its input; iterates must not alias
-        L.call("pnp_admm_uupdate", ctx, L.ptr(u), L.ptr(x), L.ptr(v), L.ptr(v_prev), L.ptr(gt),
-               B, n, float(config.rho), L.ptr(stats[k - 1]), L.ptr(fk))
+        fz = frozen_for(k) if frozen_for is not None else None
+        if fz is not None:  # frozen apply + u-update in one fixup epilogue
+            v = torch.empty_like(x)
+            fz.apply_admm(z, v, u, x, v_prev, gt, float(config.rho), stats[k - 1], fk)
+        else:
+            v = den(z, k)
+            if not isinstance(v, torch.Tensor) or v.dtype != torch.float32 or not v.is_contiguous():
+                v = A.to_device(v, dev).reshape(x.shape)
+            if v.data_ptr() in (z.data_ptr(), x.data_ptr(), u.data_ptr(), v_prev.data_ptr()):
+                v = v.clone()  # a plug-in may hand back its input; iterates must not alias
+            L.call("pnp_admm_uupdate", ctx, L.ptr(u), L.ptr(x), L.ptr(v), L.ptr(v_prev),
+                   L.ptr(gt), B, n, float(config.rho), L.ptr(stats[k - 1]), L.ptr(fk))
         state["v"] = v
         if record:
             events[k].record()
@@ -408,6 +426,9 @@ def make_sr_problem(op: SuperResOp, observed, ground_truth=None) -> Problem:
     def device_gradient(x, out, data_out=None):
         return op.gradient_device(x, y, out, data_out)
 
+    def device_grad_xupdate(x, v, u, z, mu, alpha, rho, lo, hi, flags, data_out=None):
+        op.gradient_xupdate_device(x, y, v, u, z, mu, alpha, rho, lo, hi, flags, data_out)
+
     def gradient(x):
         from .forward import sr_gradient
         return sr_gradient(op, x, A.from_device(y, A.kind_of(x)))
@@ -423,7 +444,7 @@ def make_sr_problem(op: SuperResOp, observed, ground_truth=None) -> Problem:
     return Problem(shape=tuple(x0d.shape), gradient=gradient, x0=x0, objective=objective,
                    ground_truth=ground_truth, gram=gram,
                    atb=A.from_device(op.adjoint_device(y), kind),
-                   device_gradient=device_gradient)
+                   device_gradient=device_gradient, device_grad_xupdate=device_grad_xupdate)
 
 
 def make_qis_problem(counts: QisCounts, model: QisModel, ground_truth=None,
@@ -436,6 +457,10 @@ def make_qis_problem(counts: QisCounts, model: QisModel, ground_truth=None,
     def device_gradient(x, out, data_out=None):
         return qis_grad_device(x, ones, zeros, model, floor, out, data_out)
 
+    def device_grad_xupdate(x, v, u, z, mu, alpha, rho, lo, hi, flags, data_out=None):
+        qis_grad_xupdate_device(x, ones, zeros, model, floor, v, u, z, mu, alpha, rho, lo, hi,
+                                flags, data_out)
+
     def gradient(x):
         from .forward import qis_gradient
         return qis_gradient(x, counts, model, floor)
@@ -446,7 +471,7 @@ def make_qis_problem(counts: QisCounts, model: QisModel, ground_truth=None,
 
     return Problem(shape=counts.shape, gradient=gradient, x0=qis_initial_estimate(counts, floor),
                    objective=objective, ground_truth=ground_truth,
-                   device_gradient=device_gradient)
+                   device_gradient=device_gradient, device_grad_xupdate=device_grad_xupdate)
 
 
 def default_sr_alpha(op: SuperResOp, hr_shape, iters: int = 200, seed: int = 0) -> float:
