@@ -223,3 +223,41 @@ def test_graph_replay_is_bitwise_eager(pnp, golden_admm, schedule):
         assert (r1.primal, r1.dual, r1.psnr, r1.objective) == (r2.primal, r2.dual, r2.psnr,
                                                                r2.objective)
         assert math.isfinite(r2.time_ms)
+
+
+def test_fused_admm_steps_match_unfused(pnp, golden_admm):
+    """gradient + x-update and frozen apply + u-update fused into one kernel
+    epilogue each: x, z, v, u bitwise equal to the separate kernels; stats
+    (float64 partial sums in another order) to 1e-12 relative."""
+    import torch
+    from paper_1901_06110_b200 import _lib as L
+    a = golden_admm
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    y = torch.from_numpy(np.asarray(a["sr_y"], dtype=np.float32)).cuda()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    H, W = y.shape[0] * 2, y.shape[1] * 2
+    x0, v0, u0 = (torch.rand(H, W, device="cuda", generator=g) for _ in range(3))
+    u0 = u0 - 0.5
+    gt = torch.rand(H, W, device="cuda", generator=g)
+    mu, al, rho, lo, hi = 0.5, 1.0, 1.0, 0.0, 1.0
+    # unfused
+    x1, z1, f1 = x0.clone(), torch.empty_like(x0), torch.zeros(1, dtype=torch.int32, device="cuda")
+    grad = op.gradient_device(x1, y, torch.empty_like(x1))
+    ctx = L.context(0)
+    L.call("pnp_admm_xupdate", ctx, L.ptr(x1), L.ptr(v0), L.ptr(u0), L.ptr(grad), L.ptr(z1),
+           x1.numel(), mu, al, rho, lo, hi, L.ptr(f1))
+    # fused
+    x2, z2, f2 = x0.clone(), torch.empty_like(x0), torch.zeros(1, dtype=torch.int32, device="cuda")
+    op.gradient_xupdate_device(x2, y, v0, u0, z2, mu, al, rho, lo, hi, f2)
+    assert torch.equal(x1, x2) and torch.equal(z1, z2) and int(f1) == int(f2) == 0
+    fz = pnp.freeze_guide(a["sr_gauss_guide"], pnp.PatchParams(5, 4, 0.1, 1.5))
+    v1 = fz.apply_device(z1)
+    u1 = u0.clone()
+    s1 = torch.zeros(1, 4, dtype=torch.float64, device="cuda")
+    L.call("pnp_admm_uupdate", ctx, L.ptr(u1), L.ptr(x1), L.ptr(v1), L.ptr(v0), L.ptr(gt), 1,
+           H * W, rho, L.ptr(s1), L.ptr(f1))
+    v2, u2 = torch.empty_like(z1), u0.clone()
+    s2 = torch.zeros(1, 4, dtype=torch.float64, device="cuda")
+    fz.apply_admm(z1, v2, u2, x1, v0, gt, rho, s2, f2)
+    assert torch.equal(v1, v2) and torch.equal(u1, u2) and int(f1) == int(f2) == 0
+    assert torch.allclose(s1[:, :3], s2[:, :3], rtol=1e-12, atol=0)
