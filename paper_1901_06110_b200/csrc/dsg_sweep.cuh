@@ -82,7 +82,7 @@ struct ChanSpec {
 // precomputed on the host.
 struct Chunk {
   int dx, dy0, kc, pad;
-  float L[4];
+  float L[kKY];
 };
 
 // Chunks of the half window at R = RB (the largest R of a bucket):
@@ -397,14 +397,14 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
     // ---------------- phase 1: squared differences + horizontal filter ----
     // packed over the offset pair: (D_k, D_k+1) = (G_partner - G_own)^2
     if (!CACHED) {
-      const float* prow0 = Gs + (lane + dy0) * GS + c0 + RB + dx;
+      const int poff = (lane + dy0) * GS + c0 + RB + dx;
 #pragma unroll
       for (int kp = 0; kp < KY / 2; ++kp) {
         if (kp == 0 || 2 * kp < kc) {
-          const float* pa = prow0 + 2 * kp * GS;
           float2 dd[SEGW];
 #pragma unroll
           for (int x = 0; x < SEGW; ++x) {
+            const float* pa = Gs + poff + 2 * kp * GS;
             const float2 t = __fadd2_rn(make_float2(pa[x], pa[GS + x]),
                                         make_float2(ngown[x], ngown[x]));
             dd[x] = __fmul2_rn(t, t);

@@ -444,7 +444,7 @@ static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
       ch.dx = dx;
       ch.dy0 = dy0;
       ch.kc = (R - dy0 + 1) < kKY ? (R - dy0 + 1) : kKY;
-      for (int k = 0; k < kKY && k < 4; ++k) {
+      for (int k = 0; k < kKY; ++k) {
         // log2 of the separable hat (denoise.py:199-201), in double, rounded once
         const int dy = dy0 + k;
         const double s = R + 1.0;
