@@ -98,3 +98,68 @@ def linearized_pnp_admm(x0, gradient: Callable, denoiser: Callable, *, rho: floa
         if stop_tol is not None and primal < stop_tol and dual < stop_tol:
             break
     return v, recs
+
+
+class CgBreakdownError(RuntimeError):
+    """solver.py:50-51."""
+
+
+def cg_solve(apply: Callable, rhs, tol: float, max_iters: int, x0=None):
+    """Conjugate gradients for an SPD operator on images (solver.py:244-282).
+    Returns (x, iterations, relative residual, converged)."""
+    rhs = np.asarray(rhs, np.float64)
+    bnorm = math.sqrt(float(np.sum(rhs * rhs)))
+    if bnorm == 0.0:
+        return np.zeros_like(rhs), 0, 0.0, True
+    x = np.zeros_like(rhs) if x0 is None else np.array(x0, np.float64)
+    r = rhs - apply(x)
+    p = r.copy()
+    rs = float(np.sum(r * r))
+    it = 0
+    for _ in range(max_iters):
+        if math.sqrt(rs) / bnorm <= tol:
+            break
+        ap = apply(p)
+        pap = float(np.sum(p * ap))
+        if not math.isfinite(pap):
+            raise DivergenceError("non-finite value inside conjugate gradients")
+        if pap <= 0.0:
+            raise CgBreakdownError(f"nonpositive curvature {pap!r}")
+        a = rs / pap
+        x = x + a * p
+        r = r - a * ap
+        rs_new = float(np.sum(r * r))
+        p = r + (rs_new / rs) * p
+        rs = rs_new
+        it += 1
+    res = math.sqrt(rs) / bnorm
+    return x, it, res, res <= tol
+
+
+def standard_pnp_admm_cg(x0, gram: Callable, atb, denoiser: Callable, *, rho: float,
+                         max_iters: int, cg_tol: float, cg_max_iters: int,
+                         cg_warm_start: bool = False, lo=None, hi=None,
+                         objective: Callable | None = None, ground_truth=None):
+    """Standard PnP-ADMM with the exact x-update by CG (solver.py:285-328):
+    (A^T A + rho I) x = A^T y + rho (v - u); the constraint is applied once,
+    to the returned v.  Returns (v, records) like linearized_pnp_admm."""
+    x = np.array(x0, np.float64)
+    v = x.copy()
+    u = np.zeros(x.shape)
+    recs = []
+    for k in range(1, max_iters + 1):
+        rhs = atb + rho * (v - u)
+        x = cg_solve(lambda z: gram(z) + rho * z, rhs, cg_tol, cg_max_iters,
+                     x0=x if cg_warm_start else None)[0]
+        _finite(k, x)
+        v_prev = v
+        dn_in = x + u
+        _finite(k, dn_in)
+        v = denoiser(dn_in, k)
+        u = u + (x - v)
+        _finite(k, v, u)
+        primal, dual = residuals(x, v, v_prev, rho)
+        q = psnr(ground_truth, v) if ground_truth is not None else math.nan
+        obj = float(objective(x)) if objective is not None else math.nan
+        recs.append((k, primal, dual, q, obj))
+    return project(v, lo, hi), recs

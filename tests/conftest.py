@@ -59,5 +59,10 @@ def golden_admm():
     return load_golden("admm.npz")
 
 
+@pytest.fixture(scope="session")
+def golden_cg():
+    return load_golden("cg.npz")
+
+
 def dsg_case_ids(g):
     return sorted({k.split("_")[0] for k in g if k.startswith("c")}, key=lambda s: int(s[1:]))

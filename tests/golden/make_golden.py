@@ -244,5 +244,47 @@ def main():
         print(f.name, f.stat().st_size)
 
 
+def cg_goldens():
+    """Conjugate gradients and the standard PnP-ADMM + CG baseline
+    (solver.py:244-328), run by the reference on small SR problems."""
+    cg = {}
+    truth = synth.scene(32, 40, 7)
+    op = ref.SuperResOp(ref.gaussian_kernel(1.0, 4), 2, "symmetric")
+    y = ref.sr_simulate(truth, op, 5 / 255, seed=107)
+    prob = ref.make_sr_problem(op, y, ground_truth=truth)
+    cg["truth"], cg["y"] = truth, y
+    rho = 0.7
+    rng = np.random.default_rng(11)
+    rhs = prob.atb + rho * rng.standard_normal(truth.shape) * 0.1
+    x0 = rng.random(truth.shape)
+    cg["rhs"], cg["x0"] = rhs, x0
+    for name, tol, its, warm in (("tight", 1e-8, 200, False), ("capped", 1e-12, 7, False),
+                                 ("warm", 1e-6, 200, True)):
+        res = ref.cg_solve(lambda z: prob.gram(z) + rho * z, rhs, tol, its,
+                           x0=x0 if warm else None)
+        cg[f"cg_{name}_x"] = res.x
+        cg[f"cg_{name}_meta"] = np.array([res.iterations, res.residual, float(res.converged)])
+    # standard PnP-ADMM + CG, frozen DSG schedule, box weights
+    cfg = ref.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=5, freeze_at=3,
+                           constraint=ref.UNIT_BOX, denoiser="dsg-fixed", patch_side=3,
+                           window_radius=3, bandwidth=0.1, cg_tol=1e-7, cg_max_iters=100)
+    v, recs = ref.standard_pnp_admm_cg(prob, cfg)
+    cg["std_v"] = v
+    cg["std_rec"] = np.array([[r.index, r.primal, r.dual, r.psnr, r.objective] for r in recs])
+    cfg2 = ref.SolverConfig(rho=0.5, lam=0.01, alpha=1.0, max_iters=4, constraint=ref.UNIT_BOX,
+                            denoiser="identity", cg_tol=1e-6, cg_max_iters=50,
+                            cg_warm_start=True)
+    v, recs = ref.standard_pnp_admm_cg(prob, cfg2)
+    cg["std_warm_v"] = v
+    cg["std_warm_rec"] = np.array([[r.index, r.primal, r.dual, r.psnr, r.objective]
+                                   for r in recs])
+    np.savez_compressed(HERE / "cg.npz", **cg)
+    print("cg.npz", (HERE / "cg.npz").stat().st_size)
+
+
 if __name__ == "__main__":
-    main()
+    if "--cg" in sys.argv:   # only the CG / standard-ADMM fixtures
+        cg_goldens()
+    else:
+        main()
+        cg_goldens()

@@ -146,3 +146,34 @@ def test_admm_runs_match_reference(golden_admm):
         ground_truth=a["qis_truth"])
     assert np.abs(v - a["qis_v"]).max() < 1e-11
     assert np.allclose(np.array(recs), a["qis_rec"], rtol=1e-9, atol=1e-14)
+
+
+def test_cg_and_standard_admm_match_reference(golden_cg):
+    """cg_solve / standard_pnp_admm_cg (solver.py:244-328) against the reference."""
+    g = golden_cg
+    k = ofw.gaussian_kernel(1.0, 4)
+    y, truth = g["y"], g["truth"]
+    gram = lambda z: ofw.sr_adjoint(k, 2, "symmetric", ofw.sr_apply(k, 2, "symmetric", z))  # noqa: E731
+    rho = 0.7
+    for name, tol, its, warm in (("tight", 1e-8, 200, False), ("capped", 1e-12, 7, False),
+                                 ("warm", 1e-6, 200, True)):
+        x, it, res, conv = oracle.cg_solve(lambda z: gram(z) + rho * z, g["rhs"], tol, its,
+                                           x0=g["x0"] if warm else None)
+        meta = g[f"cg_{name}_meta"]
+        assert it == int(meta[0]) and conv == bool(meta[2])
+        assert res == pytest.approx(float(meta[1]), rel=1e-6)
+        assert np.abs(x - g[f"cg_{name}_x"]).max() < 1e-10
+    atb = ofw.sr_adjoint(k, 2, "symmetric", y)
+    obj = lambda x: ofw.sr_data_term(k, 2, "symmetric", x, y)  # noqa: E731
+    den = oadmm.make_denoiser("dsg-fixed", 3, 3, 0.1, lam=0.01, freeze_at=3)
+    v, recs = oracle.standard_pnp_admm_cg(4 * atb, gram, atb, den, rho=1.0, max_iters=5,
+                                          cg_tol=1e-7, cg_max_iters=100, lo=0.0, hi=1.0,
+                                          objective=obj, ground_truth=truth)
+    assert np.abs(v - g["std_v"]).max() < 1e-10
+    assert np.allclose(np.array(recs), g["std_rec"], rtol=1e-8, atol=1e-14)
+    v, recs = oracle.standard_pnp_admm_cg(4 * atb, gram, atb, lambda im, k_: im.copy(), rho=0.5,
+                                          max_iters=4, cg_tol=1e-6, cg_max_iters=50,
+                                          cg_warm_start=True, lo=0.0, hi=1.0, objective=obj,
+                                          ground_truth=truth)
+    assert np.abs(v - g["std_warm_v"]).max() < 1e-10
+    assert np.allclose(np.array(recs), g["std_warm_rec"], rtol=1e-8, atol=1e-14)
