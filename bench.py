@@ -459,6 +459,20 @@ def admm_extras(pnp, dev):
     res["config2_sr_512"] = {"iters": 30, "iters_per_s": 30 / (t2 - t1),
                              "freeze_ms": (t1 - t0) * 1e3, "end_to_end_ms": (t2 - t0) * 1e3,
                              "psnr_db": recs[-1].psnr}
+    # paper Fig. 2: the standard PnP-ADMM (exact x-update by CG, native
+    # batched solver) on the same problem and denoiser
+    cfg_s = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=30,
+                             constraint=pnp.UNIT_BOX, cg_tol=1e-6, cg_max_iters=200)
+    prob2 = pnp.make_sr_problem(op, yd, ground_truth=gt)
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        vs, recs_s = pnp.standard_pnp_admm_cg(prob2, cfg_s, denoiser=fz.as_denoiser())
+        torch.cuda.synchronize()
+        t4 = time.perf_counter()
+    res["config2_standard_cg"] = {"iters": 30, "iters_per_s": 30 / (t4 - t3),
+                                  "psnr_db": recs_s[-1].psnr,
+                                  "linearized_speedup": (t4 - t3) / (t2 - t1)}
     # config 3: 512^2 QIS, K = 4x4x8 = 128 jots, alpha_s = 8 -> gain 64, 50 its, dsg-fixed @15
     truth3 = synth.scene(512, 512, 3).astype(np.float32)
     model = pnp.QisModel(128, 64.0)

@@ -187,6 +187,24 @@ int pnp_qis_grad_xupdate(pnp_ctx* ctx, float* x, const float* ones, const float*
 int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v, float* u,
                        const float* x, const float* v_prev, const float* gt, double rho,
                        double* stats, int* flags);
+/* Standard PnP-ADMM baseline (reference solver.py:244-328): the Gram operator
+ * out = A^T A x + shift x of the SR model, and conjugate gradients on
+ * (A^T A + shift I) x = rhs per image of a batch (cg_solve semantics: stop
+ * when ||r|| / ||rhs|| <= tol or after max_iters; warm = start from x, else
+ * from 0; ||rhs|| = 0 -> x = 0).  Outputs per image: iterations, relative
+ * residual, status (0 ok, 2 nonpositive curvature, 3 non-finite).  Device
+ * resident: scalars stay on the GPU, the host polls completion every few
+ * iterations. */
+/* rhs = atb + rho (v - u); z = x + u with flags |= 1 / 2 on non-finite x / z. */
+int pnp_admm_std_rhs(pnp_ctx* ctx, float* rhs, const float* atb, const float* v, const float* u,
+                     int64_t n, double rho);
+int pnp_admm_std_z(pnp_ctx* ctx, float* z, const float* x, const float* u, int64_t n,
+                   int* flags);
+int pnp_sr_gram(pnp_ctx* ctx, const float* x, float* out, int batch, int H, int W,
+                const float* taps, int radius, int factor, int boundary, double shift);
+int pnp_sr_cg(pnp_ctx* ctx, const float* rhs, float* x, int batch, int H, int W,
+              const float* taps, int radius, int factor, int boundary, double shift, double tol,
+              int max_iters, int warm, int* iters_out, double* resid_out, int* status_out);
 int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, double hi);
 /* Validation helper (reference image.py:35-40): *all_finite = 1 when no
  * element of x (n floats, device, 16 B aligned) is NaN/Inf, else 0.  One

@@ -44,6 +44,8 @@ from .image import (  # noqa: F401
     validate_image,
 )
 from .solver import (  # noqa: F401
+    CgBreakdownError,
+    CgResult,
     DivergenceError,
     IterationRecord,
     Problem,
@@ -55,6 +57,8 @@ from .solver import (  # noqa: F401
     make_qis_problem,
     make_sr_problem,
     residuals,
+    cg_solve,
+    standard_pnp_admm_cg,
     write_log_csv,
 )
 from .stream import DenoiseStream, denoise_host_sequence  # noqa: F401

@@ -75,6 +75,11 @@ _SIGS = {
     "pnp_qis_grad_xupdate": (i32, [vp, vp, vp, vp, i32, i32, f64, f64, vp,
                                    vp, vp, vp, f64, f64, f64, f64, f64, vp]),
     "pnp_dsg_apply_admm": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp]),
+    "pnp_sr_gram": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64]),
+    "pnp_admm_std_rhs": (i32, [vp, vp, vp, vp, vp, i64, f64]),
+    "pnp_admm_std_z": (i32, [vp, vp, vp, vp, i64, vp]),
+    "pnp_sr_cg": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64, f64, i32, i32,
+                        C.POINTER(i32), C.POINTER(f64), C.POINTER(i32)]),
     "pnp_check_finite": (i32, [vp, vp, i64, C.POINTER(i32)]),
     "pnp_flag_nonfinite": (i32, [vp, vp, i64, vp]),
 }

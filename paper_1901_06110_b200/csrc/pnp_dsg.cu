@@ -733,6 +733,7 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   ctx->stats.release();
   ctx->flags.release();
   ctx->kcache.release();
+  ctx->cg.release();
   for (auto& sl : ctx->slots) {
     cudaEventDestroy(sl.a);
     cudaEventDestroy(sl.b);

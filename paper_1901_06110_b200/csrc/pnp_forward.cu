@@ -105,6 +105,12 @@ __device__ __forceinline__ void flags_or(int* flags, int f) {
 // boundary-mapped once at staging) is filtered separably -- horizontal taps
 // into a row buffer, then vertical taps -- in the reference's summation order
 // (forward.py:_convolve: rows outer, columns inner).
+// per-image conjugate-gradients scalars (device; see cg_* kernels below)
+struct CgState {
+  double rs, pap, bnorm, beta;
+  int done, iters, status, stepped;  // status: 0 ok, 2 breakdown (p.Ap <= 0), 3 non-finite
+};
+
 constexpr int kSrT = 16;   // low-res outputs per tile side (residual)
 constexpr int kSrTA = 32;  // high-res outputs per tile side (adjoint)
 
@@ -112,9 +118,11 @@ constexpr int kSrTA = 32;  // high-res outputs per tile side (adjoint)
 // 0.5||r||^2 partials, one per tile: partial[b][tile].
 __global__ void __launch_bounds__(256)
 sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, float* __restrict__ r,
-                   int H, int W, int k, int rad, int sym, const Taps taps, double* partial) {
+                   int H, int W, int k, int rad, int sym, const Taps taps, double* partial,
+                   const CgState* skip = nullptr) {
   extern __shared__ float sm[];
   const int h = H / k, w = W / k, b = blockIdx.z;
+  if (skip && skip[b].done) return;  // CG: image already converged
   const int S = k * (kSrT - 1) + 1 + 2 * rad;  // staged hi-res rows / cols
   float* X = sm;                               // [S][S]
   float* Hh = sm + S * S;                      // [S][kSrT]
@@ -162,12 +170,25 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
 
 // x_out = A^T r = blur(upsample_k(r)) on the high-res grid: the zero-filled
 // upsampled tile (+ halo, boundary-mapped) is staged, then filtered.
-template <bool XU>
+// Conjugate-gradients epilogue of the Gram operator: out = A^T A p + shift p,
+// one partial of p . out per tile, converged images skipped.
+struct CgEpi {
+  const float* p;
+  double shift;
+  double* partial;
+  const CgState* skip;  // nullable
+};
+
+enum AdjMode { ADJ_PLAIN = 0, ADJ_XUPD = 1, ADJ_CG = 2 };
+
+template <int MODE>
 __global__ void __launch_bounds__(256)
 sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, int W, int k,
-                  int rad, int sym, const Taps taps, const XUpd q) {
+                  int rad, int sym, const Taps taps, const XUpd q, const CgEpi cg) {
   extern __shared__ float sm[];
   const int h = H / k, w = W / k, b = blockIdx.z;
+  if (MODE == ADJ_CG && cg.skip && cg.skip[b].done) return;
+  constexpr bool XU = MODE == ADJ_XUPD;
   const int S = kSrTA + 2 * rad;
   float* U = sm;             // [S][S]
   float* Hh = sm + S * S;    // [S][kSrTA]
@@ -190,6 +211,7 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, i
   }
   __syncthreads();
   int f = 0;
+  double dot = 0.0;
   for (int i = threadIdx.x; i < kSrTA * kSrTA; i += blockDim.x) {
     const int yy = i / kSrTA, xx = i - yy * kSrTA;
     const int py = py0 + yy, px = px0 + xx;
@@ -197,12 +219,29 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, i
     float acc = 0.f;
     for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
     const size_t o = (size_t)b * H * W + (size_t)py * W + px;
-    if (XU)
+    if (XU) {
       f |= xupdate_pixel(q, o, acc);
-    else
+    } else if (MODE == ADJ_CG) {
+      const float pv = cg.p[o];
+      const float ap = (float)((double)acc + cg.shift * (double)pv);
+      out[o] = ap;
+      dot += (double)pv * (double)ap;
+    } else {
       out[o] = acc;
+    }
   }
   if (XU) flags_or(q.flags, f);
+  if (MODE == ADJ_CG) {
+    __shared__ double red[8];
+    for (int off = 16; off; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w8 = 0; w8 < (int)(blockDim.x >> 5); ++w8) t += red[w8];
+      cg.partial[((size_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+  }
 }
 
 static size_t sr_res_smem(int k, int rad) {
@@ -227,11 +266,14 @@ static cudaError_t sr_smem_attr(size_t res, size_t adj) {
     if (e == cudaSuccess) set_res = res;
   }
   if (e == cudaSuccess && adj > set_adj) {
-    e = cudaFuncSetAttribute(sr_adjoint_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)adj);
+    e = cudaFuncSetAttribute(sr_adjoint_kernel<ADJ_PLAIN>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(sr_adjoint_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)adj);
+      e = cudaFuncSetAttribute(sr_adjoint_kernel<ADJ_XUPD>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(sr_adjoint_kernel<ADJ_CG>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj);
     if (e == cudaSuccess) set_adj = adj;
   }
   return e;
@@ -381,6 +423,166 @@ __global__ void __launch_bounds__(256) nonfinite_kernel(const float* __restrict_
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// ---- conjugate gradients on (A^T A + shift I) x = rhs, device resident ----
+// Reference cg_solve (solver.py:244-282), per image of a batch: the scalars
+// (rs, p.Ap, ||rhs||, beta, iteration count, flags) live on the device, every
+// kernel skips images that are done, and the host only polls the done flags
+// every few iterations -- no per-iteration round trip.
+
+__device__ __forceinline__ double block_sum256(double v) {
+  __shared__ double red[8];
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+  return t;  // valid in thread 0
+}
+
+// r = rhs - ap (warm start) or rhs (x zeroed); p = r; partials r.r, rhs.rhs
+__global__ void __launch_bounds__(256)
+cg_init_kernel(const float* __restrict__ rhs, const float* __restrict__ ap, float* __restrict__ x,
+               float* __restrict__ r, float* __restrict__ p, size_t n, double* partial) {
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double rr = 0.0, bb = 0.0;
+  if (i < n) {
+    const size_t o = (size_t)b * n + i;
+    const float bv = rhs[o];
+    float rv = bv;
+    if (ap) rv = (float)((double)bv - (double)ap[o]);
+    else x[o] = 0.f;
+    r[o] = rv;
+    p[o] = rv;
+    rr = (double)rv * rv;
+    bb = (double)bv * bv;
+  }
+  rr = block_sum256(rr);
+  bb = block_sum256(bb);
+  if (threadIdx.x == 0) {
+    double* pp = partial + ((size_t)b * gridDim.x + blockIdx.x) * 2;
+    pp[0] = rr;
+    pp[1] = bb;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+cg_start_kernel(const double* partial, int nblk, CgState* st, double tol, int max_iters) {
+  const int b = blockIdx.x;
+  double rr = 0.0, bb = 0.0;
+  for (int j = threadIdx.x; j < nblk; j += blockDim.x) {
+    rr += partial[((size_t)b * nblk + j) * 2];
+    bb += partial[((size_t)b * nblk + j) * 2 + 1];
+  }
+  rr = block_sum256(rr);
+  bb = block_sum256(bb);
+  if (threadIdx.x == 0) {
+    CgState s{};
+    s.rs = rr;
+    s.bnorm = sqrt(bb);
+    s.done = (s.bnorm == 0.0 || sqrt(s.rs) / s.bnorm <= tol || max_iters < 1) ? 1 : 0;
+    st[b] = s;
+  }
+}
+
+// p.Ap -> curvature checks (the reference raises on non-finite / <= 0)
+__global__ void __launch_bounds__(256) cg_curv_kernel(const double* partial, int nblk, CgState* st) {
+  const int b = blockIdx.x;
+  if (st[b].done) return;
+  double v = 0.0;
+  for (int j = threadIdx.x; j < nblk; j += blockDim.x) v += partial[(size_t)b * nblk + j];
+  v = block_sum256(v);
+  if (threadIdx.x == 0) {
+    st[b].pap = v;
+    if (!isfinite(v)) {
+      st[b].status = 3;
+      st[b].done = 1;
+    } else if (v <= 0.0) {
+      st[b].status = 2;
+      st[b].done = 1;
+    }
+  }
+}
+
+// x += a p; r -= a Ap (a = rs / p.Ap); partials of r.r
+__global__ void __launch_bounds__(256)
+cg_update_kernel(float* __restrict__ x, float* __restrict__ r, const float* __restrict__ p,
+                 const float* __restrict__ ap, size_t n, const CgState* st, double* partial) {
+  const int b = blockIdx.y;
+  if (st[b].done) return;
+  const double a = st[b].rs / st[b].pap;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double rr = 0.0;
+  if (i < n) {
+    const size_t o = (size_t)b * n + i;
+    x[o] = (float)((double)x[o] + a * (double)p[o]);
+    const float rv = (float)((double)r[o] - a * (double)ap[o]);
+    r[o] = rv;
+    rr = (double)rv * rv;
+  }
+  rr = block_sum256(rr);
+  if (threadIdx.x == 0) partial[(size_t)b * gridDim.x + blockIdx.x] = rr;
+}
+
+__global__ void __launch_bounds__(256)
+cg_step_kernel(const double* partial, int nblk, CgState* st, double tol, int max_iters) {
+  const int b = blockIdx.x;
+  if (st[b].done) {
+    if (threadIdx.x == 0) st[b].stepped = 0;
+    return;
+  }
+  double v = 0.0;
+  for (int j = threadIdx.x; j < nblk; j += blockDim.x) v += partial[(size_t)b * nblk + j];
+  v = block_sum256(v);
+  if (threadIdx.x == 0) {
+    CgState s = st[b];
+    s.beta = v / s.rs;
+    s.rs = v;
+    s.iters += 1;
+    s.stepped = 1;
+    s.done = (sqrt(s.rs) / s.bnorm <= tol || s.iters >= max_iters) ? 1 : 0;
+    st[b] = s;
+  }
+}
+
+// p = r + beta p for the images that stepped
+__global__ void __launch_bounds__(256)
+cg_dir_kernel(float* __restrict__ p, const float* __restrict__ r, size_t n, const CgState* st) {
+  const int b = blockIdx.y;
+  if (!st[b].stepped) return;
+  const double beta = st[b].beta;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const size_t o = (size_t)b * n + i;
+    p[o] = (float)((double)r[o] + beta * (double)p[o]);
+  }
+}
+
+// standard PnP-ADMM elementwise steps (solver.py:313-321)
+__global__ void __launch_bounds__(256)
+admm_std_rhs_kernel(float* __restrict__ rhs, const float* __restrict__ atb,
+                    const float* __restrict__ v, const float* __restrict__ u, size_t n,
+                    double rho) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rhs[i] = (float)((double)atb[i] + rho * ((double)v[i] - (double)u[i]));
+}
+
+__global__ void __launch_bounds__(256)
+admm_std_z_kernel(float* __restrict__ z, const float* __restrict__ x, const float* __restrict__ u,
+                  size_t n, int* flags) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int f = 0;
+  if (i < n) {
+    const float xv = x[i];
+    const float zv = (float)((double)xv + (double)u[i]);
+    if (!isfinite(xv)) f |= 1;
+    if (!isfinite(zv)) f |= 2;
+    z[i] = zv;
+  }
+  flags_or(flags, f);
+}
+
 // stats[b*4 + k] = sum_j part[b][j][k], k < 3 (fixed order)
 int reduce_stats3(pnp_ctx* ctx, const double* part, int nblk, int batch, double* stats) {
   {
@@ -424,8 +626,8 @@ int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int
   PNP_CUDA(sr_smem_attr(0, as));
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_adjoint_kernel<false><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-        y, x, H, W, factor, radius, boundary, t, XUpd{});
+    sr_adjoint_kernel<ADJ_PLAIN><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
+        y, x, H, W, factor, radius, boundary, t, XUpd{}, CgEpi{});
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
@@ -463,11 +665,11 @@ static int sr_grad_impl(pnp_ctx* ctx, const float* x, const float* yobs, float* 
   {
     ProfScope prof_(ctx, PROF_FORWARD);
     if (xu)
-      sr_adjoint_kernel<true><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, nullptr, H, W, factor, radius, boundary, t, *xu);
+      sr_adjoint_kernel<ADJ_XUPD><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
+          r, nullptr, H, W, factor, radius, boundary, t, *xu, CgEpi{});
     else
-      sr_adjoint_kernel<false><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, grad, H, W, factor, radius, boundary, t, XUpd{});
+      sr_adjoint_kernel<ADJ_PLAIN><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
+          r, grad, H, W, factor, radius, boundary, t, XUpd{}, CgEpi{});
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
@@ -678,6 +880,129 @@ int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite) {
   PNP_CUDA(cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   PNP_CUDA(cudaStreamSynchronize(ctx->stream));
   *all_finite = h ? 0 : 1;
+  return PNP_OK;
+}
+
+
+int pnp_sr_gram(pnp_ctx* ctx, const float* x, float* out, int batch, int H, int W,
+                const float* taps, int radius, int factor, int boundary, double shift) {
+  if (!ctx || !x || !out) return fail(PNP_EINVAL, "null argument");
+  Taps t;
+  int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
+  if (rc) return rc;
+  const dim3 rg = sr_res_grid(H, W, factor, batch), ag = sr_adj_grid(H, W, batch);
+  const size_t nl = (size_t)batch * (H / factor) * (W / factor);
+  if ((rc = ctx->kx.ensure(nl * sizeof(float)))) return rc;
+  if ((rc = ensure_partials(ctx, (size_t)batch * ag.x * ag.y))) return rc;
+  const size_t rs = sr_res_smem(factor, radius), as = sr_adj_smem(radius);
+  PNP_CUDA(sr_smem_attr(rs, as));
+  float* lr = ctx->kx.as<float>();
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(x, nullptr, lr, H, W, factor, radius,
+                                                     boundary, t, nullptr);
+    sr_adjoint_kernel<ADJ_CG><<<ag, 256, as, ctx->stream>>>(
+        lr, out, H, W, factor, radius, boundary, t, XUpd{},
+        CgEpi{x, shift, ctx->stats.as<double>(), nullptr});
+  }
+  PNP_LAUNCH_CHECK("sr_gram");
+  return PNP_OK;
+}
+
+int pnp_sr_cg(pnp_ctx* ctx, const float* rhs, float* x, int batch, int H, int W,
+              const float* taps, int radius, int factor, int boundary, double shift, double tol,
+              int max_iters, int warm, int* iters_out, double* resid_out, int* status_out) {
+  if (!ctx || !rhs || !x || !iters_out || !resid_out || !status_out)
+    return fail(PNP_EINVAL, "null argument");
+  if (!(tol > 0)) return fail(PNP_EINVAL, "tol must be > 0");
+  if (max_iters < 1) return fail(PNP_EINVAL, "max_iters must be >= 1");
+  Taps t;
+  int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
+  if (rc) return rc;
+  const size_t n = (size_t)H * W, nl = (size_t)(H / factor) * (W / factor);
+  const dim3 rg = sr_res_grid(H, W, factor, batch), ag = sr_adj_grid(H, W, batch);
+  const int nblk_a = ag.x * ag.y, nblk_e = (int)((n + 255) / 256);
+  // scratch: r, p, Ap (hi-res), A p (lo-res), partials, per-image state
+  if ((rc = ctx->cg.ensure((3 * n * batch + nl * batch) * sizeof(float) +
+                           (size_t)batch * sizeof(CgState) + 256)))
+    return rc;
+  const int np = (nblk_a > nblk_e ? nblk_a : nblk_e) * 2;
+  if ((rc = ensure_partials(ctx, (size_t)batch * np))) return rc;
+  float* r = ctx->cg.as<float>();
+  float* p = r + n * batch;
+  float* ap = p + n * batch;
+  float* lr = ap + n * batch;
+  CgState* st = reinterpret_cast<CgState*>(
+      (reinterpret_cast<uintptr_t>(lr + nl * batch) + 255) & ~(uintptr_t)255);
+  double* part = ctx->stats.as<double>();
+  const size_t rsm = sr_res_smem(factor, radius), asm_ = sr_adj_smem(radius);
+  PNP_CUDA(sr_smem_attr(rsm, asm_));
+  ProfScope prof_(ctx, PROF_ADMM);
+  if (warm) {
+    if ((rc = pnp_sr_gram(ctx, x, ap, batch, H, W, taps, radius, factor, boundary, shift)))
+      return rc;
+  }
+  cg_init_kernel<<<dim3(nblk_e, batch), 256, 0, ctx->stream>>>(rhs, warm ? ap : nullptr, x, r,
+                                                                p, n, part);
+  cg_start_kernel<<<batch, 256, 0, ctx->stream>>>(part, nblk_e, st, tol, max_iters);
+  PNP_LAUNCH_CHECK("cg_start");
+  std::vector<CgState> host(batch);
+  int it = 0;
+  int chunk = 4;
+  while (it < max_iters) {
+    const int m = (max_iters - it) < chunk ? (max_iters - it) : chunk;
+    for (int k = 0; k < m; ++k) {
+      sr_residual_kernel<<<rg, 256, rsm, ctx->stream>>>(p, nullptr, lr, H, W, factor, radius,
+                                                        boundary, t, nullptr, st);
+      sr_adjoint_kernel<ADJ_CG><<<ag, 256, asm_, ctx->stream>>>(
+          lr, ap, H, W, factor, radius, boundary, t, XUpd{}, CgEpi{p, shift, part, st});
+      cg_curv_kernel<<<batch, 256, 0, ctx->stream>>>(part, nblk_a, st);
+      cg_update_kernel<<<dim3(nblk_e, batch), 256, 0, ctx->stream>>>(x, r, p, ap, n, st, part);
+      cg_step_kernel<<<batch, 256, 0, ctx->stream>>>(part, nblk_e, st, tol, max_iters);
+      cg_dir_kernel<<<dim3(nblk_e, batch), 256, 0, ctx->stream>>>(p, r, n, st);
+    }
+    PNP_LAUNCH_CHECK("cg iteration");
+    it += m;
+    PNP_CUDA(cudaMemcpyAsync(host.data(), st, batch * sizeof(CgState), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    PNP_CUDA(cudaStreamSynchronize(ctx->stream));
+    bool all = true;
+    for (int b = 0; b < batch; ++b) all = all && host[b].done;
+    if (all) break;
+    if (chunk < 16) chunk *= 2;
+  }
+  for (int b = 0; b < batch; ++b) {
+    const CgState& s = host[b];
+    iters_out[b] = s.iters;
+    status_out[b] = s.status;
+    if (s.bnorm == 0.0) {
+      resid_out[b] = 0.0;
+      PNP_CUDA(cudaMemsetAsync(x + (size_t)b * n, 0, n * sizeof(float), ctx->stream));
+    } else {
+      resid_out[b] = sqrt(s.rs) / s.bnorm;
+    }
+  }
+  return PNP_OK;
+}
+
+
+int pnp_admm_std_rhs(pnp_ctx* ctx, float* rhs, const float* atb, const float* v, const float* u,
+                     int64_t n, double rho) {
+  if (!ctx || !rhs || !atb || !v || !u) return fail(PNP_EINVAL, "null argument");
+  ProfScope prof_(ctx, PROF_ADMM);
+  admm_std_rhs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(rhs, atb, v, u,
+                                                                            (size_t)n, rho);
+  PNP_LAUNCH_CHECK("admm_std_rhs_kernel");
+  return PNP_OK;
+}
+
+int pnp_admm_std_z(pnp_ctx* ctx, float* z, const float* x, const float* u, int64_t n,
+                   int* flags) {
+  if (!ctx || !z || !x || !u || !flags) return fail(PNP_EINVAL, "null argument");
+  ProfScope prof_(ctx, PROF_ADMM);
+  admm_std_z_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(z, x, u, (size_t)n,
+                                                                          flags);
+  PNP_LAUNCH_CHECK("admm_std_z_kernel");
   return PNP_OK;
 }
 

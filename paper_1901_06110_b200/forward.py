@@ -118,6 +118,27 @@ class SuperResOp:
                self._taps, self.radius, self.factor, self._bnd, L.ptr(data_out))
         return out
 
+    def gram_device(self, x: torch.Tensor, out: torch.Tensor, shift: float = 0.0) -> torch.Tensor:
+        """out = A^T A x + shift x (the standard PnP-ADMM x-update operator)."""
+        B, H, W = A.dims(x)
+        L.call("pnp_sr_gram", L.context(x.device.index), L.ptr(x), L.ptr(out), B, H, W,
+               self._taps, self.radius, self.factor, self._bnd, float(shift))
+        return out
+
+    def cg_device(self, rhs: torch.Tensor, x: torch.Tensor, shift: float, tol: float,
+                  max_iters: int, warm: bool):
+        """Solve (A^T A + shift I) x = rhs per image by conjugate gradients on
+        the device (x: in = start if warm, out = solution).  Returns per-image
+        (iterations, relative residual, status) lists."""
+        B, H, W = A.dims(x)
+        it = (C.c_int * B)()
+        res = (C.c_double * B)()
+        stat = (C.c_int * B)()
+        L.call("pnp_sr_cg", L.context(x.device.index), L.ptr(rhs), L.ptr(x), B, H, W, self._taps,
+               self.radius, self.factor, self._bnd, float(shift), float(tol), int(max_iters),
+               1 if warm else 0, it, res, stat)
+        return list(it), list(res), list(stat)
+
     def gradient_xupdate_device(self, x, y, v, u, z, mu, alpha, rho, lo, hi, flags,
                                 data_out=None) -> None:
         """grad f(x) with the linearized-ADMM x-update fused into the adjoint

@@ -48,6 +48,67 @@ class DivergenceError(RuntimeError):
     """An iterate picked up non-finite values; the run was aborted."""
 
 
+class CgBreakdownError(RuntimeError):
+    """Conjugate gradients met nonpositive curvature (operator not SPD)."""
+
+
+@dataclass
+class CgResult:
+    """Result of cg_solve (reference solver.py:236-241)."""
+
+    x: object
+    iterations: int
+    residual: float
+    converged: bool
+
+
+def cg_solve(apply: Callable, rhs, tol: float, max_iters: int, x0=None) -> CgResult:
+    """Conjugate gradients for an SPD operator on images (solver.py:244-282).
+
+    Stops when ||rhs - Op(x)|| / ||rhs|| <= tol (recursive residual) or after
+    max_iters.  ``apply`` is any operator on images; numpy in -> numpy out
+    (host operators, as in the reference), CUDA tensors in -> the iteration
+    runs on the device with torch vector updates around the user operator.
+    The SR x-update of standard_pnp_admm_cg does not come here: it runs the
+    native batched solver (pnp_sr_cg).
+    """
+    if not tol > 0:
+        raise ValueError(f"tol must be > 0, got {tol}")
+    if max_iters < 1:
+        raise ValueError(f"max_iters must be >= 1, got {max_iters}")
+    if not isinstance(rhs, torch.Tensor):
+        rhs, _ = A.validate(rhs, "rhs")
+    xp = torch if isinstance(rhs, torch.Tensor) else np
+    dot = (lambda a, b: float(torch.sum(a.double() * b.double()))) if xp is torch else \
+        (lambda a, b: float(np.sum(a * b)))
+    bnorm = math.sqrt(dot(rhs, rhs))
+    if bnorm == 0.0:
+        return CgResult(xp.zeros_like(rhs), 0, 0.0, True)
+    x = xp.zeros_like(rhs) if x0 is None else (x0.clone() if xp is torch else np.array(x0, np.float64))
+    r = rhs - apply(x)
+    p = r.clone() if xp is torch else r.copy()
+    rs = dot(r, r)
+    it = 0
+    for _ in range(max_iters):
+        if math.sqrt(rs) / bnorm <= tol:
+            break
+        ap = apply(p)
+        pap = dot(p, ap)
+        if not math.isfinite(pap):
+            raise DivergenceError("non-finite value inside conjugate gradients")
+        if pap <= 0.0:
+            raise CgBreakdownError(f"nonpositive curvature {pap!r}")
+        step = rs / pap
+        x = x + step * p
+        r = r - step * ap
+        rs_new = dot(r, r)
+        p = r + (rs_new / rs) * p
+        rs = rs_new
+        it += 1
+    res = math.sqrt(rs) / bnorm
+    return CgResult(x, it, res, res <= tol)
+
+
 def device_callable(fn, graph_from: int | None = None):
     """Mark a plug-in as device-native: it receives/returns CUDA tensors.
 
@@ -138,6 +199,10 @@ class Problem:
     # fused gradient + x-update (set by make_sr_problem / make_qis_problem):
     # (x, v, u, z, mu, alpha, rho, lo, hi, flags, data_out) -> None
     device_grad_xupdate: Callable | None = field(default=None, repr=False)
+    # native CG on (A^T A + shift I) x = rhs (set by make_sr_problem):
+    # (rhs, x, shift, tol, max_iters, warm) -> (iterations, residuals, status)
+    device_cg: Callable | None = field(default=None, repr=False)
+    device_atb: object | None = field(default=None, repr=False)
 
 
 @dataclass
@@ -413,6 +478,111 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
 
 
 # ---------------------------------------------------------------------------
+# Standard PnP-ADMM + CG baseline (solver.py:285-328)
+# ---------------------------------------------------------------------------
+
+def standard_pnp_admm_cg(problem: Problem, config: SolverConfig, denoiser=None, callback=None):
+    """Standard PnP-ADMM: the exact quadratic x-update
+    (A^T A + rho I) x = A^T y + rho (v - u) by conjugate gradients each
+    iteration (from scratch unless config.cg_warm_start); the constraint is
+    applied once, to the returned v.  Returns (v, records).
+
+    SR problems built by make_sr_problem solve the x-update with the native
+    batched CG (device scalars, no per-iteration host round trip); other
+    problems use cg_solve on their ``gram`` operator.
+    """
+    if problem.gram is None or problem.atb is None:
+        raise ValueError("standard ADMM baseline needs problem.gram and problem.atb")
+    dev = A.device_index()
+    x0, kind = A.validate(problem.x0, "x0", batch_ok=True)
+    x = A.to_device(x0, dev).clone()
+    B, H, W = A.dims(x)
+    n = H * W
+    lo, hi = bounds(config.constraint)
+    ctx = L.context(dev)
+    rho = float(config.rho)
+    if denoiser is None:
+        denoiser = _make_denoiser(config)
+    den = denoiser if _is_device(denoiser) else _host_wrap_array_fn(denoiser, None)
+    atb = problem.device_atb if problem.device_atb is not None else A.to_device(problem.atb, dev)
+    native = problem.device_cg
+    if native is None:
+        host_gram = _host_wrap_array_fn(problem.gram, None)
+        op = lambda z: host_gram(z) + rho * z  # noqa: E731
+    gt = A.to_device(problem.ground_truth, dev) if problem.ground_truth is not None else None
+    track_obj = problem.device_gradient is not None or problem.objective is not None
+    iters = config.max_iters
+    stats = torch.zeros((iters, B, 4), dtype=torch.float64, device=x.device)
+    objv = torch.full((iters, B), math.nan, dtype=torch.float64, device=x.device)
+    flags = torch.zeros(iters, dtype=torch.int32, device=x.device)
+    rhs, z, scratch = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    v = x.clone()
+    u = torch.zeros_like(x)
+    t0 = time.perf_counter()
+    times = []
+    done = iters
+    for k in range(1, iters + 1):
+        fk = flags[k - 1:k]
+        L.call("pnp_admm_std_rhs", ctx, L.ptr(rhs), L.ptr(atb), L.ptr(v), L.ptr(u), x.numel(), rho)
+        if native is not None:
+            _, _, status = native(rhs, x, rho, config.cg_tol, config.cg_max_iters,
+                                  config.cg_warm_start)
+            if any(st_ == 3 for st_ in status):
+                raise DivergenceError("non-finite value inside conjugate gradients")
+            if any(st_ == 2 for st_ in status):
+                raise CgBreakdownError("nonpositive curvature inside conjugate gradients")
+        else:
+            x = cg_solve(op, rhs, config.cg_tol, config.cg_max_iters,
+                         x0=x if config.cg_warm_start else None).x.contiguous()
+        L.call("pnp_admm_std_z", ctx, L.ptr(z), L.ptr(x), L.ptr(u), x.numel(), L.ptr(fk))
+        v_prev = v
+        v = den(z, k)
+        if not isinstance(v, torch.Tensor) or v.dtype != torch.float32 or not v.is_contiguous():
+            v = A.to_device(v, dev).reshape(x.shape)
+        if v.data_ptr() in (z.data_ptr(), x.data_ptr(), u.data_ptr(), v_prev.data_ptr()):
+            v = v.clone()
+        L.call("pnp_admm_uupdate", ctx, L.ptr(u), L.ptr(x), L.ptr(v), L.ptr(v_prev), L.ptr(gt),
+               B, n, rho, L.ptr(stats[k - 1]), L.ptr(fk))
+        if track_obj:
+            if problem.device_gradient is not None:
+                problem.device_gradient(x, scratch, objv[k - 1])
+            else:
+                objv[k - 1].fill_(float(problem.objective(x.cpu().numpy().astype(np.float64))))
+        if int(flags[k - 1]):  # the reference checks after every step (solver.py:316-321)
+            raise DivergenceError(f"non-finite iterate at iteration {k}")
+        times.append((time.perf_counter() - t0) * 1e3)
+        if callback is not None:
+            if _is_device(callback):
+                callback(k, x, v, u)
+            else:
+                callback(k, *(A.from_device(t.clone(), A.NUMPY) for t in (x, v, u)))
+        if config.stop_tol is not None:
+            s_ = stats[k - 1, 0].cpu()
+            if float(s_[0]) / n < config.stop_tol and float(s_[1]) / n < config.stop_tol:
+                done = k
+                break
+    st = stats[:done].cpu().numpy()
+    ob = objv[:done].cpu().numpy()
+    records = []
+    for i in range(done):
+        primal, dual = st[i, :, 0] / n, st[i, :, 1] / n
+        if gt is not None:
+            mse = st[i, :, 2] / n
+            q = np.where(mse == 0.0, math.inf, 10.0 * np.log10(1.0 / np.where(mse == 0, 1, mse)))
+        else:
+            q = np.full(B, math.nan)
+        obj = ob[i] if track_obj else np.full(B, math.nan)
+        if B == 1 and x.dim() == 2:
+            records.append(IterationRecord(i + 1, float(primal[0]), float(dual[0]), float(q[0]),
+                                           times[i], float(obj[0])))
+        else:
+            records.append(IterationRecord(i + 1, primal, dual, q, times[i], obj))
+    out = torch.empty_like(v)
+    L.call("pnp_project", ctx, L.ptr(v), L.ptr(out), v.numel(), lo, hi)
+    return A.from_device(out, kind), records
+
+
+# ---------------------------------------------------------------------------
 # Problem builders
 # ---------------------------------------------------------------------------
 
@@ -429,6 +599,9 @@ def make_sr_problem(op: SuperResOp, observed, ground_truth=None) -> Problem:
     def device_grad_xupdate(x, v, u, z, mu, alpha, rho, lo, hi, flags, data_out=None):
         op.gradient_xupdate_device(x, y, v, u, z, mu, alpha, rho, lo, hi, flags, data_out)
 
+    def device_cg(rhs, x, shift, tol, max_iters, warm):
+        return op.cg_device(rhs, x, shift, tol, max_iters, warm)
+
     def gradient(x):
         from .forward import sr_gradient
         return sr_gradient(op, x, A.from_device(y, A.kind_of(x)))
@@ -444,7 +617,8 @@ def make_sr_problem(op: SuperResOp, observed, ground_truth=None) -> Problem:
     return Problem(shape=tuple(x0d.shape), gradient=gradient, x0=x0, objective=objective,
                    ground_truth=ground_truth, gram=gram,
                    atb=A.from_device(op.adjoint_device(y), kind),
-                   device_gradient=device_gradient, device_grad_xupdate=device_grad_xupdate)
+                   device_gradient=device_gradient, device_grad_xupdate=device_grad_xupdate,
+                   device_cg=device_cg, device_atb=op.adjoint_device(y))
 
 
 def make_qis_problem(counts: QisCounts, model: QisModel, ground_truth=None,
