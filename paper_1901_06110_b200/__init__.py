@@ -32,6 +32,14 @@ from .forward import (  # noqa: F401
     sr_gradient,
     sr_simulate,
 )
+from .imageio import (  # noqa: F401
+    ImageFormatError,
+    MalformedHeaderError,
+    TruncatedPayloadError,
+    UnsupportedFormatError,
+    read_image,
+    write_image,
+)
 from .image import (  # noqa: F401
     NON_NEGATIVE,
     UNCONSTRAINED,

@@ -1,7 +1,7 @@
 """Image conventions and pixel primitives — drop-in for pnprestore/image.py
 (validate_image 32-41, constraint sets + project 48-90, psnr 146-157).
-Projection and PSNR run on the GPU; file I/O (image.py:169-280) is out of
-scope for this hot-path build."""
+Projection and PSNR run on the GPU; PGM / PFM file I/O (image.py:169-280)
+is in imageio.py."""
 
 from __future__ import annotations
 

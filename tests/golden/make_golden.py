@@ -282,9 +282,109 @@ def cg_goldens():
     print("cg.npz", (HERE / "cg.npz").stat().st_size)
 
 
+def io_goldens():
+    """PGM / PFM files written by the reference (image.py:169-280) and what its
+    reader returns for them, plus malformed inputs and the error it raises."""
+    from pnprestore import image as rimg
+    d = HERE / "io"
+    d.mkdir(exist_ok=True)
+    rng = np.random.default_rng(5)
+    img = rng.random((7, 11))
+    img[0, 0], img[0, 1], img[1, 0] = -0.2, 1.3, 0.5 / 255  # clamping / rounding edges
+    rimg.write_image(img, d / "w8.pgm", "pgm8")
+    rimg.write_image(img, d / "wf.pfm", "pfm")
+    files = {
+        "p2_comment.pgm": b"P2\n# a comment\n3 2 # trailing\n7\n0 1 2\n3 4 7\n",
+        "p5_16bit.pgm": b"P5 2 2 1000\n" + np.array([0, 1000, 500, 1], ">u2").tobytes(),
+        "p5_8bit.pgm": b"P5\n4 1\n255\n" + bytes([0, 128, 255, 7]),
+        "pf_be.pfm": b"Pf\n2 2\n1.0\n" + np.array([1, 2, 3, 4], ">f4").tobytes(),
+        "bad_magic.pgm": b"P3\n1 1\n255\n0\n",
+        "bad_header.pgm": b"P5\n4 x\n255\n\0\0\0\0",
+        "truncated.pgm": b"P5\n4 4\n255\n\0\0",
+        "bad_maxval.pgm": b"P2\n1 1\n70000\n1\n",
+        "ascii_junk.pgm": b"P2\n2 1\n9\n1 q\n",
+        "too_big.pgm": b"P2\n2 1\n9\n1 10\n",
+    }
+    out = {}
+    for name, data in files.items():
+        (d / name).write_bytes(data)
+    for name in sorted(p.name for p in d.iterdir()):
+        try:
+            out["read_" + name] = rimg.read_image(d / name)
+        except rimg.ImageFormatError as exc:
+            out["error_" + name] = np.array(type(exc).__name__)
+    out["written_image"] = img
+    np.savez_compressed(HERE / "io.npz", **out)
+    print("io.npz", (HERE / "io.npz").stat().st_size)
+
+
+CLI_WORK = Path("/tmp/pnp_cli_golden")  # absolute: run-dir fingerprints hash resolved paths
+
+CLI_CONFIGS = {
+    "sim_sr.ini": ("simulate-sr", "[run]\nground_truth = {w}/truth.pgm\noutput_dir = {w}/runs\n"
+                   "seed = 3\n[sr]\nfactor = 2\nblur_sigma = 1.0\nblur_radius = 4\n"
+                   "boundary = symmetric\nnoise_sigma = 0.02\n"),
+    "restore_sr.ini": ("restore", "[run]\nobservation = {w}/obs.pfm\nground_truth = {w}/truth.pgm\n"
+                       "output_dir = {w}/runs\n[sr]\nfactor = 2\nblur_sigma = 1.0\n"
+                       "blur_radius = 4\nboundary = symmetric\n[patch]\npatch_side = 3\n"
+                       "window_radius = 3\nbandwidth = 0.1\n[solver]\nrho = 1.0\n"
+                       "lambda = 0.01\nalpha = 1.0\nmax_iters = 6\nfreeze_at = 3\n"
+                       "constraint = box01\n"),
+    "restore_cg.ini": ("restore", "[run]\nobservation = {w}/obs.pfm\nground_truth = {w}/truth.pgm\n"
+                       "output_dir = {w}/runs\n[sr]\nfactor = 2\nblur_sigma = 1.0\n"
+                       "blur_radius = 4\nboundary = symmetric\n[patch]\npatch_side = 3\n"
+                       "window_radius = 3\nbandwidth = 0.1\n[solver]\nsolver = standard-cg\n"
+                       "denoiser = dsg-adaptive\nmax_iters = 4\ncg_tol = 1e-6\n"
+                       "cg_max_iters = 80\nalpha = 1.0\n"),
+    "denoise.ini": ("denoise", "[run]\ninput = {w}/truth.pgm\noutput_dir = {w}/runs\n"
+                    "[patch]\npatch_side = 5\nwindow_radius = 4\nbandwidth = 0.15\n"
+                    "[solver]\ndenoiser = dsg-adaptive\n"),
+}
+
+
+def cli_goldens():
+    """Run the reference CLI (cli.py) on small configs: run-directory names and
+    outputs the GPU CLI must reproduce (tests/golden/cli/)."""
+    import json
+    import shutil
+    from pnprestore import cli as rcli
+    from pnprestore import image as rimg
+    w = CLI_WORK
+    shutil.rmtree(w, ignore_errors=True)
+    w.mkdir(parents=True)
+    rimg.write_image(synth.scene(32, 32, 21), w / "truth.pgm", "pgm8")
+    out = HERE / "cli"
+    shutil.rmtree(out, ignore_errors=True)
+    out.mkdir()
+    shutil.copy(w / "truth.pgm", out / "truth.pgm")
+    meta = {}
+    for name, (cmd, text) in CLI_CONFIGS.items():
+        (w / name).write_text(text.format(w=w))
+        (out / name).write_text(text)
+    for name in ("sim_sr.ini", "restore_sr.ini", "restore_cg.ini", "denoise.ini"):
+        cmd = CLI_CONFIGS[name][0]
+        before = set((w / "runs").glob("*")) if (w / "runs").exists() else set()
+        rc = rcli.main([cmd, str(w / name)])
+        assert rc == 0, (name, rc)
+        (d,) = set((w / "runs").glob("*")) - before
+        meta[name] = d.name
+        for f in sorted(d.iterdir()):
+            shutil.copy(f, out / f"{name[:-4]}__{f.name}")
+        if name == "sim_sr.ini":
+            shutil.copy(d / "observation.pfm", w / "obs.pfm")
+    (out / "runs.json").write_text(json.dumps(meta, indent=1) + "\n")
+    print("cli fixtures", sorted(p.name for p in out.iterdir()))
+
+
 if __name__ == "__main__":
     if "--cg" in sys.argv:   # only the CG / standard-ADMM fixtures
         cg_goldens()
+    elif "--io" in sys.argv:
+        io_goldens()
+    elif "--cli" in sys.argv:
+        cli_goldens()
     else:
         main()
         cg_goldens()
+        io_goldens()
+        cli_goldens()

@@ -1,0 +1,50 @@
+"""The batch CLI end to end on the GPU backend vs the reference CLI's outputs
+for the same configs (tests/golden/cli/): run-directory names, observation /
+restored / denoised images (within the fp32 tolerances) and log.csv."""
+
+import json
+
+import numpy as np
+import pytest
+
+from test_cli_cpu import CLI, WORK, stage
+
+pytestmark = pytest.mark.gpu
+
+
+def _log(path):
+    lines = path.read_text().splitlines()
+    assert lines[0] == "iter,primal,dual,psnr,time_ms,objective"
+    return np.array([[float(v) for v in ln.split(",")] for ln in lines[1:]])
+
+
+def test_cli_commands_match_reference():
+    from paper_1901_06110_b200 import cli, read_image
+    runs = stage()
+    obs = WORK / "obs.pfm"
+    for name, cmd in (("sim_sr.ini", "simulate-sr"), ("restore_sr.ini", "restore"),
+                      ("restore_cg.ini", "restore"), ("denoise.ini", "denoise")):
+        if name == "sim_sr.ini":
+            obs.unlink()  # restore must read this run's own observation
+        assert cli.main([cmd, str(WORK / name)]) == 0, name
+        d = WORK / "runs" / runs[name]
+        assert d.is_dir(), name
+        tag = name[:-4]
+        for f in d.iterdir():
+            ref = CLI / f"{tag}__{f.name}"
+            assert ref.exists(), f.name
+            if f.suffix == ".pfm":
+                err = np.abs(read_image(f) - read_image(ref)).max()
+                assert err <= (2e-6 if cmd == "simulate-sr" else 1e-4), (name, f.name, err)
+            elif f.suffix == ".pgm":
+                assert np.abs(read_image(f) - read_image(ref)).max() <= 1.0 / 255 + 1e-12
+            elif f.name == "log.csv":
+                got, want = _log(f), _log(ref)
+                assert got.shape == want.shape
+                assert np.array_equal(got[:, 0], want[:, 0])
+                assert np.abs(got[:, 3] - want[:, 3]).max() < 0.02      # PSNR (dB)
+                assert np.allclose(got[:, 5], want[:, 5], rtol=1e-3)    # objective
+                assert not got[:, 4].any()                              # no --timing
+        if name == "sim_sr.ini":
+            obs.write_bytes((d / "observation.pfm").read_bytes())
+    assert json.loads((CLI / "runs.json").read_text()) == runs
