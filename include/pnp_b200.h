@@ -195,6 +195,18 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
  * residual, status (0 ok, 2 nonpositive curvature, 3 non-finite).  Device
  * resident: scalars stay on the GPU, the host polls completion every few
  * iterations. */
+/* Row-strip SR operators (sharded ADMM; batch 1).  x / r buffers hold global
+ * rows [in_r0, in_r0 + in_rows) (HR for the residual, LR for the adjoint,
+ * halos included); outputs are global rows [out_r0, out_r0 + out_rows) (LR
+ * for the residual, HR for the adjoint).  Boundary handling uses the global
+ * height Hg, so strips reproduce the whole-image operator exactly.
+ * data_out (nullable, device double): 0.5 ||A x - y||^2 over the window. */
+int pnp_sr_strip_residual(pnp_ctx* ctx, const float* x, const float* y, float* r, int Hg, int W,
+                          int in_r0, int in_rows, int out_r0, int out_rows, const float* taps,
+                          int radius, int factor, int boundary, double* data_out);
+int pnp_sr_strip_adjoint(pnp_ctx* ctx, const float* r, float* out, int Hg, int W, int in_r0,
+                         int in_rows, int out_r0, int out_rows, const float* taps, int radius,
+                         int factor, int boundary);
 /* rhs = atb + rho (v - u); z = x + u with flags |= 1 / 2 on non-finite x / z. */
 int pnp_admm_std_rhs(pnp_ctx* ctx, float* rhs, const float* atb, const float* v, const float* u,
                      int64_t n, double rho);

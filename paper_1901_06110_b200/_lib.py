@@ -77,6 +77,10 @@ _SIGS = {
     "pnp_dsg_apply_admm": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp]),
     "pnp_sr_gram": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64]),
     "pnp_admm_std_rhs": (i32, [vp, vp, vp, vp, vp, i64, f64]),
+    "pnp_sr_strip_residual": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, fptr, i32, i32,
+                                    i32, vp]),
+    "pnp_sr_strip_adjoint": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, fptr, i32, i32,
+                                   i32]),
     "pnp_admm_std_z": (i32, [vp, vp, vp, vp, i64, vp]),
     "pnp_sr_cg": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64, f64, i32, i32,
                         C.POINTER(i32), C.POINTER(f64), C.POINTER(i32)]),

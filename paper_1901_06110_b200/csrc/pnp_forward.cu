@@ -111,6 +111,15 @@ struct CgState {
   int done, iters, status, stepped;  // status: 0 ok, 2 breakdown (p.Ap <= 0), 3 non-finite
 };
 
+// Row window of an SR kernel call (row strips of a sharded image; the full
+// image is the window [0, Hg)).  Input rows are a buffer holding global rows
+// [in_r0, in_r0 + in_rows) (HR rows for the residual, LR rows for the
+// adjoint); outputs are global rows [out_r0, out_r0 + out_rows) (LR for the
+// residual, HR for the adjoint).  Boundary mapping uses the global height.
+struct SrWin {
+  int Hg, in_r0, in_rows, out_r0, out_rows;
+};
+
 constexpr int kSrT = 16;   // low-res outputs per tile side (residual)
 constexpr int kSrTA = 32;  // high-res outputs per tile side (adjoint)
 
@@ -118,20 +127,21 @@ constexpr int kSrTA = 32;  // high-res outputs per tile side (adjoint)
 // 0.5||r||^2 partials, one per tile: partial[b][tile].
 __global__ void __launch_bounds__(256)
 sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, float* __restrict__ r,
-                   int H, int W, int k, int rad, int sym, const Taps taps, double* partial,
-                   const CgState* skip = nullptr) {
+                   const SrWin win, int W, int k, int rad, int sym, const Taps taps,
+                   double* partial, const CgState* skip = nullptr) {
   extern __shared__ float sm[];
-  const int h = H / k, w = W / k, b = blockIdx.z;
+  const int H = win.Hg, w = W / k, b = blockIdx.z;
   if (skip && skip[b].done) return;  // CG: image already converged
   const int S = k * (kSrT - 1) + 1 + 2 * rad;  // staged hi-res rows / cols
   float* X = sm;                               // [S][S]
   float* Hh = sm + S * S;                      // [S][kSrT]
-  const int oy0 = blockIdx.y * kSrT, ox0 = blockIdx.x * kSrT;
+  const int oy0 = win.out_r0 + blockIdx.y * kSrT, ox0 = blockIdx.x * kSrT;
   const int y0 = k * oy0 - rad, x0 = k * ox0 - rad;
-  const float* xb = x + (size_t)b * H * W;
+  const float* xb = x + (size_t)b * win.in_rows * W;
   for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
     const int yy = i / S, xx = i - yy * S;
-    const int sy = map_index(min(y0 + yy, H - 1 + rad), H, sym);
+    int sy = map_index(min(y0 + yy, H - 1 + rad), H, sym) - win.in_r0;
+    sy = sy < 0 ? 0 : (sy >= win.in_rows ? win.in_rows - 1 : sy);  // halo rows only: never hit
     const int sx = map_index(min(x0 + xx, W - 1 + rad), W, sym);
     X[i] = xb[(size_t)sy * W + sx];
   }
@@ -147,10 +157,10 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
   const int ty = threadIdx.x / kSrT, tx = threadIdx.x - ty * kSrT;
   const int oy = oy0 + ty, ox = ox0 + tx;
   double sq = 0.0;
-  if (oy < h && ox < w) {
+  if (oy < win.out_r0 + win.out_rows && ox < w) {
     float acc = 0.f;
     for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(k * ty + a) * kSrT + tx], acc);
-    const size_t o = (size_t)b * h * w + (size_t)oy * w + ox;
+    const size_t o = (size_t)b * win.out_rows * w + (size_t)(oy - win.out_r0) * w + ox;
     if (y) acc -= y[o];
     r[o] = acc;
     sq = (double)acc * (double)acc;
@@ -183,23 +193,25 @@ enum AdjMode { ADJ_PLAIN = 0, ADJ_XUPD = 1, ADJ_CG = 2 };
 
 template <int MODE>
 __global__ void __launch_bounds__(256)
-sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, int W, int k,
-                  int rad, int sym, const Taps taps, const XUpd q, const CgEpi cg) {
+sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const SrWin win, int W,
+                  int k, int rad, int sym, const Taps taps, const XUpd q, const CgEpi cg) {
   extern __shared__ float sm[];
-  const int h = H / k, w = W / k, b = blockIdx.z;
+  const int H = win.Hg, w = W / k, b = blockIdx.z;
   if (MODE == ADJ_CG && cg.skip && cg.skip[b].done) return;
   constexpr bool XU = MODE == ADJ_XUPD;
   const int S = kSrTA + 2 * rad;
   float* U = sm;             // [S][S]
   float* Hh = sm + S * S;    // [S][kSrTA]
-  const int py0 = blockIdx.y * kSrTA, px0 = blockIdx.x * kSrTA;
-  const float* rb = r + (size_t)b * h * w;
+  const int py0 = win.out_r0 + blockIdx.y * kSrTA, px0 = blockIdx.x * kSrTA;
+  const float* rb = r + (size_t)b * win.in_rows * w;
   for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
     const int yy = i / S, xx = i - yy * S;
     const int uy = map_index(min(py0 - rad + yy, H - 1 + rad), H, sym);
     const int ux = map_index(min(px0 - rad + xx, W - 1 + rad), W, sym);
     const int qy = uy / k, qx = ux / k;
-    U[i] = (uy == qy * k && ux == qx * k) ? rb[(size_t)qy * w + qx] : 0.f;
+    int ly = qy - win.in_r0;
+    ly = ly < 0 ? 0 : (ly >= win.in_rows ? win.in_rows - 1 : ly);  // halo rows only: never hit
+    U[i] = (uy == qy * k && ux == qx * k) ? rb[(size_t)ly * w + qx] : 0.f;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < S * kSrTA; i += blockDim.x) {
@@ -215,10 +227,10 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, int H, i
   for (int i = threadIdx.x; i < kSrTA * kSrTA; i += blockDim.x) {
     const int yy = i / kSrTA, xx = i - yy * kSrTA;
     const int py = py0 + yy, px = px0 + xx;
-    if (py >= H || px >= W) continue;
+    if (py >= win.out_r0 + win.out_rows || px >= W) continue;
     float acc = 0.f;
     for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
-    const size_t o = (size_t)b * H * W + (size_t)py * W + px;
+    const size_t o = (size_t)b * win.out_rows * W + (size_t)(py - win.out_r0) * W + px;
     if (XU) {
       f |= xupdate_pixel(q, o, acc);
     } else if (MODE == ADJ_CG) {
@@ -252,12 +264,14 @@ static size_t sr_adj_smem(int rad) {
   const int S = kSrTA + 2 * rad;
   return (size_t)(S * S + S * kSrTA) * sizeof(float);
 }
-static dim3 sr_res_grid(int H, int W, int k, int batch) {
+static dim3 sr_res_grid(int H, int W, int k, int batch) {  // H: output HR rows of the window
   return dim3((W / k + kSrT - 1) / kSrT, (H / k + kSrT - 1) / kSrT, batch);
 }
 static dim3 sr_adj_grid(int H, int W, int batch) {
   return dim3((W + kSrTA - 1) / kSrTA, (H + kSrTA - 1) / kSrTA, batch);
 }
+static SrWin res_full(int H, int k) { return SrWin{H, 0, H, 0, H / k}; }
+static SrWin adj_full(int H, int k) { return SrWin{H, 0, H / k, 0, H}; }
 static cudaError_t sr_smem_attr(size_t res, size_t adj) {
   static size_t set_res = 48 * 1024, set_adj = 48 * 1024;
   cudaError_t e = cudaSuccess;
@@ -610,7 +624,7 @@ int pnp_sr_apply(pnp_ctx* ctx, const float* x, float* y, int batch, int H, int W
   {
     ProfScope prof_(ctx, PROF_FORWARD);
     sr_residual_kernel<<<sr_res_grid(H, W, factor, batch), 256, rs, ctx->stream>>>(
-        x, nullptr, y, H, W, factor, radius, boundary, t, nullptr);
+        x, nullptr, y, res_full(H, factor), W, factor, radius, boundary, t, nullptr);
   }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
   return PNP_OK;
@@ -627,7 +641,7 @@ int pnp_sr_adjoint(pnp_ctx* ctx, const float* y, float* x, int batch, int H, int
   {
     ProfScope prof_(ctx, PROF_FORWARD);
     sr_adjoint_kernel<ADJ_PLAIN><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-        y, x, H, W, factor, radius, boundary, t, XUpd{}, CgEpi{});
+        y, x, adj_full(H, factor), W, factor, radius, boundary, t, XUpd{}, CgEpi{});
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
@@ -651,8 +665,8 @@ static int sr_grad_impl(pnp_ctx* ctx, const float* x, const float* yobs, float* 
   PNP_CUDA(sr_smem_attr(rs, as));
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(x, yobs, r, H, W, factor, radius, boundary,
-                                                     t, part);
+    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(x, yobs, r, res_full(H, factor), W, factor,
+                                                     radius, boundary, t, part);
   }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
   if (data_out) {
@@ -666,10 +680,10 @@ static int sr_grad_impl(pnp_ctx* ctx, const float* x, const float* yobs, float* 
     ProfScope prof_(ctx, PROF_FORWARD);
     if (xu)
       sr_adjoint_kernel<ADJ_XUPD><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, nullptr, H, W, factor, radius, boundary, t, *xu, CgEpi{});
+          r, nullptr, adj_full(H, factor), W, factor, radius, boundary, t, *xu, CgEpi{});
     else
       sr_adjoint_kernel<ADJ_PLAIN><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, grad, H, W, factor, radius, boundary, t, XUpd{}, CgEpi{});
+          r, grad, adj_full(H, factor), W, factor, radius, boundary, t, XUpd{}, CgEpi{});
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
@@ -899,10 +913,10 @@ int pnp_sr_gram(pnp_ctx* ctx, const float* x, float* out, int batch, int H, int 
   float* lr = ctx->kx.as<float>();
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(x, nullptr, lr, H, W, factor, radius,
-                                                     boundary, t, nullptr);
+    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(x, nullptr, lr, res_full(H, factor), W,
+                                                     factor, radius, boundary, t, nullptr);
     sr_adjoint_kernel<ADJ_CG><<<ag, 256, as, ctx->stream>>>(
-        lr, out, H, W, factor, radius, boundary, t, XUpd{},
+        lr, out, adj_full(H, factor), W, factor, radius, boundary, t, XUpd{},
         CgEpi{x, shift, ctx->stats.as<double>(), nullptr});
   }
   PNP_LAUNCH_CHECK("sr_gram");
@@ -952,10 +966,11 @@ int pnp_sr_cg(pnp_ctx* ctx, const float* rhs, float* x, int batch, int H, int W,
   while (it < max_iters) {
     const int m = (max_iters - it) < chunk ? (max_iters - it) : chunk;
     for (int k = 0; k < m; ++k) {
-      sr_residual_kernel<<<rg, 256, rsm, ctx->stream>>>(p, nullptr, lr, H, W, factor, radius,
-                                                        boundary, t, nullptr, st);
+      sr_residual_kernel<<<rg, 256, rsm, ctx->stream>>>(p, nullptr, lr, res_full(H, factor), W,
+                                                        factor, radius, boundary, t, nullptr, st);
       sr_adjoint_kernel<ADJ_CG><<<ag, 256, asm_, ctx->stream>>>(
-          lr, ap, H, W, factor, radius, boundary, t, XUpd{}, CgEpi{p, shift, part, st});
+          lr, ap, adj_full(H, factor), W, factor, radius, boundary, t, XUpd{},
+          CgEpi{p, shift, part, st});
       cg_curv_kernel<<<batch, 256, 0, ctx->stream>>>(part, nblk_a, st);
       cg_update_kernel<<<dim3(nblk_e, batch), 256, 0, ctx->stream>>>(x, r, p, ap, n, st, part);
       cg_step_kernel<<<batch, 256, 0, ctx->stream>>>(part, nblk_e, st, tol, max_iters);
@@ -1003,6 +1018,61 @@ int pnp_admm_std_z(pnp_ctx* ctx, float* z, const float* x, const float* u, int64
   admm_std_z_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(z, x, u, (size_t)n,
                                                                           flags);
   PNP_LAUNCH_CHECK("admm_std_z_kernel");
+  return PNP_OK;
+}
+
+
+// ---- row-strip SR operators for sharded ADMM (batch 1, one window) ----
+int pnp_sr_strip_residual(pnp_ctx* ctx, const float* x, const float* y, float* r, int Hg, int W,
+                          int in_r0, int in_rows, int out_r0, int out_rows, const float* taps,
+                          int radius, int factor, int boundary, double* data_out) {
+  if (!ctx || !x || !r) return fail(PNP_EINVAL, "null argument");
+  Taps t;
+  int rc = sr_check(1, Hg, W, taps, radius, factor, boundary, t);
+  if (rc) return rc;
+  if (out_rows < 1 || out_r0 < 0 || (out_r0 + out_rows) * factor > Hg || in_r0 < 0 ||
+      in_r0 + in_rows > Hg)
+    return fail(PNP_EINVAL, "bad strip window");
+  const dim3 rg = sr_res_grid(out_rows * factor, W, factor, 1);
+  const int nblk = rg.x * rg.y;
+  double* part = nullptr;
+  if (data_out) {
+    if ((rc = ensure_partials(ctx, nblk))) return rc;
+    part = ctx->stats.as<double>();
+  }
+  const size_t rs = sr_res_smem(factor, radius);
+  PNP_CUDA(sr_smem_attr(rs, 0));
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(
+        x, y, r, SrWin{Hg, in_r0, in_rows, out_r0, out_rows}, W, factor, radius, boundary, t,
+        part);
+    if (data_out)
+      reduce_partials_kernel<<<dim3(1, 1), 256, 0, ctx->stream>>>(part, nblk, 1, 0.5, data_out, 1);
+  }
+  PNP_LAUNCH_CHECK("sr_strip_residual");
+  return PNP_OK;
+}
+
+int pnp_sr_strip_adjoint(pnp_ctx* ctx, const float* r, float* out, int Hg, int W, int in_r0,
+                         int in_rows, int out_r0, int out_rows, const float* taps, int radius,
+                         int factor, int boundary) {
+  if (!ctx || !r || !out) return fail(PNP_EINVAL, "null argument");
+  Taps t;
+  int rc = sr_check(1, Hg, W, taps, radius, factor, boundary, t);
+  if (rc) return rc;
+  if (out_rows < 1 || out_r0 < 0 || out_r0 + out_rows > Hg || in_r0 < 0 ||
+      (in_r0 + in_rows) * factor > Hg)
+    return fail(PNP_EINVAL, "bad strip window");
+  const size_t as = sr_adj_smem(radius);
+  PNP_CUDA(sr_smem_attr(0, as));
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_adjoint_kernel<ADJ_PLAIN><<<sr_adj_grid(out_rows, W, 1), 256, as, ctx->stream>>>(
+        r, out, SrWin{Hg, in_r0, in_rows, out_r0, out_rows}, W, factor, radius, boundary, t,
+        XUpd{}, CgEpi{});
+  }
+  PNP_LAUNCH_CHECK("sr_strip_adjoint");
   return PNP_OK;
 }
 
