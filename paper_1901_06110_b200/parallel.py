@@ -166,6 +166,22 @@ class LocalComm:
         for s in states:
             s.mbits.copy_(m)
 
+    def allreduce_sum(self, tensors):
+        """In-place sum over the virtual ranks' tensors (rank order)."""
+        tot = tensors[0].clone()
+        for t in tensors[1:]:
+            tot += t
+        for t in tensors:
+            t.copy_(tot)
+
+    def shift(self, n, send, recv, direction):
+        """recv(k) <- send(k - direction) for virtual ranks k (+1: down, -1: up)."""
+        ks = range(n - 1, 0, -1) if direction > 0 else range(n - 1)
+        for k in ks:
+            dst = recv(k)
+            if dst is not None and dst.numel():
+                dst.copy_(send(k - direction))
+
 
 class TorchComm:
     """Neighbour exchanges + max all-reduce over a torch.distributed group
@@ -211,6 +227,28 @@ class TorchComm:
         (st,) = states
         self.dist.all_reduce(st.mbits, op=self.dist.ReduceOp.MAX, group=self.group)
 
+    def allreduce_sum(self, tensors):
+        (t,) = tensors
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def shift(self, n, send, recv, direction):
+        """This rank's half of recv(k) <- send(k - direction) (k = global rank)."""
+        ops = []
+        to, frm = self.rank + direction, self.rank - direction
+        if 0 <= to < self.size:
+            ops.append(self.dist.P2POp(self.dist.isend, send(self.rank).contiguous(),
+                                       self._peer(to), self.group))
+        tmp = None
+        if 0 <= frm < self.size:
+            dst = recv(self.rank)
+            tmp = dst if dst.is_contiguous() else torch.empty_like(dst)
+            ops.append(self.dist.P2POp(self.dist.irecv, tmp, self._peer(frm), self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        if tmp is not None and tmp is not recv(self.rank):
+            recv(self.rank).copy_(tmp)
+
 
 class ShardedDSG:
     """Adaptive DSG-NLM of a Hg x W image split in row strips.
@@ -247,18 +285,20 @@ class ShardedDSG:
         return torch.cat([st.own(st.out) for st in self.states], dim=0)
 
     # ---- the sharded algorithm ----------------------------------------------
-    def _sweep(self, st, pass_, C):
+    def _sweep(self, st, pass_, C, x=None):
+        """Strip sweep; ``x`` (a window-shaped buffer) replaces the guide as the
+        filtered signal (frozen apply: pass 3 with the fixed guide)."""
         lay = st.lay
         b0, b1 = lay.window
         t0, t1 = lay.tile_rows
         part0, off, nslot = lay.part
         p = self.params
         L.call("pnp_dsg_strip_sweep", L.context(self.device.index), pass_, L.ptr(st.buf),
-               L.ptr(st.buf), L.ptr(st.rs), lay.Hg, lay.W, b0, b1 - b0, t0, t1 - t0,
-               p.window_radius, p.patch_side, self._taps, float(p.bandwidth),
+               L.ptr(st.buf if x is None else x), L.ptr(st.rs), lay.Hg, lay.W, b0, b1 - b0, t0,
+               t1 - t0, p.window_radius, p.patch_side, self._taps, float(p.bandwidth),
                L.ptr(st.partial), off, nslot, L.ptr(st.kcache))
 
-    def _fixup(self, st, mode):
+    def _fixup(self, st, mode, inv_m=None, x=None, out=None):
         lay = st.lay
         b0, b1 = lay.window
         y0, y1 = lay.rows
@@ -266,7 +306,8 @@ class ShardedDSG:
         p = self.params
         L.call("pnp_dsg_strip_fixup", L.context(self.device.index), mode, L.ptr(st.partial),
                part0, nslot, lay.Hg, lay.W, p.window_radius, p.patch_side, y0, y1, b0, b1 - b0,
-               L.ptr(st.rs), L.ptr(st.kx), L.ptr(st.d), L.ptr(st.mbits), None, None, None)
+               L.ptr(st.rs), L.ptr(st.kx), L.ptr(st.d), L.ptr(st.mbits), L.ptr(inv_m), L.ptr(x),
+               L.ptr(out))
 
     def _exchange_partials(self, C):
         def send(st):
@@ -340,3 +381,262 @@ def sharded_dsg_nlm_denoise(image: torch.Tensor, params: PatchParams, nshards: i
     sh.load(image)
     sh.denoise()
     return sh.gather()
+
+
+# ---------------------------------------------------------------------------
+# Sharded linearized PnP-ADMM for super-resolution
+# ---------------------------------------------------------------------------
+
+class ShardedSRADMM:
+    """Linearized PnP-ADMM (solver.py:199-235) on one large SR image split in
+    row strips, with a frozen-guide DSG denoiser.  Per rank and iteration:
+
+        x halo (blur radius rows)                      [P2P]
+        r = A x - y on own low-res rows (+ 0.5||r||^2) [strip residual]
+        r halo (ceil(radius/factor) low-res rows)      [P2P]
+        grad = A^T r on own rows, x-update             [strip adjoint]
+        z halo (rows the DSG sweep reads below)        [P2P]
+        v = W z: strip sweep over the frozen guide's k cache / filter, partial
+        blocks -> next rank, fixup with the global 1/m [P2P]
+        u-update + primal / dual / PSNR partial sums   [all-reduce]
+
+    Strip boundaries are DSG tile rows (multiples of TH = 32 - 2p, which the
+    decimation factor must divide), every operator reads global rows through
+    halos, so x, z, v, u are bit-identical to the single-GPU solver; the
+    records' float64 sums differ only in summation order.  ``ranks`` /
+    ``comm`` as in ShardedDSG (LocalComm = virtual ranks on one device)."""
+
+    def __init__(self, op, params: PatchParams, Hg: int, W: int, nranks: int, ranks, comm,
+                 device=None, kcache: bool = True):
+        self.op, self.params, self.comm = op, params, comm
+        self.Hg, self.W, self.k = Hg, W, op.factor
+        self.rad = op.radius
+        self.dsg = ShardedDSG(params, Hg, W, nranks, ranks, comm, device=device, kcache=kcache)
+        self.device = self.dsg.device
+        TH = self.dsg.states[0].lay.TH
+        if Hg % self.k or W % self.k or TH % self.k:
+            raise ValueError(f"factor {self.k} must divide the image and the strip tile height {TH}")
+        self.hr = -(-self.rad // self.k)
+        self.ranks = list(ranks)
+        self.nranks = nranks
+        self.st = {}
+        d = self.device
+        for rk, ds in zip(self.ranks, self.dsg.states):
+            y0, y1 = ds.lay.rows
+            if (y1 - y0 < max(self.rad, ds.lay.halo[1]) or (y1 - y0) // self.k < self.hr):
+                raise ValueError("strip too thin for the blur / DSG halos")
+            e = {"ds": ds, "rows": (y0, y1)}
+            e["xr"] = (max(0, y0 - self.rad), min(Hg, y1 + self.rad))
+            e["rr"] = (max(0, y0 // self.k - self.hr), min(Hg // self.k, y1 // self.k + self.hr))
+            e["x"] = torch.zeros((e["xr"][1] - e["xr"][0], W), dtype=torch.float32, device=d)
+            e["r"] = torch.zeros((e["rr"][1] - e["rr"][0], W // self.k), dtype=torch.float32,
+                                 device=d)
+            e["y"] = torch.zeros(((y1 - y0) // self.k, W // self.k), dtype=torch.float32, device=d)
+            own = (y1 - y0, W)
+            e["u"] = torch.zeros(own, dtype=torch.float32, device=d)
+            e["grad"] = torch.zeros(own, dtype=torch.float32, device=d)
+            e["gt"] = None
+            e["z"] = torch.zeros_like(ds.buf)   # DSG window (halos the sweep reads)
+            e["v"] = torch.zeros_like(ds.buf)   # window-shaped: the apply fixup writes own rows
+            e["flags"] = None
+            self.st[rk] = e
+        self._taps = op._taps
+        self.inv_m = torch.zeros(1, dtype=torch.float32, device=d)
+
+    # ---- helpers ----------------------------------------------------------
+    @staticmethod
+    def _own(e, name):
+        t = e[name]
+        if name in ("x",):
+            a = e["xr"][0]
+        elif name in ("z", "v", "v_prev"):
+            a = e["ds"].lay.window[0]
+        else:
+            return t
+        y0, y1 = e["rows"]
+        return t[y0 - a:y1 - a]
+
+    def _halo(self, name, r0_key, top, bottom, lowres=False):
+        """Fill ``name``'s halo rows (``top`` above, ``bottom`` below own rows)
+        from the neighbouring ranks' own edge rows."""
+        k = self.k if lowres else 1
+
+        def edges(rk):
+            e = self.st[rk]
+            y0, y1 = e["rows"]
+            base = e[r0_key][0] if r0_key else e["ds"].lay.window[0]
+            return e[name], y0 // k - base, y1 // k - base
+
+        def bottom_recv(rk):
+            t, a, b = edges(rk)
+            return t[b:b + bottom]
+
+        def bottom_send(rk):
+            t, a, b = edges(rk)
+            return t[a:a + bottom]
+
+        def top_recv(rk):
+            t, a, b = edges(rk)
+            return t[a - top:a]
+
+        def top_send(rk):
+            t, a, b = edges(rk)
+            return t[b - top:b]
+
+        if bottom:
+            self.comm.shift(self.nranks, bottom_send, bottom_recv, -1)
+        if top:
+            self.comm.shift(self.nranks, top_send, top_recv, +1)
+
+    # ---- loading -------------------------------------------------------------
+    def load(self, y_full, guide_full, truth_full=None, x0_full=None):
+        """Distribute the observation (low-res), the guide and optionally the
+        ground truth / start point (full-size host or device arrays)."""
+        self.dsg.load(guide_full)
+        for e in self.st.values():
+            y0, y1 = e["rows"]
+            e["y"].copy_(torch.as_tensor(y_full[y0 // self.k:y1 // self.k], dtype=torch.float32))
+            if truth_full is not None:
+                e["gt"] = torch.as_tensor(truth_full[y0:y1], dtype=torch.float32).to(
+                    self.device).contiguous()
+            if x0_full is not None:
+                self._own(e, "x").copy_(torch.as_tensor(x0_full[y0:y1], dtype=torch.float32))
+        if x0_full is None:  # make_sr_problem's start: k^2 A^T y (solver.py:340)
+            self._exchange_lr("y_as_r")
+            for e in self.st.values():
+                y0, y1 = e["rows"]
+                self._adjoint(e, e["r"], self._own(e, "x"))
+                self._own(e, "x").mul_(float(self.k * self.k))
+
+    def _exchange_lr(self, what):
+        for e in self.st.values():
+            a = e["rr"][0]
+            y0, y1 = e["rows"]
+            src = e["y"] if what == "y_as_r" else None
+            e["r"][y0 // self.k - a:y1 // self.k - a].copy_(src)
+        self._halo("r", "rr", self.hr, self.hr, lowres=True)
+
+    def _adjoint(self, e, rbuf, out):
+        y0, y1 = e["rows"]
+        a, b = e["rr"]
+        o = self.op
+        L.call("pnp_sr_strip_adjoint", L.context(self.device.index), L.ptr(rbuf), L.ptr(out),
+               self.Hg, self.W, a, b - a, y0, y1 - y0, self._taps, o.radius, o.factor, o._bnd)
+
+    # ---- the sharded guide freeze -------------------------------------------
+    def freeze(self):
+        """FrozenGuide.__init__ (denoise.py:367-373) on the strips: mass sweep,
+        rs, row sums d, global max m -> 1/m (bit-identical to one GPU)."""
+        dsg = self.dsg
+        dsg._exchange_rows("buf")
+        for st in dsg.states:
+            dsg._sweep(st, 0, 1)
+        dsg._exchange_partials(1)
+        for st in dsg.states:
+            dsg._fixup(st, 0)
+        dsg._exchange_rows("rs", top=False)
+        for st in dsg.states:
+            dsg._sweep(st, 2, 1)
+        dsg._exchange_partials(1)
+        for st in dsg.states:
+            st.mbits.zero_()
+            dsg._fixup(st, 2)
+        self.comm.allreduce_max(dsg.states)
+        m = dsg.states[0].mbits.view(torch.float32)
+        self.inv_m.copy_(1.0 / m)  # IEEE reciprocal, the single-GPU 1/m
+        return float(m[0])
+
+    # ---- the solver ----------------------------------------------------------
+    def run(self, config):
+        """config: SolverConfig (rho, alpha, max_iters, constraint).  Returns
+        the per-iteration records (index, primal, dual, psnr, objective)."""
+        from .image import bounds
+        lo, hi = bounds(config.constraint)
+        rho, alpha = float(config.rho), float(config.alpha)
+        mu = 1.0 / (alpha + rho)
+        n_total = self.Hg * self.W
+        iters = config.max_iters
+        ctx = L.context(self.device.index)
+        o = self.op
+        for e in self.st.values():
+            xo = self._own(e, "x")
+            L.call("pnp_project", ctx, L.ptr(xo), L.ptr(xo), xo.numel(), lo, hi)
+            self._own(e, "v").copy_(xo)
+            e["u"].zero_()
+            e["stats"] = torch.zeros((iters, 1, 4), dtype=torch.float64, device=self.device)
+            e["obj"] = torch.zeros((iters + 1, 1), dtype=torch.float64, device=self.device)
+            e["flags"] = torch.zeros(iters, dtype=torch.int32, device=self.device)
+        for k in range(1, iters + 1):
+            self._halo("x", "xr", self.rad, self.rad)
+            for e in self.st.values():
+                y0, y1 = e["rows"]
+                a, b = e["xr"]
+                ra = e["rr"][0]
+                r_own = e["r"][y0 // self.k - ra:y1 // self.k - ra]
+                L.call("pnp_sr_strip_residual", ctx, L.ptr(e["x"]), L.ptr(e["y"]), L.ptr(r_own),
+                       self.Hg, self.W, a, b - a, y0 // self.k, (y1 - y0) // self.k, self._taps,
+                       o.radius, o.factor, o._bnd, L.ptr(e["obj"][k - 1]))
+            self._halo("r", "rr", self.hr, self.hr, lowres=True)
+            for e in self.st.values():
+                self._adjoint(e, e["r"], e["grad"])
+                xo, zo, vo = self._own(e, "x"), self._own(e, "z"), self._own(e, "v")
+                L.call("pnp_admm_xupdate", ctx, L.ptr(xo), L.ptr(vo), L.ptr(e["u"]),
+                       L.ptr(e["grad"]), L.ptr(zo), xo.numel(), mu, alpha, rho, lo, hi,
+                       L.ptr(e["flags"][k - 1:k]))
+            self._halo("z", None, 0, self.dsg.states[0].lay.halo[1])
+            for e in self.st.values():
+                e["v_prev"] = e["v"]
+                e["v"] = torch.zeros_like(e["z"])
+                self.dsg._sweep(e["ds"], 3, 1, x=e["z"])
+            self.dsg._exchange_partials(1)
+            for e in self.st.values():
+                self.dsg._fixup(e["ds"], 3, inv_m=self.inv_m, x=e["z"], out=e["v"])
+                xo, vo, vp = self._own(e, "x"), self._own(e, "v"), self._own(e, "v_prev")
+                L.call("pnp_admm_uupdate", ctx, L.ptr(e["u"]), L.ptr(xo), L.ptr(vo), L.ptr(vp),
+                       L.ptr(e["gt"]), 1, xo.numel(), rho, L.ptr(e["stats"][k - 1]),
+                       L.ptr(e["flags"][k - 1:k]))
+        # objective of the final iterate
+        self._halo("x", "xr", self.rad, self.rad)
+        for e in self.st.values():
+            y0, y1 = e["rows"]
+            a, b = e["xr"]
+            ra = e["rr"][0]
+            L.call("pnp_sr_strip_residual", ctx, L.ptr(e["x"]), L.ptr(e["y"]),
+                   L.ptr(e["r"][y0 // self.k - ra:y1 // self.k - ra]), self.Hg, self.W, a, b - a,
+                   y0 // self.k, (y1 - y0) // self.k, self._taps, o.radius, o.factor, o._bnd,
+                   L.ptr(e["obj"][iters]))
+        es = list(self.st.values())
+        self.comm.allreduce_sum([e["stats"] for e in es])
+        self.comm.allreduce_sum([e["obj"] for e in es])
+        self.comm.allreduce_sum([e["flags"] for e in es])
+        st = es[0]["stats"].cpu().numpy()
+        ob = es[0]["obj"].cpu().numpy()
+        fl = es[0]["flags"].cpu().numpy()
+        bad = [i for i in range(iters) if fl[i]]
+        if bad:
+            from .solver import DivergenceError
+            raise DivergenceError(f"non-finite iterate at iteration {bad[0] + 1}")
+        import math
+        recs = []
+        for i in range(iters):
+            mse = st[i, 0, 2] / n_total
+            q = math.inf if mse == 0 else 10.0 * math.log10(1.0 / mse)
+            recs.append((i + 1, st[i, 0, 0] / n_total, st[i, 0, 1] / n_total,
+                         q if es[0]["gt"] is not None else math.nan, ob[i + 1, 0]))
+        return recs
+
+    def gather(self) -> torch.Tensor:
+        """v of every local rank, concatenated (the full image for LocalComm)."""
+        return torch.cat([self._own(self.st[rk], "v") for rk in self.ranks], dim=0)
+
+
+def sharded_linearized_pnp_admm_sr(op, y, guide, params: PatchParams, config, nshards: int,
+                                   ground_truth=None, kcache: bool = True):
+    """Virtual-shard run on one device (N strips, LocalComm) of the frozen-guide
+    SR ADMM; same v as ``linearized_pnp_admm`` with ``freeze_guide(guide)``."""
+    H, W = guide.shape
+    sh = ShardedSRADMM(op, params, H, W, nshards, range(nshards), LocalComm(), kcache=kcache)
+    sh.load(y, guide, ground_truth)
+    sh.freeze()
+    recs = sh.run(config)
+    return sh.gather(), recs

@@ -57,7 +57,13 @@ def _worker(rank, world, port, q):
         comm.shift_down([st], lambda s: s.t[4:6], lambda s: s.t[0:2])
         comm.shift_up([st], lambda s: s.t[2:4], lambda s: s.t[4:6])
         comm.allreduce_max([st])
-        q.put((rank, st.t.tolist(), int(st.mbits[0])))
+        # index-addressed shifts and the sum all-reduce used by ShardedSRADMM
+        buf = [torch.arange(4, dtype=torch.float64) + 10 * rank]
+        comm.shift(world, lambda k: buf[0][2:4], lambda k: buf[0][0:2], +1)
+        comm.shift(world, lambda k: buf[0][0:1], lambda k: buf[0][3:4], -1)
+        tot = torch.tensor([1.5 * (rank + 1), float(rank)], dtype=torch.float64)
+        comm.allreduce_sum([tot])
+        q.put((rank, st.t.tolist(), int(st.mbits[0]), buf[0].tolist(), tot.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -76,7 +82,7 @@ def test_torch_comm_gloo_world2_matches_local():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict((r, (t, m)) for r, t, m in (q.get(timeout=120) for _ in range(world)))
+    res = dict((r, (t, m, b, s)) for r, t, m, b, s in (q.get(timeout=120) for _ in range(world)))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -90,3 +96,12 @@ def test_torch_comm_gloo_world2_matches_local():
         assert res[r][0] == states[r].t.tolist()
         assert res[r][1] == int(states[r].mbits[0]) == 13
     assert res[0][0] == [0, 0, 0, 0, 1, 1] and res[1][0] == [0, 0, 1, 1, 1, 1]
+    bufs = [torch.arange(4, dtype=torch.float64) + 10 * r for r in range(world)]
+    comm.shift(world, lambda k: bufs[k][2:4], lambda k: bufs[k][0:2], +1)
+    comm.shift(world, lambda k: bufs[k][0:1], lambda k: bufs[k][3:4], -1)
+    tots = [torch.tensor([1.5 * (r + 1), float(r)], dtype=torch.float64) for r in range(world)]
+    comm.allreduce_sum(tots)
+    for r in range(world):
+        assert res[r][2] == bufs[r].tolist()
+        assert res[r][3] == tots[r].tolist() == [4.5, 1.0]
+    assert bufs[0].tolist() == [0, 1, 2, 2] and bufs[1].tolist() == [2, 3, 12, 13]
