@@ -226,6 +226,19 @@ int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite);
  * a NaN/Inf; no synchronization. */
 int pnp_flag_nonfinite(pnp_ctx* ctx, const float* x, int64_t n, int* flag);
 
+/* SplitMix64 on the device (reference forward.py:36-79, SplitMix64): the n
+ * uniforms a host stream with state `state` would return next
+ * (uniforms(n), forward.py:58-67), bit-identical; out = n device doubles.
+ * Stream-ordered, no synchronization. */
+int pnp_splitmix_uniforms(pnp_ctx* ctx, uint64_t state, int64_t n, double* out);
+/* Noise step of sr_simulate (forward.py:205-212): y + sigma * normals(n) of
+ * SplitMix64(seed) (Box-Muller, forward.py:70-79) over the flat y (n device
+ * floats), in float64; written as float32 to out32 and/or float64 to out64
+ * (either may be NULL, not both).  The transcendental calls are CUDA float64
+ * (within 2 ulp of the host's libm). */
+int pnp_sr_add_noise(pnp_ctx* ctx, const float* y, int64_t n, uint64_t seed, double sigma,
+                     float* out32, double* out64);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,8 @@ _SIGS = {
                         C.POINTER(i32), C.POINTER(f64), C.POINTER(i32)]),
     "pnp_check_finite": (i32, [vp, vp, i64, C.POINTER(i32)]),
     "pnp_flag_nonfinite": (i32, [vp, vp, i64, vp]),
+    "pnp_splitmix_uniforms": (i32, [vp, C.c_uint64, i64, vp]),
+    "pnp_sr_add_noise": (i32, [vp, vp, i64, C.c_uint64, f64, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -14,6 +14,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "pnp_internal.h"
@@ -435,6 +436,53 @@ __global__ void __launch_bounds__(256) nonfinite_kernel(const float* __restrict_
   for (size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     bad |= !isfinite(x[i]);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// ---- SplitMix64 streams on the device (reference forward.py:36-79) ----
+// Output k (k = 1, 2, ...) of a stream with state s is mix(s + k*GOLDEN), so
+// every element is independent of the others and the device reproduces the
+// host stream bit for bit (uniforms) -- no sequential state to carry.
+__device__ __forceinline__ double splitmix_uniform(unsigned long long state,
+                                                   unsigned long long k) {
+  unsigned long long z = state + 0x9E3779B97F4A7C15ull * k;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * 0x1.0p-53;
+}
+
+__global__ void __launch_bounds__(256) splitmix_uniform_kernel(unsigned long long state,
+                                                               size_t n, double* out) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = splitmix_uniform(state, i + 1);
+}
+
+// Observation noise of sr_simulate (forward.py:205-212): Box-Muller on the
+// uniform pairs (u1, u2) = outputs (2j+1, 2j+2): r = sqrt(-2 log1p(-u1)),
+// n_2j = r cos(2 pi u2), n_2j+1 = r sin(2 pi u2) (forward.py:70-79), then
+// y + sigma * n in float64, written as float32 and/or float64.  The libm
+// calls are float64 (CUDA's are within 2 ulp of numpy's).
+__global__ void __launch_bounds__(256) sr_noise_kernel(const float* __restrict__ y, size_t n,
+                                                       unsigned long long state, double sigma,
+                                                       float* out32, double* out64) {
+  const size_t pairs = (n + 1) / 2;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < pairs; j += stride) {
+    const double u1 = splitmix_uniform(state, 2 * j + 1);
+    const double u2 = splitmix_uniform(state, 2 * j + 2);
+    const double r = sqrt(-2.0 * log1p(-u1));
+    const double th = 6.283185307179586 * u2;  // 2.0 * math.pi, then * u2
+    const size_t i0 = 2 * j;
+    const double v0 = (double)y[i0] + sigma * (r * cos(th));
+    if (out32) out32[i0] = (float)v0;
+    if (out64) out64[i0] = v0;
+    if (i0 + 1 < n) {
+      const double v1 = (double)y[i0 + 1] + sigma * (r * sin(th));
+      if (out32) out32[i0 + 1] = (float)v1;
+      if (out64) out64[i0 + 1] = v1;
+    }
+  }
 }
 
 // ---- conjugate gradients on (A^T A + shift I) x = rhs, device resident ----
@@ -894,6 +942,36 @@ int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite) {
   PNP_CUDA(cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   PNP_CUDA(cudaStreamSynchronize(ctx->stream));
   *all_finite = h ? 0 : 1;
+  return PNP_OK;
+}
+
+
+int pnp_splitmix_uniforms(pnp_ctx* ctx, uint64_t state, int64_t n, double* out) {
+  if (!ctx || (!out && n > 0) || n < 0) return fail(PNP_EINVAL, "null argument");
+  if (n == 0) return PNP_OK;
+  const size_t need = ((size_t)n + 255) / 256;
+  const int blocks = (int)std::min<size_t>(need, (size_t)ctx->sms * 16);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    splitmix_uniform_kernel<<<blocks, 256, 0, ctx->stream>>>(state, (size_t)n, out);
+  }
+  PNP_LAUNCH_CHECK("splitmix_uniform_kernel");
+  return PNP_OK;
+}
+
+int pnp_sr_add_noise(pnp_ctx* ctx, const float* y, int64_t n, uint64_t seed, double sigma,
+                     float* out32, double* out64) {
+  if (!ctx || n < 0 || (n > 0 && (!y || (!out32 && !out64))))
+    return fail(PNP_EINVAL, "null argument");
+  if (!(sigma >= 0.0)) return fail(PNP_EINVAL, "noise_sigma must be >= 0");
+  if (n == 0) return PNP_OK;
+  const size_t need = ((size_t)n + 511) / 512;
+  const int blocks = (int)std::min<size_t>(need, (size_t)ctx->sms * 16);
+  {
+    ProfScope prof_(ctx, PROF_FORWARD);
+    sr_noise_kernel<<<blocks, 256, 0, ctx->stream>>>(y, (size_t)n, seed, sigma, out32, out64);
+  }
+  PNP_LAUNCH_CHECK("sr_noise_kernel");
   return PNP_OK;
 }
 

@@ -26,7 +26,7 @@ import torch
 
 from . import _arrays as A
 from . import _lib as L
-from .synth import SplitMix64
+from .synth import SplitMix64  # noqa: F401  (reference forward.SplitMix64)
 
 QIS_FLOOR = 1e-6
 
@@ -205,36 +205,52 @@ def sr_gradient(op: SuperResOp, x, y):
 
 def power_iteration_lipschitz(op: SuperResOp, hr_shape: tuple[int, int],
                               iters: int = 200, seed: int = 0) -> float:
-    """Largest eigenvalue of A^T A by power iteration (forward.py:188-203)."""
+    """Largest eigenvalue of A^T A by power iteration (forward.py:188-203).
+    The start vector is SplitMix64(seed) uniforms + 0.5 drawn on the device
+    (bit-identical to the host stream); the loop never synchronizes -- a zero
+    norm (the reference's early ``return 0.0``) is detected once at the end."""
     if iters < 1:
         raise ValueError(f"iters must be >= 1, got {iters}")
     op._check_hr(*hr_shape)
-    rng = SplitMix64(seed)
-    x = A.to_device((rng.uniforms(hr_shape[0] * hr_shape[1]).reshape(hr_shape) + 0.5))
-    x = x.double()
+    n = hr_shape[0] * hr_shape[1]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    u = torch.empty(n, dtype=torch.float64, device=dev)
+    L.call("pnp_splitmix_uniforms", L.context(dev.index), seed & ((1 << 64) - 1), n, L.ptr(u))
+    x = (u + 0.5).reshape(hr_shape)
     x = (x / torch.sqrt((x * x).sum())).float()
+    zero = torch.zeros((), dtype=torch.bool, device=dev)
     for _ in range(iters):
         z = op.adjoint_device(op.apply_device(x)).double()
         norm = torch.sqrt((z * z).sum())
-        if float(norm) == 0.0:
-            return 0.0
+        zero |= norm == 0.0
         x = (z / norm).float()
     z = op.adjoint_device(op.apply_device(x)).double()
     xd = x.double()
-    return float((xd * z).sum() / (xd * xd).sum())
+    ray = (xd * z).sum() / (xd * xd).sum()
+    return 0.0 if bool(zero) else float(ray)
 
 
 def sr_simulate(x, op: SuperResOp, noise_sigma: float, seed: int):
-    """Observation A x plus iid Gaussian noise, bit-reproducible per seed."""
+    """Observation A x plus iid Gaussian noise, bit-reproducible per seed
+    (forward.py:206-214).  Blur/decimate and the SplitMix64 Box-Muller noise
+    both run on the device; y + sigma * n is formed in float64 (numpy in ->
+    float64 out, tensor in -> float32 out)."""
     if noise_sigma < 0:
         raise ValueError(f"noise_sigma must be >= 0, got {noise_sigma}")
     t, kind = _hr_input(op, x)
     y = op.apply_device(t)
     if noise_sigma > 0:
-        n = SplitMix64(seed).normals(y.numel()).reshape(tuple(y.shape))
+        ctx = L.context(y.device.index)
+        s64 = seed & ((1 << 64) - 1)
         if kind == A.NUMPY:
-            return y.cpu().numpy().astype(np.float64) + noise_sigma * n
-        y = y + torch.from_numpy(noise_sigma * n).to(y.device, torch.float32)
+            out = torch.empty(y.shape, dtype=torch.float64, device=y.device)
+            L.call("pnp_sr_add_noise", ctx, L.ptr(y), y.numel(), s64, float(noise_sigma),
+                   None, L.ptr(out))
+            return out.cpu().numpy()
+        out = torch.empty_like(y)
+        L.call("pnp_sr_add_noise", ctx, L.ptr(y), y.numel(), s64, float(noise_sigma),
+               L.ptr(out), None)
+        y = out
     return A.from_device(y, kind)
 
 

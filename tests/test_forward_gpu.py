@@ -106,3 +106,43 @@ def test_qis_ops_match_reference(pnp, golden_forward):
 def oracle_scene16():
     from paper_1901_06110_b200 import synth
     return synth.scene(16, 16, 3)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 4097, (1 << 21) + 3])
+def test_device_splitmix_uniforms_bit_exact(pnp, n):
+    """pnp_splitmix_uniforms == the host stream's next n uniforms, bit for bit
+    (counter-based: output k of state s is mix(s + k*GOLDEN))."""
+    import torch
+    from paper_1901_06110_b200 import _lib as L
+
+    for seed in (0, 12345, (1 << 64) - 1):
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        L.call("pnp_splitmix_uniforms", L.context(0), seed, n, L.ptr(out))
+        assert np.array_equal(out.cpu().numpy(), oracle.forward.SplitMix64(seed).uniforms(n))
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (64, 63), (1024, 1025)])
+def test_device_sr_noise_matches_host_box_muller(pnp, shape):
+    """sr_simulate's noise drawn on the device equals sigma * SplitMix64.normals
+    (float64 libm calls: a few ulp); odd sizes exercise the half pair."""
+    import torch
+
+    delta = np.zeros((1, 1))
+    delta[0, 0] = 1.0
+    op = pnp.SuperResOp(delta, 1)
+    rng = np.random.default_rng(3)
+    x = rng.random(shape)
+    sigma = 5 / 255
+    clean = x.astype(np.float32).astype(np.float64)
+    y = pnp.sr_simulate(x, op, sigma, seed=77)
+    n = oracle.forward.SplitMix64(77).normals(x.size).reshape(shape)
+    assert y.dtype == np.float64
+    assert np.abs((y - clean) - sigma * n).max() <= 1e-15 + 4e-16 * np.abs(n).max()
+    yt = pnp.sr_simulate(torch.from_numpy(x).float().cuda(), op, sigma, seed=77)
+    assert yt.dtype == torch.float32
+    ref32 = (clean + sigma * n).astype(np.float32)
+    got = yt.cpu().numpy()
+    ulp = np.spacing(np.abs(ref32))
+    assert np.all(np.abs(got - ref32) <= ulp)
+    assert np.mean(got == ref32) > 0.999
+    assert np.array_equal(pnp.sr_simulate(x, op, 0.0, seed=77), clean)
