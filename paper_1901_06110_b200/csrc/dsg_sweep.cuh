@@ -250,7 +250,11 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 
   // ---- stage guide (reflected), channel planes (zero outside), clear A ----
   // warps walk rows, lanes walk columns: index math once per row / column.
+  // Rows go in batches of kSB per warp with every load of a batch issued
+  // before its first shared store (the prologue is latency-bound otherwise:
+  // a small image's CTAs only run a few chunks after it).
   // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
+  constexpr int kSB = 6, kWarps = kThreads / 32;
   if (!CACHED) {
     constexpr int NJ = (GC + 31) / 32;
     int gcol[NJ];
@@ -259,15 +263,24 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
       const int cc = lane + 32 * j;
       gcol[j] = cc < GC ? reflect_index(c0g - RB - p + cc, W) : -1;
     }
-#pragma unroll 2
-    for (int q = warp; q < GR; q += kThreads / 32) {
-      int lr = reflect_index(r0g - p + q, Hg) - br0;
-      lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
-      const float* src = Gimg + (size_t)lr * W;
-      float* dst = Gs + q * GS + lane;
+    for (int q0 = 0; q0 < GR; q0 += kSB * kWarps) {
+      float v[kSB][NJ];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
-        if (gcol[j] >= 0) dst[32 * j] = __ldg(src + gcol[j]);
+      for (int i = 0; i < kSB; ++i) {
+        const int q = q0 + warp + kWarps * i;
+        int lr = reflect_index(r0g - p + q, Hg) - br0;
+        lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
+        const float* src = Gimg + (size_t)lr * W;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) v[i][j] = (q < GR && gcol[j] >= 0) ? __ldg(src + gcol[j]) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < kSB; ++i) {
+        const int q = q0 + warp + kWarps * i;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          if (q < GR && gcol[j] >= 0) Gs[q * GS + lane + 32 * j] = v[i][j];
+      }
     }
   }
   {
@@ -282,22 +295,33 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
     for (int c_ = 0; c_ < C; ++c_) {
       const float* pa = a.ch[c_].a ? a.ch[c_].a + (size_t)b * plane : nullptr;
       const float* pb = a.ch[c_].b ? a.ch[c_].b + (size_t)b * plane : nullptr;
-#pragma unroll 2
-      for (int r = warp; r < YR; r += kThreads / 32) {
-        const int gr = r0g + r, lr = gr - br0;
-        const bool rv = gr < Hg && lr >= 0 && lr < brows;
-        const size_t ro = (size_t)(rv ? lr : 0) * W;
-        float* dst = Ys + (c_ * YR + r) * YC + lane;
+      for (int r0_ = 0; r0_ < YR; r0_ += kSB * kWarps) {
+        float va[kSB][NJ], vb[kSB][NJ];
+        bool ok[kSB][NJ];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          if (ycol[j] == -2) continue;
-          float v = 0.f;
-          if (rv && ycol[j] >= 0) {
-            v = 1.f;
-            if (pa) v = __ldg(pa + ro + ycol[j]);
-            if (pb) v = __fmul_rn(v, __ldg(pb + ro + ycol[j]));
+        for (int i = 0; i < kSB; ++i) {
+          const int r = r0_ + warp + kWarps * i;
+          const int gr = r0g + r, lr = gr - br0;
+          const bool rv = r < YR && gr < Hg && lr >= 0 && lr < brows;
+          const size_t ro = (size_t)(rv ? lr : 0) * W;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            ok[i][j] = rv && ycol[j] >= 0;
+            va[i][j] = (pa && ok[i][j]) ? __ldg(pa + ro + ycol[j]) : 1.f;
+            vb[i][j] = (pb && ok[i][j]) ? __ldg(pb + ro + ycol[j]) : 1.f;
           }
-          dst[32 * j] = v;
+        }
+#pragma unroll
+        for (int i = 0; i < kSB; ++i) {
+          const int r = r0_ + warp + kWarps * i;
+          float* dst = Ys + (c_ * YR + r) * YC + lane;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            if (r >= YR || ycol[j] == -2) continue;
+            // same floats as 1 -> *a -> *b: a*b, a, b or 1
+            const float v = pa ? (pb ? __fmul_rn(va[i][j], vb[i][j]) : va[i][j]) : vb[i][j];
+            dst[32 * j] = ok[i][j] ? v : 0.f;
+          }
         }
       }
     }

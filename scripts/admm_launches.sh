@@ -1,7 +1,8 @@
 #!/bin/bash
 # ncu launch list (device time per kernel) of config-2 ADMM runs (scripts/admm_prof.py).
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c ${1:-400} \
-  python scripts/admm_prof.py > gpurun_out/admm_ll.csv 2>&1
+# $1 = launch cap, $2 = cache control (all = cold, none = warm L2 like the real loop)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control ${2:-all} \
+  --csv -c ${1:-400} python scripts/admm_prof.py > gpurun_out/admm_ll.csv 2>&1
 grep -E "^\"[0-9]" gpurun_out/admm_ll.csv | python3 -c "
 import sys,csv
 from collections import defaultdict
