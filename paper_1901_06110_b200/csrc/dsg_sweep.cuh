@@ -56,6 +56,9 @@ constexpr int kThreads = 128;  // 64 columns x 2 row groups in phase 2
 #define PNP_KY 4
 #endif
 constexpr int kKY = PNP_KY;
+#ifndef PNP_SB
+#define PNP_SB 6  // rows per warp per batch of prologue loads
+#endif
 #ifndef PNP_KPF
 #define PNP_KPF 3  // k-cache stream: chunks of L2 prefetch lead (TMA path)
 #endif    // offsets per chunk (same dx, consecutive dy)
@@ -254,7 +257,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   // before its first shared store (the prologue is latency-bound otherwise:
   // a small image's CTAs only run a few chunks after it).
   // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
-  constexpr int kSB = 6, kWarps = kThreads / 32;
+  constexpr int kSB = PNP_SB, kWarps = kThreads / 32;
   if (!CACHED) {
     constexpr int NJ = (GC + 31) / 32;
     int gcol[NJ];

@@ -95,6 +95,23 @@ __device__ __forceinline__ int admm_u_pixel(const FixIO& io, size_t o, float v, 
   return (!isfinite(vv) || !isfinite(un)) ? 4 : 0;
 }
 
+// the same u-update from preloaded values (vprev / gt ignored when null)
+__device__ __forceinline__ int admm_u_values(const FixIO& io, size_t o, float v, float u,
+                                             float xa, float vprev, float gt, double& s0,
+                                             double& s1, double& s2) {
+  const double xv = xa, vv = v;
+  const float un = (float)((double)u + (xv - vv));
+  io.u[o] = un;
+  s0 += (xv - vv) * (xv - vv);
+  const double dv = io.rho * (vv - (io.vprev ? (double)vprev : 0.0));
+  s1 += dv * dv;
+  if (io.gt) {
+    const double e = (double)gt - vv;
+    s2 += e * e;
+  }
+  return (!isfinite(vv) || !isfinite(un)) ? 4 : 0;
+}
+
 // block-level epilogue of FIX_APPLY_U: flags + deterministic stats partials
 __device__ __forceinline__ void admm_u_block(const FixIO& io, int b, int f, double s0, double s1,
                                              double s2) {
@@ -146,13 +163,15 @@ __device__ __forceinline__ float ldg_pred(const float* p, bool on) {
 
 // Small images (many offset groups): one thread per pixel; a CTA covers 4
 // rows x 64 columns of one tile
-// (blockIdx.y = tile row * ceil(TH/4) + row quarter).  A pixel is covered by at
-// most 3 x 3 partial blocks per offset group (R <= 32 < 2 TH, R <= 64); the
+// (blockIdx.y = tile row * ceil(TH/4) + row quarter).  A pixel is covered by
+// at most 3 tile rows x 2 tile columns of partial blocks per offset group
+// (only one side column lies within R <= 32 of the pixel); their offsets are
+// computed once per pixel.  The
 // loads of kFixGB groups are all issued before any add, then summed in the
 // fixed order (group, tile row, tile col) that every variant (single GPU,
 // strips, apply) shares -> bit-reproducible, and latency-tolerant when NG is
-// large (small images split the offsets into many groups).
-
+// large (small images split the offsets into many groups).  The epilogue's
+// per-pixel inputs are loaded up front so their latency hides under the sums.
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, const FixIO io) {
   constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
@@ -172,18 +191,41 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
   const int ti0 = max(max(f.part_tr0, 0), ti - dti), ti1 = min(ti, f.part_tr0 + f.part_ntr - 1);
   const int tj0 = max(0, tj - 1), tj1 = min(f.tiles_x - 1, tj + 1);
 
-  // per-pixel block offsets (independent of the group)
-  unsigned okm = 0;  // bit (3*i + j): block (ti0+i, tj0+j) covers the pixel
-  size_t boff[3][3];
+  // per-pixel epilogue inputs, issued before the partial sums
+  const size_t o = (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x;
+  float e_rs = 0.f, e_d = 0.f, e_x = 0.f, e_u = 0.f, e_xa = 0.f, e_vp = 0.f, e_gt = 0.f;
+  if (own) {
+    if (MODE == FIX_APPLY_U || MODE == FIX_KXD || MODE == FIX_D || MODE == FIX_APPLY)
+      e_rs = io.rs[o];
+    if (MODE == FIX_APPLY_U || MODE == FIX_APPLY) {
+      e_d = io.d[o];
+      e_x = io.x[o];
+    }
+    if (MODE == FIX_APPLY_U) {
+      e_u = io.u[o];
+      e_xa = io.xa[o];
+      if (io.vprev) e_vp = io.vprev[o];
+      if (io.gt) e_gt = io.gt[o];
+    }
+  }
+
+  // covering blocks of this pixel, in (tile row, tile col) order: per tile
+  // row, the own tile column and at most one side column (left when lx < R,
+  // right when lx >= 64 - R; R <= 32 so never both) -> slots (i, 0..1)
+  const bool sideL = lx < R, sideR = !sideL && lx >= kTW - R;
+  size_t boff[3][2];
+  unsigned okm = 0;  // bit 2*i + k
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const int t_i = ti0 + i, t_j = tj0 + j;
+    for (int k = 0; k < 2; ++k) {
+      const int t_i = ti0 + i;
+      const int t_j = sideL ? tj - 1 + k : tj + k;
       const int br = y - t_i * TH, bc = x - t_j * kTW + R;
-      const bool ok = own && t_i <= ti1 && t_j <= tj1 && br < BR && bc >= 0 && bc < BC;
-      okm |= (ok ? 1u : 0u) << (3 * i + j);
-      boff[i][j] = ok ? ((size_t)(t_i - f.part_tr0) * f.NG * f.tiles_x + t_j) * blk +
+      const bool ok = own && (k == 0 || sideL || sideR) && t_i <= ti1 && t_j >= tj0 &&
+                      t_j <= tj1 && br < BR && bc >= 0 && bc < BC;
+      okm |= (ok ? 1u : 0u) << (2 * i + k);
+      boff[i][k] = ok ? ((size_t)(t_i - f.part_tr0) * f.NG * f.tiles_x + t_j) * blk +
                             (size_t)(br * BC + bc)
                       : 0;
     }
@@ -191,53 +233,51 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
 
   float s[C] = {};
   for (int g0 = 0; g0 < f.NG; g0 += kFixGB) {
-    float v[kFixGB][3][3][C];
+    float v[kFixGB][3][2][C];
 #pragma unroll
     for (int gg = 0; gg < kFixGB; ++gg)
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const bool ok = g0 + gg < f.NG && ((okm >> (3 * i + j)) & 1u);
-          const float* p = base + (size_t)(g0 + gg) * gstride + boff[i][j];
+        for (int k = 0; k < 2; ++k) {
+          const bool ok = g0 + gg < f.NG && ((okm >> (2 * i + k)) & 1u);
+          const float* p = base + (size_t)(g0 + gg) * gstride + boff[i][k];
 #pragma unroll
-          for (int c_ = 0; c_ < C; ++c_) v[gg][i][j][c_] = ldg_pred(p + (size_t)c_ * BR * BC, ok);
+          for (int c_ = 0; c_ < C; ++c_) v[gg][i][k][c_] = ldg_pred(p + (size_t)c_ * BR * BC, ok);
         }
 #pragma unroll
     for (int gg = 0; gg < kFixGB; ++gg)
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (g0 + gg < f.NG && ((okm >> (3 * i + j)) & 1u))
+        for (int k = 0; k < 2; ++k)
+          if (g0 + gg < f.NG && ((okm >> (2 * i + k)) & 1u))
 #pragma unroll
-            for (int c_ = 0; c_ < C; ++c_) s[c_] = __fadd_rn(s[c_], v[gg][i][j][c_]);
+            for (int c_ = 0; c_ < C; ++c_) s[c_] = __fadd_rn(s[c_], v[gg][i][k][c_]);
   }
 
   float dmax = 0.f;
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
   int uf = 0;
   if (own) {
-    const size_t o = (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x;
     const float s0 = s[0];
     if (MODE == FIX_APPLY_U) {
-      const float kx = __fmul_rn(io.rs[o], s0);
-      const float v = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
+      const float kx = __fmul_rn(e_rs, s0);
+      const float v = dsg_finish(kx, e_d, io.inv_m[b], e_x);
       io.out[o] = v;
-      uf = admm_u_pixel(io, o, v, u0, u1, u2);
+      uf = admm_u_values(io, o, v, e_u, e_xa, e_vp, e_gt, u0, u1, u2);
     } else if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
-      const float r = io.rs[o];
-      io.kx[o] = __fmul_rn(r, s0);
-      dmax = __fmul_rn(r, s[C - 1]);
+      io.kx[o] = __fmul_rn(e_rs, s0);
+      dmax = __fmul_rn(e_rs, s[C - 1]);
       io.d[o] = dmax;
     } else if (MODE == FIX_D) {
-      dmax = __fmul_rn(io.rs[o], s0);
+      dmax = __fmul_rn(e_rs, s0);
       io.d[o] = dmax;
     } else if (MODE == FIX_APPLY) {
-      const float kx = __fmul_rn(io.rs[o], s0);
-      io.out[o] = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
+      const float kx = __fmul_rn(e_rs, s0);
+      io.out[o] = dsg_finish(kx, e_d, io.inv_m[b], e_x);
     } else {  // FIX_NLM: num / den
       io.out[o] = __fdiv_rn(s0, s[C - 1]);
     }
