@@ -100,8 +100,10 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
  * A rank owns global rows [y0, y1) = whole tile rows of height
  * pnp_tile_height(P).  Per-pixel buffers are windows: rows [buf_r0, buf_r0 +
  * buf_rows) of the Hg x W image (own rows plus halos received from
- * neighbours).  Partial buffers hold part_ntr tile rows x pnp_dsg_groups()
- * offset groups x ceil(W/64) tiles of C*(TH+R)*(64+2R) floats; slot 0 is
+ * neighbours).  Partial buffers hold part_ntr tile rows x partial groups
+ * (pnp_dsg_groups() offset groups, reduced on chip by thread-block clusters of
+ * min(groups, 8) CTAs) x ceil(W/64) tiles of C*(TH+R)*(64+2R) floats
+ * (pnp_dsg_partial_floats gives the total); slot 0 is
  * global tile row part_tr0 (a neighbour's rows are received into the
  * prefix).  A sharded run sums in exactly the single-GPU order, so its
  * output is bit-identical.

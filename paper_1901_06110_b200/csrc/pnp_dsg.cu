@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
   const int x = tj * kTW + lx, y = ti * TH + ly;
   const bool own = ly < TH && x < W && y >= f.y0 && y < f.y0 + f.nrows && y < f.Hg;
   const size_t blk = (size_t)f.C * BR * BC;
-  const float* base = f.partial + (size_t)b * f.part_ntr * f.NG * f.tiles_x * blk;
+  const float* base = f.partial + (size_t)b * f.part_ntr * f.NP * f.tiles_x * blk;
   const int dti = (R + TH - 1) / TH;
   const int ti0 = max(max(f.part_tr0, 0), ti - dti), ti1 = min(ti, f.part_tr0 + f.part_ntr - 1);
   const int tj0 = max(0, tj - 1), tj1 = min(f.tiles_x - 1, tj + 1);
@@ -225,14 +225,14 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
       const bool ok = own && (k == 0 || sideL || sideR) && t_i <= ti1 && t_j >= tj0 &&
                       t_j <= tj1 && br < BR && bc >= 0 && bc < BC;
       okm |= (ok ? 1u : 0u) << (2 * i + k);
-      boff[i][k] = ok ? ((size_t)(t_i - f.part_tr0) * f.NG * f.tiles_x + t_j) * blk +
+      boff[i][k] = ok ? ((size_t)(t_i - f.part_tr0) * f.NP * f.tiles_x + t_j) * blk +
                             (size_t)(br * BC + bc)
                       : 0;
     }
   const size_t gstride = (size_t)f.tiles_x * blk;  // next group, same tile
 
   float s[C] = {};
-  for (int g0 = 0; g0 < f.NG; g0 += kFixGB) {
+  for (int g0 = 0; g0 < f.NP; g0 += kFixGB) {
     float v[kFixGB][3][2][C];
 #pragma unroll
     for (int gg = 0; gg < kFixGB; ++gg)
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
       for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const bool ok = g0 + gg < f.NG && ((okm >> (2 * i + k)) & 1u);
+          const bool ok = g0 + gg < f.NP && ((okm >> (2 * i + k)) & 1u);
           const float* p = base + (size_t)(g0 + gg) * gstride + boff[i][k];
 #pragma unroll
           for (int c_ = 0; c_ < C; ++c_) v[gg][i][k][c_] = ldg_pred(p + (size_t)c_ * BR * BC, ok);
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
       for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int k = 0; k < 2; ++k)
-          if (g0 + gg < f.NG && ((okm >> (2 * i + k)) & 1u))
+          if (g0 + gg < f.NP && ((okm >> (2 * i + k)) & 1u))
 #pragma unroll
             for (int c_ = 0; c_ < C; ++c_) s[c_] = __fadd_rn(s[c_], v[gg][i][k][c_]);
   }
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
   const int x = tj * kTW + lx;
   const int ylo = max(f.y0, ti * TH), yhi = min(min(f.y0 + f.nrows, f.Hg), ti * TH + TH);
   const size_t blk = (size_t)f.C * BR * BC;
-  const float* base = f.partial + (size_t)b * f.part_ntr * f.NG * f.tiles_x * blk;
+  const float* base = f.partial + (size_t)b * f.part_ntr * f.NP * f.tiles_x * blk;
   const int dti = (R + TH - 1) / TH, dtj = (R + kTW - 1) / kTW;
   const int ti0 = max(max(f.part_tr0, 0), ti - dti), ti1 = min(ti, f.part_tr0 + f.part_ntr - 1);
   const int tj0 = max(0, tj - dtj), tj1 = min(f.tiles_x - 1, tj + dtj);
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
   // so the per-thread loads below see L2 latency rather than HBM latency.
   {
     const int nti = ti1 - ti0 + 1, ntj = tj1 - tj0 + 1;
-    const int nq = f.NG * nti * ntj * C;
+    const int nq = f.NP * nti * ntj * C;
     for (int q = threadIdx.x; q < nq; q += blockDim.x) {
       int r_ = q;
       const int c_ = r_ % C; r_ /= C;
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
       const int gg = r_ / nti;
       const int br0 = ti * TH - t_i * TH, br1 = min(BR, br0 + TH);
       if (br0 >= br1) continue;
-      const float* p = base + (((size_t)(t_i - f.part_tr0) * f.NG + gg) * f.tiles_x + t_j) * blk +
+      const float* p = base + (((size_t)(t_i - f.part_tr0) * f.NP + gg) * f.tiles_x + t_j) * blk +
                        (size_t)c_ * BR * BC + (size_t)br0 * BC;
       const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
       const uintptr_t a1 = ((uintptr_t)(p + (size_t)(br1 - br0) * BC) + 15) & ~(uintptr_t)15;
@@ -351,9 +351,9 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
 #pragma unroll
     for (int k = 0; k < kFixRows; ++k) s[c_][k] = 0.f;
 
-  for (int gg = 0; gg < f.NG; ++gg)
+  for (int gg = 0; gg < f.NP; ++gg)
     for (int t_i = ti0; t_i <= ti1; ++t_i) {
-      const float* row = base + ((size_t)(t_i - f.part_tr0) * f.NG + gg) * f.tiles_x * blk;
+      const float* row = base + ((size_t)(t_i - f.part_tr0) * f.NP + gg) * f.tiles_x * blk;
       for (int t_j = tj0; t_j <= tj1; ++t_j) {
         const int bc = x - t_j * kTW + R;
         if (bc < 0 || bc >= BC || x >= W) continue;
@@ -456,6 +456,7 @@ __global__ void dsg_alpha_kernel(const unsigned* mbits, float* mv, int B) {
 // batch, so single-GPU and sharded runs sum in the same order.
 struct Geom {
   int B, Hg, W, R, P, TH, tiles_x, tiles_y, nchunks, NG;
+  int CG, NP;  // sweep cluster size (offset groups reduced on chip), partial groups NG / CG
   const Chunk* chunks;        // hat-tapered table (DSG), host
   const Chunk* chunks_nohat;  // same offsets, L = 0 (plain NLM), host
   const int* grp;             // NG+1 group starts, host
@@ -497,14 +498,28 @@ static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
   }
 }
 
+#ifndef PNP_CLUSTER
+#define PNP_CLUSTER 1  // largest cluster of one tile's offset-group CTAs (1: off, measured best)
+#endif
+
 static int pick_groups(int ntiles, int nchunks) {
   // Offset-group split so small images still fill 148 SMs (~8 CTAs each).
-  const int target = 148 * 8;
+  // Above PNP_CLUSTER groups the count is a multiple of it: the groups of one
+  // tile run as thread-block clusters (cluster_size).
+  const int target = 148 * 8, cm = PNP_CLUSTER;
   int ng = (target + ntiles - 1) / ntiles;
   if (ng > nchunks) ng = nchunks;
-  if (ng > 64) ng = 64;
+  if (ng > kMaxGroups) ng = kMaxGroups;
+  if (ng > cm) {
+    const int up = (ng + cm - 1) / cm * cm;
+    ng = up <= nchunks ? up : nchunks / cm * cm;
+  }
   return ng < 1 ? 1 : ng;
 }
+
+// CTAs of one tile's offset groups that reduce their far/near planes through
+// distributed shared memory before writing one partial block (the cluster).
+static int cluster_size(int ng) { return ng <= PNP_CLUSTER ? ng : PNP_CLUSTER; }
 
 static int check_geometry(int B, int H, int W, int R, int P, double bw) {
   if (B < 1) return fail(PNP_EINVAL, "batch must be >= 1");
@@ -547,6 +562,8 @@ static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, Geom& g) 
   build_chunks(R, false, ch0);
   g.nchunks = (int)ch.size();
   g.NG = pick_groups(g.tiles_x * g.tiles_y, g.nchunks);
+  g.CG = cluster_size(g.NG);
+  g.NP = g.NG / g.CG;
   auto key = std::make_pair(R, g.NG);
   auto it = ctx->tables.find(key);
   if (it == ctx->tables.end()) {
@@ -572,7 +589,13 @@ static size_t block_floats(const Geom& g, int C) {
 }
 
 static size_t partial_floats(const Geom& g, int ntr, int C) {
-  return (size_t)g.B * ntr * g.NG * g.tiles_x * block_floats(g, C);
+  return (size_t)g.B * ntr * g.NP * g.tiles_x * block_floats(g, C);
+}
+
+// Fixup variant: one thread per pixel when there are many partial groups or
+// too few tiles to fill the GPU with one CTA per tile (same sums either way).
+static bool fixup_px(const Geom& g) {
+  return g.NP > 2 || (long long)g.B * g.tiles_x * g.tiles_y < 2 * 148;
 }
 
 template <int RB, int C, int MODE>
@@ -639,6 +662,7 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   a.part_ntr = w.part_ntr;
   a.kcache = reinterpret_cast<float2*>(kcache);
   a.kc_npairs = g.nchunks * (kKY / 2);
+  a.cg = g.CG;
   a.kc_img = (long long)w.ntr * g.tiles_x * a.kc_npairs * g.TH * kTW;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
@@ -673,7 +697,7 @@ static int run_fixup(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   f.R = g.R;
   f.TH = g.TH;
   f.tiles_x = g.tiles_x;
-  f.NG = g.NG;
+  f.NP = g.NP;
   f.C = C;
   f.part_tr0 = w.part_tr0;
   f.part_ntr = w.part_ntr;
@@ -683,7 +707,7 @@ static int run_fixup(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   f.buf_rows = w.buf_rows;
   const int tr_first = w.y0 / g.TH, tr_last = (w.y0 + w.nrows - 1) / g.TH;
   ProfScope prof(ctx, PROF_FIXUP);
-  if (g.NG <= 2) {  // same summation order either way
+  if (!fixup_px(g)) {  // same summation order either way
     dim3 grid(g.tiles_x, tr_last - tr_first + 1, g.B);
     dsg_fixup_tile_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
   } else {
@@ -980,7 +1004,7 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
   if (rc) return rc;
   if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   const Window w = full_window(g);
-  const int rows = g.NG <= 2 ? g.tiles_y : g.tiles_y * ((g.TH + 3) / 4);
+  const int rows = fixup_px(g) ? g.tiles_y * ((g.TH + 3) / 4) : g.tiles_y;
   const size_t nblk = (size_t)g.tiles_x * rows;
   if ((rc = ctx->stats.ensure((size_t)g.B * nblk * 3 * sizeof(double)))) return rc;
   float* part = ctx->partial.as<float>();
@@ -1079,7 +1103,8 @@ int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr) {
   if (check_geometry(1, Hg, W, R, P, 1.0) || C < 1 || C > 2 || ntr < 0) return -1;
   const int TH = tile_height(P);
   const int64_t blk = (int64_t)C * (TH + R) * (kTW + 2 * R);
-  return (int64_t)ntr * groups_for(Hg, W, R, P) * ((W + kTW - 1) / kTW) * blk;
+  const int ng = groups_for(Hg, W, R, P);  // partial groups: NG / cluster size
+  return (int64_t)ntr * (ng / cluster_size(ng)) * ((W + kTW - 1) / kTW) * blk;
 }
 
 int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int ntr) {

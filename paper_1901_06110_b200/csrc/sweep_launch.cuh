@@ -24,8 +24,26 @@ cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaSt
   memset(&tab, 0, sizeof(tab));
   memcpy(tab.c, t.ch, sizeof(Chunk) * t.nch);
   memcpy(tab.grp, t.grp, sizeof(int) * (t.ng + 1));
-  dsg_sweep_kernel<P, RB, C, MODE><<<grid, kThreads, smem, st>>>(a, tab);
-  return cudaGetLastError();
+  if (a.cg <= 1) {
+    dsg_sweep_kernel<P, RB, C, MODE><<<grid, kThreads, smem, st>>>(a, tab);
+    return cudaGetLastError();
+  }
+  // a tile's offset groups as one thread-block cluster (grid.y = NG, a
+  // multiple of cg): they reduce their planes on chip (dsg_sweep.cuh)
+  if (a.cg > kMaxCluster || grid.y % a.cg) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = (unsigned)a.cg;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dsg_sweep_kernel<P, RB, C, MODE>, a, tab);
 }
 
 
