@@ -172,10 +172,14 @@ __device__ __forceinline__ float ldg_pred(const float* p, bool on) {
 // strips, apply) shares -> bit-reproducible, and latency-tolerant when NG is
 // large (small images split the offsets into many groups).  The epilogue's
 // per-pixel inputs are loaded up front so their latency hides under the sums.
+#ifndef PNP_FIXGB
+#define PNP_FIXGB 4
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, const FixIO io) {
   constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
-  constexpr int kFixGB = C == 1 ? 4 : 2;  // offset groups loaded per batch
+  constexpr int kFixGB = C == 1 ? PNP_FIXGB : PNP_FIXGB / 2;  // offset groups per batch of loads
   const int b = blockIdx.z;
   const int TH = f.TH, R = f.R, W = f.W;
   const int BR = TH + R, BC = kTW + 2 * R;
@@ -211,9 +215,11 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
 
   // covering blocks of this pixel, in (tile row, tile col) order: per tile
   // row, the own tile column and at most one side column (left when lx < R,
-  // right when lx >= 64 - R; R <= 32 so never both) -> slots (i, 0..1)
+  // right when lx >= 64 - R; R <= 32 so never both) -> slots (i, 0..1).
+  // 32-bit float offsets from the image's partial base (the host keeps an
+  // image's partial array below 2^32 floats for this kernel).
   const bool sideL = lx < R, sideR = !sideL && lx >= kTW - R;
-  size_t boff[3][2];
+  unsigned boff[3][2];
   unsigned okm = 0;  // bit 2*i + k
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -225,14 +231,16 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
       const bool ok = own && (k == 0 || sideL || sideR) && t_i <= ti1 && t_j >= tj0 &&
                       t_j <= tj1 && br < BR && bc >= 0 && bc < BC;
       okm |= (ok ? 1u : 0u) << (2 * i + k);
-      boff[i][k] = ok ? ((size_t)(t_i - f.part_tr0) * f.NP * f.tiles_x + t_j) * blk +
-                            (size_t)(br * BC + bc)
-                      : 0;
+      boff[i][k] = ok ? (unsigned)(((t_i - f.part_tr0) * f.NP * f.tiles_x + t_j) * blk) +
+                            (unsigned)(br * BC + bc)
+                      : 0u;
     }
-  const size_t gstride = (size_t)f.tiles_x * blk;  // next group, same tile
+  const unsigned gstride = (unsigned)(f.tiles_x * blk);  // next group, same tile
+  const unsigned cstride = (unsigned)(BR * BC);
 
   float s[C] = {};
   for (int g0 = 0; g0 < f.NP; g0 += kFixGB) {
+    const float* gb = base + (size_t)g0 * gstride;
     float v[kFixGB][3][2][C];
 #pragma unroll
     for (int gg = 0; gg < kFixGB; ++gg)
@@ -241,9 +249,9 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const bool ok = g0 + gg < f.NP && ((okm >> (2 * i + k)) & 1u);
-          const float* p = base + (size_t)(g0 + gg) * gstride + boff[i][k];
+          const unsigned off = (unsigned)gg * gstride + boff[i][k];
 #pragma unroll
-          for (int c_ = 0; c_ < C; ++c_) v[gg][i][k][c_] = ldg_pred(p + (size_t)c_ * BR * BC, ok);
+          for (int c_ = 0; c_ < C; ++c_) v[gg][i][k][c_] = ldg_pred(gb + (off + c_ * cstride), ok);
         }
 #pragma unroll
     for (int gg = 0; gg < kFixGB; ++gg)
@@ -595,6 +603,9 @@ static size_t partial_floats(const Geom& g, int ntr, int C) {
 // Fixup variant: one thread per pixel when there are many partial groups or
 // too few tiles to fill the GPU with one CTA per tile (same sums either way).
 static bool fixup_px(const Geom& g) {
+  // (32-bit offsets inside one image's partial array)
+  if ((double)g.tiles_y * g.NP * g.tiles_x * 2 * (g.TH + g.R) * (kTW + 2 * g.R) >= 4294967295.0)
+    return false;
   return g.NP > 2 || (long long)g.B * g.tiles_x * g.tiles_y < 2 * 148;
 }
 
