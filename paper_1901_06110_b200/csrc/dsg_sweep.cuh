@@ -56,9 +56,13 @@ constexpr int kThreads = 128;  // 64 columns x 2 row groups in phase 2
 #define PNP_KY 4
 #endif
 constexpr int kKY = PNP_KY;
-#ifndef PNP_SB
-#define PNP_SB 6  // rows per warp per batch of prologue loads
+#ifndef PNP_CLUSTER
+#define PNP_CLUSTER 1  // largest cluster of one tile's offset-group CTAs (1: off, measured best)
 #endif
+#ifndef PNP_SB
+#define PNP_SB 6  // rows per warp per batch of prologue loads (k-cache sweeps)
+#endif
+
 #ifndef PNP_KPF
 #define PNP_KPF 3  // k-cache stream: chunks of L2 prefetch lead (TMA path)
 #endif    // offsets per chunk (same dx, consecutive dy)
@@ -135,11 +139,11 @@ struct SweepArgs {
   float2* kcache;
   long long kc_img;
   int kc_npairs;
+  float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
+  float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
   // offset groups per cluster: the cg CTAs of a tile (blockIdx.y = gp*cg + q)
   // sum their planes through DSMEM into one partial block (group gp)
   int cg;
-  float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
-  float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
 };
 
 __host__ __device__ constexpr int tile_height(int P) { return 32 - (P - 1); }
@@ -274,11 +278,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 
   // ---- stage guide (reflected), channel planes (zero outside), clear A ----
   // warps walk rows, lanes walk columns: index math once per row / column.
-  // Rows go in batches of kSB per warp with every load of a batch issued
-  // before its first shared store (the prologue is latency-bound otherwise:
-  // a small image's CTAs only run a few chunks after it).
   // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
-  constexpr int kSB = PNP_SB, kWarps = kThreads / 32;
   if (!CACHED) {
     constexpr int NJ = (GC + 31) / 32;
     int gcol[NJ];
@@ -287,24 +287,15 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
       const int cc = lane + 32 * j;
       gcol[j] = cc < GC ? reflect_index(c0g - RB - p + cc, W) : -1;
     }
-    for (int q0 = 0; q0 < GR; q0 += kSB * kWarps) {
-      float v[kSB][NJ];
+#pragma unroll 2
+    for (int q = warp; q < GR; q += kThreads / 32) {
+      int lr = reflect_index(r0g - p + q, Hg) - br0;
+      lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
+      const float* src = Gimg + (size_t)lr * W;
+      float* dst = Gs + q * GS + lane;
 #pragma unroll
-      for (int i = 0; i < kSB; ++i) {
-        const int q = q0 + warp + kWarps * i;
-        int lr = reflect_index(r0g - p + q, Hg) - br0;
-        lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
-        const float* src = Gimg + (size_t)lr * W;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) v[i][j] = (q < GR && gcol[j] >= 0) ? __ldg(src + gcol[j]) : 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < kSB; ++i) {
-        const int q = q0 + warp + kWarps * i;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-          if (q < GR && gcol[j] >= 0) Gs[q * GS + lane + 32 * j] = v[i][j];
-      }
+      for (int j = 0; j < NJ; ++j)
+        if (gcol[j] >= 0) dst[32 * j] = __ldg(src + gcol[j]);
     }
   }
   {
@@ -319,32 +310,57 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
     for (int c_ = 0; c_ < C; ++c_) {
       const float* pa = a.ch[c_].a ? a.ch[c_].a + (size_t)b * plane : nullptr;
       const float* pb = a.ch[c_].b ? a.ch[c_].b + (size_t)b * plane : nullptr;
-      for (int r0_ = 0; r0_ < YR; r0_ += kSB * kWarps) {
-        float va[kSB][NJ], vb[kSB][NJ];
-        bool ok[kSB][NJ];
+      if constexpr (CACHED) {
+        // k-cache sweeps run few chunks per CTA on small images, so the
+        // prologue's latency shows: rows go in batches of kSB per warp with
+        // every load of a batch issued before its first shared store
+        constexpr int kSB = PNP_SB, kWarps = kThreads / 32;
+        for (int r0_ = 0; r0_ < YR; r0_ += kSB * kWarps) {
+          float va[kSB][NJ], vb[kSB][NJ];
+          bool ok[kSB][NJ];
 #pragma unroll
-        for (int i = 0; i < kSB; ++i) {
-          const int r = r0_ + warp + kWarps * i;
-          const int gr = r0g + r, lr = gr - br0;
-          const bool rv = r < YR && gr < Hg && lr >= 0 && lr < brows;
-          const size_t ro = (size_t)(rv ? lr : 0) * W;
+          for (int i = 0; i < kSB; ++i) {
+            const int r = r0_ + warp + kWarps * i;
+            const int gr = r0g + r, lr = gr - br0;
+            const bool rv = r < YR && gr < Hg && lr >= 0 && lr < brows;
+            const size_t ro = (size_t)(rv ? lr : 0) * W;
 #pragma unroll
-          for (int j = 0; j < NJ; ++j) {
-            ok[i][j] = rv && ycol[j] >= 0;
-            va[i][j] = (pa && ok[i][j]) ? __ldg(pa + ro + ycol[j]) : 1.f;
-            vb[i][j] = (pb && ok[i][j]) ? __ldg(pb + ro + ycol[j]) : 1.f;
+            for (int j = 0; j < NJ; ++j) {
+              ok[i][j] = rv && ycol[j] >= 0;
+              va[i][j] = (pa && ok[i][j]) ? __ldg(pa + ro + ycol[j]) : 1.f;
+              vb[i][j] = (pb && ok[i][j]) ? __ldg(pb + ro + ycol[j]) : 1.f;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < kSB; ++i) {
+            const int r = r0_ + warp + kWarps * i;
+            float* dst = Ys + (c_ * YR + r) * YC + lane;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+              if (r >= YR || ycol[j] == -2) continue;
+              // same floats as 1 -> *a -> *b: a*b, a, b or 1
+              const float v = pa ? (pb ? __fmul_rn(va[i][j], vb[i][j]) : va[i][j]) : vb[i][j];
+              dst[32 * j] = ok[i][j] ? v : 0.f;
+            }
           }
         }
-#pragma unroll
-        for (int i = 0; i < kSB; ++i) {
-          const int r = r0_ + warp + kWarps * i;
+      } else {
+#pragma unroll 2
+        for (int r = warp; r < YR; r += kThreads / 32) {
+          const int gr = r0g + r, lr = gr - br0;
+          const bool rv = gr < Hg && lr >= 0 && lr < brows;
+          const size_t ro = (size_t)(rv ? lr : 0) * W;
           float* dst = Ys + (c_ * YR + r) * YC + lane;
 #pragma unroll
           for (int j = 0; j < NJ; ++j) {
-            if (r >= YR || ycol[j] == -2) continue;
-            // same floats as 1 -> *a -> *b: a*b, a, b or 1
-            const float v = pa ? (pb ? __fmul_rn(va[i][j], vb[i][j]) : va[i][j]) : vb[i][j];
-            dst[32 * j] = ok[i][j] ? v : 0.f;
+            if (ycol[j] == -2) continue;
+            float v = 0.f;
+            if (rv && ycol[j] >= 0) {
+              v = 1.f;
+              if (pa) v = __ldg(pa + ro + ycol[j]);
+              if (pb) v = __fmul_rn(v, __ldg(pb + ro + ycol[j]));
+            }
+            dst[32 * j] = v;
           }
         }
       }
@@ -617,11 +633,17 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
     }
   __syncthreads();
   const int BR = TH + R, BC = kTW + 2 * R;
+#if PNP_CLUSTER > 1
   const int cgs = a.cg > 1 ? a.cg : 1, np = gridDim.y / cgs;
   const size_t slot =
       (((size_t)b * a.part_ntr + a.part_off + tyl) * np + blockIdx.y / cgs) * a.tiles_x + tx;
+#else
+  constexpr int cgs = 1;
+  const size_t slot =
+      (((size_t)b * a.part_ntr + a.part_off + tyl) * gridDim.y + blockIdx.y) * a.tiles_x + tx;
+#endif
   float* out = a.partial + slot * (size_t)(C * BR * BC);
-  if (cgs == 1) {
+  if (PNP_CLUSTER == 1 || cgs == 1) {
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_) {
       const float* A0 = As + c_ * AR * YC + (RB - R);
@@ -629,7 +651,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
       for (int br = warp; br < BR; br += kThreads / 32)
         for (int bc = lane; bc < BC; bc += 32) o[br * BC + bc] = A0[br * YC + bc];
     }
-  } else {
+  } else if constexpr (PNP_CLUSTER > 1) {
     // cluster of the tile's offset groups: CTA q of the cluster sums rows
     // [q*BR/cgs, (q+1)*BR/cgs) of all cgs planes in group order (DSMEM loads)
     // and writes them; the second cluster barrier keeps every plane alive

@@ -506,10 +506,6 @@ static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
   }
 }
 
-#ifndef PNP_CLUSTER
-#define PNP_CLUSTER 1  // largest cluster of one tile's offset-group CTAs (1: off, measured best)
-#endif
-
 static int pick_groups(int ntiles, int nchunks) {
   // Offset-group split so small images still fill 148 SMs (~8 CTAs each).
   // Above PNP_CLUSTER groups the count is a multiple of it: the groups of one
