@@ -189,6 +189,25 @@ int pnp_qis_grad_xupdate(pnp_ctx* ctx, float* x, const float* ones, const float*
 int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v, float* u,
                        const float* x, const float* v_prev, const float* gt, double rho,
                        double* stats, int* flags);
+/* Native iteration loop of linearized_pnp_admm with a frozen guide
+ * (reference solver.py:199-235): iterations k0..k1 (1-based) of
+ *   x <- proj(mu (alpha x + rho (v - u) - grad f(x))), z = x + u   (fused)
+ *   v <- W z, u += x - v, stats / flags                         (fused)
+ * issuing, per iteration, exactly pnp_sr_grad_xupdate (kind 0: obs = y,
+ * taps/radius/factor/boundary) or pnp_qis_grad_xupdate (kind 1: obs = ones,
+ * obs2 = zeros, gain_over_K, floor_) followed by pnp_dsg_apply_admm, with the
+ * same per-iteration pointers the Python loop uses: flags + k-1, stats +
+ * (k-1)*batch*4, objv + (k-2)*batch (objective of the previous iterate; objv
+ * may be NULL).  v0 holds the current v on entry; the new v alternates
+ * between v1 and v0, *v_last tells which holds the final one (0 = v0).
+ * ms_out (nullable, host, k1-k0+1 floats): device time from the call's start
+ * to the end of each iteration (synchronizes once at the end). */
+int pnp_admm_run(pnp_ctx* ctx, int kind, const float* obs, const float* obs2, int batch, int H,
+                 int W, const float* taps, int radius, int factor, int boundary,
+                 double gain_over_K, double floor_, const pnp_frozen* fz, int k0, int k1, float* x,
+                 float* v0, float* v1, float* u, float* z, const float* gt, double mu,
+                 double alpha, double rho, double lo, double hi, double* stats, double* objv,
+                 int* flags, float* ms_out, int* v_last);
 /* Standard PnP-ADMM baseline (reference solver.py:244-328): the Gram operator
  * out = A^T A x + shift x of the SR model, and conjugate gradients on
  * (A^T A + shift I) x = rhs per image of a batch (cg_solve semantics: stop

@@ -809,6 +809,7 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
     cudaEventDestroy(sl.a);
     cudaEventDestroy(sl.b);
   }
+  for (cudaEvent_t e : ctx->iter_events) cudaEventDestroy(e);
   delete ctx;
   return PNP_OK;
 }

@@ -71,6 +71,8 @@ struct pnp_ctx {
     std::vector<int> grp;
   };
   std::map<std::pair<int, int>, Tables> tables;
+  // per-iteration timing events of the native ADMM loop (pnp_admm_run)
+  std::vector<cudaEvent_t> iter_events;
   // optional per-launch CUDA-event timing (pnp_ctx_profile)
   bool prof = false;
   std::vector<pnp::ProfSlot> slots;

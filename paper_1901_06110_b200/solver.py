@@ -26,6 +26,7 @@ receive float32 CUDA tensors and stay on device.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import time
 from dataclasses import dataclass, field
@@ -203,6 +204,10 @@ class Problem:
     # (rhs, x, shift, tol, max_iters, warm) -> (iterations, residuals, status)
     device_cg: Callable | None = field(default=None, repr=False)
     device_atb: object | None = field(default=None, repr=False)
+    # the gradient's native description for the C++ iteration loop
+    # (pnp_admm_run): (kind, obs, obs2, taps, radius, factor, boundary,
+    # gain_over_K, floor) with kind 0 = SR, 1 = QIS
+    native_grad: tuple | None = field(default=None, repr=False)
 
 
 @dataclass
@@ -301,7 +306,7 @@ def _host_wrap_array_fn(fn, kind_shape):
 
 
 def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, callback=None,
-                        graph: bool = False):
+                        graph: bool = False, native: bool = True):
     """Gradient-step PnP-ADMM; returns (final v, per-iteration records).
 
     Per iteration: x <- proj(mu (alpha x + rho (v - u) - grad f(x))) with
@@ -318,6 +323,11 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
     saves, because the eager host loop already keeps pace with the device.
     Results are bitwise identical to the eager loop; the captured
     iterations' ``time_ms`` are interpolated over the replay.
+
+    ``native``: with a frozen-guide denoiser, a device forward model and no
+    callback / stop_tol / graph, the iterations from the first frozen one on
+    run in the library's C++ loop (``pnp_admm_run``; same calls, bitwise
+    identical iterates); ``native=False`` keeps the Python loop.
     """
     dev = A.device_index()
     x0, kind = A.validate(problem.x0, "x0", batch_ok=True)
@@ -355,7 +365,12 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
     grad = torch.empty_like(x)
     z = torch.empty_like(x)
     mu = 1.0 / (config.alpha + config.rho)
-    events = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+    events = [None] * (iters + 1)  # created on demand (the C++ loop keeps its own)
+
+    def _event(k):
+        if events[k] is None:
+            events[k] = torch.cuda.Event(enable_timing=True)
+        return events[k]
 
     L.call("pnp_project", ctx, L.ptr(x), L.ptr(x), x.numel(), lo, hi)
     v = x.clone()
@@ -368,7 +383,7 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
         if graph and iters - max(gfrom, 2) + 1 >= 3:
             k_cap = max(gfrom, 2)
     t0 = time.perf_counter()
-    events[0].record()
+    _event(0).record()
     done = iters
     state = {"x": x, "v": v, "u": u}
 
@@ -401,9 +416,40 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
                    L.ptr(gt), B, n, float(config.rho), L.ptr(stats[k - 1]), L.ptr(fk))
         state["v"] = v
         if record:
-            events[k].record()
+            _event(k).record()
+
+    # Native loop: once the denoiser is a frozen guide (from its first frozen
+    # iteration on) and nothing needs the host between iterations, the
+    # remaining iterations run in C++ (pnp_admm_run): the same two fused calls
+    # per iteration with the same arguments -> bitwise-identical iterates, no
+    # interpreter cost per iteration.
+    native_spec = problem.native_grad if native else None
+    if sync_each or k_cap <= iters or frozen_for is None or fused_grad is None:
+        native_spec = None
+    native_times = None
+
+    def run_native(k, fzk):
+        nk = native_spec
+        v_cur = state["v"]
+        v_other = torch.empty_like(x)
+        ms = (C.c_float * (iters - k + 1))()
+        vlast = C.c_int(0)
+        L.call("pnp_admm_run", ctx, nk[0], L.ptr(nk[1]), L.ptr(nk[2]), B, H, W, nk[3], nk[4],
+               nk[5], nk[6], float(nk[7]), float(nk[8]), fzk._h, k, iters, L.ptr(state["x"]),
+               L.ptr(v_cur), L.ptr(v_other), L.ptr(state["u"]), L.ptr(z), L.ptr(gt), mu,
+               float(config.alpha), float(config.rho), lo, hi, L.ptr(stats),
+               L.ptr(objv) if track_obj else None, L.ptr(flags), ms, C.byref(vlast))
+        state["v"] = v_other if vlast.value else v_cur
+        return list(ms)
 
     for k in range(1, iters + 1):
+        if native_spec is not None:
+            fzk = frozen_for(k)
+            if fzk is not None and getattr(fzk, "_dev", dev) == dev:
+                native_times = (k, run_native(k, fzk))
+                for kk in range(k, iters + 1):
+                    events[kk] = None
+                break
         if k == k_cap:  # capture the remaining iterations once, replay once
             # raw capture on a side stream (torch.cuda.graph would also run
             # gc.collect + empty_cache on every call)
@@ -420,7 +466,7 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
                     g.capture_end()
             cur.wait_stream(side)
             g.replay()
-            events[iters].record()
+            _event(iters).record()
             for kk in range(k, iters):
                 events[kk] = None
             break
@@ -443,36 +489,45 @@ def linearized_pnp_admm(problem: Problem, config: SolverConfig, denoiser=None, c
     x, v, u = state["x"], state["v"], state["u"]
     if track_obj:  # objective at the final iterate
         grad_fn(x, grad, objv[done - 1])
-    torch.cuda.synchronize(dev)
-    fl = flags[:done].cpu().numpy()
+    # one device->host read for flags, stats and objectives (it also waits
+    # for the loop, so the timing events below are complete)
+    packed = torch.cat([flags[:done].to(torch.float64), stats[:done].reshape(-1),
+                        objv[:done].reshape(-1)]).cpu().numpy()
+    fl = packed[:done]
     bad = np.nonzero(fl)[0]
     if bad.size:
         raise DivergenceError(f"non-finite iterate at iteration {int(bad[0]) + 1}")
-    st = stats[:done].cpu().numpy()
-    ob = objv[:done].cpu().numpy()
+    st = packed[done:done + done * B * 4].reshape(done, B, 4)
+    ob = packed[done + done * B * 4:].reshape(done, B)
     wall = (time.perf_counter() - t0) * 1e3
     times = [events[0].elapsed_time(events[k]) if events[k] is not None else math.nan
              for k in range(1, done + 1)]
+    if native_times is not None:  # C++ loop: its own per-iteration events
+        k_n, ms = native_times
+        base = events[0].elapsed_time(events[k_n - 1]) if k_n > 1 else 0.0
+        for i, t in enumerate(ms):
+            times[k_n - 1 + i] = base + float(t)
     if k_cap <= done:  # captured iterations: spread the replay time evenly
         t_a = times[k_cap - 2] if k_cap >= 2 else 0.0
         t_b = times[done - 1]
         for i in range(k_cap - 1, done):
             times[i] = t_a + (t_b - t_a) * (i - k_cap + 2) / (done - k_cap + 1)
-    records = []
-    for i in range(done):
-        primal = st[i, :, 0] / n
-        dual = st[i, :, 1] / n
-        if gt is not None:
-            mse = st[i, :, 2] / n
-            q = np.where(mse == 0.0, math.inf, 10.0 * np.log10(1.0 / np.where(mse == 0, 1, mse)))
-        else:
-            q = np.full(B, math.nan)
-        obj = ob[i] if track_obj else np.full(B, math.nan)
-        if B == 1 and x.dim() == 2:
-            records.append(IterationRecord(i + 1, float(primal[0]), float(dual[0]), float(q[0]),
-                                           float(times[i]), float(obj[0])))
-        else:
-            records.append(IterationRecord(i + 1, primal, dual, q, float(times[i]), obj))
+    # per-iteration log, vectorized over the iterations (host cost ~ constant)
+    prim = st[:done, :, 0] / n
+    dual = st[:done, :, 1] / n
+    if gt is not None:
+        mse = st[:done, :, 2] / n
+        q = np.where(mse == 0.0, math.inf, 10.0 * np.log10(1.0 / np.where(mse == 0, 1, mse)))
+    else:
+        q = np.full((done, B), math.nan)
+    objs = ob[:done] if track_obj else np.full((done, B), math.nan)
+    if B == 1 and x.dim() == 2:
+        records = [IterationRecord(i + 1, p_, d_, q_, float(t_), o_) for i, (p_, d_, q_, t_, o_)
+                   in enumerate(zip(prim[:, 0].tolist(), dual[:, 0].tolist(), q[:, 0].tolist(),
+                                    times, objs[:, 0].tolist()))]
+    else:
+        records = [IterationRecord(i + 1, prim[i], dual[i], q[i], float(times[i]), objs[i])
+                   for i in range(done)]
     del wall
     return A.from_device(v, kind), records
 
@@ -618,7 +673,8 @@ def make_sr_problem(op: SuperResOp, observed, ground_truth=None) -> Problem:
                    ground_truth=ground_truth, gram=gram,
                    atb=A.from_device(op.adjoint_device(y), kind),
                    device_gradient=device_gradient, device_grad_xupdate=device_grad_xupdate,
-                   device_cg=device_cg, device_atb=op.adjoint_device(y))
+                   device_cg=device_cg, device_atb=op.adjoint_device(y),
+                   native_grad=(0, y, None, op._taps, op.radius, op.factor, op._bnd, 0.0, 0.0))
 
 
 def make_qis_problem(counts: QisCounts, model: QisModel, ground_truth=None,
@@ -645,7 +701,9 @@ def make_qis_problem(counts: QisCounts, model: QisModel, ground_truth=None,
 
     return Problem(shape=counts.shape, gradient=gradient, x0=qis_initial_estimate(counts, floor),
                    objective=objective, ground_truth=ground_truth,
-                   device_gradient=device_gradient, device_grad_xupdate=device_grad_xupdate)
+                   device_gradient=device_gradient, device_grad_xupdate=device_grad_xupdate,
+                   native_grad=(1, ones, zeros, None, 0, 0, 0,
+                                model.gain / model.oversampling, float(floor)))
 
 
 def default_sr_alpha(op: SuperResOp, hr_shape, iters: int = 200, seed: int = 0) -> float:

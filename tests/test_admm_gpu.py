@@ -261,3 +261,50 @@ def test_fused_admm_steps_match_unfused(pnp, golden_admm):
     fz.apply_admm(z1, v2, u2, x1, v0, gt, rho, s2, f2)
     assert torch.equal(v1, v2) and torch.equal(u1, u2) and int(f1) == int(f2) == 0
     assert torch.allclose(s1[:, :3], s2[:, :3], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("case", ["sr-frozen", "sr-dsg-fixed", "sr-batch", "qis-dsg-fixed"])
+def test_native_loop_is_bitwise_python_loop(pnp, golden_admm, case):
+    """The C++ iteration loop (pnp_admm_run) == the Python loop, bit for bit:
+    same fused calls with the same per-iteration arguments."""
+    import torch
+    a = golden_admm
+    kw = dict(rho=1.0, lam=0.01, alpha=1.0, max_iters=11, constraint=pnp.UNIT_BOX,
+              patch_side=5, window_radius=4, bandwidth=0.1, patch_sigma=1.5)
+    den = None
+    if case.startswith("qis"):
+        ones = np.asarray(a["qis_ones"])
+        counts = pnp.QisCounts(ones, 128 - ones)
+        model = pnp.QisModel(128, 64.0)
+        prob = pnp.make_qis_problem(counts, model, ground_truth=a["qis_truth"])
+        kw.update(alpha=pnp.default_qis_alpha(counts, model), denoiser="dsg-fixed", freeze_at=4)
+    else:
+        op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+        y = torch.from_numpy(np.asarray(a["sr_y"], dtype=np.float32)).cuda()
+        gt = torch.from_numpy(np.asarray(a["sr_truth"], dtype=np.float32)).cuda()
+        if case == "sr-batch":
+            y = torch.stack([y, y.flip(0)])
+            gt = torch.stack([gt, gt.flip(0)])
+        prob = pnp.make_sr_problem(op, y, ground_truth=gt)
+        if case == "sr-dsg-fixed":
+            kw.update(denoiser="dsg-fixed", freeze_at=3)
+        else:
+            guide = torch.from_numpy(np.asarray(a["sr_gauss_guide"], dtype=np.float32)).cuda()
+            if case == "sr-batch":
+                guide = torch.stack([guide, guide.flip(0)])
+            den = pnp.freeze_guide(guide, pnp.PatchParams(5, 4, 0.1, 1.5)).as_denoiser()
+    cfg = pnp.SolverConfig(**kw)
+    vp, rp = pnp.linearized_pnp_admm(prob, cfg, denoiser=den, native=False)
+    vn, rn = pnp.linearized_pnp_admm(prob, cfg, denoiser=den, native=True)
+    if isinstance(vp, torch.Tensor):
+        assert torch.equal(vp, vn)
+    else:
+        assert np.array_equal(vp, vn)
+    assert len(rp) == len(rn) == 11
+    last = 0.0
+    for r1, r2 in zip(rp, rn):
+        for f in ("primal", "dual", "psnr", "objective"):
+            assert np.array_equal(np.asarray(getattr(r1, f)), np.asarray(getattr(r2, f)),
+                                  equal_nan=True), f
+        assert math.isfinite(r2.time_ms) and r2.time_ms >= last
+        last = r2.time_ms
