@@ -62,6 +62,10 @@ def test_known_answers(pnp):
     ((40, 45), 21, 3, None, 0.2),        # R larger than the tile height
     ((50, 50), 2, 13, 3.0, 0.2),
     ((24, 30), 3, 15, None, 0.3),
+    ((90, 150), 16, 5, 1.5, 0.2),        # R bucket 16
+    ((60, 70), 12, 9, None, 0.2),
+    ((80, 100), 32, 1, None, 0.2),       # largest R, P = 1
+    ((70, 75), 30, 3, 1.0, 0.25),
 ])
 def test_random_vs_oracle(pnp, rng, shape, R, P, sigma, bw):
     img = rng.random(shape)
