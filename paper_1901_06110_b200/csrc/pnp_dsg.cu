@@ -20,6 +20,7 @@
 #include "dsg_sweep.cuh"
 #include "sweep_launch.cuh"
 #include "pnp_internal.h"
+#include "pnp_reduce.cuh"
 
 namespace pnp {
 
@@ -77,6 +78,9 @@ struct FixIO {
   double rho;
   double* part3;       // [B][gridDim.y * gridDim.x][3]
   int* flags;
+  // when set, the last CTA reduces part3 into stats_out[b][0..2] (stride 4)
+  double* stats_out;
+  unsigned* counter;   // zero between launches (the last CTA resets it)
 };
 
 // u-update of one pixel (same arithmetic as admm_uupdate_kernel)
@@ -142,6 +146,16 @@ __device__ __forceinline__ void admm_u_block(const FixIO& io, int b, int f, doub
     pp[1] = a1;
     pp[2] = a2;
   }
+}
+
+// The per-image sums of FIX_APPLY_U's partials, folded into the fixup: the
+// last CTA to finish reduces them (same arithmetic as reduce_partials_kernel).
+__device__ __forceinline__ void admm_stats_last(const FixIO& io) {
+  if (!io.stats_out || !cta_is_last(io.counter)) return;
+  __shared__ double red[3][8];
+  const int nblk = gridDim.x * gridDim.y;
+  for (int b = 0; b < (int)gridDim.z; ++b)
+    cta_reduce_partials3(io.part3, nblk, b, 1.0, io.stats_out, 4, red);
 }
 
 __device__ __forceinline__ float dsg_finish(float kx, float d, float inv_m, float x) {
@@ -290,7 +304,7 @@ __global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, co
       io.out[o] = __fdiv_rn(s0, s[C - 1]);
     }
   }
-  if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2);
+  if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2), admm_stats_last(io);
   if (MODE == FIX_KXD || MODE == FIX_D) {
     // d > 0, so the int ordering of the bits is the float ordering; max is
     // exact and order-free -> deterministic.
@@ -416,7 +430,7 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
       io.out[o] = __fdiv_rn(s0, s[C - 1][k]);
     }
   }
-  if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2);
+  if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2), admm_stats_last(io);
   if (MODE == FIX_KXD || MODE == FIX_D) {
     // d > 0, so the int ordering of the bits is the float ordering; max is
     // exact and order-free -> deterministic.
@@ -594,6 +608,16 @@ static size_t block_floats(const Geom& g, int C) {
 
 static size_t partial_floats(const Geom& g, int ntr, int C) {
   return (size_t)g.B * ntr * g.NP * g.tiles_x * block_floats(g, C);
+}
+
+// Device counter of the last-CTA reductions: allocated and zeroed once; every
+// kernel that uses it leaves it at zero.
+static int ensure_counter(pnp_ctx* ctx) {
+  if (ctx->counter.bytes) return PNP_OK;
+  int rc = ctx->counter.ensure(sizeof(unsigned));
+  if (rc) return rc;
+  PNP_CUDA(cudaMemsetAsync(ctx->counter.ptr, 0, sizeof(unsigned), ctx->stream));
+  return PNP_OK;
 }
 
 // Fixup variant: one thread per pixel when there are many partial groups or
@@ -805,6 +829,7 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   ctx->flags.release();
   ctx->kcache.release();
   ctx->cg.release();
+  ctx->counter.release();
   for (auto& sl : ctx->slots) {
     cudaEventDestroy(sl.a);
     cudaEventDestroy(sl.b);
@@ -1033,8 +1058,10 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
   io.rho = rho;
   io.part3 = ctx->stats.as<double>();
   io.flags = flags;
-  if ((rc = run_fixup<FIX_APPLY_U>(ctx, g, w, 1, part, io))) return rc;
-  return reduce_stats3(ctx, io.part3, (int)nblk, g.B, stats);
+  if ((rc = ensure_counter(ctx))) return rc;
+  io.stats_out = stats;
+  io.counter = ctx->counter.as<unsigned>();
+  return run_fixup<FIX_APPLY_U>(ctx, g, w, 1, part, io);
 }
 
 int pnp_frozen_destroy(pnp_frozen* fz) {

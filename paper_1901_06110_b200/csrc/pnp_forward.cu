@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "pnp_internal.h"
+#include "pnp_reduce.cuh"
 
 namespace pnp {
 
@@ -56,18 +57,24 @@ __device__ __forceinline__ void block_sum_store(double v, double* partial) {
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const double* partial, int nblk,
                                                               int nvec, double scale, double* out,
                                                               int stride) {
-  const int b = blockIdx.x, k = blockIdx.y;
-  double s = 0.0;
-  for (int j = threadIdx.x; j < nblk; j += blockDim.x) s += partial[((size_t)b * nblk + j) * nvec + k];
   __shared__ double red[8];
-  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    out[(size_t)b * stride + k] = scale * t;
-  }
+  cta_reduce_partials(partial, nblk, nvec, blockIdx.x, blockIdx.y, scale, out, stride, red);
+}
+
+// A reduce_partials_kernel launch folded into the next kernel: its CTA
+// (0, 0, 0) reduces partials the previous kernel wrote (out[b] = scale *
+// sum_j partial[b][j], b < batch) -- same arithmetic, one launch fewer.
+struct RedEpi {
+  const double* part;
+  double* out;
+  double scale;
+  int nblk, batch;
+};
+
+__device__ __forceinline__ void red_epilogue(const RedEpi& e) {
+  if (!e.out || blockIdx.x || blockIdx.y || blockIdx.z) return;
+  __shared__ double red[8];
+  for (int b = 0; b < e.batch; ++b) cta_reduce_partials(e.part, e.nblk, 1, b, 0, e.scale, e.out, 1, red);
 }
 
 // The linearized-ADMM x-update (solver.py:219-221) fused into a gradient
@@ -195,7 +202,8 @@ enum AdjMode { ADJ_PLAIN = 0, ADJ_XUPD = 1, ADJ_CG = 2 };
 template <int MODE>
 __global__ void __launch_bounds__(256)
 sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const SrWin win, int W,
-                  int k, int rad, int sym, const Taps taps, const XUpd q, const CgEpi cg) {
+                  int k, int rad, int sym, const Taps taps, const XUpd q, const CgEpi cg,
+                  const RedEpi red = RedEpi{}) {
   extern __shared__ float sm[];
   const int H = win.Hg, w = W / k, b = blockIdx.z;
   if (MODE == ADJ_CG && cg.skip && cg.skip[b].done) return;
@@ -245,16 +253,17 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
   }
   if (XU) flags_or(q.flags, f);
   if (MODE == ADJ_CG) {
-    __shared__ double red[8];
+    __shared__ double red8[8];
     for (int off = 16; off; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+    if ((threadIdx.x & 31) == 0) red8[threadIdx.x >> 5] = dot;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w8 = 0; w8 < (int)(blockDim.x >> 5); ++w8) t += red[w8];
+      for (int w8 = 0; w8 < (int)(blockDim.x >> 5); ++w8) t += red8[w8];
       cg.partial[((size_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
     }
   }
+  if (MODE != ADJ_CG) red_epilogue(red);  // data term of the residual kernel
 }
 
 static size_t sr_res_smem(int k, int rad) {
@@ -717,21 +726,16 @@ static int sr_grad_impl(pnp_ctx* ctx, const float* x, const float* yobs, float* 
                                                      radius, boundary, t, part);
   }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
-  if (data_out) {
-    {
-      ProfScope prof_(ctx, PROF_ADMM);
-      reduce_partials_kernel<<<dim3(batch, 1), 256, 0, ctx->stream>>>(part, nblk, 1, 0.5, data_out, 1);
-    }
-    PNP_LAUNCH_CHECK("reduce_partials_kernel");
-  }
+  // the data term 0.5 ||r||^2 is reduced by the adjoint kernel's first CTA
+  const RedEpi red{part, data_out, 0.5, nblk, batch};
   {
     ProfScope prof_(ctx, PROF_FORWARD);
     if (xu)
       sr_adjoint_kernel<ADJ_XUPD><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, nullptr, adj_full(H, factor), W, factor, radius, boundary, t, *xu, CgEpi{});
+          r, nullptr, adj_full(H, factor), W, factor, radius, boundary, t, *xu, CgEpi{}, red);
     else
       sr_adjoint_kernel<ADJ_PLAIN><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, grad, adj_full(H, factor), W, factor, radius, boundary, t, XUpd{}, CgEpi{});
+          r, grad, adj_full(H, factor), W, factor, radius, boundary, t, XUpd{}, CgEpi{}, red);
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;

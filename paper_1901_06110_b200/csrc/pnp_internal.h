@@ -63,6 +63,7 @@ struct pnp_ctx {
   pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
   pnp::DevBuf kcache;              // pair weights of the last adaptive denoise
   pnp::DevBuf cg;                  // conjugate-gradients work vectors + state
+  pnp::DevBuf counter;             // last-CTA reduction counter (kept at zero)
   size_t cache_limit = (size_t)-1;  // bytes; 0 disables the k cache
   // offset tables keyed by (R, NG): host blobs of Chunk (hat, no-hat) + NG+1
   // group starts; they reach the kernels through the launch parameters
