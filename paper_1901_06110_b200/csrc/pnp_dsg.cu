@@ -13,6 +13,7 @@
 #include <float.h>
 #include <math.h>
 
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -521,13 +522,25 @@ static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
 }
 
 static int pick_groups(int ntiles, int nchunks) {
-  // Offset-group split so small images still fill 148 SMs (~8 CTAs each).
-  // Above PNP_CLUSTER groups the count is a multiple of it: the groups of one
-  // tile run as thread-block clusters (cluster_size).
-  const int target = 148 * 8, cm = PNP_CLUSTER;
-  int ng = (target + ntiles - 1) / ntiles;
+  // Offset groups per tile -- a function of the image geometry only, so every
+  // path (adaptive, frozen, batched, sharded) sums in the same order.  Fitted
+  // to B200 measurements of the frozen apply at R = 10 (k-cache sweep with
+  // 4 CTAs/SM = 592 slots, then the fixup; profiles/sweep_history.md): about
+  // 480 CTAs in all (one memory-bound wave; more groups cost more in the
+  // per-pixel fixup than they gain), at most 7 groups, and 2 instead of 1
+  // when one group per tile would spill a small tail wave.
+  int ng = 480 / (ntiles > 0 ? ntiles : 1);
+  if (ng > 7) ng = 7;
+  if (ng < 1) ng = 1;
+  if (ng == 1) {
+    const double w = ntiles / (148.0 * 4);
+    if (w > 1.0 && w < 4.0 && w - std::floor(w) < 0.35) ng = 2;
+  }
   if (ng > nchunks) ng = nchunks;
-  if (ng > kMaxGroups) ng = kMaxGroups;
+#ifdef PNP_NG_OVERRIDE
+  ng = PNP_NG_OVERRIDE;
+#endif
+  const int cm = PNP_CLUSTER;  // clusters (off by default) need a multiple of cm
   if (ng > cm) {
     const int up = (ng + cm - 1) / cm * cm;
     ng = up <= nchunks ? up : nchunks / cm * cm;
