@@ -623,6 +623,25 @@ static size_t partial_floats(const Geom& g, int ntr, int C) {
   return (size_t)g.B * ntr * g.NP * g.tiles_x * block_floats(g, C);
 }
 
+// Stream-ordered allocation from the device's default memory pool, which is
+// told once to keep freed memory (release threshold = max) so that frozen
+// guides created and destroyed by successive ADMM runs reuse it without
+// cudaMalloc / cudaFree (both can stall the host for milliseconds and the
+// latter synchronizes the device).
+static cudaError_t pool_alloc(pnp_ctx* ctx, void** p, size_t bytes) {
+  static bool configured[64] = {};
+  const int dev = ctx->device;
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    configured[dev] = true;
+  }
+  return cudaMallocAsync(p, bytes, ctx->stream);
+}
+
 // Device counter of the last-CTA reductions: allocated and zeroed once; every
 // kernel that uses it leaves it at zero.
 static int ensure_counter(pnp_ctx* ctx) {
@@ -970,10 +989,11 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   fz->P = P;
   fz->bw = bandwidth;
   for (int i = 0; i < P; ++i) fz->taps[i] = taps[i];
-  cudaError_t e = cudaMalloc(&fz->guide, n * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&fz->rs, n * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&fz->d, n * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&fz->mv, 2 * batch * sizeof(float));
+  fz->stream = ctx->stream;
+  cudaError_t e = pool_alloc(ctx, (void**)&fz->guide, n * sizeof(float));
+  if (e == cudaSuccess) e = pool_alloc(ctx, (void**)&fz->rs, n * sizeof(float));
+  if (e == cudaSuccess) e = pool_alloc(ctx, (void**)&fz->d, n * sizeof(float));
+  if (e == cudaSuccess) e = pool_alloc(ctx, (void**)&fz->mv, 2 * batch * sizeof(float));
   if (e != cudaSuccess) {
     pnp_frozen_destroy(fz);
     return cuda_fail(e, "cudaMalloc(frozen)");
@@ -987,7 +1007,7 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return bail(rc);
   const size_t kcf = kcache_floats(g, g.tiles_y);
   if (kcache_fits(ctx, kcf, 0)) {
-    e = cudaMalloc(&fz->kcache, kcf * sizeof(float));
+    e = pool_alloc(ctx, (void**)&fz->kcache, kcf * sizeof(float));
     if (e != cudaSuccess) {
       cudaGetLastError();
       fz->kcache = nullptr;  // not fatal: recompute instead
@@ -1016,6 +1036,7 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
 }
 
 int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out) {
+  if (fz && ctx) fz->stream = ctx->stream;
   if (!ctx || !fz || !x || !out) return fail(PNP_EINVAL, "null argument");
   if (fz->device != ctx->device) return fail(PNP_EINVAL, "handle belongs to another device");
   PNP_CUDA(cudaSetDevice(ctx->device));
@@ -1041,6 +1062,7 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
 int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v,
                        float* u, const float* x, const float* v_prev, const float* gt,
                        double rho, double* stats, int* flags) {
+  if (fz && ctx) fz->stream = ctx->stream;
   if (!ctx || !fz || !z || !v || !u || !x || !stats || !flags)
     return fail(PNP_EINVAL, "null argument");
   if (fz->device != ctx->device) return fail(PNP_EINVAL, "handle belongs to another device");
@@ -1080,11 +1102,12 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
 int pnp_frozen_destroy(pnp_frozen* fz) {
   if (!fz) return PNP_OK;
   cudaSetDevice(fz->device);
-  if (fz->guide) cudaFree(fz->guide);
-  if (fz->rs) cudaFree(fz->rs);
-  if (fz->d) cudaFree(fz->d);
-  if (fz->mv) cudaFree(fz->mv);
-  if (fz->kcache) cudaFree(fz->kcache);
+  for (void* p : {(void*)fz->guide, (void*)fz->rs, (void*)fz->d, (void*)fz->mv,
+                  (void*)fz->kcache})
+    if (p && cudaFreeAsync(p, fz->stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(p);  // stream gone: synchronous free
+    }
   delete fz;
   return PNP_OK;
 }
@@ -1098,6 +1121,7 @@ int pnp_frozen_alpha(const pnp_frozen* fz, float* alpha_host) {
 
 int pnp_frozen_export(pnp_ctx* ctx, const pnp_frozen* fz, float* guide_out, float* d_out) {
   if (!ctx || !fz) return fail(PNP_EINVAL, "null argument");
+  fz->stream = ctx->stream;
   const size_t n = (size_t)fz->B * fz->H * fz->W * sizeof(float);
   PNP_CUDA(cudaSetDevice(ctx->device));
   if (guide_out)

@@ -118,4 +118,8 @@ struct pnp_frozen {
   float* d = nullptr;      // B*H*W
   float* mv = nullptr;     // B floats: m; then B floats: 1/m
   float* kcache = nullptr; // pair weights (null: recompute on apply)
+  // buffers come from the device's stream-ordered pool (cudaMallocAsync) and
+  // go back to it on the stream of the handle's last use: no device-wide
+  // synchronization and no page-mapping cost when ADMM runs re-freeze
+  mutable cudaStream_t stream = 0;
 };
