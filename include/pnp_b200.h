@@ -189,6 +189,27 @@ int pnp_qis_grad_xupdate(pnp_ctx* ctx, float* x, const float* ones, const float*
 int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v, float* u,
                        const float* x, const float* v_prev, const float* gt, double rho,
                        double* stats, int* flags);
+/* ---- float64 distance-engine helpers (reference image.py:97-143,
+ * denoise.py:70-88, 106-174).  Off the fp32 sweep path; computed on the
+ * device in float64.  All pointers are device pointers. ----
+ * pad_symmetric: out ((H+2m) x (W+2m)) = half-sample mirror pad of img,
+ *   0 <= margin <= min(H, W) (image.py:97-113).
+ * integral_image: out ((H+1) x (W+1)) = summed-area table with a zero leading
+ *   row / column, sequential cumsums like numpy's (image.py:116-126; bitwise).
+ * patch_distance_map: out (H x W) = sum over the P x P patch of
+ *   (G(s+ab) - G(s+t+ab))^2, t = (dy, dx), |t| <= R, reflected guide with
+ *   margin R + (P-1)/2 <= min(H, W); the shifted-add order of the reference's
+ *   method="direct" (denoise.py:131-142; bitwise).
+ * patch_ssd_pairs: out[i] = patch SSD between pixels (pairs[4i], pairs[4i+1])
+ *   and (pairs[4i+2], pairs[4i+3]) (nlm_kernel, denoise.py:70-88); pairs is
+ *   a device int array. */
+int pnp_pad_symmetric_f64(pnp_ctx* ctx, const double* img, int H, int W, int margin, double* out);
+int pnp_integral_image_f64(pnp_ctx* ctx, const double* img, int H, int W, double* out);
+int pnp_patch_distance_map_f64(pnp_ctx* ctx, const double* guide, int H, int W, int P, int R,
+                               int dy, int dx, double* out);
+int pnp_patch_ssd_pairs_f64(pnp_ctx* ctx, const double* guide, int H, int W, int P,
+                            const int* pairs, int n, double* out);
+
 /* Native iteration loop of linearized_pnp_admm with a frozen guide
  * (reference solver.py:199-235): iterations k0..k1 (1-based) of
  *   x <- proj(mu (alpha x + rho (v - u) - grad f(x))), z = x + u   (fused)

@@ -14,6 +14,8 @@ from .denoise import (  # noqa: F401
     freeze_guide,
     hat_weight,
     nlm_denoise,
+    nlm_kernel,
+    patch_distance_map,
 )
 from .forward import (  # noqa: F401
     QIS_FLOOR,
@@ -47,6 +49,9 @@ from .image import (  # noqa: F401
     Box,
     NonNegative,
     Unconstrained,
+    box_sum,
+    integral_image,
+    pad_symmetric,
     project,
     psnr,
     validate_image,
@@ -71,5 +76,6 @@ from .solver import (  # noqa: F401
 )
 from .stream import DenoiseStream, denoise_host_sequence  # noqa: F401
 from .synth import SplitMix64  # noqa: F401
+
 
 __version__ = "0.1.0"

@@ -70,6 +70,21 @@ def to_device(a, dev: int | None = None) -> torch.Tensor:
     return torch.from_numpy(arr).to(torch.device("cuda", dev), non_blocking=False)
 
 
+def to_device64(a, dev: int | None = None) -> torch.Tensor:
+    """float64, contiguous, on the CUDA device (the float64 helper kernels)."""
+    if dev is None:
+        dev = device_index()
+    if isinstance(a, torch.Tensor):
+        return a.detach().to(device=torch.device("cuda", dev), dtype=torch.float64).contiguous()
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return torch.from_numpy(arr).to(torch.device("cuda", dev))
+
+
+def from_device64(t: torch.Tensor, kind: str):
+    """float64 device result -> float64 numpy (drop-in) or the tensor."""
+    return t if kind == TORCH else t.cpu().numpy()
+
+
 def from_device(t: torch.Tensor, kind: str):
     if kind == TORCH:
         return t

@@ -87,6 +87,10 @@ _SIGS = {
     "pnp_check_finite": (i32, [vp, vp, i64, C.POINTER(i32)]),
     "pnp_flag_nonfinite": (i32, [vp, vp, i64, vp]),
     "pnp_splitmix_uniforms": (i32, [vp, C.c_uint64, i64, vp]),
+    "pnp_pad_symmetric_f64": (i32, [vp, vp, i32, i32, i32, vp]),
+    "pnp_integral_image_f64": (i32, [vp, vp, i32, i32, vp]),
+    "pnp_patch_distance_map_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp]),
+    "pnp_patch_ssd_pairs_f64": (i32, [vp, vp, i32, i32, i32, vp, i32, vp]),
     "pnp_admm_run": (i32, [vp, i32, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64, f64, vp,
                            i32, i32, vp, vp, vp, vp, vp, vp, f64, f64, f64, f64, f64, vp, vp, vp,
                            C.POINTER(C.c_float), C.POINTER(i32)]),

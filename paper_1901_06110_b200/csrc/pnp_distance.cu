@@ -1,0 +1,174 @@
+// Float64 patch-distance primitives on the device: the public helpers of the
+// reference's distance engine (pnprestore/image.py:97-143 pad_symmetric /
+// integral_image, denoise.py:70-88 nlm_kernel, 106-174 _DistanceEngine /
+// patch_distance_map).  They are not on the fp32 sweep path (the sweep kernel
+// reflects indices at load and never materializes padded guides, SATs or
+// per-offset maps); they exist so callers of those reference functions keep
+// working, computed on the GPU in the reference's precision and, where the
+// reference's order is sequential, in its exact summation order:
+//   * pad_symmetric: a copy (exact);
+//   * integral_image: column cumsums then row cumsums, each sequential like
+//     numpy's cumsum -> bitwise equal;
+//   * patch distances: the "direct" shifted-add order (py outer, px inner) of
+//     _DistanceEngine.map, explicit _rn intrinsics so nothing is contracted
+//     into FMAs -> bitwise equal to method="direct".
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pnp_internal.h"
+
+namespace pnp {
+namespace {
+
+// half-sample symmetric index (np.pad mode="symmetric", single reflection)
+__device__ __forceinline__ int reflect1(int i, int n) {
+  if (i < 0) i = -i - 1;
+  if (i >= n) i = 2 * n - 1 - i;
+  return i;
+}
+
+__global__ void pad_symmetric_kernel(const double* __restrict__ img, int H, int W, int M,
+                                     double* __restrict__ out) {
+  const int Wo = W + 2 * M, Ho = H + 2 * M;
+  const size_t n = (size_t)Ho * Wo;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / Wo), x = (int)(i % Wo);
+    out[i] = img[(size_t)reflect1(y - M, H) * W + reflect1(x - M, W)];
+  }
+}
+
+// out is (H+1) x (W+1) with a zero leading row / column.  Pass 1: thread per
+// column, running sum down the rows (numpy cumsum axis 0); pass 2: thread per
+// row, running sum along the columns (axis 1) in place.
+__global__ void integral_cols_kernel(const double* __restrict__ img, int H, int W,
+                                     double* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int Wo = W + 1;
+  if (x > W) return;
+  out[x] = 0.0;
+  if (x == 0) {
+    for (int y = 1; y <= H; ++y) out[(size_t)y * Wo] = 0.0;
+    return;
+  }
+  double s = 0.0;
+  for (int y = 0; y < H; ++y) {
+    s = __dadd_rn(s, img[(size_t)y * W + (x - 1)]);
+    out[(size_t)(y + 1) * Wo + x] = s;
+  }
+}
+
+__global__ void integral_rows_kernel(int H, int W, double* __restrict__ out) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (y > H) return;
+  double* row = out + (size_t)y * (W + 1);
+  double s = 0.0;
+  for (int x = 1; x <= W; ++x) {
+    s = __dadd_rn(s, row[x]);
+    row[x] = s;
+  }
+}
+
+// SSD between the P x P patches at s and s + t (reflected guide), in the
+// shifted-add order of _DistanceEngine.map(method="direct")
+__device__ __forceinline__ double patch_ssd(const double* __restrict__ g, int H, int W, int P,
+                                            int sy, int sx, int dy, int dx) {
+  const int h = (P - 1) / 2;
+  double acc = 0.0;
+  for (int py = 0; py < P; ++py) {
+    const int ya = reflect1(sy + py - h, H), yb = reflect1(sy + py - h + dy, H);
+    for (int px = 0; px < P; ++px) {
+      const double d = __dsub_rn(g[(size_t)ya * W + reflect1(sx + px - h, W)],
+                                 g[(size_t)yb * W + reflect1(sx + px - h + dx, W)]);
+      acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+  }
+  return acc;
+}
+
+__global__ void patch_distance_kernel(const double* __restrict__ g, int H, int W, int P, int dy,
+                                      int dx, double* __restrict__ out) {
+  const size_t n = (size_t)H * W;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    out[i] = patch_ssd(g, H, W, P, (int)(i / W), (int)(i % W), dy, dx);
+}
+
+__global__ void patch_ssd_pairs_kernel(const double* __restrict__ g, int H, int W, int P,
+                                       const int* __restrict__ pairs, int n,
+                                       double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int sy = pairs[4 * i], sx = pairs[4 * i + 1], ry = pairs[4 * i + 2], rx = pairs[4 * i + 3];
+  out[i] = patch_ssd(g, H, W, P, sy, sx, ry - sy, rx - sx);
+}
+
+int grid_for(size_t n, int sms) {
+  const size_t b = (n + 255) / 256;
+  const size_t cap = (size_t)sms * 16;
+  return (int)(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+}  // namespace
+}  // namespace pnp
+
+using namespace pnp;
+
+extern "C" {
+
+int pnp_pad_symmetric_f64(pnp_ctx* ctx, const double* img, int H, int W, int margin, double* out) {
+  if (!ctx || !img || !out) return fail(PNP_EINVAL, "null argument");
+  if (H < 1 || W < 1) return fail(PNP_EINVAL, "image must be at least 1x1");
+  if (margin < 0) return fail(PNP_EINVAL, "margin must be >= 0, got " + std::to_string(margin));
+  if (margin > (H < W ? H : W))
+    return fail(PNP_EINVAL, "margin " + std::to_string(margin) + " exceeds min image extent " +
+                                std::to_string(H < W ? H : W));
+  const size_t n = (size_t)(H + 2 * margin) * (W + 2 * margin);
+  pad_symmetric_kernel<<<grid_for(n, ctx->sms), 256, 0, ctx->stream>>>(img, H, W, margin, out);
+  PNP_LAUNCH_CHECK("pad_symmetric_kernel");
+  return PNP_OK;
+}
+
+int pnp_integral_image_f64(pnp_ctx* ctx, const double* img, int H, int W, double* out) {
+  if (!ctx || !img || !out) return fail(PNP_EINVAL, "null argument");
+  if (H < 1 || W < 1) return fail(PNP_EINVAL, "image must be at least 1x1");
+  integral_cols_kernel<<<(W + 1 + 127) / 128, 128, 0, ctx->stream>>>(img, H, W, out);
+  PNP_LAUNCH_CHECK("integral_cols_kernel");
+  integral_rows_kernel<<<(H + 127) / 128, 128, 0, ctx->stream>>>(H, W, out);
+  PNP_LAUNCH_CHECK("integral_rows_kernel");
+  return PNP_OK;
+}
+
+int pnp_patch_distance_map_f64(pnp_ctx* ctx, const double* guide, int H, int W, int P, int R,
+                               int dy, int dx, double* out) {
+  if (!ctx || !guide || !out) return fail(PNP_EINVAL, "null argument");
+  if (H < 1 || W < 1) return fail(PNP_EINVAL, "image must be at least 1x1");
+  if (P < 1 || P % 2 == 0) return fail(PNP_EINVAL, "patch_side must be odd and >= 1");
+  if (R < 1) return fail(PNP_EINVAL, "window_radius must be >= 1");
+  if ((dy < 0 ? -dy : dy) > R || (dx < 0 ? -dx : dx) > R)
+    return fail(PNP_EINVAL, "offset outside window radius " + std::to_string(R));
+  const int margin = R + (P - 1) / 2;
+  if (margin > (H < W ? H : W))
+    return fail(PNP_EINVAL, "margin " + std::to_string(margin) + " exceeds min image extent " +
+                                std::to_string(H < W ? H : W));
+  const size_t n = (size_t)H * W;
+  patch_distance_kernel<<<grid_for(n, ctx->sms), 256, 0, ctx->stream>>>(guide, H, W, P, dy, dx,
+                                                                        out);
+  PNP_LAUNCH_CHECK("patch_distance_kernel");
+  return PNP_OK;
+}
+
+int pnp_patch_ssd_pairs_f64(pnp_ctx* ctx, const double* guide, int H, int W, int P,
+                            const int* pairs, int n, double* out) {
+  if (!ctx || !guide || (n > 0 && (!pairs || !out))) return fail(PNP_EINVAL, "null argument");
+  if (H < 1 || W < 1 || n < 0) return fail(PNP_EINVAL, "bad shape");
+  if (P < 1 || P % 2 == 0) return fail(PNP_EINVAL, "patch_side must be odd and >= 1");
+  if ((P - 1) / 2 > (H < W ? H : W))
+    return fail(PNP_EINVAL, "patch half-width exceeds min image extent");
+  if (n == 0) return PNP_OK;
+  patch_ssd_pairs_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(guide, H, W, P, pairs, n, out);
+  PNP_LAUNCH_CHECK("patch_ssd_pairs_kernel");
+  return PNP_OK;
+}
+
+}  // extern "C"

@@ -77,6 +77,49 @@ def hat_weight(s: tuple[int, int], r: tuple[int, int], window_radius: int) -> fl
     return (1.0 - abs(dy) / scale) * (1.0 - abs(dx) / scale)
 
 
+def nlm_kernel(guide, s: tuple[int, int], r: tuple[int, int], params: PatchParams) -> float:
+    """exp(-||P_s - P_r||^2 / (2 P^2 bw^2)) for two pixels, patches from the
+    mirror-padded guide (denoise.py:70-88); the SSD is a float64 device kernel."""
+    guide, _ = A.validate(guide, "guide")
+    h, w = int(guide.shape[0]), int(guide.shape[1])
+    for name, (py, px) in (("s", s), ("r", r)):
+        if not (0 <= py < h and 0 <= px < w):
+            raise ValueError(f"pixel {name}={py, px} outside {h}x{w} image")
+    half = (params.patch_side - 1) // 2
+    if half > min(h, w):
+        raise ValueError(f"margin {half} exceeds min image extent {min(h, w)}")
+    g = A.to_device64(guide)
+    pairs = torch.tensor([s[0], s[1], r[0], r[1]], dtype=torch.int32, device=g.device)
+    out = torch.empty(1, dtype=torch.float64, device=g.device)
+    L.call("pnp_patch_ssd_pairs_f64", L.context(g.device.index), L.ptr(g), h, w,
+           params.patch_side, L.ptr(pairs), 1, L.ptr(out))
+    ssd = float(out.item())
+    side = params.patch_side
+    return float(np.exp(-ssd / (2.0 * side * side * params.bandwidth ** 2)))
+
+
+def patch_distance_map(guide, offset: tuple[int, int], params: PatchParams,
+                       method: str = "integral"):
+    """||P_s - P_{s+t}||^2 for every pixel s and one window offset t
+    (denoise.py:161-174), float64 on the device.  Both methods are computed
+    the reference's "direct" way (exact shifted-add order: bitwise equal to
+    method="direct"; within the reference's own 1e-9 agreement of
+    method="integral", whose summed-area table only reorders the sums)."""
+    if method not in ("integral", "direct"):
+        raise ValueError(f"unknown distance method {method!r}")
+    guide, kind = A.validate(guide, "guide")
+    dy, dx = offset
+    if max(abs(dy), abs(dx)) > params.window_radius:
+        raise ValueError(f"offset {offset} outside window radius {params.window_radius}")
+    h, w = int(guide.shape[0]), int(guide.shape[1])
+    _check_margin(params, h, w)
+    g = A.to_device64(guide)
+    out = torch.empty((h, w), dtype=torch.float64, device=g.device)
+    L.call("pnp_patch_distance_map_f64", L.context(g.device.index), L.ptr(g), h, w,
+           params.patch_side, params.window_radius, int(dy), int(dx), L.ptr(out))
+    return A.from_device64(out, kind)
+
+
 def _pair(image, guide):
     """_check_pair (denoise.py:244-251) -> device tensors + result kind."""
     image, kind = A.validate(image, "image", batch_ok=True)

@@ -1,7 +1,8 @@
 """Image conventions and pixel primitives — drop-in for pnprestore/image.py
-(validate_image 32-41, constraint sets + project 48-90, psnr 146-157).
-Projection and PSNR run on the GPU; PGM / PFM file I/O (image.py:169-280)
-is in imageio.py."""
+(validate_image 32-41, constraint sets + project 48-90, pad_symmetric /
+integral_image / box_sum 97-143, psnr 146-157).  Projection, PSNR, padding
+and summed-area tables run on the GPU (the last two in float64, bitwise equal
+to the reference); PGM / PFM file I/O (image.py:169-280) is in imageio.py."""
 
 from __future__ import annotations
 
@@ -74,10 +75,52 @@ def project(img, constraint):
     return A.from_device(out, kind)
 
 
+def pad_symmetric(img, margin: int):
+    """Half-sample mirror pad (i -> -i-1), margin <= min extent (image.py:97-113)."""
+    img, kind = A.validate(img)
+    if margin < 0:
+        raise ValueError(f"margin must be >= 0, got {margin}")
+    H, W = int(img.shape[0]), int(img.shape[1])
+    if margin > min(H, W):
+        raise ValueError(f"margin {margin} exceeds min image extent {min(H, W)}")
+    g = A.to_device64(img)
+    out = torch.empty((H + 2 * margin, W + 2 * margin), dtype=torch.float64, device=g.device)
+    L.call("pnp_pad_symmetric_f64", L.context(g.device.index), L.ptr(g), H, W, int(margin),
+           L.ptr(out))
+    return A.from_device64(out, kind)
+
+
+def integral_image(img):
+    """Summed-area table with a zero leading row and column: entry (i, j) =
+    sum of img over rows < i, columns < j (image.py:116-126)."""
+    img, kind = A.validate(img)
+    g = A.to_device64(img)
+    H, W = int(g.shape[0]), int(g.shape[1])
+    out = torch.empty((H + 1, W + 1), dtype=torch.float64, device=g.device)
+    L.call("pnp_integral_image_f64", L.context(g.device.index), L.ptr(g), H, W, L.ptr(out))
+    return A.from_device64(out, kind)
+
+
+def box_sum(ii, top: int, left: int, size: int) -> float:
+    """Sum of the size x size box at (top, left) from an integral image: four
+    lookups (image.py:129-140)."""
+    if size < 1:
+        raise ValueError(f"box size must be >= 1, got {size}")
+    height, width = int(ii.shape[0]) - 1, int(ii.shape[1]) - 1
+    if top < 0 or left < 0 or top + size > height or left + size > width:
+        raise ValueError(f"box ({top},{left}) of size {size} outside {height}x{width} extent")
+    b, r = top + size, left + size
+    if isinstance(ii, torch.Tensor):
+        v = ii[[b, top, b, top], [r, r, left, left]].double().cpu().tolist()
+    else:
+        v = [float(ii[b, r]), float(ii[top, r]), float(ii[b, left]), float(ii[top, left])]
+    return float(v[0] - v[1] - v[2] + v[3])
+
+
 def psnr(reference, test, peak: float = 1.0) -> float:
     """Peak signal-to-noise ratio in dB; +inf when the images are identical."""
-    r = A.to_device(A.validate(reference, "reference")[0]).double()
-    t = A.to_device(A.validate(test, "test")[0]).double()
+    r = A.to_device64(A.validate(reference, "reference")[0])
+    t = A.to_device64(A.validate(test, "test")[0])
     if r.shape != t.shape:
         raise ValueError(f"dimension mismatch: {tuple(r.shape)} vs {tuple(t.shape)}")
     if peak <= 0:

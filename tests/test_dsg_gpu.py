@@ -202,3 +202,47 @@ def test_denoise_stream_pipeline(pnp, rng):
     bad[3][10, 20] = float("nan")
     with pytest.raises(ValueError, match="image 3"):
         pnp.DenoiseStream(p, (150, 210)).run(bad)
+
+
+def test_distance_helpers_match_reference_semantics(pnp, rng):
+    """pad_symmetric / integral_image bitwise equal to numpy; patch distances
+    bitwise equal to the reference's method="direct" shifted-add order
+    (restated here), box_sum / nlm_kernel against direct sums
+    (reference tests/test_image.py, tests/test_denoise.py)."""
+    img = rng.random((13, 17))
+    for m in (0, 1, 5, 13):
+        assert np.array_equal(pnp.pad_symmetric(img, m), np.pad(img, m, mode="symmetric"))
+    with pytest.raises(ValueError):
+        pnp.pad_symmetric(img, 14)
+    ii = pnp.integral_image(img)
+    ref = np.zeros((14, 18))
+    np.cumsum(img, axis=0, out=ref[1:, 1:])
+    np.cumsum(ref[1:, 1:], axis=1, out=ref[1:, 1:])
+    assert np.array_equal(ii, ref)
+    assert pnp.box_sum(ii, 2, 3, 4) == pytest.approx(img[2:6, 3:7].sum(), abs=1e-12)
+    with pytest.raises(ValueError):
+        pnp.box_sum(ii, 10, 0, 4)
+    p = pnp.PatchParams(5, 3, 0.2)
+    g = rng.random((20, 23))
+    half, M = 2, 5
+    pad = np.pad(g, M, mode="symmetric")
+    for t in [(0, 0), (1, -2), (-3, 3), (3, 0)]:
+        got = pnp.patch_distance_map(g, t, p, method="direct")
+        a = M - half
+        base = pad[a:a + 24, a:a + 27]
+        d = base - pad[a + t[0]:a + t[0] + 24, a + t[1]:a + t[1] + 27]
+        d *= d
+        want = np.zeros((20, 23))
+        for py in range(5):
+            for px in range(5):
+                want += d[py:py + 20, px:px + 23]
+        assert np.array_equal(got, want)
+        assert np.abs(pnp.patch_distance_map(g, t, p) - want).max() < 1e-9
+    with pytest.raises(ValueError):
+        pnp.patch_distance_map(g, (4, 0), p)
+    assert pnp.nlm_kernel(g, (4, 4), (4, 4), p) == 1.0
+    assert pnp.nlm_kernel(np.full((9, 9), 0.3), (1, 2), (7, 5), p) == 1.0
+    k = pnp.nlm_kernel(g, (2, 3), (10, 15), p)
+    ps, pr = np.pad(g, 2, mode="symmetric")[2:7, 3:8], np.pad(g, 2, mode="symmetric")[10:15, 15:20]
+    assert k == pytest.approx(float(np.exp(-((ps - pr) ** 2).sum() / (2 * 25 * 0.04))), abs=1e-14)
+    assert k == pytest.approx(pnp.nlm_kernel(g, (10, 15), (2, 3), p), abs=1e-14)
