@@ -209,6 +209,13 @@ int pnp_patch_distance_map_f64(pnp_ctx* ctx, const double* guide, int H, int W, 
                                int dy, int dx, double* out);
 int pnp_patch_ssd_pairs_f64(pnp_ctx* ctx, const double* guide, int H, int W, int P,
                             const int* pairs, int n, double* out);
+/* build_dense_weights (denoise.py:389-418): out = the n x n (n = H*W) doubly
+ * stochastic W of the guide in float64 -- hat * exp(-SSD/(2 P^2 bw^2)) on the
+ * clipped window (direct SSD order), scaled by row^-1/2 and col^-1/2, divided
+ * by the max row sum, diagonal completed to row sums of 1.  scratch: 2n+1
+ * doubles.  Test-scale (the caller bounds n). */
+int pnp_dense_weights_f64(pnp_ctx* ctx, const double* guide, int H, int W, int P, int R,
+                          double bandwidth, double* out, double* scratch);
 
 /* Native iteration loop of linearized_pnp_admm with a frozen guide
  * (reference solver.py:199-235): iterations k0..k1 (1-based) of

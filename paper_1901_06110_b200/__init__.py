@@ -8,7 +8,9 @@ package loads the native library; there is no CPU fallback.
 
 from . import _lib  # noqa: F401  (loads libpnpb200.so, fails loudly if missing)
 from .denoise import (  # noqa: F401
+    DENSE_WEIGHTS_MAX_PIXELS,
     FrozenGuide,
+    build_dense_weights,
     PatchParams,
     dsg_nlm_denoise,
     freeze_guide,

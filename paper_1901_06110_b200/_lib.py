@@ -91,6 +91,7 @@ _SIGS = {
     "pnp_integral_image_f64": (i32, [vp, vp, i32, i32, vp]),
     "pnp_patch_distance_map_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp]),
     "pnp_patch_ssd_pairs_f64": (i32, [vp, vp, i32, i32, i32, vp, i32, vp]),
+    "pnp_dense_weights_f64": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp]),
     "pnp_admm_run": (i32, [vp, i32, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64, f64, vp,
                            i32, i32, vp, vp, vp, vp, vp, vp, f64, f64, f64, f64, f64, vp, vp, vp,
                            C.POINTER(C.c_float), C.POINTER(i32)]),

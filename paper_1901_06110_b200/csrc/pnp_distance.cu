@@ -103,6 +103,85 @@ __global__ void patch_ssd_pairs_kernel(const double* __restrict__ g, int H, int 
   out[i] = patch_ssd(g, H, W, P, sy, sx, ry - sy, rx - sx);
 }
 
+// ---- dense W (build_dense_weights, denoise.py:389-418), test-scale ----
+// W[s][s+t] = hat_t * exp(-inv * ssd(s, t)) for every in-image pair of the
+// clipped window; the scaling steps follow the reference's matrix transforms.
+__global__ void dense_fill_kernel(const double* __restrict__ g, int H, int W, int P, int R,
+                                  double inv, double* __restrict__ Wm) {
+  const int n = H * W, side = 2 * R + 1;
+  const size_t total = (size_t)n * side * side;
+  const double scale = R + 1;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int s = (int)(i / ((size_t)side * side)), o = (int)(i % ((size_t)side * side));
+    const int dy = o / side - R, dx = o % side - R;
+    const int sy = s / W, sx = s % W, ry = sy + dy, rx = sx + dx;
+    if (ry < 0 || ry >= H || rx < 0 || rx >= W) continue;
+    const double k = exp(__dmul_rn(-inv, patch_ssd(g, H, W, P, sy, sx, dy, dx)));
+    const double hat = __dmul_rn(1.0 - fabs((double)dy) / scale, 1.0 - fabs((double)dx) / scale);
+    Wm[(size_t)s * n + (size_t)ry * W + rx] = __dmul_rn(hat, k);
+  }
+}
+
+// per-row sums (one warp per row, fixed tree) and per-column sums (thread per
+// column, rows in order): deterministic
+__global__ void dense_rowsum_kernel(const double* __restrict__ Wm, int n, double* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s = __dadd_rn(s, Wm[(size_t)row * n + j]);
+  for (int off = 16; off; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+  if (lane == 0) out[row] = s;
+}
+
+__global__ void dense_colsum_kernel(const double* __restrict__ Wm, int n, double* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = __dadd_rn(s, Wm[(size_t)i * n + col]);
+  out[col] = s;
+}
+
+// W[i][j] = (W[i][j] * (1 / sqrt(row_i))) * (1 / sqrt(col_j))
+__global__ void dense_scale_kernel(double* __restrict__ Wm, int n, const double* __restrict__ row,
+                                   const double* __restrict__ col) {
+  const size_t total = (size_t)n * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / n), c = (int)(i % n);
+    Wm[i] = __dmul_rn(__dmul_rn(Wm[i], 1.0 / sqrt(row[r])), 1.0 / sqrt(col[c]));
+  }
+}
+
+// m = max_i rowsum_i (single CTA), then W /= m
+__global__ void dense_max_kernel(const double* __restrict__ v, int n, double* __restrict__ m) {
+  __shared__ double red[32];
+  double x = -1.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x = fmax(x, v[i]);
+  for (int off = 16; off; off >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+    *m = r;
+  }
+}
+
+__global__ void dense_div_kernel(double* __restrict__ Wm, int n, const double* __restrict__ m) {
+  const size_t total = (size_t)n * n;
+  const double mm = *m;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x)
+    Wm[i] = __ddiv_rn(Wm[i], mm);
+}
+
+// W[i][i] += 1 - rowsum_i
+__global__ void dense_diag_kernel(double* __restrict__ Wm, int n, const double* __restrict__ row) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) Wm[(size_t)i * n + i] = __dadd_rn(Wm[(size_t)i * n + i], 1.0 - row[i]);
+}
+
 int grid_for(size_t n, int sms) {
   const size_t b = (n + 255) / 256;
   const size_t cap = (size_t)sms * 16;
@@ -155,6 +234,37 @@ int pnp_patch_distance_map_f64(pnp_ctx* ctx, const double* guide, int H, int W, 
   patch_distance_kernel<<<grid_for(n, ctx->sms), 256, 0, ctx->stream>>>(guide, H, W, P, dy, dx,
                                                                         out);
   PNP_LAUNCH_CHECK("patch_distance_kernel");
+  return PNP_OK;
+}
+
+int pnp_dense_weights_f64(pnp_ctx* ctx, const double* guide, int H, int W, int P, int R,
+                          double bandwidth, double* out, double* scratch) {
+  if (!ctx || !guide || !out || !scratch) return fail(PNP_EINVAL, "null argument");
+  if (H < 1 || W < 1) return fail(PNP_EINVAL, "image must be at least 1x1");
+  if (P < 1 || P % 2 == 0 || R < 1 || !(bandwidth > 0)) return fail(PNP_EINVAL, "bad params");
+  const int margin = R + (P - 1) / 2;
+  if (margin > (H < W ? H : W))
+    return fail(PNP_EINVAL, "margin " + std::to_string(margin) + " exceeds min image extent " +
+                                std::to_string(H < W ? H : W));
+  const int n = H * W;
+  const size_t nn = (size_t)n * n;
+  const double inv = 1.0 / (2.0 * P * P * bandwidth * bandwidth);
+  double* row = scratch;
+  double* col = scratch + n;
+  double* m = scratch + 2 * (size_t)n;
+  const int gb = grid_for(nn, ctx->sms);
+  PNP_CUDA(cudaMemsetAsync(out, 0, nn * sizeof(double), ctx->stream));
+  const size_t pairs = (size_t)n * (2 * R + 1) * (2 * R + 1);
+  dense_fill_kernel<<<grid_for(pairs, ctx->sms), 256, 0, ctx->stream>>>(guide, H, W, P, R, inv, out);
+  dense_rowsum_kernel<<<(n + 7) / 8, 256, 0, ctx->stream>>>(out, n, row);
+  dense_colsum_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(out, n, col);
+  dense_scale_kernel<<<gb, 256, 0, ctx->stream>>>(out, n, row, col);
+  dense_rowsum_kernel<<<(n + 7) / 8, 256, 0, ctx->stream>>>(out, n, row);
+  dense_max_kernel<<<1, 1024, 0, ctx->stream>>>(row, n, m);
+  dense_div_kernel<<<gb, 256, 0, ctx->stream>>>(out, n, m);
+  dense_rowsum_kernel<<<(n + 7) / 8, 256, 0, ctx->stream>>>(out, n, row);
+  dense_diag_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(out, n, row);
+  PNP_LAUNCH_CHECK("dense_weights kernels");
   return PNP_OK;
 }
 

@@ -120,6 +120,26 @@ def patch_distance_map(guide, offset: tuple[int, int], params: PatchParams,
     return A.from_device64(out, kind)
 
 
+DENSE_WEIGHTS_MAX_PIXELS = 4096
+
+
+def build_dense_weights(guide, params: PatchParams):
+    """Explicit n x n doubly stochastic W (test-scale oracle, denoise.py:389-418),
+    built on the device in float64 with the reference's literal matrix steps."""
+    guide, kind = A.validate(guide, "guide")
+    h, w = int(guide.shape[0]), int(guide.shape[1])
+    n = h * w
+    if n > DENSE_WEIGHTS_MAX_PIXELS:
+        raise ValueError(f"{h}x{w} image too large for dense weights (n={n})")
+    _check_margin(params, h, w)
+    g = A.to_device64(guide)
+    out = torch.empty((n, n), dtype=torch.float64, device=g.device)
+    scratch = torch.empty(2 * n + 1, dtype=torch.float64, device=g.device)
+    L.call("pnp_dense_weights_f64", L.context(g.device.index), L.ptr(g), h, w, params.patch_side,
+           params.window_radius, float(params.bandwidth), L.ptr(out), L.ptr(scratch))
+    return A.from_device64(out, kind)
+
+
 def _pair(image, guide):
     """_check_pair (denoise.py:244-251) -> device tensors + result kind."""
     image, kind = A.validate(image, "image", batch_ok=True)

@@ -246,3 +246,24 @@ def test_distance_helpers_match_reference_semantics(pnp, rng):
     ps, pr = np.pad(g, 2, mode="symmetric")[2:7, 3:8], np.pad(g, 2, mode="symmetric")[10:15, 15:20]
     assert k == pytest.approx(float(np.exp(-((ps - pr) ** 2).sum() / (2 * 25 * 0.04))), abs=1e-14)
     assert k == pytest.approx(pnp.nlm_kernel(g, (10, 15), (2, 3), p), abs=1e-14)
+
+
+def test_dense_weights_match_reference_golden(pnp, golden_extra, rng):
+    """build_dense_weights on the device (float64) against the real
+    reference's dense W (golden) and the known 1x1 / 1x2 answers; W x equals
+    the denoiser (reference tests/test_denoise.py:186-230)."""
+    e = golden_extra
+    W = pnp.build_dense_weights(e["dense_guide"], pnp.PatchParams(3, 2, 0.25))
+    assert np.abs(W - e["dense_W"]).max() < 1e-12
+    assert np.array_equal(pnp.build_dense_weights(np.array([[0.4]]), pnp.PatchParams(1, 1, 0.2)),
+                          e["w1x1"])
+    assert np.abs(pnp.build_dense_weights(np.full((1, 2), 0.9), pnp.PatchParams(1, 1, 0.2))
+                  - e["w1x2"]).max() < 1e-14
+    guide = rng.random((9, 11))
+    p = pnp.PatchParams(3, 2, 0.2)
+    W = pnp.build_dense_weights(guide, p)
+    assert np.abs(W - W.T).max() < 1e-12 and np.abs(W.sum(axis=1) - 1).max() < 1e-12
+    x = rng.random((9, 11))
+    assert np.abs((W @ x.ravel()).reshape(9, 11) - pnp.dsg_nlm_denoise(x, p, guide=guide)).max() < 1e-4
+    with pytest.raises(ValueError):
+        pnp.build_dense_weights(rng.random((65, 64)), p)
