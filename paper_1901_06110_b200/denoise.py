@@ -121,6 +121,9 @@ def patch_distance_map(guide, offset: tuple[int, int], params: PatchParams,
 
 
 DENSE_WEIGHTS_MAX_PIXELS = 4096
+# the reference memoizes kernel maps below this many bytes (denoise.py:27-29);
+# here the analogue is the HBM k cache (profiling.set_cache_limit)
+KERNEL_CACHE_BYTES = 1 << 30
 
 
 def build_dense_weights(guide, params: PatchParams):

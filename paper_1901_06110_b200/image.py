@@ -127,3 +127,14 @@ def psnr(reference, test, peak: float = 1.0) -> float:
         raise ValueError(f"peak must be > 0, got {peak}")
     mse = float(((r - t) ** 2).mean())
     return math.inf if mse == 0.0 else 10.0 * math.log10(peak * peak / mse)
+
+
+# the reference keeps its PGM / PFM file I/O in image.py (169-280)
+from .imageio import (  # noqa: E402,F401
+    ImageFormatError,
+    MalformedHeaderError,
+    TruncatedPayloadError,
+    UnsupportedFormatError,
+    read_image,
+    write_image,
+)
