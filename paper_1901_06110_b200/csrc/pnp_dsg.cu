@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -629,16 +630,16 @@ static size_t partial_floats(const Geom& g, int ntr, int C) {
 // cudaMalloc / cudaFree (both can stall the host for milliseconds and the
 // latter synchronizes the device).
 static cudaError_t pool_alloc(pnp_ctx* ctx, void** p, size_t bytes) {
-  static bool configured[64] = {};
+  static std::once_flag once[64];
   const int dev = ctx->device;
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    configured[dev] = true;
-  }
+  if (dev >= 0 && dev < 64)
+    std::call_once(once[dev], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    });
   return cudaMallocAsync(p, bytes, ctx->stream);
 }
 

@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "pnp_internal.h"
@@ -283,13 +284,24 @@ static dim3 sr_adj_grid(int H, int W, int batch) {
 static SrWin res_full(int H, int k) { return SrWin{H, 0, H, 0, H / k}; }
 static SrWin adj_full(int H, int k) { return SrWin{H, 0, H / k, 0, H}; }
 static cudaError_t sr_smem_attr(size_t res, size_t adj) {
-  static size_t set_res = 48 * 1024, set_adj = 48 * 1024;
+  // opt-in shared-memory sizes are per-device function attributes: remember
+  // the largest set per device (raised under a lock; reads are racy-benign
+  // because a stale value only repeats an idempotent call)
+  static std::mutex mu;
+  static size_t set_res[64], set_adj[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (res <= std::max<size_t>(set_res[dev], 48 * 1024) &&
+      adj <= std::max<size_t>(set_adj[dev], 48 * 1024))
+    return cudaSuccess;
+  std::lock_guard<std::mutex> lock(mu);
   cudaError_t e = cudaSuccess;
-  if (res > set_res) {
+  if (res > std::max<size_t>(set_res[dev], 48 * 1024)) {
     e = cudaFuncSetAttribute(sr_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res);
-    if (e == cudaSuccess) set_res = res;
+    if (e == cudaSuccess) set_res[dev] = res;
   }
-  if (e == cudaSuccess && adj > set_adj) {
+  if (e == cudaSuccess && adj > std::max<size_t>(set_adj[dev], 48 * 1024)) {
     e = cudaFuncSetAttribute(sr_adjoint_kernel<ADJ_PLAIN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj);
     if (e == cudaSuccess)
@@ -298,7 +310,7 @@ static cudaError_t sr_smem_attr(size_t res, size_t adj) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(sr_adjoint_kernel<ADJ_CG>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj);
-    if (e == cudaSuccess) set_adj = adj;
+    if (e == cudaSuccess) set_adj[dev] = adj;
   }
   return e;
 }

@@ -2,6 +2,7 @@
 // side in pnp_sweep_p*.cu (compiled in parallel), dispatched in pnp_dsg.cu.
 #pragma once
 
+#include <atomic>
 #include <cstring>
 
 #include "dsg_sweep.cuh"
@@ -12,12 +13,16 @@ template <int P, int RB, int C, int MODE>
 cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st) {
   constexpr size_t smem = (size_t)Cfg<P, RB, C, MODE>::TOTAL * sizeof(float);
   static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the opt-in shared-memory size is a per-device function attribute
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(dsg_sweep_kernel<P, RB, C, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   if (t.nch > max_chunks(RB) || t.ng > kMaxGroups) return cudaErrorInvalidValue;
   ChunkTab<RB> tab;

@@ -1,5 +1,7 @@
+"""freeze_guide wall time at 512^2 (allocation + sweeps) and its kernel split
+(development aid)."""
 import sys, time
-sys.path.insert(0, ".")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import torch
 import paper_1901_06110_b200 as pnp
 from paper_1901_06110_b200 import profiling
