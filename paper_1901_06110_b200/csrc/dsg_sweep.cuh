@@ -86,9 +86,10 @@ struct ChanSpec {
 
 // One chunk of the half-window offset table: KY offsets (dx, dy0 + k),
 // k < kc, with their log2(hat) (0 for plain NLM; -inf for k >= kc)
-// precomputed on the host.
+// precomputed on the host, and the chunk's place in a tile's k-cache run
+// (koff planes of TH x 64 floats: one plane per offset).
 struct Chunk {
-  int dx, dy0, kc, pad;
+  int dx, dy0, kc, koff;
   float L[kKY];
 };
 
@@ -131,14 +132,15 @@ struct SweepArgs {
   int buf_r0, buf_rows;
   int tr0, tiles_x;
   int part_off, part_ntr;
-  // k cache, tile-major, offset pairs packed: the weights of offsets
-  // (2kp, 2kp+1) of chunk ci for a pixel of a tile are one float2 in pair
-  // plane (tile*kc_npairs + ci*KY/2 + kp) of TH*64 float2 (row groups of N
-  // rows, row pairs interleaved per column: kpos) -> a chunk is one
-  // contiguous 2*TH*64*8 B run per tile
-  float2* kcache;
-  long long kc_img;
-  int kc_npairs;
+  // k cache, tile-major, exactly one float per pixel and half-window offset:
+  // a tile's run is kc_tile floats; chunk ci starts koff planes (TH*64
+  // floats) into it.  Offsets (2kp, 2kp+1) of a chunk share one float2 "pair
+  // plane" (2 planes); an odd last offset of a chunk (kc = 1 or 3) has a
+  // float "single plane".  Within either, a row group's N rows are stored
+  // row-pair interleaved per column (kpos) -> 128-bit (pair) / 64-bit
+  // (single) accesses, and a chunk is one contiguous kc*TH*64*4 B run.
+  float* kcache;
+  long long kc_img, kc_tile;
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
   // offset groups per cluster: the cg CTAs of a tile (blockIdx.y = gp*cg + q)
@@ -171,7 +173,7 @@ struct Cfg {
   // CACHED with C = 2 streams the k cache through SMEM: two chunk buffers
   // filled by bulk async copies (TMA engine) one chunk ahead + 2 mbarriers
   static constexpr bool TMAK = CACHED && C == 2;
-  static constexpr int KCH = (KY / 2) * TH * kTW * 2;  // floats per chunk
+  static constexpr int KCH = KY * TH * kTW;  // floats per chunk (KY offset planes)
   static constexpr int OFF_K = (OFF_A + C * AR * YC + 3) & ~3;
   static constexpr int OFF_MB = OFF_K + (TMAK ? 2 * KCH : 0);
   static constexpr int TOTAL = OFF_MB + (TMAK ? 4 : 0);  // floats
@@ -234,9 +236,9 @@ __device__ __forceinline__ float ld_dsmem(unsigned addr) {
   return v;
 }
 
-// Offset (float2 units) of row r, column c inside one row group of a k-cache
-// pair plane: rows (2i, 2i+1) interleaved per column (16 B), an odd last row
-// stored plainly after them.
+// Offset (in elements: float2 in a pair plane, float in a single plane) of row
+// r, column c inside one row group of a k-cache plane: rows (2i, 2i+1)
+// interleaved per column, an odd last row stored plainly after them.
 template <int N>
 __device__ __forceinline__ int kpos(int c, int r) {
   return (r < (N & ~1)) ? ((r >> 1) * kTW + c) * 2 + (r & 1) : (N & ~1) * kTW + c;
@@ -369,17 +371,16 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   for (int i = tid; i < C * AR * YC; i += kThreads) As[i] = 0.f;
 
   constexpr bool TMAK = K::TMAK;
-  constexpr unsigned KPB = TH * kTW * 8;  // bytes of one pair plane
-  float* Ks = smem + K::OFF_K;            // [2][KY/2][TH][64] float2 (TMAK)
+  constexpr int HPF = TH * kTW;              // floats of one offset plane
+  constexpr unsigned HPB = HPF * 4;           // its bytes
+  float* Ks = smem + K::OFF_K;                // [2][KY planes] (TMAK)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + K::OFF_MB);
   const int cbeg = tab.grp[blockIdx.y], cend = tab.grp[blockIdx.y + 1];
-  const float2* kimg = CACHED || STORE ? a.kcache + (long long)b * a.kc_img +
-                                             (long long)tile * a.kc_npairs * (TH * kTW)
-                                       : nullptr;
+  const float* kimg =
+      CACHED || STORE ? a.kcache + (long long)b * a.kc_img + (long long)tile * a.kc_tile : nullptr;
   auto issue_chunk = [&](int ci) {  // TMAK: chunk ci -> buffer ci & 1
-    const unsigned bytes = (tab.c[ci].kc > 2 ? 2u : 1u) * KPB;
-    bulk_load(Ks + (ci & 1) * K::KCH, kimg + (long long)ci * (KY / 2) * (TH * kTW), bytes,
-              mbar + (ci & 1));
+    bulk_load(Ks + (ci & 1) * K::KCH, kimg + (long long)tab.c[ci].koff * HPF,
+              (unsigned)tab.c[ci].kc * HPB, mbar + (ci & 1));
   };
   if (TMAK && tid == 0) {
     mbar_init(mbar, 1);
@@ -497,71 +498,94 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 #pragma unroll
       for (int j = 0; j < WIN - 1; ++j) pf[c_][j] = make_float2(0.f, 0.f);
     }
-    // this chunk's pair planes; thread (c, g) owns rows r0.. of column c.
-    // Within a plane, a row group's N rows are stored row-pair interleaved:
-    // rows (2i, 2i+1) of column c are one 16 B vector (kpos), so stores and
-    // loads are 128-bit (N odd: the last row is a plain float2 row).
-    const float2* kq = CACHED || STORE ? kimg + (long long)ci * (KY / 2) * (TH * kTW) + r0 * kTW
-                                       : nullptr;
+    // this chunk's planes; thread (c, g) owns rows r0.. of column c, stored
+    // row-pair interleaved (kpos): pair planes as 16 B (rows 2i, 2i+1 of both
+    // offsets), single planes as 8 B (rows 2i, 2i+1); N odd: last row plain.
+    // Plane of kp: 2kp planes into the chunk, a pair plane iff 2kp+1 < kc.
+    const float* kq = CACHED || STORE ? kimg + (long long)chk.koff * HPF : nullptr;
     float2 kcl[CACHED && !TMAK ? KY / 2 : 1][N];
     if (CACHED && !TMAK) {
       // register path (C = 1): all the chunk's loads in flight together
       // (predicated, not branched)
 #pragma unroll
       for (int kp = 0; kp < KY / 2; ++kp) {
+        const bool pairp = 2 * kp + 1 < kc;
+        const float* plane = kq + 2 * kp * HPF;
+        if (pairp) {
+          const float2* q2 = reinterpret_cast<const float2*>(plane) + r0 * kTW;
 #pragma unroll
-        for (int r = 0; r + 1 < N; r += 2) {
-          const float2* src = kq + kp * TH * kTW + kpos<N>(c, r);
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          asm volatile(
-              "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %5, %6;\n\t"
-              "@q ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
-              : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
-              : "l"(src), "r"(2 * kp), "r"(kc));
-          kcl[kp][r] = make_float2(v.x, v.y);
-          kcl[kp][r + 1] = make_float2(v.z, v.w);
-        }
-        if (N & 1) {
-          const float2* src = kq + kp * TH * kTW + kpos<N>(c, N - 1);
-          float2 v = make_float2(0.f, 0.f);
-          asm volatile(
-              "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %3, %4;\n\t"
-              "@q ld.global.cs.v2.f32 {%0, %1}, [%2];\n\t}"
-              : "+f"(v.x), "+f"(v.y)
-              : "l"(src), "r"(2 * kp), "r"(kc));
-          kcl[kp][N - 1] = v;
+          for (int r = 0; r + 1 < N; r += 2) {
+            const float4 v = __ldcs(reinterpret_cast<const float4*>(q2 + kpos<N>(c, r)));
+            kcl[kp][r] = make_float2(v.x, v.y);
+            kcl[kp][r + 1] = make_float2(v.z, v.w);
+          }
+          if (N & 1) kcl[kp][N - 1] = __ldcs(q2 + kpos<N>(c, N - 1));
+        } else {
+          const float* q1 = plane + r0 * kTW;
+#pragma unroll
+          for (int r = 0; r + 1 < N; r += 2) {
+            float2 v = make_float2(0.f, 0.f);
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %3, %4;\n\t"
+                "@q ld.global.cs.v2.f32 {%0, %1}, [%2];\n\t}"
+                : "+f"(v.x), "+f"(v.y)
+                : "l"(q1 + kpos<N>(c, r)), "r"(2 * kp), "r"(kc));
+            kcl[kp][r] = make_float2(v.x, 0.f);
+            kcl[kp][r + 1] = make_float2(v.y, 0.f);
+          }
+          if (N & 1) {
+            float v = 0.f;
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %2, %3;\n\t"
+                "@q ld.global.cs.f32 %0, [%1];\n\t}"
+                : "+f"(v)
+                : "l"(q1 + kpos<N>(c, N - 1)), "r"(2 * kp), "r"(kc));
+            kcl[kp][N - 1] = make_float2(v, 0.f);
+          }
         }
       }
     }
-    const float2* kb = nullptr;  // TMAK: SMEM copy of this chunk
+    const float* kb = nullptr;  // TMAK: SMEM copy of this chunk
     if (TMAK) {
       if (tid == 0 && ci + 1 < cend) {
         issue_chunk(ci + 1);  // buffer freed by the last barrier
         if (ci + PNP_KPF < cend) {  // and warm L2 further ahead
-          const int cj = ci + PNP_KPF;
-          const unsigned bytes = (tab.c[cj].kc > 2 ? 2u : 1u) * KPB;
+          const Chunk& cj = tab.c[ci + PNP_KPF];
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                           kimg + (long long)cj * (KY / 2) * (TH * kTW)),
-                       "r"(bytes)
+                           kimg + (long long)cj.koff * HPF),
+                       "r"((unsigned)cj.kc * HPB)
                        : "memory");
         }
       }
       mbar_wait(mbar + (ci & 1), (kphase >> (ci & 1)) & 1u);
       kphase ^= 1u << (ci & 1);
-      kb = reinterpret_cast<const float2*>(Ks + (ci & 1) * K::KCH) + r0 * kTW;
+      kb = Ks + (ci & 1) * K::KCH;
     }
 #pragma unroll
     for (int kp = 0; kp < KY / 2; ++kp) {
       if (kp == 0 || 2 * kp < kc) {
+        const bool pairp = 2 * kp + 1 < kc;
         float2 kk[N];
         if (TMAK) {
+          if (pairp) {
+            const float2* q2 = reinterpret_cast<const float2*>(kb + 2 * kp * HPF) + r0 * kTW;
 #pragma unroll
-          for (int r = 0; r + 1 < N; r += 2) {
-            const float4 v = *reinterpret_cast<const float4*>(kb + kp * TH * kTW + kpos<N>(c, r));
-            kk[r] = make_float2(v.x, v.y);
-            kk[r + 1] = make_float2(v.z, v.w);
+            for (int r = 0; r + 1 < N; r += 2) {
+              const float4 v = *reinterpret_cast<const float4*>(q2 + kpos<N>(c, r));
+              kk[r] = make_float2(v.x, v.y);
+              kk[r + 1] = make_float2(v.z, v.w);
+            }
+            if (N & 1) kk[N - 1] = q2[kpos<N>(c, N - 1)];
+          } else {
+            const float* q1 = kb + 2 * kp * HPF + r0 * kTW;
+#pragma unroll
+            for (int r = 0; r + 1 < N; r += 2) {
+              const float2 v = *reinterpret_cast<const float2*>(q1 + kpos<N>(c, r));
+              kk[r] = make_float2(v.x, 0.f);
+              kk[r + 1] = make_float2(v.y, 0.f);
+            }
+            if (N & 1) kk[N - 1] = make_float2(q1[kpos<N>(c, N - 1)], 0.f);
           }
-          if (N & 1) kk[N - 1] = kb[kp * TH * kTW + kpos<N>(c, N - 1)];
         } else if (CACHED) {
 #pragma unroll
           for (int r = 0; r < N; ++r) kk[r] = kcl[CACHED && !TMAK ? kp : 0][r];
@@ -579,12 +603,21 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
               v = __ffma2_rn(make_float2(a.taps_v[aa], a.taps_v[aa]), hcol[r + aa], v);
             kk[r] = make_float2(ex2_approx(v.x), ex2_approx(v.y));
             if (STORE) {
-              float2* dst = const_cast<float2*>(kq) + kp * TH * kTW + kpos<N>(c, r & ~1);
-              if (r & 1)
-                __stcs(reinterpret_cast<float4*>(dst),
-                       make_float4(kk[r - 1].x, kk[r - 1].y, kk[r].x, kk[r].y));
-              else if (r == N - 1)
-                __stcs(dst, kk[r]);
+              float* plane = const_cast<float*>(kq) + 2 * kp * HPF;
+              if (pairp) {
+                float2* dst = reinterpret_cast<float2*>(plane) + r0 * kTW + kpos<N>(c, r & ~1);
+                if (r & 1)
+                  __stcs(reinterpret_cast<float4*>(dst),
+                         make_float4(kk[r - 1].x, kk[r - 1].y, kk[r].x, kk[r].y));
+                else if (r == N - 1)
+                  __stcs(dst, kk[r]);
+              } else {  // single plane: the even offset only
+                float* dst = plane + r0 * kTW + kpos<N>(c, r & ~1);
+                if (r & 1)
+                  __stcs(reinterpret_cast<float2*>(dst), make_float2(kk[r - 1].x, kk[r].x));
+                else if (r == N - 1)
+                  __stcs(dst, kk[r].x);
+              }
             }
           }
         }

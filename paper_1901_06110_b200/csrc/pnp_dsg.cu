@@ -501,6 +501,7 @@ static Window full_window(const Geom& g) {
 // Half-window offsets grouped in chunks of KY consecutive dy sharing dx.
 static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
   out.clear();
+  int koff = 0;  // k-cache offset of the chunk in a tile's run (offset planes)
   for (int dx = -R; dx <= R; ++dx) {
     const int dy_first = dx > 0 ? 0 : 1;
     for (int dy0 = dy_first; dy0 <= R; dy0 += kKY) {
@@ -509,6 +510,8 @@ static void build_chunks(int R, bool hat, std::vector<Chunk>& out) {
       ch.dx = dx;
       ch.dy0 = dy0;
       ch.kc = (R - dy0 + 1) < kKY ? (R - dy0 + 1) : kKY;
+      ch.koff = koff;
+      koff += ch.kc;
       for (int k = 0; k < kKY; ++k) {
         // log2 of the separable hat (denoise.py:199-201), in double, rounded once
         const int dy = dy0 + k;
@@ -688,9 +691,13 @@ static cudaError_t launch_sweep_cm(const SweepArgs& a, const HostTab& t, const G
   }
 }
 
-// Floats of a k cache covering `ntr` tile rows of a (batched) image.
+// Half-window offsets (one k-cache plane of TH x 64 floats each per tile).
+static int half_window(int R) { return 2 * R * R + 2 * R; }
+
+// Floats of a k cache covering `ntr` tile rows of a (batched) image: exactly
+// one float per pixel (of the tile grid) and half-window offset.
 static size_t kcache_floats(const Geom& g, int ntr) {
-  return (size_t)g.nchunks * kKY * g.B * ((size_t)ntr * g.TH) * (g.tiles_x * kTW);
+  return (size_t)half_window(g.R) * g.B * ((size_t)ntr * g.TH) * (g.tiles_x * kTW);
 }
 
 // Decide whether the k cache of this call fits (ctx budget, free HBM).
@@ -724,10 +731,10 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   a.tiles_x = g.tiles_x;
   a.part_off = w.part_off;
   a.part_ntr = w.part_ntr;
-  a.kcache = reinterpret_cast<float2*>(kcache);
-  a.kc_npairs = g.nchunks * (kKY / 2);
+  a.kcache = kcache;
+  a.kc_tile = (long long)half_window(g.R) * g.TH * kTW;
   a.cg = g.CG;
-  a.kc_img = (long long)w.ntr * g.tiles_x * a.kc_npairs * g.TH * kTW;
+  a.kc_img = (long long)w.ntr * g.tiles_x * a.kc_tile;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
   for (int i = 0; i < g.P; ++i) {
@@ -1182,9 +1189,7 @@ int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr) {
 
 int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int ntr) {
   if (check_geometry(1, Hg, W, R, P, 1.0) || ntr < 0) return -1;
-  int nch = 0;
-  for (int dx = -R; dx <= R; ++dx) nch += (R - (dx > 0 ? 0 : 1) + kKY) / kKY;
-  return (int64_t)nch * kKY * ntr * tile_height(P) * (((W + kTW - 1) / kTW) * kTW);
+  return (int64_t)half_window(R) * ntr * tile_height(P) * (((W + kTW - 1) / kTW) * kTW);
 }
 
 int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float* x,
