@@ -118,6 +118,7 @@ class _RankState:
         self.block_floats_c1 = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, 1, 1))
         self.block_floats_c2 = 2 * self.block_floats_c1
         self.kcache = None
+        self.kc_per_tile_row = 0
 
     def enable_kcache(self, headroom: int = 4 << 30) -> bool:
         """Keep this strip's pair weights in HBM (sweep A stores, sweep B
@@ -129,6 +130,7 @@ class _RankState:
         if n <= 0 or 4 * n + headroom > free:
             return False
         self.kcache = torch.empty(n, dtype=torch.float32, device=self.buf.device)
+        self.kc_per_tile_row = n // (t1 - t0)
         return True
 
     # row views of the window (global row indices)
@@ -160,6 +162,12 @@ class LocalComm:
             dst = recv(states[k])
             if dst is not None and dst.numel():
                 dst.copy_(send(states[k + 1]))
+
+    def start_shift(self, states, send, recv, direction):
+        """shift_down (+1) / shift_up (-1) whose completion can be deferred:
+        returns a finisher (here the copies are already done)."""
+        (self.shift_down if direction > 0 else self.shift_up)(states, send, recv)
+        return lambda: None
 
     def allreduce_max(self, states):
         m = torch.stack([s.mbits for s in states]).max(dim=0).values
@@ -199,6 +207,13 @@ class TorchComm:
         return self.dist.get_global_rank(self.group, r) if self.group is not None else r
 
     def _exchange(self, states, send, recv, direction):
+        self.start_shift(states, send, recv, direction)()
+
+    def start_shift(self, states, send, recv, direction):
+        """Post this rank's half of a neighbour shift (NCCL runs it on its own
+        stream once the current stream's prior work is done) and return a
+        finisher that makes the current stream wait for it; work issued in
+        between overlaps the transfer."""
         (st,) = states
         ops = []
         to = self.rank + direction
@@ -206,16 +221,19 @@ class TorchComm:
         if 0 <= to < self.size:
             t = send(st).contiguous()
             ops.append(self.dist.P2POp(self.dist.isend, t, self._peer(to), self.group))
-        tmp = None
+        tmp, dst = None, None
         if 0 <= frm < self.size:
             dst = recv(st)
             tmp = dst if dst.is_contiguous() else torch.empty_like(dst)
             ops.append(self.dist.P2POp(self.dist.irecv, tmp, self._peer(frm), self.group))
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
+        reqs = self.dist.batch_isend_irecv(ops) if ops else []
+
+        def finish():
+            for req in reqs:
                 req.wait()
-        if tmp is not None and tmp is not recv(st):
-            recv(st).copy_(tmp)
+            if tmp is not None and tmp is not dst:
+                dst.copy_(tmp)
+        return finish
 
     def shift_down(self, states, send, recv):
         self._exchange(states, send, recv, +1)
@@ -285,23 +303,33 @@ class ShardedDSG:
         return torch.cat([st.own(st.out) for st in self.states], dim=0)
 
     # ---- the sharded algorithm ----------------------------------------------
-    def _sweep(self, st, pass_, C, x=None):
+    def _sweep(self, st, pass_, C, x=None, tiles=None):
         """Strip sweep; ``x`` (a window-shaped buffer) replaces the guide as the
-        filtered signal (frozen apply: pass 3 with the fixed guide)."""
+        filtered signal (frozen apply: pass 3 with the fixed guide).  ``tiles``
+        = (ta, tb) restricts it to some of the strip's tile rows (same bits:
+        tiles are independent)."""
         lay = st.lay
         b0, b1 = lay.window
         t0, t1 = lay.tile_rows
+        ta, tb = (t0, t1) if tiles is None else tiles
+        if tb <= ta:
+            return
         part0, off, nslot = lay.part
         p = self.params
+        kc = st.kcache
+        if kc is not None and ta > t0:
+            kc = kc[(ta - t0) * st.kc_per_tile_row:]
         L.call("pnp_dsg_strip_sweep", L.context(self.device.index), pass_, L.ptr(st.buf),
-               L.ptr(st.buf if x is None else x), L.ptr(st.rs), lay.Hg, lay.W, b0, b1 - b0, t0,
-               t1 - t0, p.window_radius, p.patch_side, self._taps, float(p.bandwidth),
-               L.ptr(st.partial), off, nslot, L.ptr(st.kcache))
+               L.ptr(st.buf if x is None else x), L.ptr(st.rs), lay.Hg, lay.W, b0, b1 - b0, ta,
+               tb - ta, p.window_radius, p.patch_side, self._taps, float(p.bandwidth),
+               L.ptr(st.partial), off + (ta - t0), nslot, L.ptr(kc))
 
-    def _fixup(self, st, mode, inv_m=None, x=None, out=None):
+    def _fixup(self, st, mode, inv_m=None, x=None, out=None, rows=None):
         lay = st.lay
         b0, b1 = lay.window
-        y0, y1 = lay.rows
+        y0, y1 = lay.rows if rows is None else rows
+        if y1 <= y0:
+            return
         part0, off, nslot = lay.part
         p = self.params
         L.call("pnp_dsg_strip_fixup", L.context(self.device.index), mode, L.ptr(st.partial),
@@ -309,7 +337,29 @@ class ShardedDSG:
                L.ptr(st.rs), L.ptr(st.kx), L.ptr(st.d), L.ptr(st.mbits), L.ptr(inv_m), L.ptr(x),
                L.ptr(out))
 
-    def _exchange_partials(self, C):
+    @staticmethod
+    def _split_rows(st):
+        """Own rows that need the partial blocks received from the rank above
+        (the first R rows) and the rest: ((y0, ya), (ya, y1))."""
+        y0, y1 = st.lay.rows
+        ya = min(y1, y0 + (st.lay.R if st.lay.rank > 0 else 0))
+        return (y0, ya), (ya, y1)
+
+    @staticmethod
+    def _split_tiles(st):
+        """Tile rows whose sweep reads the rs halo from the rank below (rows
+        past y1 within R + KY - 1 of the tile) and the rest: (early, late)."""
+        lay = st.lay
+        t0, t1 = lay.tile_rows
+        _, y1 = lay.rows
+        if lay.rank == lay.nranks - 1:
+            return (t0, t1), (t1, t1)
+        tb = t0
+        while tb < t1 and (tb + 1) * lay.TH + lay.R + KY - 1 <= y1:
+            tb += 1
+        return (t0, tb), (tb, t1)
+
+    def _exchange_partials(self, C, start=False):
         def send(st):
             _, off, nslot = st.lay.part
             return st.partial_rows(C, nslot - st.lay.dti, nslot)
@@ -318,9 +368,12 @@ class ShardedDSG:
             _, off, _ = st.lay.part
             return st.partial_rows(C, 0, off)
 
-        self.comm.shift_down(self.states, send, recv)
+        fin = self.comm.start_shift(self.states, send, recv, +1)
+        if not start:
+            fin()
+        return fin
 
-    def _exchange_rows(self, name, top=True):
+    def _exchange_rows(self, name, top=True, start=False):
         def up_send(st):   # our first rows -> rank above's bottom halo
             y0, y1 = st.lay.rows
             return st.rows_view(getattr(st, name), y0, y0 + st.lay.halo[1])
@@ -339,25 +392,41 @@ class ShardedDSG:
             b0, _ = st.lay.window
             return st.rows_view(getattr(st, name), b0, y0)
 
+        if not top and start:  # the bottom halo only, completion deferred
+            return self.comm.start_shift(self.states, up_send, up_recv, -1)
         self.comm.shift_up(self.states, up_send, up_recv)
         if top and self.states[0].lay.halo[0] > 0:
             self.comm.shift_down(self.states, down_send, down_recv)
+        return lambda: None
 
     def denoise(self) -> None:
-        """One adaptive DSG-NLM of the loaded image; results in each state's out."""
+        """One adaptive DSG-NLM of the loaded image; results in each state's out.
+        Each neighbour exchange overlaps the work that does not need it: the
+        partial blocks from the rank above only reach our first R rows (the
+        other rows' fixups run while they travel), the rs halo from the rank
+        below only feeds our last tile row(s) (the others' sweeps run first)."""
         self._exchange_rows("buf")
         for st in self.states:
             self._sweep(st, 0, 1)
-        self._exchange_partials(1)
+        fin = self._exchange_partials(1, start=True)
         for st in self.states:
-            self._fixup(st, 0)
-        self._exchange_rows("rs", top=False)  # y channels only read rows below
+            self._fixup(st, 0, rows=self._split_rows(st)[1])
+        fin()
         for st in self.states:
-            self._sweep(st, 1, 2)
-        self._exchange_partials(2)
+            self._fixup(st, 0, rows=self._split_rows(st)[0])
+        fin = self._exchange_rows("rs", top=False, start=True)  # y channels read rows below
+        for st in self.states:
+            self._sweep(st, 1, 2, tiles=self._split_tiles(st)[0])
+        fin()
+        for st in self.states:
+            self._sweep(st, 1, 2, tiles=self._split_tiles(st)[1])
+        fin = self._exchange_partials(2, start=True)
         for st in self.states:
             st.mbits.zero_()
-            self._fixup(st, 1)
+            self._fixup(st, 1, rows=self._split_rows(st)[1])
+        fin()
+        for st in self.states:
+            self._fixup(st, 1, rows=self._split_rows(st)[0])
         self.comm.allreduce_max(self.states)
         for st in self.states:
             lay = st.lay

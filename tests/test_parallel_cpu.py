@@ -63,6 +63,12 @@ def _worker(rank, world, port, q):
         comm.shift(world, lambda k: buf[0][0:1], lambda k: buf[0][3:4], -1)
         tot = torch.tensor([1.5 * (rank + 1), float(rank)], dtype=torch.float64)
         comm.allreduce_sum([tot])
+        # deferred completion: post, do unrelated work, then finish
+        st2 = _S(rank + 5)
+        fin = comm.start_shift([st2], lambda s: s.t[4:6], lambda s: s.t[0:2], +1)
+        st2.t[2:4] += 100.0
+        fin()
+        tot = torch.cat([tot, st2.t.to(torch.float64)])
         q.put((rank, st.t.tolist(), int(st.mbits[0]), buf[0].tolist(), tot.tolist()))
     finally:
         dist.destroy_process_group()
@@ -101,7 +107,15 @@ def test_torch_comm_gloo_world2_matches_local():
     comm.shift(world, lambda k: bufs[k][0:1], lambda k: bufs[k][3:4], -1)
     tots = [torch.tensor([1.5 * (r + 1), float(r)], dtype=torch.float64) for r in range(world)]
     comm.allreduce_sum(tots)
+    st2 = [_S(r + 5) for r in range(world)]
+    fin = comm.start_shift(st2, lambda s: s.t[4:6], lambda s: s.t[0:2], +1)
+    for s_ in st2:
+        s_.t[2:4] += 100.0
+    fin()
+    tots = [torch.cat([tots[r], st2[r].t.to(torch.float64)]) for r in range(world)]
     for r in range(world):
         assert res[r][2] == bufs[r].tolist()
-        assert res[r][3] == tots[r].tolist() == [4.5, 1.0]
+        assert res[r][3] == tots[r].tolist()
+        assert res[r][3][:2] == [4.5, 1.0]
+    assert res[1][3][2:] == [5, 5, 106, 106, 6, 6] and res[0][3][2:] == [5, 5, 105, 105, 5, 5]
     assert bufs[0].tolist() == [0, 1, 2, 2] and bufs[1].tolist() == [2, 3, 12, 13]
