@@ -40,26 +40,33 @@ int pnp_admm_run(pnp_ctx* ctx, int kind, const float* obs, const float* obs2, in
     }
     PNP_CUDA(cudaEventRecord(ev[0], ctx->stream));
   }
-  float* vcur = v0;
-  float* vnext = v1;
   int cur = 0;
-  for (int k = k0; k <= k1; ++k) {
-    int* fk = flags + (k - 1);
-    double* obj = (objv && k >= 2) ? objv + (size_t)(k - 2) * batch : nullptr;
-    int rc = kind == 0
-                 ? pnp_sr_grad_xupdate(ctx, x, obs, batch, H, W, taps, radius, factor, boundary,
-                                       obj, vcur, u, z, mu, alpha, rho, lo, hi, fk)
-                 : pnp_qis_grad_xupdate(ctx, x, obs, obs2, batch, H * W, gain_over_K, floor_, obj,
-                                        vcur, u, z, mu, alpha, rho, lo, hi, fk);
+  if (kind == 0 && n_it > 0) {  // SR: next residual pipelined on a side stream
+    int rc = sr_admm_pipelined(ctx, obs, batch, H, W, taps, radius, factor, boundary, fz, k0, k1,
+                               x, v0, v1, u, z, gt, mu, alpha, rho, lo, hi, stats, objv, flags,
+                               ms_out ? &ev : nullptr, &cur);
     if (rc) return rc;
-    rc = pnp_dsg_apply_admm(ctx, fz, z, vnext, u, x, vcur, gt, rho,
-                            stats + (size_t)(k - 1) * batch * 4, fk);
-    if (rc) return rc;
-    float* t = vcur;
-    vcur = vnext;
-    vnext = t;
-    cur ^= 1;
-    if (ms_out) PNP_CUDA(cudaEventRecord(ev[k - k0 + 1], ctx->stream));
+  } else {
+    float* vcur = v0;
+    float* vnext = v1;
+    for (int k = k0; k <= k1; ++k) {
+      int* fk = flags + (k - 1);
+      double* obj = (objv && k >= 2) ? objv + (size_t)(k - 2) * batch : nullptr;
+      int rc = kind == 0
+                   ? pnp_sr_grad_xupdate(ctx, x, obs, batch, H, W, taps, radius, factor, boundary,
+                                         obj, vcur, u, z, mu, alpha, rho, lo, hi, fk)
+                   : pnp_qis_grad_xupdate(ctx, x, obs, obs2, batch, H * W, gain_over_K, floor_,
+                                          obj, vcur, u, z, mu, alpha, rho, lo, hi, fk);
+      if (rc) return rc;
+      rc = pnp_dsg_apply_admm(ctx, fz, z, vnext, u, x, vcur, gt, rho,
+                              stats + (size_t)(k - 1) * batch * 4, fk);
+      if (rc) return rc;
+      float* t = vcur;
+      vcur = vnext;
+      vnext = t;
+      cur ^= 1;
+      if (ms_out) PNP_CUDA(cudaEventRecord(ev[k - k0 + 1], ctx->stream));
+    }
   }
   if (v_last) *v_last = cur;
   if (ms_out && n_it > 0) {

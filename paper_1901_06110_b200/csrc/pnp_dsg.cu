@@ -875,6 +875,11 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
     cudaEventDestroy(sl.b);
   }
   for (cudaEvent_t e : ctx->iter_events) cudaEventDestroy(e);
+  if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
+  if (ctx->ev_res) cudaEventDestroy(ctx->ev_res);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  ctx->admm_r.release();
+  ctx->admm_part.release();
   delete ctx;
   return PNP_OK;
 }

@@ -1171,3 +1171,77 @@ int pnp_sr_strip_adjoint(pnp_ctx* ctx, const float* r, float* out, int Hg, int W
 }
 
 }  // extern "C"
+
+namespace pnp {
+
+// pnp_admm_run for the SR model, pipelined: iteration k+1's residual
+// r = A x_k - y needs only x_k, so it runs on a side stream while iteration
+// k's denoiser (frozen apply + u-update) runs on the main stream; the adjoint
+// + x-update of k+1 waits for it.  Same kernels with the same arguments as
+// pnp_sr_grad_xupdate + pnp_dsg_apply_admm per iteration (bitwise equal);
+// the residual uses its own r / partial buffers (the apply's statistics
+// partials live in ctx->stats).
+int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, const float* taps,
+                      int radius, int factor, int boundary, const pnp_frozen* fz, int k0, int k1,
+                      float* x, float* v0, float* v1, float* u, float* z, const float* gt,
+                      double mu, double alpha, double rho, double lo, double hi, double* stats,
+                      double* objv, int* flags, std::vector<cudaEvent_t>* timing, int* v_last) {
+  Taps t;
+  int rc = sr_check(batch, H, W, taps, radius, factor, boundary, t);
+  if (rc) return rc;
+  if (!ctx->side) {
+    PNP_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
+    PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_res, cudaEventDisableTiming));
+  }
+  const int nl = (H / factor) * (W / factor);
+  const dim3 rg = sr_res_grid(H, W, factor, batch), ag = sr_adj_grid(H, W, batch);
+  const int nblk = rg.x * rg.y;
+  if ((rc = ctx->admm_r.ensure((size_t)batch * nl * sizeof(float)))) return rc;
+  if ((rc = ctx->admm_part.ensure((size_t)batch * nblk * sizeof(double)))) return rc;
+  float* r = ctx->admm_r.as<float>();
+  double* part = objv ? ctx->admm_part.as<double>() : nullptr;
+  const size_t rsm = sr_res_smem(factor, radius), asm_ = sr_adj_smem(radius);
+  PNP_CUDA(sr_smem_attr(rsm, asm_));
+  const cudaStream_t main = ctx->stream, side = ctx->side;
+  auto residual = [&](cudaStream_t st) {
+    sr_residual_kernel<<<rg, 256, rsm, st>>>(x, y, r, res_full(H, factor), W, factor, radius,
+                                             boundary, t, part);
+  };
+  // the first iteration's residual on the main stream (x is x_{k0-1})
+  residual(main);
+  PNP_LAUNCH_CHECK("sr_residual_kernel");
+  float* vcur = v0;
+  float* vnext = v1;
+  int cur = 0;
+  for (int k = k0; k <= k1; ++k) {
+    int* fk = flags + (k - 1);
+    double* obj = (objv && k >= 2) ? objv + (size_t)(k - 2) * batch : nullptr;
+    if (k > k0) PNP_CUDA(cudaStreamWaitEvent(main, ctx->ev_res, 0));
+    const XUpd q = make_xupd(x, vcur, u, z, mu, alpha, rho, lo, hi, fk);
+    const RedEpi red{part, obj, 0.5, nblk, batch};
+    sr_adjoint_kernel<ADJ_XUPD><<<ag, 256, asm_, main>>>(r, nullptr, adj_full(H, factor), W,
+                                                         factor, radius, boundary, t, q,
+                                                         CgEpi{}, red);
+    PNP_LAUNCH_CHECK("sr_adjoint_kernel");
+    if (k < k1) {  // next iteration's residual overlaps this denoise
+      PNP_CUDA(cudaEventRecord(ctx->ev_x, main));
+      PNP_CUDA(cudaStreamWaitEvent(side, ctx->ev_x, 0));
+      residual(side);
+      PNP_LAUNCH_CHECK("sr_residual_kernel");
+      PNP_CUDA(cudaEventRecord(ctx->ev_res, side));
+    }
+    if ((rc = pnp_dsg_apply_admm(ctx, fz, z, vnext, u, x, vcur, gt, rho,
+                                 stats + (size_t)(k - 1) * batch * 4, fk)))
+      return rc;
+    float* tmp = vcur;
+    vcur = vnext;
+    vnext = tmp;
+    cur ^= 1;
+    if (timing) PNP_CUDA(cudaEventRecord((*timing)[k - k0 + 1], main));
+  }
+  if (v_last) *v_last = cur;
+  return PNP_OK;
+}
+
+}  // namespace pnp

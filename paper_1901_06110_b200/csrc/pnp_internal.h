@@ -74,6 +74,11 @@ struct pnp_ctx {
   std::map<std::pair<int, int>, Tables> tables;
   // per-iteration timing events of the native ADMM loop (pnp_admm_run)
   std::vector<cudaEvent_t> iter_events;
+  // its side stream (the next iteration's SR residual overlaps the denoiser),
+  // two ordering events, and the residual / partial buffers it owns
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_res = nullptr;
+  pnp::DevBuf admm_r, admm_part;
   // optional per-launch CUDA-event timing (pnp_ctx_profile)
   bool prof = false;
   std::vector<pnp::ProfSlot> slots;
@@ -106,6 +111,13 @@ struct ProfScope {
 namespace pnp {
 // stats[b*4 + k] = sum_j part[b][j][k] for k < 3 (pnp_forward.cu)
 int reduce_stats3(pnp_ctx* ctx, const double* part, int nblk, int batch, double* stats);
+// pnp_admm_run's SR loop with the next iteration's residual on a side stream
+// (pnp_forward.cu): same launches and arguments as the sequential loop.
+int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, const float* taps,
+                      int radius, int factor, int boundary, const pnp_frozen* fz, int k0, int k1,
+                      float* x, float* v0, float* v1, float* u, float* z, const float* gt,
+                      double mu, double alpha, double rho, double lo, double hi, double* stats,
+                      double* objv, int* flags, std::vector<cudaEvent_t>* timing, int* v_last);
 }  // namespace pnp
 
 struct pnp_frozen {
