@@ -292,7 +292,7 @@ def run_gpu(args, rank, world, local_rank):
     half = ((2 * R_C4 + 1) ** 2 - 1) / 2 / (2 * R_C4 + 1) ** 2
     ops_a, ops_b = (2 * P_C4 + 5) * half, (2 * P_C4 + 9) * half
     ops_unit = ops_a + (ops_b if cached_n == 0 else 0.0)
-    kbytes_unit = 8.0 * half / 2  # k cache: one float2 per offset pair = 4 B per half-window pair
+    kbytes_unit = 4.0 * half  # k cache: one float per pixel and half-window offset
     kernels = []
     if sweep_ms > 0:
         ach = ops_unit * units_rank / (sweep_ms * 1e-3) / 1e12
