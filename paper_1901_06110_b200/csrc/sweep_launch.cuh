@@ -6,11 +6,42 @@
 #include <cstring>
 
 #include "dsg_sweep.cuh"
+#include "dsg_sweep_ws.cuh"
+
+#ifndef PNP_WS
+#define PNP_WS 0  // warp-specialized sweep A (dsg_sweep_ws.cuh)
+#endif
 
 namespace pnp {
 
+template <int P, int RB, int MODE>
+cudaError_t launch_sweep_ws(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st) {
+  constexpr size_t smem = (size_t)CfgWs<P, RB, MODE>::TOTAL * sizeof(float);
+  static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(dsg_sweep_ws_kernel<P, RB, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  ChunkTab<RB> tab;
+  memset(&tab, 0, sizeof(tab));
+  memcpy(tab.c, t.ch, sizeof(Chunk) * t.nch);
+  memcpy(tab.grp, t.grp, sizeof(int) * (t.ng + 1));
+  dsg_sweep_ws_kernel<P, RB, MODE><<<grid, kWsThreads, smem, st>>>(a, tab);
+  return cudaGetLastError();
+}
+
 template <int P, int RB, int C, int MODE>
 cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st) {
+  if constexpr (PNP_WS && C == 1 && MODE != MODE_CACHED) {
+    if (a.cg <= 1 && t.nch <= max_chunks(RB) && t.ng <= kMaxGroups)
+      return launch_sweep_ws<P, RB, MODE>(a, t, grid, st);
+  }
   constexpr size_t smem = (size_t)Cfg<P, RB, C, MODE>::TOTAL * sizeof(float);
   static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
   // the opt-in shared-memory size is a per-device function attribute
