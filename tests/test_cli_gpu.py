@@ -48,3 +48,25 @@ def test_cli_commands_match_reference():
         if name == "sim_sr.ini":
             obs.write_bytes((d / "observation.pfm").read_bytes())
     assert json.loads((CLI / "runs.json").read_text()) == runs
+
+
+def test_denoise_oracle_flag(tmp_path, capsys):
+    """denoise --oracle: the dense-W brute force (built on the device) agrees
+    with the fast denoiser; too-large images and non-DSG denoisers are config
+    errors (reference cli.py denoise --oracle)."""
+    import numpy as np
+
+    from paper_1901_06110_b200 import cli, write_image
+    rng = np.random.default_rng(3)
+    write_image(rng.random((24, 30)), tmp_path / "small.pfm", "pfm")
+    write_image(rng.random((70, 70)), tmp_path / "big.pfm", "pfm")
+    ini = tmp_path / "d.ini"
+    ini.write_text(f"[run]\ninput = small.pfm\noutput_dir = {tmp_path}/runs\n"
+                   "[patch]\npatch_side = 3\nwindow_radius = 3\nbandwidth = 0.2\n"
+                   "[solver]\ndenoiser = dsg-adaptive\n")
+    assert cli.main(["denoise", str(ini), "--oracle"]) == 0
+    line = [ln for ln in capsys.readouterr().out.splitlines() if "oracle max-abs diff" in ln][0]
+    assert float(line.split("=")[1]) < 1e-4
+    assert cli.main(["denoise", str(ini), "--oracle", "--denoiser", "nlm"]) == 2
+    ini.write_text(ini.read_text().replace("small.pfm", "big.pfm"))
+    assert cli.main(["denoise", str(ini), "--oracle"]) == 2
