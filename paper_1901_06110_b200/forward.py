@@ -18,7 +18,6 @@ library on the host, bit-exact with the reference.
 from __future__ import annotations
 
 import ctypes as C
-import math
 from dataclasses import dataclass
 
 import numpy as np

@@ -37,10 +37,10 @@ import torch
 
 from . import _arrays as A
 from . import _lib as L
-from .denoise import PatchParams, dsg_nlm_denoise, freeze_guide, nlm_denoise
+from .denoise import PatchParams, freeze_guide
 from .forward import (QIS_FLOOR, QisCounts, QisModel, SuperResOp, power_iteration_lipschitz,
                       qis_grad_device, qis_grad_xupdate_device, qis_initial_estimate, sr_adjoint)
-from .image import UNCONSTRAINED, Box, Constraint, NonNegative, Unconstrained, bounds
+from .image import UNCONSTRAINED, Constraint, bounds
 
 DENOISERS = ("identity", "nlm", "dsg-adaptive", "dsg-fixed")
 
