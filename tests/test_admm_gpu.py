@@ -308,3 +308,22 @@ def test_native_loop_is_bitwise_python_loop(pnp, golden_admm, case):
                                   equal_nan=True), f
         assert math.isfinite(r2.time_ms) and r2.time_ms >= last
         last = r2.time_ms
+
+
+def test_native_loop_on_a_side_stream(pnp, golden_admm):
+    """The pipelined C++ loop on a non-default torch stream (its own side
+    stream and events hang off the context): same bits as the Python loop."""
+    import torch
+    a = golden_admm
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    y = torch.from_numpy(np.asarray(a["sr_y"], dtype=np.float32)).cuda()
+    prob = pnp.make_sr_problem(op, y)
+    guide = torch.from_numpy(np.asarray(a["sr_gauss_guide"], dtype=np.float32)).cuda()
+    den = pnp.freeze_guide(guide, pnp.PatchParams(5, 4, 0.1, 1.5)).as_denoiser()
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=7, constraint=pnp.UNIT_BOX)
+    vp, _ = pnp.linearized_pnp_admm(prob, cfg, denoiser=den, native=False)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        vn, rn = pnp.linearized_pnp_admm(prob, cfg, denoiser=den, native=True)
+    s.synchronize()
+    assert torch.equal(vp, vn) and len(rn) == 7
