@@ -96,6 +96,18 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
                     int batch, int H, int W, int R, int P, const float* taps,
                     double bandwidth);
 
+/* Single-image denoise whose sweep A starts before the whole image is on the
+ * device (pipelined uploads, DenoiseStream): the image is split into
+ * `nbands` bands of tile rows (pnp_dsg_band_rows gives band j's last tile
+ * row + 1 in tile_end[j] and the input rows [0, rows_needed[j]) it reads);
+ * band j's sweep A waits for events[j] (a cudaEvent_t recorded once those
+ * rows are uploaded; NULL = no wait), the rest of the denoise runs after the
+ * last band.  Guide = x.  Bitwise equal to pnp_dsg_denoise. */
+int pnp_dsg_band_rows(int H, int W, int R, int P, int nbands, int* tile_end, int* rows_needed);
+int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
+                           const float* taps, double bandwidth, int nbands,
+                           void* const* events);
+
 /* ---- row-strip building blocks (multi-GPU sharding) ---- *
  * A rank owns global rows [y0, y1) = whole tile rows of height
  * pnp_tile_height(P).  Per-pixel buffers are windows: rows [buf_r0, buf_r0 +

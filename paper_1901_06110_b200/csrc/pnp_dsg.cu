@@ -982,6 +982,91 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   return run_finalize(ctx, g, w, kx, d, ctx->mbits.as<unsigned>(), x, out, alpha_out);
 }
 
+// Row bands of a single image for pnp_dsg_denoise_banded: band j sweeps tile
+// rows [tile_end[j-1], tile_end[j]) and needs input rows [0, rows_needed[j]).
+static void band_split(int H, int R, int P, int nbands, int* tile_end, int* rows_needed) {
+  const int TH = tile_height(P), T = (H + TH - 1) / TH, p = (P - 1) / 2, RB = r_bucket(R);
+  for (int j = 0; j < nbands; ++j) {
+    const int tb = (int)((long long)(j + 1) * T / nbands);
+    tile_end[j] = tb;
+    // the guide tile of tile row tb-1 reads rows up to (tb-1)*TH - p + 32 + RB
+    const int need = (tb - 1) * TH - p + 33 + RB;
+    rows_needed[j] = j == nbands - 1 ? H : (need < H ? need : H);
+  }
+}
+
+int pnp_dsg_band_rows(int H, int W, int R, int P, int nbands, int* tile_end, int* rows_needed) {
+  if (!tile_end || !rows_needed || nbands < 1) return fail(PNP_EINVAL, "bad arguments");
+  int rc = check_geometry(1, H, W, R, P, 1.0);
+  if (rc) return rc;
+  if (nbands > (H + tile_height(P) - 1) / tile_height(P))
+    return fail(PNP_EINVAL, "more bands than tile rows");
+  band_split(H, R, P, nbands, tile_end, rows_needed);
+  return PNP_OK;
+}
+
+int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
+                           const float* taps, double bandwidth, int nbands,
+                           void* const* events) {
+  if (!ctx || !x || !out || !events || nbands < 1) return fail(PNP_EINVAL, "null argument");
+  int rc = check_geometry(1, H, W, R, P, bandwidth);
+  if (rc) return rc;
+  if ((rc = validate_taps(taps, P))) return rc;
+  PNP_CUDA(cudaSetDevice(ctx->device));
+  Geom g;
+  if ((rc = make_geom(ctx, 1, H, W, R, P, g))) return rc;
+  if (nbands > g.tiles_y) return fail(PNP_EINVAL, "more bands than tile rows");
+  const size_t n = (size_t)H * W;
+  if ((rc = ensure_planes(ctx, n))) return rc;
+  if ((rc = ctx->mbits.ensure(sizeof(unsigned)))) return rc;
+  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
+  float* rs = ctx->rs.as<float>();
+  float* kx = ctx->kx.as<float>();
+  float* d = ctx->d.as<float>();
+  float* part = ctx->partial.as<float>();
+  const Window w = full_window(g);
+  float* kc = nullptr;
+  const size_t kcf = kcache_floats(g, g.tiles_y);
+  if (kcache_fits(ctx, kcf, ctx->kcache.bytes)) {
+    if ((rc = ctx->kcache.ensure(kcf * sizeof(float)))) return rc;
+    kc = ctx->kcache.as<float>();
+  }
+  std::vector<int> tend(nbands), need(nbands);
+  band_split(H, R, P, nbands, tend.data(), need.data());
+  // sweep A band by band, each after its rows arrived: same tiles, same
+  // partial slots and k-cache runs as the one-launch sweep -> same bits
+  const size_t kc_row = (size_t)g.tiles_x * half_window(g.R) * g.TH * kTW;
+  int t0 = 0;
+  for (int j = 0; j < nbands; ++j) {
+    if (events[j]) PNP_CUDA(cudaStreamWaitEvent(ctx->stream, (cudaEvent_t)events[j], 0));
+    const int t1 = tend[j];
+    if (t1 > t0) {
+      Window wj{0, H, t0, t1 - t0, 0, t0, g.tiles_y, 0, H};
+      if ((rc = run_sweep(ctx, g, wj, 1, x, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
+                          taps, bandwidth, true, part, kc ? MODE_STORE : MODE_RECOMPUTE,
+                          kc ? kc + (size_t)t0 * kc_row : nullptr)))
+        return rc;
+    }
+    t0 = t1;
+  }
+  {
+    FixIO io{};
+    io.rs = rs;
+    if ((rc = run_fixup<FIX_RS>(ctx, g, w, 1, part, io))) return rc;
+  }
+  if ((rc = run_sweep(ctx, g, w, 2, x, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps, bandwidth,
+                      true, part, kc ? MODE_CACHED : MODE_RECOMPUTE, kc)))
+    return rc;
+  PNP_CUDA(cudaMemsetAsync(ctx->mbits.ptr, 0, sizeof(unsigned), ctx->stream));
+  FixIO io{};
+  io.rs = rs;
+  io.kx = kx;
+  io.d = d;
+  io.mbits = ctx->mbits.as<unsigned>();
+  if ((rc = run_fixup<FIX_KXD>(ctx, g, w, 2, part, io))) return rc;
+  return run_finalize(ctx, g, w, kx, d, ctx->mbits.as<unsigned>(), x, out, nullptr);
+}
+
 int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, int R, int P,
                    const float* taps, double bandwidth, pnp_frozen** out) {
   if (!ctx || !guide || !out) return fail(PNP_EINVAL, "null argument");

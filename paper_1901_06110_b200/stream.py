@@ -12,6 +12,8 @@ stream order, and is reported when the batch is collected.
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -41,6 +43,17 @@ class DenoiseStream:
         self._taps = params._ctaps()
         L.call("pnp_ctx_reserve", L.context(self.dev), B, H, W, params.window_radius,
                params.patch_side)
+        # the first image of a run has no earlier image to hide its upload
+        # behind: it goes up in row bands and its sweep A starts band by band
+        # (pnp_dsg_denoise_banded); later images overlap the previous denoise
+        self._bands = None
+        nb = 4
+        TH = 32 - (params.patch_side - 1)
+        if B == 1 and -(-H // TH) >= 4 * nb:
+            te, need = (C.c_int * nb)(), (C.c_int * nb)()
+            L.call("pnp_dsg_band_rows", H, W, params.window_radius, params.patch_side, nb, te,
+                   need)
+            self._bands = list(need)
 
     def run(self, host_images, host_outs=None):
         n = len(host_images)
@@ -61,24 +74,45 @@ class DenoiseStream:
         p = self.params
         for i in range(n):
             k = i % self.depth
+            banded = i == 0 and self._bands is not None
+            band_ev = []
             with torch.cuda.stream(self.s_h2d):
                 if i >= self.depth:
                     self.s_h2d.wait_event(done[i - self.depth])   # din[k] consumed
                 src = host_images[i]
                 if not isinstance(src, torch.Tensor):
                     src = torch.from_numpy(np.ascontiguousarray(src, dtype=np.float32))
-                self.din[k].copy_(src, non_blocking=True)
+                if banded:
+                    r0 = 0
+                    for r1 in self._bands:
+                        if r1 > r0:
+                            self.din[k][r0:r1].copy_(src[r0:r1], non_blocking=True)
+                            r0 = r1
+                        ev = torch.cuda.Event()
+                        ev.record(self.s_h2d)
+                        band_ev.append(ev)
+                else:
+                    self.din[k].copy_(src, non_blocking=True)
                 up[i].record(self.s_h2d)
             with torch.cuda.stream(self.s_comp):
-                self.s_comp.wait_event(up[i])
+                if not banded:
+                    self.s_comp.wait_event(up[i])
                 if i >= self.depth:
                     self.s_comp.wait_event(down[i - self.depth])  # dout[k] downloaded
                 ctx = L.context(self.dev)
                 x = self.din[k]
-                L.call("pnp_flag_nonfinite", ctx, L.ptr(x), x.numel(), L.ptr(flags[i:i + 1]))
-                L.call("pnp_dsg_denoise", ctx, L.ptr(x), L.ptr(x), L.ptr(self.dout[k]), self.B,
-                       self.H, self.W, p.window_radius, p.patch_side, self._taps,
-                       float(p.bandwidth), None, None)
+                if banded:  # sweep A band by band as the rows arrive
+                    evs = (C.c_void_p * len(band_ev))(*[e.cuda_event for e in band_ev])
+                    L.call("pnp_dsg_denoise_banded", ctx, L.ptr(x), L.ptr(self.dout[k]), self.H,
+                           self.W, p.window_radius, p.patch_side, self._taps,
+                           float(p.bandwidth), len(band_ev), evs)
+                    self.s_comp.wait_event(up[i])
+                    L.call("pnp_flag_nonfinite", ctx, L.ptr(x), x.numel(), L.ptr(flags[i:i + 1]))
+                else:
+                    L.call("pnp_flag_nonfinite", ctx, L.ptr(x), x.numel(), L.ptr(flags[i:i + 1]))
+                    L.call("pnp_dsg_denoise", ctx, L.ptr(x), L.ptr(x), L.ptr(self.dout[k]),
+                           self.B, self.H, self.W, p.window_radius, p.patch_side, self._taps,
+                           float(p.bandwidth), None, None)
                 done[i].record(self.s_comp)
             with torch.cuda.stream(self.s_d2h):
                 self.s_d2h.wait_event(done[i])

@@ -202,6 +202,17 @@ def test_denoise_stream_pipeline(pnp, rng):
     bad[3][10, 20] = float("nan")
     with pytest.raises(ValueError, match="image 3"):
         pnp.DenoiseStream(p, (150, 210)).run(bad)
+    # tall enough for the banded first upload (>= 16 tile rows): same bits
+    tall = [torch.tensor(rng.random((700, 130)), dtype=torch.float32).pin_memory()
+            for _ in range(3)]
+    st = pnp.DenoiseStream(p, (700, 130))
+    assert st._bands is not None
+    for im, o in zip(tall, st.run(tall)):
+        assert torch.equal(o, pnp.dsg_nlm_denoise(im.cuda(), p).cpu())
+    bad = [im.clone() for im in tall]
+    bad[0][600, 5] = float("inf")
+    with pytest.raises(ValueError, match="image 0"):
+        st.run(bad)
 
 
 def test_distance_helpers_match_reference_semantics(pnp, rng):
