@@ -711,6 +711,21 @@ static bool kcache_fits(pnp_ctx* ctx, size_t floats, size_t already) {
   return bytes - already + ((size_t)4 << 30) <= free_b;  // keep 4 GiB headroom
 }
 
+// Tile rows (counted from the top of every image) whose k cache fits: all of
+// them when the whole cache fits, else as many as the budget allows (the
+// rest is recomputed -- same bits either way), 0 below 1/8 of the image.
+static int kcache_rows(pnp_ctx* ctx, const Geom& g, size_t already) {
+  if (ctx->cache_limit == 0) return 0;
+  if (kcache_fits(ctx, kcache_floats(g, g.tiles_y), already)) return g.tiles_y;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
+  const size_t head = (size_t)4 << 30, row_b = kcache_floats(g, 1) * sizeof(float);
+  size_t budget = free_b + already > head ? free_b + already - head : 0;
+  if (budget > ctx->cache_limit) budget = ctx->cache_limit;
+  const int rows = (int)(budget / row_b);
+  return rows * 8 >= g.tiles_y ? (rows < g.tiles_y ? rows : g.tiles_y) : 0;
+}
+
 static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const float* guide,
                      ChanSpec c0, ChanSpec c1, const float* taps, double bw, bool use_hat,
                      float* partial, int mode = MODE_RECOMPUTE, float* kcache = nullptr) {
@@ -755,6 +770,23 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   }
   if (e != cudaSuccess) return cuda_fail(e, "dsg_sweep_kernel");
   return PNP_OK;
+}
+
+// A full-window sweep with the k cache covering tile rows [0, kc_rows):
+// those run in `kmode` (STORE or CACHED) on the cache, the rest recompute.
+static int run_sweep_kc(pnp_ctx* ctx, const Geom& g, int C, const float* guide, ChanSpec c0,
+                        ChanSpec c1, const float* taps, double bw, float* partial, int kmode,
+                        float* kc, int kc_rows) {
+  const Window w = full_window(g);
+  if (!kc || kc_rows <= 0)
+    return run_sweep(ctx, g, w, C, guide, c0, c1, taps, bw, true, partial, MODE_RECOMPUTE);
+  if (kc_rows >= g.tiles_y)
+    return run_sweep(ctx, g, w, C, guide, c0, c1, taps, bw, true, partial, kmode, kc);
+  const Window wa{0, g.Hg, 0, kc_rows, 0, 0, g.tiles_y, 0, g.Hg};
+  const Window wb{0, g.Hg, kc_rows, g.tiles_y - kc_rows, 0, kc_rows, g.tiles_y, 0, g.Hg};
+  int rc = run_sweep(ctx, g, wa, C, guide, c0, c1, taps, bw, true, partial, kmode, kc);
+  if (rc) return rc;
+  return run_sweep(ctx, g, wb, C, guide, c0, c1, taps, bw, true, partial, MODE_RECOMPUTE);
 }
 
 template <int MODE>
@@ -822,11 +854,11 @@ static int validate_taps(const float* taps, int P) {
 
 // sweep A + fixup: g -> rs (guide-only; shared by adaptive and freeze)
 static int mass_and_rs(pnp_ctx* ctx, const Geom& g, const float* guide, const float* taps,
-                       double bw, float* rs, float* kcache = nullptr) {
+                       double bw, float* rs, float* kcache = nullptr, int kc_rows = 0) {
   const Window w = full_window(g);
   float* part = ctx->partial.as<float>();
-  int rc = run_sweep(ctx, g, w, 1, guide, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
-                     taps, bw, true, part, kcache ? MODE_STORE : MODE_RECOMPUTE, kcache);
+  int rc = run_sweep_kc(ctx, g, 1, guide, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
+                        taps, bw, part, MODE_STORE, kcache, kc_rows);
   if (rc) return rc;
   FixIO io{};
   io.rs = rs;
@@ -963,14 +995,14 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   float* part = ctx->partial.as<float>();
   const Window w = full_window(g);
   float* kc = nullptr;
-  const size_t kcf = kcache_floats(g, g.tiles_y);
-  if (kcache_fits(ctx, kcf, ctx->kcache.bytes)) {
-    if ((rc = ctx->kcache.ensure(kcf * sizeof(float)))) return rc;
+  const int kc_rows = kcache_rows(ctx, g, ctx->kcache.bytes);
+  if (kc_rows > 0) {
+    if ((rc = ctx->kcache.ensure(kcache_floats(g, kc_rows) * sizeof(float)))) return rc;
     kc = ctx->kcache.as<float>();
   }
-  if ((rc = mass_and_rs(ctx, g, guide, taps, bandwidth, rs, kc))) return rc;
-  if ((rc = run_sweep(ctx, g, w, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps,
-                      bandwidth, true, part, kc ? MODE_CACHED : MODE_RECOMPUTE, kc)))
+  if ((rc = mass_and_rs(ctx, g, guide, taps, bandwidth, rs, kc, kc_rows))) return rc;
+  if ((rc = run_sweep_kc(ctx, g, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps,
+                         bandwidth, part, MODE_CACHED, kc, kc_rows)))
     return rc;
   PNP_CUDA(cudaMemsetAsync(ctx->mbits.ptr, 0, batch * sizeof(unsigned), ctx->stream));
   FixIO io{};
@@ -1026,9 +1058,9 @@ int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int 
   float* part = ctx->partial.as<float>();
   const Window w = full_window(g);
   float* kc = nullptr;
-  const size_t kcf = kcache_floats(g, g.tiles_y);
-  if (kcache_fits(ctx, kcf, ctx->kcache.bytes)) {
-    if ((rc = ctx->kcache.ensure(kcf * sizeof(float)))) return rc;
+  const int kc_rows = kcache_rows(ctx, g, ctx->kcache.bytes);
+  if (kc_rows > 0) {
+    if ((rc = ctx->kcache.ensure(kcache_floats(g, kc_rows) * sizeof(float)))) return rc;
     kc = ctx->kcache.as<float>();
   }
   std::vector<int> tend(nbands), need(nbands);
@@ -1040,11 +1072,18 @@ int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int 
   for (int j = 0; j < nbands; ++j) {
     if (events[j]) PNP_CUDA(cudaStreamWaitEvent(ctx->stream, (cudaEvent_t)events[j], 0));
     const int t1 = tend[j];
-    if (t1 > t0) {
-      Window wj{0, H, t0, t1 - t0, 0, t0, g.tiles_y, 0, H};
+    // cached tile rows [t0, min(t1, kc_rows)) store, the rest recompute
+    const int tm = kc ? (t1 < kc_rows ? t1 : (t0 > kc_rows ? t0 : kc_rows)) : t0;
+    if (tm > t0) {
+      Window wj{0, H, t0, tm - t0, 0, t0, g.tiles_y, 0, H};
       if ((rc = run_sweep(ctx, g, wj, 1, x, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
-                          taps, bandwidth, true, part, kc ? MODE_STORE : MODE_RECOMPUTE,
-                          kc ? kc + (size_t)t0 * kc_row : nullptr)))
+                          taps, bandwidth, true, part, MODE_STORE, kc + (size_t)t0 * kc_row)))
+        return rc;
+    }
+    if (t1 > tm) {
+      Window wj{0, H, tm, t1 - tm, 0, tm, g.tiles_y, 0, H};
+      if ((rc = run_sweep(ctx, g, wj, 1, x, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
+                          taps, bandwidth, true, part, MODE_RECOMPUTE)))
         return rc;
     }
     t0 = t1;
@@ -1054,8 +1093,8 @@ int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int 
     io.rs = rs;
     if ((rc = run_fixup<FIX_RS>(ctx, g, w, 1, part, io))) return rc;
   }
-  if ((rc = run_sweep(ctx, g, w, 2, x, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps, bandwidth,
-                      true, part, kc ? MODE_CACHED : MODE_RECOMPUTE, kc)))
+  if ((rc = run_sweep_kc(ctx, g, 2, x, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps, bandwidth,
+                         part, MODE_CACHED, kc, kc_rows)))
     return rc;
   PNP_CUDA(cudaMemsetAsync(ctx->mbits.ptr, 0, sizeof(unsigned), ctx->stream));
   FixIO io{};
@@ -1103,20 +1142,23 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   e = cudaMemcpyAsync(fz->guide, guide, n * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemcpyAsync(guide)"));
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return bail(rc);
-  const size_t kcf = kcache_floats(g, g.tiles_y);
-  if (kcache_fits(ctx, kcf, 0)) {
-    e = pool_alloc(ctx, (void**)&fz->kcache, kcf * sizeof(float));
+  const int kc_rows = kcache_rows(ctx, g, 0);
+  if (kc_rows > 0) {
+    e = pool_alloc(ctx, (void**)&fz->kcache, kcache_floats(g, kc_rows) * sizeof(float));
     if (e != cudaSuccess) {
       cudaGetLastError();
       fz->kcache = nullptr;  // not fatal: recompute instead
+    } else {
+      fz->kc_rows = kc_rows;
     }
   }
-  if ((rc = mass_and_rs(ctx, g, fz->guide, taps, bandwidth, fz->rs, fz->kcache))) return bail(rc);
+  if ((rc = mass_and_rs(ctx, g, fz->guide, taps, bandwidth, fz->rs, fz->kcache, fz->kc_rows)))
+    return bail(rc);
   const Window w = full_window(g);
   float* part = ctx->partial.as<float>();
-  if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, nullptr},
-                      ChanSpec{nullptr, nullptr}, taps, bandwidth, true, part,
-                      fz->kcache ? MODE_CACHED : MODE_RECOMPUTE, fz->kcache)))
+  if ((rc = run_sweep_kc(ctx, g, 1, fz->guide, ChanSpec{fz->rs, nullptr},
+                         ChanSpec{nullptr, nullptr}, taps, bandwidth, part, MODE_CACHED,
+                         fz->kcache, fz->kc_rows)))
     return bail(rc);
   e = cudaMemsetAsync(ctx->mbits.ptr, 0, batch * sizeof(unsigned), ctx->stream);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemsetAsync"));
@@ -1144,9 +1186,8 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
   if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   const Window w = full_window(g);
   float* part = ctx->partial.as<float>();
-  if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, x}, ChanSpec{nullptr, nullptr},
-                      fz->taps, fz->bw, true, part, fz->kcache ? MODE_CACHED : MODE_RECOMPUTE,
-                      fz->kcache)))
+  if ((rc = run_sweep_kc(ctx, g, 1, fz->guide, ChanSpec{fz->rs, x}, ChanSpec{nullptr, nullptr},
+                         fz->taps, fz->bw, part, MODE_CACHED, fz->kcache, fz->kc_rows)))
     return rc;
   FixIO io{};
   io.rs = fz->rs;
@@ -1174,9 +1215,8 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
   const size_t nblk = (size_t)g.tiles_x * rows;
   if ((rc = ctx->stats.ensure((size_t)g.B * nblk * 3 * sizeof(double)))) return rc;
   float* part = ctx->partial.as<float>();
-  if ((rc = run_sweep(ctx, g, w, 1, fz->guide, ChanSpec{fz->rs, z}, ChanSpec{nullptr, nullptr},
-                      fz->taps, fz->bw, true, part, fz->kcache ? MODE_CACHED : MODE_RECOMPUTE,
-                      fz->kcache)))
+  if ((rc = run_sweep_kc(ctx, g, 1, fz->guide, ChanSpec{fz->rs, z}, ChanSpec{nullptr, nullptr},
+                         fz->taps, fz->bw, part, MODE_CACHED, fz->kcache, fz->kc_rows)))
     return rc;
   FixIO io{};
   io.rs = fz->rs;

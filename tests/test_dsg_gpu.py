@@ -184,9 +184,24 @@ def test_k_cache_is_bitwise_neutral(pnp, rng):
         fb = pnp.freeze_guide(g, p)
         assert pnp._lib.lib.pnp_frozen_cached(fb._h) == 0
         yb = fb.apply(x)
+        # a budget for 2 of the 5 tile rows: those cached, the rest recomputed
+        row_bytes = 220 * 2 * 26 * 4 * 64 * 4
+        profiling.set_cache_limit(int(2.5 * row_bytes))
+        c = pnp.dsg_nlm_denoise(x, p, guide=g)
+        fc = pnp.freeze_guide(g, p)
+        assert pnp._lib.lib.pnp_frozen_cached(fc._h) == 1
+        yc = fc.apply(x)
+        tall = torch.tensor(rng.random((700, 130)), dtype=torch.float32).pin_memory()
+        st = pnp.DenoiseStream(p, (700, 130))
+        profiling.set_cache_limit(int(6.5 * 220 * 26 * 3 * 64 * 4))  # 6 of 27 tile rows
+        sc = st.run([tall])[0]
+        profiling.set_cache_limit(0)
+        sd = st.run([tall])[0]
     finally:
         profiling.set_cache_limit(None)
     assert torch.equal(a, b) and torch.equal(ya, yb) and torch.equal(a, ya)
+    assert torch.equal(a, c) and torch.equal(ya, yc)
+    assert torch.equal(sc, sd)
 
 
 def test_denoise_stream_pipeline(pnp, rng):
