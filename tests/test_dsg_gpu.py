@@ -293,3 +293,24 @@ def test_dense_weights_match_reference_golden(pnp, golden_extra, rng):
     assert np.abs((W @ x.ravel()).reshape(9, 11) - pnp.dsg_nlm_denoise(x, p, guide=guide)).max() < 1e-4
     with pytest.raises(ValueError):
         pnp.build_dense_weights(rng.random((65, 64)), p)
+
+
+def test_large_numpy_inputs_take_the_pinned_path(pnp, rng):
+    """>= 1 M-element numpy arrays go through pinned staging with threaded
+    casts: same values as the tensor path, float64 out, non-finite rejected."""
+    p = pnp.PatchParams(5, 4, 0.2, 1.5)
+    img = rng.random((1100, 1000))
+    out = pnp.dsg_nlm_denoise(img, p)
+    ref = pnp.dsg_nlm_denoise(torch.tensor(img, dtype=torch.float32, device="cuda"), p)
+    assert out.dtype == np.float64 and out.flags.writeable
+    assert np.array_equal(out, ref.cpu().numpy().astype(np.float64))
+    ro = img.copy()
+    ro.setflags(write=False)
+    assert np.array_equal(pnp.dsg_nlm_denoise(ro, p), out)
+    bad = img.copy()
+    bad[700, 3] = np.inf
+    with pytest.raises(ValueError):
+        pnp.dsg_nlm_denoise(bad, p)
+    bad[700, 3] = np.nan
+    with pytest.raises(ValueError):
+        pnp.dsg_nlm_denoise(bad, p)
