@@ -436,6 +436,24 @@ def admm_extras(pnp, dev):
 
     from paper_1901_06110_b200 import synth
     res = {}
+    # config 1 (the reference's CPU-runnable case): one 256^2 image, radius 5,
+    # patch 5 Gaussian sigma_p 1.5, h = 10/255, noise 20/255; W x and row sums d
+    img1 = torch.from_numpy(synth.noisy(synth.scene(256, 256, 1), 20 / 255, 2).astype(np.float32))
+    img1 = img1.to(dev)
+    p1 = pnp.PatchParams.from_h(5, 5, 10 / 255, 1.5)
+    for _ in range(3):
+        pnp.dsg_nlm_denoise(img1, p1, return_aux=True)
+    torch.cuda.synchronize()
+    e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_a.record()
+    for _ in range(50):
+        pnp.dsg_nlm_denoise(img1, p1, return_aux=True)
+    e_b.record()
+    torch.cuda.synchronize()
+    ms1 = e_a.elapsed_time(e_b) / 50
+    res["config1_denoise_256"] = {"ms_per_denoise": ms1,
+                                  "gpixel_offsets_per_s": 256 * 256 * 121 / (ms1 * 1e-3) / 1e9,
+                                  "reference_cpu_note": "survey: pnprestore 0.31 s on 1 CPU core"}
     # config 2: 512^2 SR, blur 9x9 sigma 1 symmetric, x2, noise 5/255, 30 its, frozen bicubic guide
     truth = synth.scene(512, 512, 2).astype(np.float32)
     op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
