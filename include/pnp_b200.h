@@ -49,8 +49,11 @@ int pnp_ctx_synchronize(pnp_ctx* ctx);
 /* k cache: the pair weights hat*k of sweep A are kept in HBM (half window,
  * 4 B per pixel and offset pair) when they fit, so sweep B / frozen applies
  * stream them instead of recomputing the patch filter; results are bitwise
- * identical either way.  bytes = 0 disables, < 0 = no limit (default; a call
- * still falls back to recompute when free HBM is short). */
+ * identical either way.  bytes = 0 disables, < 0 = no limit (default).  When
+ * the whole cache does not fit (the budget or free HBM less 4 GiB), the tile
+ * rows that fit are cached and the rest recomputed (at least 1/8 of them, else
+ * none).  Frozen guides allocate theirs from the device's stream-ordered pool
+ * (cudaMallocAsync) and free it on the stream of their last use. */
 int pnp_ctx_set_cache_limit(pnp_ctx* ctx, int64_t bytes);
 int pnp_frozen_cached(const pnp_frozen* fz);
 /* Per-launch CUDA-event timing on the context stream (off by default).
