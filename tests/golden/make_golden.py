@@ -376,9 +376,42 @@ def cli_goldens():
     print("cli fixtures", sorted(p.name for p in out.iterdir()))
 
 
+def helper_goldens():
+    """The reference's distance-engine helpers on small seeded inputs:
+    pad_symmetric, integral_image, box_sum, patch_distance_map (both methods),
+    nlm_kernel, build_dense_weights (helpers.npz)."""
+    from pnprestore import image as rimg
+    rng = np.random.default_rng(77)
+    out = {}
+    g = rng.random((14, 17))
+    out["g"] = g
+    for m in (0, 2, 9):
+        out[f"pad{m}"] = rimg.pad_symmetric(g, m)
+    ii = rimg.integral_image(g)
+    out["ii"] = ii
+    out["box"] = np.array([rimg.box_sum(ii, t, l, sz) for t, l, sz in
+                           ((0, 0, 3), (2, 5, 7), (10, 12, 4))])
+    p = ref.PatchParams(5, 3, 0.21)
+    offs = [(0, 0), (2, -1), (-3, 3), (1, 2)]
+    out["offs"] = np.array(offs)
+    for i, t in enumerate(offs):
+        out[f"dmap{i}"] = rden.patch_distance_map(g, t, p)
+        out[f"dmap_direct{i}"] = rden.patch_distance_map(g, t, p, method="direct")
+    pairs = [((0, 0), (13, 16)), ((4, 5), (6, 9)), ((7, 7), (7, 7)), ((13, 0), (0, 16))]
+    out["pairs"] = np.array([[a[0], a[1], b[0], b[1]] for a, b in pairs])
+    out["nlmk"] = np.array([ref.nlm_kernel(g, a, b, p) for a, b in pairs])
+    gw = rng.random((6, 7))
+    out["gw"] = gw
+    out["W"] = ref.build_dense_weights(gw, ref.PatchParams(3, 2, 0.25))
+    np.savez_compressed(HERE / "helpers.npz", **out)
+    print("helpers", sorted(out))
+
+
 if __name__ == "__main__":
     if "--cg" in sys.argv:   # only the CG / standard-ADMM fixtures
         cg_goldens()
+    elif "--helpers" in sys.argv:
+        helper_goldens()
     elif "--io" in sys.argv:
         io_goldens()
     elif "--cli" in sys.argv:
@@ -388,3 +421,4 @@ if __name__ == "__main__":
         cg_goldens()
         io_goldens()
         cli_goldens()
+        helper_goldens()

@@ -314,3 +314,29 @@ def test_large_numpy_inputs_take_the_pinned_path(pnp, rng):
     bad[700, 3] = np.nan
     with pytest.raises(ValueError):
         pnp.dsg_nlm_denoise(bad, p)
+
+
+def test_helpers_match_reference_goldens(pnp):
+    """Distance-engine helpers against the real reference's outputs
+    (tests/golden/helpers.npz, make_golden.py --helpers): pad / SAT / box sums
+    and the direct distance maps bitwise, the SAT-based maps and nlm_kernel to
+    the reference's own fast-vs-direct agreement, dense W to 1e-12."""
+    from conftest import load_golden
+    h = load_golden("helpers.npz")
+    g = h["g"]
+    for m in (0, 2, 9):
+        assert np.array_equal(pnp.pad_symmetric(g, m), h[f"pad{m}"])
+    ii = pnp.integral_image(g)
+    assert np.array_equal(ii, h["ii"])
+    boxes = [pnp.box_sum(ii, t, l, sz) for t, l, sz in ((0, 0, 3), (2, 5, 7), (10, 12, 4))]
+    assert np.array_equal(np.array(boxes), h["box"])
+    p = pnp.PatchParams(5, 3, 0.21)
+    for i, t in enumerate(h["offs"]):
+        t = (int(t[0]), int(t[1]))
+        assert np.array_equal(pnp.patch_distance_map(g, t, p, method="direct"), h[f"dmap_direct{i}"])
+        assert np.abs(pnp.patch_distance_map(g, t, p) - h[f"dmap{i}"]).max() < 1e-9
+    for (sy, sx, ry, rx), want in zip(h["pairs"], h["nlmk"]):
+        got = pnp.nlm_kernel(g, (int(sy), int(sx)), (int(ry), int(rx)), p)
+        assert got == pytest.approx(float(want), abs=1e-14)
+    W = pnp.build_dense_weights(h["gw"], pnp.PatchParams(3, 2, 0.25))
+    assert np.abs(W - h["W"]).max() < 1e-12
