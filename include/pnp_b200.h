@@ -93,6 +93,11 @@ int pnp_frozen_destroy(pnp_frozen* fz);
 int pnp_frozen_alpha(const pnp_frozen* fz, float* alpha_host);
 int pnp_frozen_export(pnp_ctx* ctx, const pnp_frozen* fz, float* guide_out, float* d_out);
 int pnp_frozen_shape(const pnp_frozen* fz, int* batch, int* H, int* W, int* R, int* P);
+/* Residency of the handle's pair-weight (k) cache: tile rows per image it
+ * covers (from the top; the rest recompute on apply), tile rows per image and
+ * its bytes.  No reference counterpart (the reference recomputes weights). */
+int pnp_frozen_cache(const pnp_frozen* fz, int* rows_cached, int* tile_rows,
+                     unsigned long long* bytes);
 
 /* nlm_denoise(image, params, guide) — denoise.py:254-269 (row-stochastic). */
 int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out,

@@ -51,6 +51,7 @@ _SIGS = {
     "pnp_frozen_alpha": (i32, [vp, fptr]),
     "pnp_frozen_export": (i32, [vp, vp, vp, vp]),
     "pnp_frozen_shape": (i32, [vp] + [C.POINTER(i32)] * 5),
+    "pnp_frozen_cache": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(C.c_ulonglong)]),
     "pnp_nlm_denoise": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64]),
     "pnp_tile_height": (i32, [i32]),
     "pnp_dsg_groups": (i32, [i32, i32, i32, i32]),

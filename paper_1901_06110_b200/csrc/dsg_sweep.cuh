@@ -48,6 +48,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "pnp_pdl.cuh"
+
 namespace pnp {
 
 constexpr int kTW = 64;        // tile width (output columns)
@@ -260,6 +262,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   constexpr int YC = K::YC, YR = K::YR, AR = K::AR;
   static_assert(kTW / SEG == kThreads / 32, "one phase-1 segment per warp");
   static_assert(KY % 2 == 0, "offsets are processed in packed pairs");
+  pdl_begin();
   extern __shared__ float smem[];
   float* Gs = smem;
   float* Hs = smem + K::OFF_H;

@@ -189,11 +189,15 @@ __device__ __forceinline__ float ldg_pred(const float* p, bool on) {
 // large (small images split the offsets into many groups).  The epilogue's
 // per-pixel inputs are loaded up front so their latency hides under the sums.
 #ifndef PNP_FIXGB
-#define PNP_FIXGB 4
+#define PNP_FIXGB 2
+#endif
+#ifndef PNP_FIXLB
+#define PNP_FIXLB 4  // min resident CTAs per SM (register cap)
 #endif
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) dsg_fixup_px_kernel(const FixGeo f, const FixIO io) {
+__global__ void __launch_bounds__(256, PNP_FIXLB) dsg_fixup_px_kernel(const FixGeo f, const FixIO io) {
+  pdl_begin();
   constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
   constexpr int kFixGB = C == 1 ? PNP_FIXGB : PNP_FIXGB / 2;  // offset groups per batch of loads
   const int b = blockIdx.z;
@@ -333,6 +337,7 @@ constexpr int kFixRows = 8;  // rows per thread (TH <= 32, 4 row phases)
 
 template <int MODE>
 __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, const FixIO io) {
+  pdl_begin();
   constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
   const int b = blockIdx.z;
   const int TH = f.TH, R = f.R, W = f.W;
@@ -453,6 +458,7 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
 __global__ void dsg_finalize_kernel(const float* kx, const float* d, const unsigned* mbits,
                                     const float* x, float* out, float* alpha_out, int y0,
                                     int nrows, int W, int buf_r0, int buf_rows) {
+  pdl_begin();
   const int b = blockIdx.y;
   const float m = __uint_as_float(mbits[b]);
   const float inv_m = __frcp_rn(m);
@@ -465,6 +471,7 @@ __global__ void dsg_finalize_kernel(const float* kx, const float* d, const unsig
 }
 
 __global__ void dsg_alpha_kernel(const unsigned* mbits, float* mv, int B) {
+  pdl_begin();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) {
     const float m = __uint_as_float(mbits[b]);
@@ -812,10 +819,10 @@ static int run_fixup(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   ProfScope prof(ctx, PROF_FIXUP);
   if (!fixup_px(g)) {  // same summation order either way
     dim3 grid(g.tiles_x, tr_last - tr_first + 1, g.B);
-    dsg_fixup_tile_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
+    PNP_CUDA(launch_pdl(dsg_fixup_tile_kernel<MODE>, grid, dim3(256), 0, ctx->stream, f, io));
   } else {
     dim3 grid(g.tiles_x, (tr_last - tr_first + 1) * ((g.TH + 3) / 4), g.B);
-    dsg_fixup_px_kernel<MODE><<<grid, 256, 0, ctx->stream>>>(f, io);
+    PNP_CUDA(launch_pdl(dsg_fixup_px_kernel<MODE>, grid, dim3(256), 0, ctx->stream, f, io));
   }
   PNP_LAUNCH_CHECK("dsg_fixup_kernel");
   return PNP_OK;
@@ -827,8 +834,8 @@ static int run_finalize(pnp_ctx* ctx, const Geom& g, const Window& w, const floa
   const size_t npix = (size_t)w.nrows * g.W;
   dim3 grid((unsigned)((npix + 255) / 256), g.B);
   ProfScope prof(ctx, PROF_FIXUP);
-  dsg_finalize_kernel<<<grid, 256, 0, ctx->stream>>>(kx, d, mbits, x, out, alpha_out, w.y0,
-                                                     w.nrows, g.W, w.buf_r0, w.buf_rows);
+  PNP_CUDA(launch_pdl(dsg_finalize_kernel, grid, dim3(256), 0, ctx->stream, kx, d, mbits, x, out,
+                      alpha_out, w.y0, w.nrows, g.W, w.buf_r0, w.buf_rows));
   PNP_LAUNCH_CHECK("dsg_finalize_kernel");
   return PNP_OK;
 }
@@ -1125,6 +1132,7 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   fz->R = R;
   fz->P = P;
   fz->bw = bandwidth;
+  fz->tiles_y = g.tiles_y;
   for (int i = 0; i < P; ++i) fz->taps[i] = taps[i];
   fz->stream = ctx->stream;
   cudaError_t e = pool_alloc(ctx, (void**)&fz->guide, n * sizeof(float));
@@ -1150,6 +1158,7 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
       fz->kcache = nullptr;  // not fatal: recompute instead
     } else {
       fz->kc_rows = kc_rows;
+      fz->kc_bytes = kcache_floats(g, kc_rows) * sizeof(float);
     }
   }
   if ((rc = mass_and_rs(ctx, g, fz->guide, taps, bandwidth, fz->rs, fz->kcache, fz->kc_rows)))
@@ -1167,9 +1176,8 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   io.d = fz->d;
   io.mbits = ctx->mbits.as<unsigned>();
   if ((rc = run_fixup<FIX_D>(ctx, g, w, 1, part, io))) return bail(rc);
-  dsg_alpha_kernel<<<(batch + 127) / 128, 128, 0, ctx->stream>>>(ctx->mbits.as<unsigned>(),
-                                                                 fz->mv, batch);
-  e = cudaGetLastError();
+  e = launch_pdl(dsg_alpha_kernel, dim3((batch + 127) / 128), dim3(128), 0, ctx->stream,
+                 ctx->mbits.as<unsigned>(), fz->mv, batch);
   if (e != cudaSuccess) return bail(cuda_fail(e, "dsg_alpha_kernel"));
   *out = fz;
   return PNP_OK;
@@ -1275,6 +1283,15 @@ int pnp_frozen_shape(const pnp_frozen* fz, int* batch, int* H, int* W, int* R, i
   if (W) *W = fz->W;
   if (R) *R = fz->R;
   if (P) *P = fz->P;
+  return PNP_OK;
+}
+
+int pnp_frozen_cache(const pnp_frozen* fz, int* rows_cached, int* tile_rows,
+                     unsigned long long* bytes) {
+  if (!fz) return fail(PNP_EINVAL, "null argument");
+  if (rows_cached) *rows_cached = fz->kcache ? fz->kc_rows : 0;
+  if (tile_rows) *tile_rows = fz->tiles_y;
+  if (bytes) *bytes = fz->kcache ? (unsigned long long)fz->kc_bytes : 0ull;
   return PNP_OK;
 }
 

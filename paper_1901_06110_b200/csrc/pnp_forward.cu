@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "pnp_internal.h"
+#include "pnp_pdl.cuh"
 #include "pnp_reduce.cuh"
 
 namespace pnp {
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(256)
 sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, float* __restrict__ r,
                    const SrWin win, int W, int k, int rad, int sym, const Taps taps,
                    double* partial, const CgState* skip = nullptr) {
+  pdl_begin();
   extern __shared__ float sm[];
   const int H = win.Hg, w = W / k, b = blockIdx.z;
   if (skip && skip[b].done) return;  // CG: image already converged
@@ -205,6 +207,7 @@ __global__ void __launch_bounds__(256)
 sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const SrWin win, int W,
                   int k, int rad, int sym, const Taps taps, const XUpd q, const CgEpi cg,
                   const RedEpi red = RedEpi{}) {
+  pdl_begin();
   extern __shared__ float sm[];
   const int H = win.Hg, w = W / k, b = blockIdx.z;
   if (MODE == ADJ_CG && cg.skip && cg.skip[b].done) return;
@@ -320,6 +323,7 @@ __global__ void __launch_bounds__(256)
 qis_grad_kernel(const float* __restrict__ x, const float* __restrict__ ones,
                 const float* __restrict__ zeros, float* __restrict__ grad, size_t n,
                 double gk, double floor_, double* partial, const XUpd q) {
+  pdl_begin();
   const int b = blockIdx.y;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   double term = 0.0;
@@ -734,8 +738,9 @@ static int sr_grad_impl(pnp_ctx* ctx, const float* x, const float* yobs, float* 
   PNP_CUDA(sr_smem_attr(rs, as));
   {
     ProfScope prof_(ctx, PROF_FORWARD);
-    sr_residual_kernel<<<rg, 256, rs, ctx->stream>>>(x, yobs, r, res_full(H, factor), W, factor,
-                                                     radius, boundary, t, part);
+    PNP_CUDA(launch_pdl(sr_residual_kernel, rg, dim3(256), rs, ctx->stream, x, yobs, r,
+                        res_full(H, factor), W, factor, radius, boundary, t, part,
+                        (const CgState*)nullptr));
   }
   PNP_LAUNCH_CHECK("sr_residual_kernel");
   // the data term 0.5 ||r||^2 is reduced by the adjoint kernel's first CTA
@@ -743,11 +748,13 @@ static int sr_grad_impl(pnp_ctx* ctx, const float* x, const float* yobs, float* 
   {
     ProfScope prof_(ctx, PROF_FORWARD);
     if (xu)
-      sr_adjoint_kernel<ADJ_XUPD><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, nullptr, adj_full(H, factor), W, factor, radius, boundary, t, *xu, CgEpi{}, red);
+      PNP_CUDA(launch_pdl(sr_adjoint_kernel<ADJ_XUPD>, sr_adj_grid(H, W, batch), dim3(256), as,
+                          ctx->stream, (const float*)r, (float*)nullptr, adj_full(H, factor), W,
+                          factor, radius, boundary, t, *xu, CgEpi{}, red));
     else
-      sr_adjoint_kernel<ADJ_PLAIN><<<sr_adj_grid(H, W, batch), 256, as, ctx->stream>>>(
-          r, grad, adj_full(H, factor), W, factor, radius, boundary, t, XUpd{}, CgEpi{}, red);
+      PNP_CUDA(launch_pdl(sr_adjoint_kernel<ADJ_PLAIN>, sr_adj_grid(H, W, batch), dim3(256), as,
+                          ctx->stream, (const float*)r, grad, adj_full(H, factor), W, factor,
+                          radius, boundary, t, XUpd{}, CgEpi{}, red));
   }
   PNP_LAUNCH_CHECK("sr_adjoint_kernel");
   return PNP_OK;
@@ -769,11 +776,12 @@ static int qis_grad_impl(pnp_ctx* ctx, const float* x, const float* ones, const 
   {
     ProfScope prof_(ctx, PROF_FORWARD);
     if (xu)
-      qis_grad_kernel<true><<<dim3(nblk, batch), 256, 0, ctx->stream>>>(
-          x, ones, zeros, nullptr, (size_t)n, gain_over_K, floor_, part, *xu);
+      PNP_CUDA(launch_pdl(qis_grad_kernel<true>, dim3(nblk, batch), dim3(256), 0, ctx->stream, x,
+                          ones, zeros, (float*)nullptr, (size_t)n, gain_over_K, floor_, part,
+                          *xu));
     else
-      qis_grad_kernel<false><<<dim3(nblk, batch), 256, 0, ctx->stream>>>(
-          x, ones, zeros, grad, (size_t)n, gain_over_K, floor_, part, XUpd{});
+      PNP_CUDA(launch_pdl(qis_grad_kernel<false>, dim3(nblk, batch), dim3(256), 0, ctx->stream,
+                          x, ones, zeros, grad, (size_t)n, gain_over_K, floor_, part, XUpd{}));
   }
   PNP_LAUNCH_CHECK("qis_grad_kernel");
   if (data_out) {
@@ -1205,12 +1213,11 @@ int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, con
   PNP_CUDA(sr_smem_attr(rsm, asm_));
   const cudaStream_t main = ctx->stream, side = ctx->side;
   auto residual = [&](cudaStream_t st) {
-    sr_residual_kernel<<<rg, 256, rsm, st>>>(x, y, r, res_full(H, factor), W, factor, radius,
-                                             boundary, t, part);
+    return launch_pdl(sr_residual_kernel, rg, dim3(256), rsm, st, x, y, r, res_full(H, factor), W,
+                      factor, radius, boundary, t, part, (const CgState*)nullptr);
   };
   // the first iteration's residual on the main stream (x is x_{k0-1})
-  residual(main);
-  PNP_LAUNCH_CHECK("sr_residual_kernel");
+  PNP_CUDA(residual(main));
   float* vcur = v0;
   float* vnext = v1;
   int cur = 0;
@@ -1220,15 +1227,13 @@ int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, con
     if (k > k0) PNP_CUDA(cudaStreamWaitEvent(main, ctx->ev_res, 0));
     const XUpd q = make_xupd(x, vcur, u, z, mu, alpha, rho, lo, hi, fk);
     const RedEpi red{part, obj, 0.5, nblk, batch};
-    sr_adjoint_kernel<ADJ_XUPD><<<ag, 256, asm_, main>>>(r, nullptr, adj_full(H, factor), W,
-                                                         factor, radius, boundary, t, q,
-                                                         CgEpi{}, red);
-    PNP_LAUNCH_CHECK("sr_adjoint_kernel");
+    PNP_CUDA(launch_pdl(sr_adjoint_kernel<ADJ_XUPD>, ag, dim3(256), asm_, main, (const float*)r,
+                        (float*)nullptr, adj_full(H, factor), W, factor, radius, boundary, t, q,
+                        CgEpi{}, red));
     if (k < k1) {  // next iteration's residual overlaps this denoise
       PNP_CUDA(cudaEventRecord(ctx->ev_x, main));
       PNP_CUDA(cudaStreamWaitEvent(side, ctx->ev_x, 0));
-      residual(side);
-      PNP_LAUNCH_CHECK("sr_residual_kernel");
+      PNP_CUDA(residual(side));
       PNP_CUDA(cudaEventRecord(ctx->ev_res, side));
     }
     if ((rc = pnp_dsg_apply_admm(ctx, fz, z, vnext, u, x, vcur, gt, rho,

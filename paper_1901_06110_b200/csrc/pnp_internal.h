@@ -130,7 +130,9 @@ struct pnp_frozen {
   float* d = nullptr;      // B*H*W
   float* mv = nullptr;     // B floats: m; then B floats: 1/m
   float* kcache = nullptr; // pair weights (null: recompute on apply)
-  int kc_rows = 0;         // tile rows (per image, from the top) the k cache covers
+  int kc_rows = 0;
+  int tiles_y = 0;         // tile rows per image (kc_rows == tiles_y: fully cached)
+  size_t kc_bytes = 0;         // tile rows (per image, from the top) the k cache covers
   // buffers come from the device's stream-ordered pool (cudaMallocAsync) and
   // go back to it on the stream of the handle's last use: no device-wide
   // synchronization and no page-mapping cost when ADMM runs re-freeze

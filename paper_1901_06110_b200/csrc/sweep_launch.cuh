@@ -61,8 +61,7 @@ cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaSt
   memcpy(tab.c, t.ch, sizeof(Chunk) * t.nch);
   memcpy(tab.grp, t.grp, sizeof(int) * (t.ng + 1));
   if (a.cg <= 1) {
-    dsg_sweep_kernel<P, RB, C, MODE><<<grid, kThreads, smem, st>>>(a, tab);
-    return cudaGetLastError();
+    return launch_pdl(dsg_sweep_kernel<P, RB, C, MODE>, grid, dim3(kThreads), smem, st, a, tab);
   }
   // a tile's offset groups as one thread-block cluster (grid.y = NG, a
   // multiple of cg): they reduce their planes on chip (dsg_sweep.cuh)

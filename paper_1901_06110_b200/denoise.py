@@ -244,6 +244,13 @@ class FrozenGuide:
         L.call("pnp_frozen_alpha", self._h, out)
         return np.array(out[:], dtype=np.float64)
 
+    def cache_info(self) -> dict:
+        """Pair-weight cache residency: tile rows per image cached (the rest
+        recompute their weights on every apply), tile rows, bytes."""
+        rows, total, nbytes = C.c_int(), C.c_int(), C.c_ulonglong()
+        L.call("pnp_frozen_cache", self._h, C.byref(rows), C.byref(total), C.byref(nbytes))
+        return {"rows_cached": rows.value, "tile_rows": total.value, "bytes": nbytes.value}
+
     def row_sums(self) -> torch.Tensor:
         d = torch.empty(self._shape, dtype=torch.float32, device=torch.device("cuda", self._dev))
         L.call("pnp_frozen_export", L.context(self._dev), self._h, None, L.ptr(d))

@@ -178,11 +178,14 @@ def test_k_cache_is_bitwise_neutral(pnp, rng):
         a = pnp.dsg_nlm_denoise(x, p, guide=g)
         fa = pnp.freeze_guide(g, p)
         assert pnp._lib.lib.pnp_frozen_cached(fa._h) == 1
+        info = fa.cache_info()
+        assert info["rows_cached"] == info["tile_rows"] == 5 and info["bytes"] > 0
         ya = fa.apply(x)
         profiling.set_cache_limit(0)
         b = pnp.dsg_nlm_denoise(x, p, guide=g)
         fb = pnp.freeze_guide(g, p)
         assert pnp._lib.lib.pnp_frozen_cached(fb._h) == 0
+        assert fb.cache_info() == {"rows_cached": 0, "tile_rows": 5, "bytes": 0}
         yb = fb.apply(x)
         # a budget for 2 of the 5 tile rows: those cached, the rest recomputed
         row_bytes = 220 * 2 * 26 * 4 * 64 * 4
@@ -190,6 +193,7 @@ def test_k_cache_is_bitwise_neutral(pnp, rng):
         c = pnp.dsg_nlm_denoise(x, p, guide=g)
         fc = pnp.freeze_guide(g, p)
         assert pnp._lib.lib.pnp_frozen_cached(fc._h) == 1
+        assert fc.cache_info()["rows_cached"] == 2
         yc = fc.apply(x)
         tall = torch.tensor(rng.random((700, 130)), dtype=torch.float32).pin_memory()
         st = pnp.DenoiseStream(p, (700, 130))
