@@ -13,6 +13,7 @@
 #include <float.h>
 #include <math.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -335,8 +336,11 @@ __global__ void __launch_bounds__(256, PNP_FIXLB) dsg_fixup_px_kernel(const FixG
 // thread keeps up to 8 independent loads in flight per block.
 constexpr int kFixRows = 8;  // rows per thread (TH <= 32, 4 row phases)
 
+// 4 resident CTAs per SM (64 registers): the fixups are latency-bound, and
+// occupancy beats keeping more rows' loads in registers (8192^2 launch list:
+// -12..-38% per mode against no register cap); FIX_NLM (two channels) at 3.
 template <int MODE>
-__global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, const FixIO io) {
+__global__ void __launch_bounds__(256, MODE == FIX_NLM ? 3 : 4) dsg_fixup_tile_kernel(const FixGeo f, const FixIO io) {
   pdl_begin();
   constexpr int C = (MODE == FIX_KXD || MODE == FIX_NLM) ? 2 : 1;
   const int b = blockIdx.z;
@@ -372,6 +376,17 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0))
                    : "memory");
     }
+  }
+
+  // per-pixel epilogue inputs of the plain modes, issued before the sums
+  constexpr bool HOIST = MODE == FIX_KXD || MODE == FIX_D;  // (FIX_APPLY: measured slower)
+  float e_rs[kFixRows];
+#pragma unroll
+  for (int k = 0; k < kFixRows; ++k) {
+    const int y = ti * TH + ly0 + 4 * k;
+    const bool ok = HOIST && ly0 + 4 * k < TH && y >= ylo && y < yhi && x < W;
+    const size_t o = ok ? (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x : 0;
+    e_rs[k] = ldg_pred(io.rs + o, ok);
   }
 
   float s[C][kFixRows];
@@ -421,13 +436,13 @@ __global__ void __launch_bounds__(256) dsg_fixup_tile_kernel(const FixGeo f, con
     } else if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
-      const float r = io.rs[o];
+      const float r = e_rs[k];
       io.kx[o] = __fmul_rn(r, s0);
       const float dv = __fmul_rn(r, s[C - 1][k]);
       io.d[o] = dv;
       dmax = fmaxf(dmax, dv);
     } else if (MODE == FIX_D) {
-      const float dv = __fmul_rn(io.rs[o], s0);
+      const float dv = __fmul_rn(e_rs[k], s0);
       io.d[o] = dv;
       dmax = fmaxf(dmax, dv);
     } else if (MODE == FIX_APPLY) {
@@ -467,6 +482,36 @@ __global__ void dsg_finalize_kernel(const float* kx, const float* d, const unsig
   if (i < (size_t)nrows * W) {
     const size_t o = (size_t)b * buf_rows * W + (size_t)(y0 - buf_r0) * W + i;
     out[o] = dsg_finish(kx[o], d[o], inv_m, x[o]);
+  }
+}
+
+// The same per pixel, four pixels per thread with 16-byte accesses (every
+// plane 16-byte aligned and W % 4 == 0); grid-stride over the window.
+__global__ void __launch_bounds__(256) dsg_finalize4_kernel(const float* kx, const float* d,
+                                                            const unsigned* mbits, const float* x,
+                                                            float* out, float* alpha_out, int y0,
+                                                            int nrows, int W, int buf_r0,
+                                                            int buf_rows) {
+  pdl_begin();
+  const int b = blockIdx.y;
+  const float m = __uint_as_float(mbits[b]);
+  const float inv_m = __frcp_rn(m);
+  if (alpha_out && blockIdx.x == 0 && threadIdx.x == 0) alpha_out[b] = m;
+  const size_t n4 = (size_t)nrows * W / 4;
+  const size_t base = ((size_t)b * buf_rows * W + (size_t)(y0 - buf_r0) * W) / 4;
+  const float4* k4 = reinterpret_cast<const float4*>(kx) + base;
+  const float4* d4 = reinterpret_cast<const float4*>(d) + base;
+  const float4* x4 = reinterpret_cast<const float4*>(x) + base;
+  float4* o4 = reinterpret_cast<float4*>(out) + base;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldcs(k4 + i), dd = __ldcs(d4 + i), xx = __ldg(x4 + i);
+    float4 r;
+    r.x = dsg_finish(a.x, dd.x, inv_m, xx.x);
+    r.y = dsg_finish(a.y, dd.y, inv_m, xx.y);
+    r.z = dsg_finish(a.z, dd.z, inv_m, xx.z);
+    r.w = dsg_finish(a.w, dd.w, inv_m, xx.w);
+    __stcs(o4 + i, r);
   }
 }
 
@@ -832,8 +877,17 @@ static int run_finalize(pnp_ctx* ctx, const Geom& g, const Window& w, const floa
                         const float* d, const unsigned* mbits, const float* x, float* out,
                         float* alpha_out) {
   const size_t npix = (size_t)w.nrows * g.W;
-  dim3 grid((unsigned)((npix + 255) / 256), g.B);
   ProfScope prof(ctx, PROF_FIXUP);
+  auto a16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  if (g.W % 4 == 0 && a16(kx) && a16(d) && a16(x) && a16(out)) {
+    const size_t n4 = npix / 4;
+    const unsigned per_img = (unsigned)std::min<size_t>((n4 + 255) / 256,
+                                                        (size_t)ctx->sms * 8 / g.B + 1);
+    PNP_CUDA(launch_pdl(dsg_finalize4_kernel, dim3(per_img, g.B), dim3(256), 0, ctx->stream, kx,
+                        d, mbits, x, out, alpha_out, w.y0, w.nrows, g.W, w.buf_r0, w.buf_rows));
+    return PNP_OK;
+  }
+  dim3 grid((unsigned)((npix + 255) / 256), g.B);
   PNP_CUDA(launch_pdl(dsg_finalize_kernel, grid, dim3(256), 0, ctx->stream, kx, d, mbits, x, out,
                       alpha_out, w.y0, w.nrows, g.W, w.buf_r0, w.buf_rows));
   PNP_LAUNCH_CHECK("dsg_finalize_kernel");
