@@ -115,6 +115,16 @@ int pnp_dsg_band_rows(int H, int W, int R, int P, int nbands, int* tile_end, int
 int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
                            const float* taps, double bandwidth, int nbands,
                            void* const* events);
+/* The same denoise driven band by band by a caller that produces the image on
+ * the host as it goes (the numpy drop-in path: cast + upload of band j+1
+ * overlaps sweep A of band j).  Call pnp_dsg_band_sweep for j = 0 .. nbands-1
+ * in order, each after the context stream is ordered behind the upload of
+ * input rows [0, rows_needed[j]); then pnp_dsg_band_finish.  Band 0 sizes the
+ * buffers and the k cache.  Guide = x.  Bitwise equal to pnp_dsg_denoise. */
+int pnp_dsg_band_sweep(pnp_ctx* ctx, const float* x, int H, int W, int R, int P,
+                       const float* taps, double bandwidth, int nbands, int j);
+int pnp_dsg_band_finish(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
+                        const float* taps, double bandwidth);
 
 /* ---- row-strip building blocks (multi-GPU sharding) ---- *
  * A rank owns global rows [y0, y1) = whole tile rows of height

@@ -138,6 +138,74 @@ def from_device(t: torch.Tensor, kind: str):
     return t.detach().to("cpu").numpy().astype(np.float64)
 
 
+class _Staging:
+    """Named grow-only pinned float32 buffers, used under one lock."""
+
+    def __init__(self):
+        self.bufs: dict = {}
+
+    def f32(self, name: str, n: int) -> torch.Tensor:
+        buf = self.bufs.get(name)
+        if buf is None or buf.numel() < n:
+            buf = self.bufs[name] = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        return buf[:n]
+
+
+_staging = _Staging()
+
+
+class staging:
+    """``with staging() as st``: exclusive use of the named pinned buffers
+    (a call's copies out of / into them complete before the block ends)."""
+
+    def __enter__(self):
+        _stage_lock.acquire()
+        return _staging
+
+    def __exit__(self, *exc):
+        _stage_lock.release()
+        return False
+
+
+_streams: dict = {}
+
+
+def copy_stream(dev: int, name: str) -> torch.cuda.Stream:
+    """A cached side stream per (device, role) for copy-engine transfers."""
+    s = _streams.get((dev, name))
+    if s is None:
+        s = _streams[(dev, name)] = torch.cuda.Stream(torch.device("cuda", dev))
+    return s
+
+
+def download64_banded(t: torch.Tensor, st: _Staging, nbands: int, res=None) -> np.ndarray:
+    """float32 device image -> float64 numpy array (``res``, else a new one):
+    row bands go down on a copy stream into pinned staging while the host
+    casts the bands that already arrived (ordered after the current stream's
+    work on ``t``)."""
+    H, W = int(t.shape[0]), int(t.shape[1])
+    dev = t.device.index
+    if res is None:
+        res = np.empty((H, W), dtype=np.float64)
+    dst = torch.from_numpy(res)
+    stage = st.f32("out", H * W).view(H, W)
+    d2h = copy_stream(dev, "d2h")
+    d2h.wait_stream(torch.cuda.current_stream(t.device))
+    rows = [(H * k // nbands, H * (k + 1) // nbands) for k in range(nbands)]
+    evs = []
+    with torch.cuda.stream(d2h):
+        for r0, r1 in rows:
+            stage[r0:r1].copy_(t[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(d2h)
+            evs.append(ev)
+    t.record_stream(d2h)
+    for (r0, r1), ev in zip(rows, evs):
+        ev.synchronize()
+        dst[r0:r1].copy_(stage[r0:r1])  # multi-threaded cast
+    return res
+
+
 def dims(t: torch.Tensor):
     """(batch, H, W) of a 2-D or 3-D tensor."""
     if t.dim() == 2:

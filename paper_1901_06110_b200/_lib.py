@@ -96,6 +96,8 @@ _SIGS = {
     "pnp_dsg_band_rows": (i32, [i32, i32, i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]),
     "pnp_dsg_denoise_banded": (i32, [vp, vp, vp, i32, i32, i32, i32, fptr, f64, i32,
                                      C.POINTER(vp)]),
+    "pnp_dsg_band_sweep": (i32, [vp, vp, i32, i32, i32, i32, fptr, f64, i32, i32]),
+    "pnp_dsg_band_finish": (i32, [vp, vp, vp, i32, i32, i32, i32, fptr, f64]),
     "pnp_admm_run": (i32, [vp, i32, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64, f64, vp,
                            i32, i32, vp, vp, vp, vp, vp, vp, f64, f64, f64, f64, f64, vp, vp, vp,
                            C.POINTER(C.c_float), C.POINTER(i32)]),

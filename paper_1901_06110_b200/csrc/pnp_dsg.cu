@@ -1098,57 +1098,81 @@ int pnp_dsg_band_rows(int H, int W, int R, int P, int nbands, int* tile_end, int
   return PNP_OK;
 }
 
-int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
-                           const float* taps, double bandwidth, int nbands,
-                           void* const* events) {
-  if (!ctx || !x || !out || !events || nbands < 1) return fail(PNP_EINVAL, "null argument");
+// Incremental banded denoise: band j's sweep A (tile rows [tile_end[j-1],
+// tile_end[j])) is enqueued by pnp_dsg_band_sweep; the caller orders the
+// context stream behind the upload of the rows it reads first.  Band 0 sizes
+// the buffers and the k cache and pins the cached tile-row count for the
+// rest of the call.  Same tiles, partial slots and k-cache runs as the
+// one-launch sweep -> same bits.
+int pnp_dsg_band_sweep(pnp_ctx* ctx, const float* x, int H, int W, int R, int P,
+                       const float* taps, double bandwidth, int nbands, int j) {
+  if (!ctx || !x || nbands < 1) return fail(PNP_EINVAL, "null argument");
   int rc = check_geometry(1, H, W, R, P, bandwidth);
   if (rc) return rc;
   if ((rc = validate_taps(taps, P))) return rc;
+  if (j < 0 || j >= nbands) return fail(PNP_EINVAL, "band index out of range");
+  if (j > 0 && ctx->band_next != j) return fail(PNP_EINVAL, "bands must be swept in order from 0");
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
   if ((rc = make_geom(ctx, 1, H, W, R, P, g))) return rc;
   if (nbands > g.tiles_y) return fail(PNP_EINVAL, "more bands than tile rows");
-  const size_t n = (size_t)H * W;
-  if ((rc = ensure_planes(ctx, n))) return rc;
-  if ((rc = ctx->mbits.ensure(sizeof(unsigned)))) return rc;
-  if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
+  if (j == 0) {
+    if ((rc = ensure_planes(ctx, (size_t)H * W))) return rc;
+    if ((rc = ctx->mbits.ensure(sizeof(unsigned)))) return rc;
+    if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
+    const int kc_rows = kcache_rows(ctx, g, ctx->kcache.bytes);
+    if (kc_rows > 0 && (rc = ctx->kcache.ensure(kcache_floats(g, kc_rows) * sizeof(float))))
+      return rc;
+    ctx->band_kc_rows = kc_rows;
+  }
+  float* part = ctx->partial.as<float>();
+  const int kc_rows = ctx->band_kc_rows;
+  float* kc = kc_rows > 0 ? ctx->kcache.as<float>() : nullptr;
+  std::vector<int> tend(nbands), need(nbands);
+  band_split(H, R, P, nbands, tend.data(), need.data());
+  const size_t kc_row = (size_t)g.tiles_x * half_window(g.R) * g.TH * kTW;
+  const int t0 = j ? tend[j - 1] : 0, t1 = tend[j];
+  // cached tile rows [t0, min(t1, kc_rows)) store, the rest recompute
+  const int tm = kc ? (t1 < kc_rows ? t1 : (t0 > kc_rows ? t0 : kc_rows)) : t0;
+  ctx->band_next = -1;
+  if (tm > t0) {
+    Window wj{0, H, t0, tm - t0, 0, t0, g.tiles_y, 0, H};
+    if ((rc = run_sweep(ctx, g, wj, 1, x, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
+                        taps, bandwidth, true, part, MODE_STORE, kc + (size_t)t0 * kc_row)))
+      return rc;
+  }
+  if (t1 > tm) {
+    Window wj{0, H, tm, t1 - tm, 0, tm, g.tiles_y, 0, H};
+    if ((rc = run_sweep(ctx, g, wj, 1, x, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
+                        taps, bandwidth, true, part, MODE_RECOMPUTE)))
+      return rc;
+  }
+  ctx->band_next = j + 1 < nbands ? j + 1 : nbands;
+  ctx->band_count = nbands;
+  return PNP_OK;
+}
+
+// The rest of a banded denoise once every band is swept: rs fixup, cached
+// sweep B, Kx / d fixup, finalize.
+int pnp_dsg_band_finish(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
+                        const float* taps, double bandwidth) {
+  if (!ctx || !x || !out) return fail(PNP_EINVAL, "null argument");
+  int rc = check_geometry(1, H, W, R, P, bandwidth);
+  if (rc) return rc;
+  if ((rc = validate_taps(taps, P))) return rc;
+  if (ctx->band_next < 0 || ctx->band_next != ctx->band_count)
+    return fail(PNP_EINVAL, "pnp_dsg_band_finish before every band was swept");
+  ctx->band_next = -1;
+  PNP_CUDA(cudaSetDevice(ctx->device));
+  Geom g;
+  if ((rc = make_geom(ctx, 1, H, W, R, P, g))) return rc;
   float* rs = ctx->rs.as<float>();
   float* kx = ctx->kx.as<float>();
   float* d = ctx->d.as<float>();
   float* part = ctx->partial.as<float>();
+  const int kc_rows = ctx->band_kc_rows;
+  float* kc = kc_rows > 0 ? ctx->kcache.as<float>() : nullptr;
   const Window w = full_window(g);
-  float* kc = nullptr;
-  const int kc_rows = kcache_rows(ctx, g, ctx->kcache.bytes);
-  if (kc_rows > 0) {
-    if ((rc = ctx->kcache.ensure(kcache_floats(g, kc_rows) * sizeof(float)))) return rc;
-    kc = ctx->kcache.as<float>();
-  }
-  std::vector<int> tend(nbands), need(nbands);
-  band_split(H, R, P, nbands, tend.data(), need.data());
-  // sweep A band by band, each after its rows arrived: same tiles, same
-  // partial slots and k-cache runs as the one-launch sweep -> same bits
-  const size_t kc_row = (size_t)g.tiles_x * half_window(g.R) * g.TH * kTW;
-  int t0 = 0;
-  for (int j = 0; j < nbands; ++j) {
-    if (events[j]) PNP_CUDA(cudaStreamWaitEvent(ctx->stream, (cudaEvent_t)events[j], 0));
-    const int t1 = tend[j];
-    // cached tile rows [t0, min(t1, kc_rows)) store, the rest recompute
-    const int tm = kc ? (t1 < kc_rows ? t1 : (t0 > kc_rows ? t0 : kc_rows)) : t0;
-    if (tm > t0) {
-      Window wj{0, H, t0, tm - t0, 0, t0, g.tiles_y, 0, H};
-      if ((rc = run_sweep(ctx, g, wj, 1, x, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
-                          taps, bandwidth, true, part, MODE_STORE, kc + (size_t)t0 * kc_row)))
-        return rc;
-    }
-    if (t1 > tm) {
-      Window wj{0, H, tm, t1 - tm, 0, tm, g.tiles_y, 0, H};
-      if ((rc = run_sweep(ctx, g, wj, 1, x, ChanSpec{nullptr, nullptr}, ChanSpec{nullptr, nullptr},
-                          taps, bandwidth, true, part, MODE_RECOMPUTE)))
-        return rc;
-    }
-    t0 = t1;
-  }
   {
     FixIO io{};
     io.rs = rs;
@@ -1165,6 +1189,19 @@ int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int 
   io.mbits = ctx->mbits.as<unsigned>();
   if ((rc = run_fixup<FIX_KXD>(ctx, g, w, 2, part, io))) return rc;
   return run_finalize(ctx, g, w, kx, d, ctx->mbits.as<unsigned>(), x, out, nullptr);
+}
+
+int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
+                           const float* taps, double bandwidth, int nbands,
+                           void* const* events) {
+  if (!ctx || !x || !out || !events || nbands < 1) return fail(PNP_EINVAL, "null argument");
+  // sweep A band by band, each after its rows arrived
+  for (int j = 0; j < nbands; ++j) {
+    if (events[j]) PNP_CUDA(cudaStreamWaitEvent(ctx->stream, (cudaEvent_t)events[j], 0));
+    int rc = pnp_dsg_band_sweep(ctx, x, H, W, R, P, taps, bandwidth, nbands, j);
+    if (rc) return rc;
+  }
+  return pnp_dsg_band_finish(ctx, x, out, H, W, R, P, taps, bandwidth);
 }
 
 int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, int R, int P,

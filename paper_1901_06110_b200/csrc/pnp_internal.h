@@ -79,6 +79,9 @@ struct pnp_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_x = nullptr, ev_res = nullptr;
   pnp::DevBuf admm_r, admm_part;
+  // incremental banded denoise (pnp_dsg_band_sweep / _finish): the next band
+  // expected (-1: none in progress), the call's band count and cached tile rows
+  int band_next = -1, band_count = 0, band_kc_rows = 0;
   // optional per-launch CUDA-event timing (pnp_ctx_profile)
   bool prof = false;
   std::vector<pnp::ProfSlot> slots;

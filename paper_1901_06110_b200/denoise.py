@@ -174,6 +174,10 @@ def dsg_nlm_denoise(image, params: PatchParams, guide=None, distances: str = "in
     """
     if distances not in ("integral", "direct"):
         raise ValueError(f"unknown distance method {distances!r}")
+    if guide is None and not return_aux:
+        bands = _numpy_bands(image, params)
+        if bands:
+            return _dsg_numpy_banded(image, params, bands)
     x, g, kind, dev = _pair(image, guide)
     B, H, W = A.dims(x)
     _check_margin(params, H, W)
@@ -187,6 +191,74 @@ def dsg_nlm_denoise(image, params: PatchParams, guide=None, distances: str = "in
     res = A.from_device(out, kind)
     if return_aux:
         return res, A.from_device(d, kind), (alpha if kind == A.TORCH else alpha.cpu().numpy().astype(np.float64))
+    return res
+
+
+# numpy drop-in path of one large image: host cast + upload of band j+1
+# overlaps sweep A of band j (pnp_dsg_band_sweep), the download + float64 cast
+# of the result goes band by band as well
+_NP_BANDS = 8
+
+
+def _numpy_bands(image, params: PatchParams):
+    """Input rows [0, need[j]) of each band when the banded numpy path
+    applies (a large finite-typed 2-D numpy image, guide = image), else None."""
+    if isinstance(image, torch.Tensor):
+        return None
+    a = np.asarray(image)
+    if a.ndim != 2 or a.size < A._BIG or a.dtype.kind not in "fiu":
+        return None
+    H, W = a.shape
+    TH = 32 - (params.patch_side - 1)
+    if -(-H // TH) < 2 * _NP_BANDS or params.pad_margin > min(H, W):
+        return None
+    te, need = (C.c_int * _NP_BANDS)(), (C.c_int * _NP_BANDS)()
+    L.call("pnp_dsg_band_rows", H, W, params.window_radius, params.patch_side, _NP_BANDS, te,
+           need)
+    return list(need)
+
+
+def _dsg_numpy_banded(image, params: PatchParams, bands):
+    """dsg_nlm_denoise(numpy) with the upload overlapping sweep A; same bits
+    as the one-shot path.  Non-finite input is detected on the device (one
+    flag pass over the uploaded float32 image) and confirmed in float64 on the
+    host before raising, as image.py:35-40 does."""
+    src = A._host_tensor(np.asarray(image))
+    H, W = src.shape
+    dev = A.device_index()
+    d = torch.device("cuda", dev)
+    x = torch.empty((H, W), dtype=torch.float32, device=d)
+    out = torch.empty_like(x)
+    flag = torch.zeros(1, dtype=torch.int32, device=d)
+    cur = torch.cuda.current_stream(d)
+    h2d = A.copy_stream(dev, "h2d")
+    h2d.wait_stream(cur)
+    ctx = L.context(dev)
+    taps, R, P, bw = params._ctaps(), params.window_radius, params.patch_side, float(params.bandwidth)
+    with A.staging() as st:
+        stage = st.f32("in", H * W).view(H, W)
+        r0 = 0
+        for j, r1 in enumerate(bands):
+            if r1 > r0:
+                stage[r0:r1].copy_(src[r0:r1])  # multi-threaded cast
+                ev = torch.cuda.Event()
+                with torch.cuda.stream(h2d):
+                    x[r0:r1].copy_(stage[r0:r1], non_blocking=True)
+                    ev.record(h2d)
+                cur.wait_event(ev)
+                r0 = r1
+            L.call("pnp_dsg_band_sweep", ctx, L.ptr(x), H, W, R, P, taps, bw, len(bands), j)
+        L.call("pnp_flag_nonfinite", ctx, L.ptr(x), x.numel(), L.ptr(flag))
+        L.call("pnp_dsg_band_finish", ctx, L.ptr(x), L.ptr(out), H, W, R, P, taps, bw)
+        # fault the result's pages in (threaded) while the device denoises
+        res = np.empty((H, W), dtype=np.float64)
+        torch.from_numpy(res).zero_()
+        res = A.download64_banded(out, st, 2 * _NP_BANDS, res)
+    if int(flag.item()):
+        a = np.asarray(image, dtype=np.float64)
+        if not np.all(np.isfinite(a)):
+            raise ValueError("image contains non-finite values")
+        raise ValueError("image values exceed the float32 range of the device path")
     return res
 
 

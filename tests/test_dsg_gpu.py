@@ -320,6 +320,52 @@ def test_large_numpy_inputs_take_the_pinned_path(pnp, rng):
         pnp.dsg_nlm_denoise(bad, p)
 
 
+def test_numpy_banded_upload_path(pnp, rng, monkeypatch):
+    """Large numpy images take the banded path (host cast + upload of band
+    j+1 overlapping sweep A of band j, pnp_dsg_band_sweep / _finish): same
+    bits as the device-tensor path for float64 and integer inputs, a fresh
+    writeable float64 result, ValueError for non-finite input and for finite
+    values the float32 device path cannot hold; C-ABI misuse is rejected."""
+    from paper_1901_06110_b200 import _lib as L
+    from paper_1901_06110_b200 import denoise as D
+    calls = []
+    real = D._dsg_numpy_banded
+    monkeypatch.setattr(D, "_dsg_numpy_banded", lambda *a: calls.append(1) or real(*a))
+    p = pnp.PatchParams.from_h(7, 10, 12 / 255, 2.0)
+    img = rng.random((1300, 1032))
+    out = pnp.dsg_nlm_denoise(img, p)
+    assert calls and out.dtype == np.float64 and out.flags.writeable
+    ref = pnp.dsg_nlm_denoise(torch.tensor(img, dtype=torch.float32, device="cuda"), p)
+    assert np.array_equal(out, ref.cpu().numpy().astype(np.float64))
+    assert np.array_equal(pnp.dsg_nlm_denoise(img, p), out)  # rerun: same bits
+    ints = rng.integers(0, 256, (1024, 1024)).astype(np.uint8)
+    got = pnp.dsg_nlm_denoise(ints, pnp.PatchParams(5, 4, 20.0, 1.5))
+    ref = pnp.dsg_nlm_denoise(torch.tensor(ints, dtype=torch.float32, device="cuda"),
+                              pnp.PatchParams(5, 4, 20.0, 1.5))
+    assert np.array_equal(got, ref.cpu().numpy().astype(np.float64))
+    n_calls = len(calls)
+    for v in (np.nan, -np.inf, 1e300):
+        bad = img.copy()
+        bad[1200, 1031] = v
+        with pytest.raises(ValueError):
+            pnp.dsg_nlm_denoise(bad, p)
+    assert len(calls) == n_calls + 3
+    # sweeping out of order / finishing early fails loudly
+    ctx = L.context(torch.cuda.current_device())
+    x = torch.zeros(1300, 1032, device="cuda")
+    args = (1300, 1032, p.window_radius, p.patch_side, p._ctaps(), float(p.bandwidth))
+    assert L.lib.pnp_dsg_band_sweep(ctx, L.ptr(x), *args, 8, 1) != 0
+    assert L.lib.pnp_dsg_band_finish(ctx, L.ptr(x), L.ptr(x), *args) != 0
+    assert L.lib.pnp_dsg_band_sweep(ctx, L.ptr(x), *args, 8, 0) == 0
+    assert L.lib.pnp_dsg_band_finish(ctx, L.ptr(x), L.ptr(x), *args) != 0
+    assert L.lib.pnp_dsg_band_sweep(ctx, L.ptr(x), *args, 8, 2) != 0
+    assert L.lib.pnp_dsg_band_sweep(ctx, L.ptr(x), *args, 8, 0) == 0  # restart is allowed
+    for j in range(1, 8):
+        assert L.lib.pnp_dsg_band_sweep(ctx, L.ptr(x), *args, 8, j) == 0
+    assert L.lib.pnp_dsg_band_finish(ctx, L.ptr(x), L.ptr(x), *args) == 0
+    torch.cuda.synchronize()
+
+
 def test_helpers_match_reference_goldens(pnp):
     """Distance-engine helpers against the real reference's outputs
     (tests/golden/helpers.npz, make_golden.py --helpers): pad / SAT / box sums
