@@ -405,6 +405,23 @@ def run_gpu(args, rank, world, local_rank):
                                          "ms_per_step": float(t[0]),
                                          "api": "host->device copy, dsg_nlm_denoise, "
                                                 "device->host copy, one image at a time"}}
+            # the reference's own call shape: float64 numpy in, new float64
+            # numpy out (validation, casts and both transfers included)
+            img64 = host_in.numpy().astype(np.float64)
+            out64 = pnp.dsg_nlm_denoise(img64, params)  # warm-up
+            assert np.array_equal(out64, ref_out.numpy().astype(np.float64)), "numpy != denoise"
+            walls = []
+            for _ in range(max(3, min(args.steps, 5))):
+                w0 = time.perf_counter()
+                pnp.dsg_nlm_denoise(img64, params)
+                walls.append((time.perf_counter() - w0) * 1e3)
+            ms_np = float(np.median(walls))
+            line["e2e"]["numpy_dropin"] = {
+                "value": units / (ms_np * 1e-3) / 1e9, "ms_per_step": ms_np,
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "api": "paper_1901_06110_b200.dsg_nlm_denoise(float64 numpy) -> float64 numpy "
+                       "(banded cast + upload overlapping sweep A, banded download); "
+                       "median wall time of the synchronous call"}
         else:
             line["e2e"] = {"value": units / (float(t[0]) * 1e-3) / 1e9, "unit": "Gpixel*offset/s",
                            "h2d_bytes_per_step": nbytes * world,
