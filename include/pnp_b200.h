@@ -53,8 +53,15 @@ int pnp_ctx_synchronize(pnp_ctx* ctx);
  * the whole cache does not fit (the budget or free HBM less 4 GiB), the tile
  * rows that fit are cached and the rest recomputed (at least 1/8 of them, else
  * none).  Frozen guides allocate theirs from the device's stream-ordered pool
- * (cudaMallocAsync) and free it on the stream of their last use. */
+ * (cudaMallocAsync) and free it on the stream of their last use.  An adaptive
+ * denoise holds its cache only for the duration of the call: a buffer the
+ * caller bound with pnp_ctx_bind_kcache (the Python layer binds memory from
+ * torch's caching allocator, so torch sees and reuses it), else a
+ * stream-ordered pool allocation freed at the end of the call
+ * (pnp_ctx_trim returns the pool's idle memory to the device). */
 int pnp_ctx_set_cache_limit(pnp_ctx* ctx, int64_t bytes);
+int pnp_ctx_bind_kcache(pnp_ctx* ctx, void* ptr, int64_t bytes);
+int pnp_ctx_trim(pnp_ctx* ctx);
 int pnp_frozen_cached(const pnp_frozen* fz);
 /* Per-launch CUDA-event timing on the context stream (off by default).
  * profile_read syncs the stream, returns summed device ms and launch counts
@@ -66,14 +73,18 @@ int pnp_ctx_profile_read(pnp_ctx* ctx, double* ms, int* launches);
 /* Measured FFMA / MUFU.EX2 instruction throughput of the device (per second,
  * whole GPU) — the roofline denominators of the DSG sweep. */
 int pnp_peak_rates(int device, double* ffma_per_s, double* ex2_per_s);
-/* Pre-size scratch for (batch, H, W, R, P) so later calls allocate nothing
- * (required before CUDA-graph capture). */
-int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P);
+/* Pre-size scratch for (batch, H, W, R, P, box taps?) so later calls allocate
+ * nothing (required before CUDA-graph capture). */
+int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P, int box);
 
 /* ---- DSG-NLM ------------------------------------------------------------ */
 /* dsg_nlm_denoise(image, params, guide) — reference denoise.py:272-288.
  * out = K x / m + (1 - d / m) x with K = D^-1/2 (hat o K_nlm) D^-1/2,
  * d = K 1 (normalized row sums), m = max d per image.
+ * taps: P normalized 1-D patch taps.  Equal taps (1/P) are the reference's
+ * box patch distance and run the general sweep with running-sum box filters
+ * (cost flat in P; any odd P <= 63, any R); other taps (Gaussian) run the
+ * P-templated sweep for P <= 15, R <= 32 and the general sweep beyond.
  * guide may equal x.  d_out (B*H*W) and alpha_out (B floats, = m) are
  * optional device outputs. */
 int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out,
@@ -111,7 +122,8 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
  * band j's sweep A waits for events[j] (a cudaEvent_t recorded once those
  * rows are uploaded; NULL = no wait), the rest of the denoise runs after the
  * last band.  Guide = x.  Bitwise equal to pnp_dsg_denoise. */
-int pnp_dsg_band_rows(int H, int W, int R, int P, int nbands, int* tile_end, int* rows_needed);
+int pnp_dsg_band_rows(int H, int W, int R, int P, int box, int nbands, int* tile_end,
+                      int* rows_needed);
 int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int W, int R, int P,
                            const float* taps, double bandwidth, int nbands,
                            void* const* events);
@@ -127,12 +139,11 @@ int pnp_dsg_band_finish(pnp_ctx* ctx, const float* x, float* out, int H, int W, 
                         const float* taps, double bandwidth);
 
 /* ---- row-strip building blocks (multi-GPU sharding) ---- *
- * A rank owns global rows [y0, y1) = whole tile rows of height
- * pnp_tile_height(P).  Per-pixel buffers are windows: rows [buf_r0, buf_r0 +
+ * A rank owns global rows [y0, y1) = whole tile rows of height TH
+ * (pnp_dsg_geometry).  Per-pixel buffers are windows: rows [buf_r0, buf_r0 +
  * buf_rows) of the Hg x W image (own rows plus halos received from
- * neighbours).  Partial buffers hold part_ntr tile rows x partial groups
- * (pnp_dsg_groups() offset groups, reduced on chip by thread-block clusters of
- * min(groups, 8) CTAs) x ceil(W/64) tiles of C*(TH+R)*(64+2R) floats
+ * neighbours).  Partial buffers hold part_ntr tile rows x pnp_dsg_groups()
+ * offset groups x ceil(W/64) tiles of C*(TH+Rb)*(64+2Rb) floats
  * (pnp_dsg_partial_floats gives the total); slot 0 is
  * global tile row part_tr0 (a neighbour's rows are received into the
  * prefix).  A sharded run sums in exactly the single-GPU order, so its
@@ -145,17 +156,21 @@ int pnp_dsg_band_finish(pnp_ctx* ctx, const float* x, float* out, int H, int W, 
  * kcache (nullable, pnp_dsg_kcache_floats(.., ntr) floats, caller-owned):
  * pass 0 also stores the strip's pair weights, passes 1-3 then stream them
  * instead of recomputing the patch filter (bitwise identical results). */
-int pnp_tile_height(int P);
-int pnp_dsg_groups(int Hg, int W, int R, int P);
-int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr);
-int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int ntr);
+/* out[8] = {TH tile height, offset groups, Rb far band of a partial block
+ * (R; 0 when blocks are tile-only), sweep path (0 P-templated, 1 general
+ * half window, 2 general full window), input halo rows above, input halo
+ * rows below, rows of the channel (rs) planes read below, 0}. */
+int pnp_dsg_geometry(int Hg, int W, int R, int P, int box, int* out);
+int pnp_dsg_groups(int Hg, int W, int R, int P, int box);
+int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int box, int C, int ntr);
+int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int box, int ntr);
 int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float* x,
                         const float* rs, int Hg, int W, int buf_r0, int buf_rows, int tr0,
                         int ntr, int R, int P, const float* taps, double bandwidth,
                         float* partial, int part_off, int part_ntr, float* kcache);
 int pnp_dsg_strip_fixup(pnp_ctx* ctx, int mode, const float* partial, int part_tr0,
-                        int part_ntr, int Hg, int W, int R, int P, int y0, int y1, int buf_r0,
-                        int buf_rows, float* rs, float* kx, float* d, unsigned* mbits,
+                        int part_ntr, int Hg, int W, int R, int P, int box, int y0, int y1,
+                        int buf_r0, int buf_rows, float* rs, float* kx, float* d, unsigned* mbits,
                         const float* inv_m, const float* x, float* out);
 int pnp_dsg_strip_finalize(pnp_ctx* ctx, const float* kx, const float* d, const float* x,
                            float* out, const unsigned* mbits, int Hg, int W, int y0, int y1,

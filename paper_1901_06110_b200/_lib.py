@@ -38,8 +38,10 @@ _SIGS = {
     "pnp_ctx_destroy": (i32, [vp]),
     "pnp_ctx_set_stream": (i32, [vp, vp]),
     "pnp_ctx_synchronize": (i32, [vp]),
-    "pnp_ctx_reserve": (i32, [vp, i32, i32, i32, i32, i32]),
+    "pnp_ctx_reserve": (i32, [vp, i32, i32, i32, i32, i32, i32]),
     "pnp_ctx_set_cache_limit": (i32, [vp, i64]),
+    "pnp_ctx_bind_kcache": (i32, [vp, vp, i64]),
+    "pnp_ctx_trim": (i32, [vp]),
     "pnp_frozen_cached": (i32, [vp]),
     "pnp_ctx_profile": (i32, [vp, i32]),
     "pnp_ctx_profile_read": (i32, [vp, C.POINTER(f64), C.POINTER(i32)]),
@@ -53,14 +55,14 @@ _SIGS = {
     "pnp_frozen_shape": (i32, [vp] + [C.POINTER(i32)] * 5),
     "pnp_frozen_cache": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(C.c_ulonglong)]),
     "pnp_nlm_denoise": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64]),
-    "pnp_tile_height": (i32, [i32]),
-    "pnp_dsg_groups": (i32, [i32, i32, i32, i32]),
-    "pnp_dsg_partial_floats": (i64, [i32, i32, i32, i32, i32, i32]),
-    "pnp_dsg_kcache_floats": (i64, [i32, i32, i32, i32, i32]),
+    "pnp_dsg_geometry": (i32, [i32, i32, i32, i32, i32, C.POINTER(i32)]),
+    "pnp_dsg_groups": (i32, [i32, i32, i32, i32, i32]),
+    "pnp_dsg_partial_floats": (i64, [i32, i32, i32, i32, i32, i32, i32]),
+    "pnp_dsg_kcache_floats": (i64, [i32, i32, i32, i32, i32, i32]),
     "pnp_dsg_strip_sweep": (i32, [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
                                   fptr, f64, vp, i32, i32, vp]),
     "pnp_dsg_strip_fixup": (i32, [vp, i32, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
-                                  vp, vp, vp, vp, vp, vp, vp]),
+                                  i32, vp, vp, vp, vp, vp, vp, vp]),
     "pnp_dsg_strip_finalize": (i32, [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32]),
     "pnp_sr_apply": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
     "pnp_sr_adjoint": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32]),
@@ -93,7 +95,7 @@ _SIGS = {
     "pnp_patch_distance_map_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp]),
     "pnp_patch_ssd_pairs_f64": (i32, [vp, vp, i32, i32, i32, vp, i32, vp]),
     "pnp_dense_weights_f64": (i32, [vp, vp, i32, i32, i32, i32, f64, vp, vp]),
-    "pnp_dsg_band_rows": (i32, [i32, i32, i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]),
+    "pnp_dsg_band_rows": (i32, [i32, i32, i32, i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]),
     "pnp_dsg_denoise_banded": (i32, [vp, vp, vp, i32, i32, i32, i32, fptr, f64, i32,
                                      C.POINTER(vp)]),
     "pnp_dsg_band_sweep": (i32, [vp, vp, i32, i32, i32, i32, fptr, f64, i32, i32]),
@@ -138,12 +140,49 @@ def ptr(t) -> vp:
     return None if t is None else vp(t.data_ptr())
 
 
+_GEOM: dict = {}
+
+
+def dsg_geometry(Hg: int, W: int, R: int, P: int, box: bool) -> tuple:
+    """pnp_dsg_geometry: (TH, offset groups, block band Rb, sweep path, input
+    halo above, input halo below, channel rows read below, 0)."""
+    key = (Hg, W, R, P, bool(box))
+    g = _GEOM.get(key)
+    if g is None:
+        out = (C.c_int * 8)()
+        check(lib.pnp_dsg_geometry(Hg, W, R, P, int(bool(box)), out))
+        g = _GEOM[key] = tuple(out)
+    return g
+
+
 def host_floats(values) -> C.Array:
     arr = (C.c_float * len(values))(*[float(v) for v in values])
     return arr
 
 
 _tls = threading.local()
+# k-cache budget per device as set through profiling.set_cache_limit
+# (None: no limit, 0: disabled) -- the Python layer sizes the torch buffer
+# it binds for each adaptive call from it
+cache_limits: dict = {}
+
+
+class _Ctx:
+    """Owns one native context; destroyed when its thread's local storage
+    goes away (thread exit) or at interpreter shutdown."""
+
+    __slots__ = ("h",)
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h and lib is not None:
+                lib.pnp_ctx_destroy(self.h)
+        except Exception:  # interpreter shutdown
+            pass
+        self.h = None
 
 
 def _raw_stream(device: int) -> int:
@@ -165,9 +204,12 @@ def context(device: int):
     if ent is None:
         h = vp()
         check(lib.pnp_ctx_create(device, C.byref(h)))
-        ent = ctxs[device] = [h, None]
+        ent = ctxs[device] = [_Ctx(h), None]
+        lim = cache_limits.get(device, None)
+        if lim is not None:
+            check(lib.pnp_ctx_set_cache_limit(h, int(lim)))
     stream = _raw_stream(device)
     if stream != ent[1]:
-        check(lib.pnp_ctx_set_stream(ent[0], vp(stream)))
+        check(lib.pnp_ctx_set_stream(ent[0].h, vp(stream)))
         ent[1] = stream
-    return ent[0]
+    return ent[0].h

@@ -1,0 +1,290 @@
+// DSG-NLM offset sweep for any patch side and search radius (sm_100a).
+//
+// The P-templated sweep (dsg_sweep.cuh) covers Gaussian patch weights with
+// P <= 15, R <= 32.  This kernel is the general one, and the one used for the
+// reference's own box patch weights at every P: the box patch distance
+//   SSD_t(s) = sum_{a,b < P} (G(s+ab) - G(s+t+ab))^2       (denoise.py:131-158)
+// is computed with running sums (a horizontal then a vertical running box
+// sum over the squared-difference rows), so the cost per pixel-offset does
+// not grow with P -- the property the reference gets from its summed-area
+// table ("cost independent of patch_side", denoise.py:11-15; Table 1 of the
+// paper).  The running sums restart every 32 columns / TH/2 rows, so fp32
+// rounding never accumulates over the image (the reference itself
+// mean-centres its float64 table for the same reason, denoise.py:143-157).
+// Gaussian taps (patch_sigma) use the direct separable filter instead (cost
+// 2P per pair).
+//
+// Work decomposition: one CTA per output tile (TH x 64) and offset group;
+// offsets are walked dy-major.  Per dy (and per chunk of at most kGenDXC dx
+// values) the partner guide rows and partner channel rows are staged into
+// shared memory (reflected guide, zero channel planes outside the image), then
+// per offset: phase H (thread = map row x 32-column segment: running / direct
+// horizontal filter of the squared differences into an H map), phase V
+// (thread = column x half of the tile rows: vertical filter, ex2 with the
+// hat folded into the exponent, near-end accumulation in registers).
+//
+// SYM (the default): the half window only; each unordered pair credited to
+// both ends, the far end into a shared-memory plane over the tile + its
+// R-wide band that is written as the tile's partial block (exactly the
+// P-templated kernel's block format, summed by the same fixups).  Within one
+// offset every far cell has one writer; offsets are separated by barriers and
+// walked in a fixed order -> no atomics, bit-reproducible.
+// !SYM (search radii whose far plane does not fit in shared memory): the full
+// window from each end, near sums only, a TH x 64 block per tile.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dsg_sweep.cuh"
+
+namespace pnp {
+
+constexpr int kGenThreads = 128;  // 64 columns x 2 row halves in phase V
+constexpr int kGenDXC = 32;       // dx values per staged chunk
+constexpr int kGenMaxP = 63;      // largest patch side (shared memory)
+constexpr int kGenSeg = 32;       // phase-H segment (running-sum restart)
+
+struct GenArgs {
+  const float* guide;  // [B][buf_rows][W]
+  ChanSpec ch[2];
+  float* partial;
+  const float* ltab;   // log2 hat per offset, [(dy+R)*(2R+1) + dx+R]; null: 0 (NLM)
+  int Hg, W, R, P, TH;
+  int buf_r0, buf_rows;
+  int tr0, tiles_x;
+  int part_off, part_ntr;
+  float cv;                 // box: -log2(e) / (2 P^2 bw^2)
+  float taps_h[kGenMaxP];   // Gaussian: normalized taps w_b
+  float taps_v[kGenMaxP];   // Gaussian: -log2(e)/(2 bw^2) * w_a
+  int grp[kMaxGroups + 1];  // offset groups: dy-index ranges (dy = dyi + dy_min)
+};
+
+// Shared-memory geometry of one CTA (floats); also used by the host to pick TH.
+struct GenSmem {
+  int M, GOS, GPS, HS, YS, AR, AC;
+  int off_gp, off_h, off_y, off_a, total;
+};
+
+__host__ __device__ inline GenSmem gen_smem(int TH, int P, int R, int C, bool sym) {
+  GenSmem s;
+  const int p = (P - 1) / 2;
+  s.M = TH + 2 * p;
+  s.GOS = (kTW + 2 * p) | 1;
+  s.GPS = (kTW + 2 * p + kGenDXC) | 1;
+  s.HS = kTW + 1;
+  s.YS = kTW + kGenDXC;
+  s.AR = sym ? TH + R : 0;
+  s.AC = sym ? kTW + 2 * R : 0;
+  s.off_gp = s.M * s.GOS;
+  s.off_h = s.off_gp + s.M * s.GPS;
+  s.off_y = s.off_h + s.M * s.HS;
+  s.off_a = s.off_y + C * TH * s.YS;
+  s.total = s.off_a + C * s.AR * s.AC;
+  return s;
+}
+
+__device__ __forceinline__ float sqd(float a, float b) {
+  const float t = __fsub_rn(a, b);
+  return __fmul_rn(t, t);
+}
+
+template <int C, bool BOX, bool SYM>
+__global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs a) {
+  pdl_begin();
+  extern __shared__ float smem[];
+  const int R = a.R, P = a.P, TH = a.TH, p = (P - 1) / 2;
+  const GenSmem L = gen_smem(TH, P, R, C, SYM);
+  float* Gown = smem;
+  float* Gpart = smem + L.off_gp;
+  float* Hs = smem + L.off_h;
+  float* Ys = smem + L.off_y;
+  float* As = smem + L.off_a;
+
+  const int Hg = a.Hg, W = a.W, br0 = a.buf_r0, brows = a.buf_rows;
+  const int tile = blockIdx.x;
+  const int tyl = tile / a.tiles_x, tx = tile - tyl * a.tiles_x;
+  const int r0g = (a.tr0 + tyl) * TH, c0g = tx * kTW;
+  const size_t plane = (size_t)brows * W;
+  const int b = blockIdx.z;
+  const float* Gimg = a.guide + (size_t)b * plane;
+  const int tid = threadIdx.x;
+  const int M = L.M;
+
+  auto grow = [&](int gr) {  // reflected guide row -> buffer row
+    int lr = reflect_index(gr, Hg) - br0;
+    return lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
+  };
+  const float* pa[C];
+  const float* pb[C];
+#pragma unroll
+  for (int c_ = 0; c_ < C; ++c_) {
+    pa[c_] = a.ch[c_].a ? a.ch[c_].a + (size_t)b * plane : nullptr;
+    pb[c_] = a.ch[c_].b ? a.ch[c_].b + (size_t)b * plane : nullptr;
+  }
+  // channel value y = a*b at global (gr, gc); +0 outside the image / buffer
+  auto yval = [&](int c_, int gr, int gc) {
+    const int lr = gr - br0;
+    if (gr < 0 || gr >= Hg || lr < 0 || lr >= brows || gc < 0 || gc >= W) return 0.f;
+    const size_t o = (size_t)lr * W + gc;
+    float v = 1.f;
+    if (pa[c_]) v = __ldg(pa[c_] + o);
+    if (pb[c_]) v = __fmul_rn(v, __ldg(pb[c_] + o));
+    return v;
+  };
+
+  // ---- own guide rows (map rows q <-> image row r0g - p + q, map col j <->
+  // image col c0g - p + j), far plane cleared ----
+  for (int q = tid / 32; q < M; q += kGenThreads / 32) {
+    const float* src = Gimg + (size_t)grow(r0g - p + q) * W;
+    for (int j = tid & 31; j < kTW + 2 * p; j += 32)
+      Gown[q * L.GOS + j] = __ldg(src + reflect_index(c0g - p + j, W));
+  }
+  if (SYM)
+    for (int i = tid; i < C * L.AR * L.AC; i += kGenThreads) As[i] = 0.f;
+
+  const int x = tid & (kTW - 1), g = tid / kTW;
+  const int N = TH / 2, rA = g * N;  // phase-V rows [rA, rA + N)
+  float near[C][16], yown[C][16];
+#pragma unroll
+  for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float v = i < N ? yval(c_, r0g + rA + i, c0g + x) : 0.f;
+      yown[c_][i] = v;
+      near[c_][i] = blockIdx.y == 0 ? v : 0.f;  // self pair: k = hat = 1
+    }
+
+  const int dy_min = SYM ? 0 : -R;
+  const int n_dx = 2 * R + 1;
+  for (int dyi = a.grp[blockIdx.y]; dyi < a.grp[blockIdx.y + 1]; ++dyi) {
+    const int dy = dyi + dy_min;
+    // half window: dy == 0 -> dx in [1, R]; full window skips (0, 0) only
+    const int dx_lo = (SYM && dy == 0) ? 1 : -R;
+    for (int dxa = dx_lo; dxa <= R; dxa += kGenDXC) {
+      const int dxb = min(dxa + kGenDXC, R + 1);
+      __syncthreads();  // previous users of Gpart / Ys are done
+      // partner guide rows: map row q <-> image row r0g - p + q + dy, col j
+      // <-> image col c0g - p + dxa + j
+      const int gpw = kTW + 2 * p + (dxb - dxa) - 1;
+      for (int q = tid / 32; q < M; q += kGenThreads / 32) {
+        const float* src = Gimg + (size_t)grow(r0g - p + q + dy) * W;
+        for (int j = tid & 31; j < gpw; j += 32)
+          Gpart[q * L.GPS + j] = __ldg(src + reflect_index(c0g - p + dxa + j, W));
+      }
+      // partner channel rows: row r <-> image row r0g + r + dy, col j <->
+      // image col c0g + dxa + j
+      const int yw = kTW + (dxb - dxa) - 1;
+#pragma unroll
+      for (int c_ = 0; c_ < C; ++c_)
+        for (int r = tid / 32; r < TH; r += kGenThreads / 32)
+          for (int j = tid & 31; j < yw; j += 32)
+            Ys[(c_ * TH + r) * L.YS + j] = yval(c_, r0g + r + dy, c0g + dxa + j);
+      __syncthreads();
+
+      for (int dx = dxa; dx < dxb; ++dx) {
+        if (!SYM && dy == 0 && dx == 0) continue;  // self pair: analytic
+        const int cdx = dx - dxa;
+        // ---- phase H: map row q, columns [x0, x0 + 32) ----
+        for (int it = tid; it < 2 * M; it += kGenThreads) {
+          const int q = it >> 1, x0 = (it & 1) * kGenSeg;
+          const float* own = Gown + q * L.GOS + x0;
+          const float* part = Gpart + q * L.GPS + x0 + cdx;
+          float* h = Hs + q * L.HS + x0;
+          if (BOX) {
+            float s = sqd(part[0], own[0]);
+            for (int bb = 1; bb < P; ++bb) s = __fadd_rn(s, sqd(part[bb], own[bb]));
+            h[0] = s;
+#pragma unroll 4
+            for (int i = 1; i < kGenSeg; ++i) {
+              s = __fsub_rn(__fadd_rn(s, sqd(part[i + P - 1], own[i + P - 1])),
+                            sqd(part[i - 1], own[i - 1]));
+              h[i] = s;
+            }
+          } else {
+#pragma unroll 2
+            for (int i = 0; i < kGenSeg; ++i) {
+              float s = __fmul_rn(a.taps_h[0], sqd(part[i], own[i]));
+              for (int bb = 1; bb < P; ++bb)
+                s = __fmaf_rn(a.taps_h[bb], sqd(part[i + bb], own[i + bb]), s);
+              h[i] = s;
+            }
+          }
+        }
+        __syncthreads();
+        // ---- phase V: column x, rows [rA, rA + N) ----
+        {
+          const float Lt = a.ltab ? a.ltab[(dy + R) * n_dx + dx + R] : 0.f;
+          const float* hc = Hs + rA * L.HS + x;
+          const float* yp = Ys + rA * L.YS + x + cdx;
+          float* ap = SYM ? As + (rA + dy) * L.AC + x + dx + R : nullptr;
+          float s = 0.f;
+          if (BOX) {
+            s = hc[0];
+            for (int aa = 1; aa < P; ++aa) s = __fadd_rn(s, hc[aa * L.HS]);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i >= N) break;
+            float e;
+            if (BOX) {
+              e = __fmaf_rn(s, a.cv, Lt);
+              if (i + 1 < N)
+                s = __fsub_rn(__fadd_rn(s, hc[(i + P) * L.HS]), hc[i * L.HS]);
+            } else {
+              e = Lt;
+              for (int aa = 0; aa < P; ++aa) e = __fmaf_rn(a.taps_v[aa], hc[(i + aa) * L.HS], e);
+            }
+            const float k = ex2_approx(e);
+#pragma unroll
+            for (int c_ = 0; c_ < C; ++c_) {
+              near[c_][i] = __fmaf_rn(k, yp[(c_ * TH + i) * L.YS], near[c_][i]);
+              if (SYM) {
+                float* q = ap + (c_ * L.AR + i) * L.AC;
+                *q = __fmaf_rn(k, yown[c_][i], *q);
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  // ---- emit: own pixels get near + far; the block is tile + band (SYM) or
+  // the tile alone ----
+  const int BR = SYM ? TH + R : TH, BC = SYM ? kTW + 2 * R : kTW;
+  const size_t slot =
+      (((size_t)b * a.part_ntr + a.part_off + tyl) * gridDim.y + blockIdx.y) * a.tiles_x + tx;
+  float* out = a.partial + slot * (size_t)(C * BR * BC);
+  if (SYM) {
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i >= N) break;
+        float* q = As + (c_ * L.AR + rA + i) * L.AC + x + R;
+        *q = __fadd_rn(near[c_][i], *q);
+      }
+    __syncthreads();
+    for (int c_ = 0; c_ < C; ++c_)
+      for (int i = tid; i < BR * BC; i += kGenThreads)
+        out[(size_t)c_ * BR * BC + i] = As[c_ * L.AR * L.AC + i];
+  } else {
+#pragma unroll
+    for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i >= N) break;
+        out[((size_t)c_ * BR + rA + i) * BC + x] = near[c_][i];
+      }
+  }
+}
+
+}  // namespace pnp
+
+namespace pnp {
+// pnp_generic.cu
+cudaError_t launch_generic(const GenArgs& a, int C, bool box, bool sym, dim3 grid,
+                           cudaStream_t st);
+}  // namespace pnp

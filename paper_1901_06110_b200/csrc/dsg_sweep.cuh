@@ -58,9 +58,6 @@ constexpr int kThreads = 128;  // 64 columns x 2 row groups in phase 2
 #define PNP_KY 4
 #endif
 constexpr int kKY = PNP_KY;
-#ifndef PNP_CLUSTER
-#define PNP_CLUSTER 1  // largest cluster of one tile's offset-group CTAs (1: off, measured best)
-#endif
 #ifndef PNP_SB
 #define PNP_SB 6  // rows per warp per batch of prologue loads (k-cache sweeps)
 #endif
@@ -123,7 +120,7 @@ struct HostTab {
 // buf_rows) of a Hg x W image (single GPU: buf_r0 = 0, buf_rows = Hg; a row
 // strip on one rank of a sharded run: its rows plus halos).  The launch
 // covers global tile rows [tr0, tr0 + gridDim.x / tiles_x).  Partial blocks
-// go to slot (part_off + local tile row) of a [B][part_ntr][NG/cg][tiles_x]
+// go to slot (part_off + local tile row) of a [B][part_ntr][NG][tiles_x]
 // array of C*(TH+R)*(TW+2R) floats; tile rows are outermost so a
 // neighbour's rows can be received into a contiguous prefix.
 struct SweepArgs {
@@ -145,9 +142,6 @@ struct SweepArgs {
   long long kc_img, kc_tile;
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
-  // offset groups per cluster: the cg CTAs of a tile (blockIdx.y = gp*cg + q)
-  // sum their planes through DSMEM into one partial block (group gp)
-  int cg;
 };
 
 __host__ __device__ constexpr int tile_height(int P) { return 32 - (P - 1); }
@@ -218,24 +212,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
   } while (!ok);
-}
-
-// ---- thread-block cluster helpers (offset-group reduction via DSMEM) ----
-constexpr int kMaxCluster = 8;
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
-               ::: "memory");
-}
-// shared::cta address -> the same offset in CTA `rank` of the cluster
-__device__ __forceinline__ unsigned mapa_u32(unsigned addr, int rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float ld_dsmem(unsigned addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-  return v;
 }
 
 // Offset (in elements: float2 in a pair plane, float in a single plane) of row
@@ -669,53 +645,15 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
     }
   __syncthreads();
   const int BR = TH + R, BC = kTW + 2 * R;
-#if PNP_CLUSTER > 1
-  const int cgs = a.cg > 1 ? a.cg : 1, np = gridDim.y / cgs;
-  const size_t slot =
-      (((size_t)b * a.part_ntr + a.part_off + tyl) * np + blockIdx.y / cgs) * a.tiles_x + tx;
-#else
-  constexpr int cgs = 1;
   const size_t slot =
       (((size_t)b * a.part_ntr + a.part_off + tyl) * gridDim.y + blockIdx.y) * a.tiles_x + tx;
-#endif
   float* out = a.partial + slot * (size_t)(C * BR * BC);
-  if (PNP_CLUSTER == 1 || cgs == 1) {
 #pragma unroll
-    for (int c_ = 0; c_ < C; ++c_) {
-      const float* A0 = As + c_ * AR * YC + (RB - R);
-      float* o = out + (size_t)c_ * BR * BC;
-      for (int br = warp; br < BR; br += kThreads / 32)
-        for (int bc = lane; bc < BC; bc += 32) o[br * BC + bc] = A0[br * YC + bc];
-    }
-  } else if constexpr (PNP_CLUSTER > 1) {
-    // cluster of the tile's offset groups: CTA q of the cluster sums rows
-    // [q*BR/cgs, (q+1)*BR/cgs) of all cgs planes in group order (DSMEM loads)
-    // and writes them; the second cluster barrier keeps every plane alive
-    // until all its readers are done.
-    cluster_sync();
-    const int q = blockIdx.y % cgs;
-    const int br0 = q * BR / cgs, br1 = (q + 1) * BR / cgs;
-    const unsigned a_loc = smem_u32(As);
-    unsigned a_rem[kMaxCluster];
-#pragma unroll
-    for (int r = 0; r < kMaxCluster; ++r) a_rem[r] = r < cgs ? mapa_u32(a_loc, r) : 0u;
-#pragma unroll
-    for (int c_ = 0; c_ < C; ++c_) {
-      float* o = out + (size_t)c_ * BR * BC;
-      for (int br = br0 + warp; br < br1; br += kThreads / 32)
-        for (int bc = lane; bc < BC; bc += 32) {
-          const unsigned off = 4u * (unsigned)(c_ * AR * YC + (RB - R) + br * YC + bc);
-          float v[kMaxCluster];
-#pragma unroll
-          for (int r = 0; r < kMaxCluster; ++r) v[r] = r < cgs ? ld_dsmem(a_rem[r] + off) : 0.f;
-          float sacc = v[0];
-#pragma unroll
-          for (int r = 1; r < kMaxCluster; ++r)
-            if (r < cgs) sacc = __fadd_rn(sacc, v[r]);
-          o[br * BC + bc] = sacc;
-        }
-    }
-    cluster_sync();
+  for (int c_ = 0; c_ < C; ++c_) {
+    const float* A0 = As + c_ * AR * YC + (RB - R);
+    float* o = out + (size_t)c_ * BR * BC;
+    for (int br = warp; br < BR; br += kThreads / 32)
+      for (int bc = lane; bc < BC; bc += 32) o[br * BC + bc] = A0[br * YC + bc];
   }
 }
 
@@ -724,7 +662,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 // (pnp_dsg.cu).  Slot 0 of the partial array holds global tile row part_tr0.
 struct FixGeo {
   const float* partial;
-  int Hg, W, R, TH, tiles_x, NP, C;  // NP = partial groups (offset groups / cluster)
+  int Hg, W, R, TH, tiles_x, NP, C;  // R: block band (0: tile-only blocks); NP = offset groups
   int part_tr0, part_ntr;
   int y0, nrows;          // output rows [y0, y0 + nrows) (global)
   int buf_r0, buf_rows;   // per-pixel buffers' window

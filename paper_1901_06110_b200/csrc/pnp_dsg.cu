@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "dsg_generic.cuh"
 #include "dsg_sweep.cuh"
 #include "sweep_launch.cuh"
 #include "pnp_internal.h"
@@ -532,10 +533,14 @@ __global__ void dsg_alpha_kernel(const unsigned* mbits, float* mv, int B) {
 // batch, so single-GPU and sharded runs sum in the same order.
 struct Geom {
   int B, Hg, W, R, P, TH, tiles_x, tiles_y, nchunks, NG;
-  int CG, NP;  // sweep cluster size (offset groups reduced on chip), partial groups NG / CG
-  const Chunk* chunks;        // hat-tapered table (DSG), host
+  int NP;            // partial groups per tile (= NG)
+  int kind;          // PATH_FAST / PATH_GEN_SYM / PATH_GEN_NEAR
+  bool box;          // equal patch taps: running-sum box filter (general kernel)
+  int Rb;            // far band of a partial block (R, or 0 for tile-only blocks)
+  const Chunk* chunks;        // hat-tapered table (DSG), host (fast kernel)
   const Chunk* chunks_nohat;  // same offsets, L = 0 (plain NLM), host
-  const int* grp;             // NG+1 group starts, host
+  const int* grp;             // NG+1 group starts (chunks, or dy indices), host
+  const float* ltab;          // general kernel: log2 hat per offset, device
 };
 
 // A window of the global image handled by one call.
@@ -596,25 +601,72 @@ static int pick_groups(int ntiles, int nchunks) {
 #ifdef PNP_NG_OVERRIDE
   ng = PNP_NG_OVERRIDE;
 #endif
-  const int cm = PNP_CLUSTER;  // clusters (off by default) need a multiple of cm
-  if (ng > cm) {
-    const int up = (ng + cm - 1) / cm * cm;
-    ng = up <= nchunks ? up : nchunks / cm * cm;
-  }
   return ng < 1 ? 1 : ng;
 }
 
-// CTAs of one tile's offset groups that reduce their far/near planes through
-// distributed shared memory before writing one partial block (the cluster).
-static int cluster_size(int ng) { return ng <= PNP_CLUSTER ? ng : PNP_CLUSTER; }
+// Which sweep kernel a geometry uses -- a function of (R, P, box) only, so
+// adaptive, frozen, batched and sharded calls agree:
+//   PATH_FAST      Gaussian taps, P <= 15, R <= 32: the P-templated sweep
+//                  (dsg_sweep.cuh; k cache, packed f32x2 filter)
+//   PATH_GEN_SYM   box taps (the reference's patch distance) at any P, or
+//                  Gaussian beyond the fast kernel: the general sweep
+//                  (dsg_generic.cuh), half window, tile + band blocks
+//   PATH_GEN_NEAR  the general sweep over the full window, tile-only blocks
+//                  (search radii whose far plane exceeds shared memory)
+enum { PATH_FAST = 0, PATH_GEN_SYM = 1, PATH_GEN_NEAR = 2 };
+
+static int choose_path(int R, int P, bool box, int& kind, int& TH) {
+  if (!box && P <= kMaxP && R <= kMaxR) {
+    kind = PATH_FAST;
+    TH = tile_height(P);
+    return PNP_OK;
+  }
+  if (P > kGenMaxP)
+    return fail(PNP_EINVAL, "patch_side > " + std::to_string(kGenMaxP) + " not supported");
+  auto bytes = [&](int th, bool sym) { return (size_t)gen_smem(th, P, R, 2, sym).total * 4; };
+  const size_t two = 113 * 1024, one = 227 * 1024;  // 2 / 1 CTAs per SM
+  for (int th : {32, 16})
+    if (bytes(th, true) <= two) { kind = PATH_GEN_SYM; TH = th; return PNP_OK; }
+  for (int th : {32, 16, 8})
+    if (bytes(th, true) <= one) { kind = PATH_GEN_SYM; TH = th; return PNP_OK; }
+  for (int th : {32, 16, 8})
+    if (bytes(th, false) <= one) { kind = PATH_GEN_NEAR; TH = th; return PNP_OK; }
+  return fail(PNP_EINVAL, "patch / window too large for shared memory");
+}
+
+// The general kernel's offset groups: ranges of dy values, balanced by offset
+// count, about 4 CTAs per SM over the whole grid.
+static void gen_groups(int R, bool sym, int ntiles, std::vector<int>& grp) {
+  const int ndy = sym ? R + 1 : 2 * R + 1;
+  std::vector<long long> cnt(ndy);
+  long long total = 0;
+  for (int i = 0; i < ndy; ++i) {
+    const int dy = sym ? i : i - R;
+    cnt[i] = sym ? (dy == 0 ? R : 2 * R + 1) : (dy == 0 ? 2 * R : 2 * R + 1);
+    total += cnt[i];
+  }
+  int ng = (4 * 148 + ntiles / 2) / (ntiles > 0 ? ntiles : 1);
+  ng = std::max(1, std::min(std::min(ng, ndy), kMaxGroups));
+  grp.assign(1, 0);
+  long long acc = 0;
+  int k = 1;
+  for (int i = 0; i < ndy; ++i) {
+    acc += cnt[i];
+    if (k < ng && acc * ng >= total * k && i + 1 < ndy) {
+      grp.push_back(i + 1);
+      ++k;
+    }
+  }
+  grp.push_back(ndy);
+}
 
 static int check_geometry(int B, int H, int W, int R, int P, double bw) {
   if (B < 1) return fail(PNP_EINVAL, "batch must be >= 1");
   if (H < 1 || W < 1) return fail(PNP_EINVAL, "image must be at least 1x1");
   if (P < 1 || P % 2 == 0)
     return fail(PNP_EINVAL, "patch_side must be odd and >= 1, got " + std::to_string(P));
-  if (P > kMaxP)
-    return fail(PNP_EINVAL, "patch_side > " + std::to_string(kMaxP) + " not supported");
+  if (P > kGenMaxP)
+    return fail(PNP_EINVAL, "patch_side > " + std::to_string(kGenMaxP) + " not supported");
   if (R < 1) return fail(PNP_EINVAL, "window_radius must be >= 1, got " + std::to_string(R));
   if (!(bw > 0)) return fail(PNP_EINVAL, "bandwidth must be > 0");
   const int margin = R + (P - 1) / 2;
@@ -622,36 +674,80 @@ static int check_geometry(int B, int H, int W, int R, int P, double bw) {
   if (margin > mn)
     return fail(PNP_EINVAL, "margin " + std::to_string(margin) + " exceeds min image extent " +
                                 std::to_string(mn));
-  if (R > kMaxR)
-    return fail(PNP_EINVAL, "window_radius > " + std::to_string(kMaxR) + " not supported");
   return PNP_OK;
 }
 
-static int groups_for(int Hg, int W, int R, int P) {
-  const int TH = tile_height(P);
+// Equal taps select the box patch distance (the reference's own; general
+// kernel with running sums), anything else the separable Gaussian filter.
+static bool taps_box(const float* taps, int P) {
+  for (int i = 1; i < P; ++i)
+    if (taps[i] != taps[0]) return false;
+  return true;
+}
+
+static int groups_for(int Hg, int W, int R, int P, bool box) {
+  int kind = 0, TH = 0;
+  if (choose_path(R, P, box, kind, TH)) return -1;
   const int ntiles = ((W + kTW - 1) / kTW) * ((Hg + TH - 1) / TH);
+  if (kind != PATH_FAST) {
+    std::vector<int> grp;
+    gen_groups(R, kind == PATH_GEN_SYM, ntiles, grp);
+    return (int)grp.size() - 1;
+  }
   int nch = 0;
   for (int dx = -R; dx <= R; ++dx) nch += (R - (dx > 0 ? 0 : 1) + kKY) / kKY;
   return pick_groups(ntiles, nch);
 }
 
-static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, Geom& g) {
+static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, bool box, Geom& g) {
   g.B = B;
   g.Hg = Hg;
   g.W = W;
   g.R = R;
   g.P = P;
-  g.TH = tile_height(P);
+  g.box = box;
+  int rc = choose_path(R, P, box, g.kind, g.TH);
+  if (rc) return rc;
+  g.Rb = g.kind == PATH_GEN_NEAR ? 0 : R;
   g.tiles_x = (W + kTW - 1) / kTW;
   g.tiles_y = (Hg + g.TH - 1) / g.TH;
+  g.chunks = g.chunks_nohat = nullptr;
+  g.ltab = nullptr;
+  const int ntiles = g.tiles_x * g.tiles_y;
+  if (g.kind != PATH_FAST) {
+    std::vector<int> grp;
+    gen_groups(R, g.kind == PATH_GEN_SYM, ntiles, grp);
+    g.NG = g.NP = (int)grp.size() - 1;
+    g.nchunks = 0;
+    auto key = std::make_tuple(R, g.NG, g.kind);
+    auto it = ctx->tables.find(key);
+    if (it == ctx->tables.end()) {
+      pnp_ctx::Tables t;
+      t.grp = grp;
+      // log2 of the separable hat (denoise.py:199-201) per offset, in double,
+      // rounded once
+      const int n = 2 * R + 1;
+      std::vector<float> lt((size_t)n * n);
+      const double sc = R + 1.0;
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx)
+          lt[(size_t)(dy + R) * n + dx + R] =
+              (float)(log2(1.0 - fabs((double)dy) / sc) + log2(1.0 - fabs((double)dx) / sc));
+      if ((rc = t.ltab.ensure(lt.size() * sizeof(float)))) return rc;
+      PNP_CUDA(cudaMemcpy(t.ltab.ptr, lt.data(), lt.size() * sizeof(float),
+                          cudaMemcpyHostToDevice));
+      it = ctx->tables.emplace(key, std::move(t)).first;
+    }
+    g.grp = it->second.grp.data();
+    g.ltab = it->second.ltab.as<float>();
+    return PNP_OK;
+  }
   std::vector<Chunk> ch, ch0;
   build_chunks(R, true, ch);
   build_chunks(R, false, ch0);
   g.nchunks = (int)ch.size();
-  g.NG = pick_groups(g.tiles_x * g.tiles_y, g.nchunks);
-  g.CG = cluster_size(g.NG);
-  g.NP = g.NG / g.CG;
-  auto key = std::make_pair(R, g.NG);
+  g.NG = g.NP = pick_groups(ntiles, g.nchunks);
+  auto key = std::make_tuple(R, g.NG, g.kind);
   auto it = ctx->tables.find(key);
   if (it == ctx->tables.end()) {
     if (g.NG > kMaxGroups) return fail(PNP_EINVAL, "too many offset groups");
@@ -672,7 +768,7 @@ static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, Geom& g) 
 }
 
 static size_t block_floats(const Geom& g, int C) {
-  return (size_t)C * (g.TH + g.R) * (kTW + 2 * g.R);
+  return (size_t)C * (g.TH + g.Rb) * (kTW + 2 * g.Rb);
 }
 
 static size_t partial_floats(const Geom& g, int ntr, int C) {
@@ -711,9 +807,11 @@ static int ensure_counter(pnp_ctx* ctx) {
 // Fixup variant: one thread per pixel when there are many partial groups or
 // too few tiles to fill the GPU with one CTA per tile (same sums either way).
 static bool fixup_px(const Geom& g) {
-  // (32-bit offsets inside one image's partial array)
-  if ((double)g.tiles_y * g.NP * g.tiles_x * 2 * (g.TH + g.R) * (kTW + 2 * g.R) >= 4294967295.0)
+  // (32-bit offsets inside one image's partial array; a pixel covered by at
+  // most 3 tile rows and one side column of blocks)
+  if ((double)g.tiles_y * g.NP * g.tiles_x * 2 * (g.TH + g.Rb) * (kTW + 2 * g.Rb) >= 4294967295.0)
     return false;
+  if (g.Rb > 32 || (g.Rb + g.TH - 1) / g.TH > 2) return false;
   return g.NP > 2 || (long long)g.B * g.tiles_x * g.tiles_y < 2 * 148;
 }
 
@@ -767,7 +865,7 @@ static bool kcache_fits(pnp_ctx* ctx, size_t floats, size_t already) {
 // them when the whole cache fits, else as many as the budget allows (the
 // rest is recomputed -- same bits either way), 0 below 1/8 of the image.
 static int kcache_rows(pnp_ctx* ctx, const Geom& g, size_t already) {
-  if (ctx->cache_limit == 0) return 0;
+  if (ctx->cache_limit == 0 || g.kind != PATH_FAST) return 0;
   if (kcache_fits(ctx, kcache_floats(g, g.tiles_y), already)) return g.tiles_y;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
@@ -778,10 +876,91 @@ static int kcache_rows(pnp_ctx* ctx, const Geom& g, size_t already) {
   return rows * 8 >= g.tiles_y ? (rows < g.tiles_y ? rows : g.tiles_y) : 0;
 }
 
+// The k cache of one adaptive call: the caller-bound buffer (as many tile
+// rows as fit), else a stream-ordered pool allocation released by
+// kcache_release at the end of the call.  rows = 0: recompute (same bits).
+static int kcache_acquire(pnp_ctx* ctx, const Geom& g, float** kc, int* rows) {
+  *kc = nullptr;
+  *rows = 0;
+  ctx->kc_call = nullptr;
+  ctx->kc_call_pooled = false;
+  if (ctx->cache_limit == 0 || g.kind != PATH_FAST) return PNP_OK;
+  const size_t row_b = kcache_floats(g, 1) * sizeof(float);
+  if (ctx->kc_ext) {
+    size_t budget = ctx->kc_ext_bytes < ctx->cache_limit ? ctx->kc_ext_bytes : ctx->cache_limit;
+    int r = (int)std::min<size_t>(budget / row_b, (size_t)g.tiles_y);
+    if (r * 8 < g.tiles_y) r = 0;
+    *kc = r ? static_cast<float*>(ctx->kc_ext) : nullptr;
+    *rows = r;
+    ctx->kc_call = *kc;
+    return PNP_OK;
+  }
+  const int r = kcache_rows(ctx, g, 0);
+  if (r <= 0) return PNP_OK;
+  void* p = nullptr;
+  if (pool_alloc(ctx, &p, (size_t)r * row_b) != cudaSuccess) {
+    cudaGetLastError();
+    return PNP_OK;  // not fatal: recompute
+  }
+  *kc = static_cast<float*>(p);
+  *rows = r;
+  ctx->kc_call = *kc;
+  ctx->kc_call_pooled = true;
+  return PNP_OK;
+}
+
+static void kcache_release(pnp_ctx* ctx) {
+  if (ctx->kc_call && ctx->kc_call_pooled) cudaFreeAsync(ctx->kc_call, ctx->stream);
+  ctx->kc_call = nullptr;
+  ctx->kc_call_pooled = false;
+}
+
+static int run_sweep_gen(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const float* guide,
+                         ChanSpec c0, ChanSpec c1, const float* taps, double bw, bool use_hat,
+                         float* partial) {
+  GenArgs a;
+  memset(&a, 0, sizeof(a));
+  a.guide = guide;
+  a.ch[0] = c0;
+  a.ch[1] = c1;
+  a.partial = partial;
+  a.ltab = use_hat ? g.ltab : nullptr;
+  a.Hg = g.Hg;
+  a.W = g.W;
+  a.R = g.R;
+  a.P = g.P;
+  a.TH = g.TH;
+  a.buf_r0 = w.buf_r0;
+  a.buf_rows = w.buf_rows;
+  a.tr0 = w.tr0;
+  a.tiles_x = g.tiles_x;
+  a.part_off = w.part_off;
+  a.part_ntr = w.part_ntr;
+  // k = exp(-SSD / (2 P^2 bw^2)) (box, denoise.py:186,194) = ex2(cv * SSD);
+  // Gaussian: exp(-sum w_a w_b D / (2 bw^2)) with the scale folded into w_a
+  const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
+  a.cv = (float)(scale / ((double)g.P * g.P));
+  for (int i = 0; i < g.P; ++i) {
+    a.taps_h[i] = taps[i];
+    a.taps_v[i] = (float)(scale * (double)taps[i]);
+  }
+  for (int i = 0; i <= g.NG; ++i) a.grp[i] = g.grp[i];
+  dim3 grid(w.ntr * g.tiles_x, g.NG, g.B);
+  ProfScope prof(ctx, PROF_SWEEP);
+  cudaError_t e = launch_generic(a, C, g.box, g.kind == PATH_GEN_SYM, grid, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dsg_generic_kernel");
+  return PNP_OK;
+}
+
 static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const float* guide,
                      ChanSpec c0, ChanSpec c1, const float* taps, double bw, bool use_hat,
                      float* partial, int mode = MODE_RECOMPUTE, float* kcache = nullptr) {
   if (w.ntr <= 0) return PNP_OK;
+  if (g.kind != PATH_FAST) {
+    if (mode != MODE_RECOMPUTE && mode != MODE_STORE)
+      return fail(PNP_EINVAL, "the general sweep has no k cache");
+    return run_sweep_gen(ctx, g, w, C, guide, c0, c1, taps, bw, use_hat, partial);
+  }
   SweepArgs a;
   memset(&a, 0, sizeof(a));
   a.guide = guide;
@@ -800,7 +979,6 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   a.part_ntr = w.part_ntr;
   a.kcache = kcache;
   a.kc_tile = (long long)half_window(g.R) * g.TH * kTW;
-  a.cg = g.CG;
   a.kc_img = (long long)w.ntr * g.tiles_x * a.kc_tile;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
@@ -849,7 +1027,7 @@ static int run_fixup(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   f.partial = partial;
   f.Hg = g.Hg;
   f.W = g.W;
-  f.R = g.R;
+  f.R = g.Rb;
   f.TH = g.TH;
   f.tiles_x = g.tiles_x;
   f.NP = g.NP;
@@ -960,9 +1138,10 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   ctx->mbits.release();
   ctx->stats.release();
   ctx->flags.release();
-  ctx->kcache.release();
+  kcache_release(ctx);
   ctx->cg.release();
   ctx->counter.release();
+  for (auto& kv : ctx->tables) kv.second.ltab.release();
   for (auto& sl : ctx->slots) {
     cudaEventDestroy(sl.a);
     cudaEventDestroy(sl.b);
@@ -992,7 +1171,28 @@ int pnp_ctx_synchronize(pnp_ctx* ctx) {
 int pnp_ctx_set_cache_limit(pnp_ctx* ctx, int64_t bytes) {
   if (!ctx) return fail(PNP_EINVAL, "ctx is null");
   ctx->cache_limit = bytes < 0 ? (size_t)-1 : (size_t)bytes;
-  if (ctx->cache_limit == 0) ctx->kcache.release();
+  return PNP_OK;
+}
+
+int pnp_ctx_bind_kcache(pnp_ctx* ctx, void* ptr, int64_t bytes) {
+  if (!ctx) return fail(PNP_EINVAL, "ctx is null");
+  if (ptr && bytes > 0) {
+    ctx->kc_ext = ptr;
+    ctx->kc_ext_bytes = (size_t)bytes;
+  } else {
+    ctx->kc_ext = nullptr;
+    ctx->kc_ext_bytes = 0;
+  }
+  return PNP_OK;
+}
+
+int pnp_ctx_trim(pnp_ctx* ctx) {
+  if (!ctx) return fail(PNP_EINVAL, "ctx is null");
+  PNP_CUDA(cudaSetDevice(ctx->device));
+  PNP_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaMemPool_t pool;
+  PNP_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+  PNP_CUDA(cudaMemPoolTrimTo(pool, 0));
   return PNP_OK;
 }
 
@@ -1022,13 +1222,13 @@ int pnp_ctx_profile_read(pnp_ctx* ctx, double* ms, int* launches) {
   return PNP_OK;
 }
 
-int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P) {
+int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P, int box) {
   if (!ctx) return fail(PNP_EINVAL, "ctx is null");
   int rc = check_geometry(batch, H, W, R, P, 1.0);
   if (rc) return rc;
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, box != 0, g))) return rc;
   if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   if ((rc = ensure_planes(ctx, (size_t)batch * H * W))) return rc;
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return rc;
@@ -1045,7 +1245,7 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   if (!guide) guide = x;
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, taps_box(taps, P), g))) return rc;
   const size_t n = (size_t)batch * H * W;
   if ((rc = ensure_planes(ctx, n))) return rc;
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return rc;
@@ -1056,15 +1256,14 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   float* part = ctx->partial.as<float>();
   const Window w = full_window(g);
   float* kc = nullptr;
-  const int kc_rows = kcache_rows(ctx, g, ctx->kcache.bytes);
-  if (kc_rows > 0) {
-    if ((rc = ctx->kcache.ensure(kcache_floats(g, kc_rows) * sizeof(float)))) return rc;
-    kc = ctx->kcache.as<float>();
-  }
-  if ((rc = mass_and_rs(ctx, g, guide, taps, bandwidth, rs, kc, kc_rows))) return rc;
-  if ((rc = run_sweep_kc(ctx, g, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps,
-                         bandwidth, part, MODE_CACHED, kc, kc_rows)))
-    return rc;
+  int kc_rows = 0;
+  if ((rc = kcache_acquire(ctx, g, &kc, &kc_rows))) return rc;
+  rc = mass_and_rs(ctx, g, guide, taps, bandwidth, rs, kc, kc_rows);
+  if (!rc)
+    rc = run_sweep_kc(ctx, g, 2, guide, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps, bandwidth,
+                      part, MODE_CACHED, kc, kc_rows);
+  kcache_release(ctx);  // stream-ordered: after sweep B
+  if (rc) return rc;
   PNP_CUDA(cudaMemsetAsync(ctx->mbits.ptr, 0, batch * sizeof(unsigned), ctx->stream));
   FixIO io{};
   io.rs = rs;
@@ -1088,10 +1287,14 @@ static void band_split(int H, int R, int P, int nbands, int* tile_end, int* rows
   }
 }
 
-int pnp_dsg_band_rows(int H, int W, int R, int P, int nbands, int* tile_end, int* rows_needed) {
+int pnp_dsg_band_rows(int H, int W, int R, int P, int box, int nbands, int* tile_end,
+                      int* rows_needed) {
   if (!tile_end || !rows_needed || nbands < 1) return fail(PNP_EINVAL, "bad arguments");
   int rc = check_geometry(1, H, W, R, P, 1.0);
   if (rc) return rc;
+  int kind = 0, th = 0;
+  if ((rc = choose_path(R, P, box != 0, kind, th))) return rc;
+  if (kind != PATH_FAST) return fail(PNP_EINVAL, "banded denoise needs the P-templated sweep");
   if (nbands > (H + tile_height(P) - 1) / tile_height(P))
     return fail(PNP_EINVAL, "more bands than tile rows");
   band_split(H, R, P, nbands, tile_end, rows_needed);
@@ -1114,20 +1317,22 @@ int pnp_dsg_band_sweep(pnp_ctx* ctx, const float* x, int H, int W, int R, int P,
   if (j > 0 && ctx->band_next != j) return fail(PNP_EINVAL, "bands must be swept in order from 0");
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, 1, H, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, 1, H, W, R, P, taps_box(taps, P), g))) return rc;
+  if (g.kind != PATH_FAST) return fail(PNP_EINVAL, "banded denoise needs the P-templated sweep");
   if (nbands > g.tiles_y) return fail(PNP_EINVAL, "more bands than tile rows");
   if (j == 0) {
     if ((rc = ensure_planes(ctx, (size_t)H * W))) return rc;
     if ((rc = ctx->mbits.ensure(sizeof(unsigned)))) return rc;
     if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
-    const int kc_rows = kcache_rows(ctx, g, ctx->kcache.bytes);
-    if (kc_rows > 0 && (rc = ctx->kcache.ensure(kcache_floats(g, kc_rows) * sizeof(float))))
-      return rc;
+    kcache_release(ctx);  // an abandoned earlier banded call
+    float* kc0 = nullptr;
+    int kc_rows = 0;
+    if ((rc = kcache_acquire(ctx, g, &kc0, &kc_rows))) return rc;
     ctx->band_kc_rows = kc_rows;
   }
   float* part = ctx->partial.as<float>();
   const int kc_rows = ctx->band_kc_rows;
-  float* kc = kc_rows > 0 ? ctx->kcache.as<float>() : nullptr;
+  float* kc = kc_rows > 0 ? ctx->kc_call : nullptr;
   std::vector<int> tend(nbands), need(nbands);
   band_split(H, R, P, nbands, tend.data(), need.data());
   const size_t kc_row = (size_t)g.tiles_x * half_window(g.R) * g.TH * kTW;
@@ -1165,22 +1370,23 @@ int pnp_dsg_band_finish(pnp_ctx* ctx, const float* x, float* out, int H, int W, 
   ctx->band_next = -1;
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, 1, H, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, 1, H, W, R, P, taps_box(taps, P), g))) return rc;
   float* rs = ctx->rs.as<float>();
   float* kx = ctx->kx.as<float>();
   float* d = ctx->d.as<float>();
   float* part = ctx->partial.as<float>();
   const int kc_rows = ctx->band_kc_rows;
-  float* kc = kc_rows > 0 ? ctx->kcache.as<float>() : nullptr;
+  float* kc = kc_rows > 0 ? ctx->kc_call : nullptr;
   const Window w = full_window(g);
   {
     FixIO io{};
     io.rs = rs;
-    if ((rc = run_fixup<FIX_RS>(ctx, g, w, 1, part, io))) return rc;
+    if ((rc = run_fixup<FIX_RS>(ctx, g, w, 1, part, io))) return kcache_release(ctx), rc;
   }
-  if ((rc = run_sweep_kc(ctx, g, 2, x, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps, bandwidth,
-                         part, MODE_CACHED, kc, kc_rows)))
-    return rc;
+  rc = run_sweep_kc(ctx, g, 2, x, ChanSpec{rs, x}, ChanSpec{rs, nullptr}, taps, bandwidth, part,
+                    MODE_CACHED, kc, kc_rows);
+  kcache_release(ctx);
+  if (rc) return rc;
   PNP_CUDA(cudaMemsetAsync(ctx->mbits.ptr, 0, sizeof(unsigned), ctx->stream));
   FixIO io{};
   io.rs = rs;
@@ -1212,7 +1418,7 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   if ((rc = validate_taps(taps, P))) return rc;
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, taps_box(taps, P), g))) return rc;
   if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   const size_t n = (size_t)batch * H * W;
   pnp_frozen* fz = new pnp_frozen();
@@ -1280,7 +1486,7 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
   if (fz->device != ctx->device) return fail(PNP_EINVAL, "handle belongs to another device");
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  int rc = make_geom(ctx, fz->B, fz->H, fz->W, fz->R, fz->P, g);
+  int rc = make_geom(ctx, fz->B, fz->H, fz->W, fz->R, fz->P, taps_box(fz->taps, fz->P), g);
   if (rc) return rc;
   if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   const Window w = full_window(g);
@@ -1306,7 +1512,7 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
   if (fz->device != ctx->device) return fail(PNP_EINVAL, "handle belongs to another device");
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  int rc = make_geom(ctx, fz->B, fz->H, fz->W, fz->R, fz->P, g);
+  int rc = make_geom(ctx, fz->B, fz->H, fz->W, fz->R, fz->P, taps_box(fz->taps, fz->P), g);
   if (rc) return rc;
   if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   const Window w = full_window(g);
@@ -1352,7 +1558,10 @@ int pnp_frozen_destroy(pnp_frozen* fz) {
 int pnp_frozen_alpha(const pnp_frozen* fz, float* alpha_host) {
   if (!fz || !alpha_host) return fail(PNP_EINVAL, "null argument");
   PNP_CUDA(cudaSetDevice(fz->device));
-  PNP_CUDA(cudaMemcpy(alpha_host, fz->mv, fz->B * sizeof(float), cudaMemcpyDeviceToHost));
+  // mv is written on the handle's stream (which may be a non-blocking one)
+  PNP_CUDA(cudaMemcpyAsync(alpha_host, fz->mv, fz->B * sizeof(float), cudaMemcpyDeviceToHost,
+                           fz->stream));
+  PNP_CUDA(cudaStreamSynchronize(fz->stream));
   return PNP_OK;
 }
 
@@ -1395,7 +1604,7 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
   if (!guide) guide = x;
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, batch, H, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, batch, H, W, R, P, taps_box(taps, P), g))) return rc;
   if ((rc = ctx->partial.ensure(partial_floats(g, g.tiles_y, 2) * sizeof(float)))) return rc;
   const Window w = full_window(g);
   float* part = ctx->partial.as<float>();
@@ -1410,24 +1619,56 @@ int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
 
 // ---------------------------------------------------------------- strips ---
 
-int pnp_tile_height(int P) { return (P >= 1 && P <= kMaxP && (P & 1)) ? tile_height(P) : -1; }
+int pnp_dsg_geometry(int Hg, int W, int R, int P, int box, int* out) {
+  if (!out) return fail(PNP_EINVAL, "null argument");
+  int rc = check_geometry(1, Hg, W, R, P, 1.0);
+  if (rc) return rc;
+  int kind = 0, TH = 0;
+  if ((rc = choose_path(R, P, box != 0, kind, TH))) return rc;
+  const int p = (P - 1) / 2;
+  out[0] = TH;
+  out[1] = groups_for(Hg, W, R, P, box != 0);
+  out[2] = kind == PATH_GEN_NEAR ? 0 : R;  // far band of a partial block
+  out[3] = kind;
+  // input rows a tile row reads above / below its own rows, and rows of the
+  // channel planes (rs) below
+  if (kind == PATH_FAST) {
+    out[4] = p;
+    out[5] = R + (p > kKY ? p : kKY);
+    out[6] = R + kKY - 1;
+  } else if (kind == PATH_GEN_SYM) {
+    out[4] = p;
+    out[5] = R + p;
+    out[6] = R;
+  } else {
+    out[4] = R + p;
+    out[5] = R + p;
+    out[6] = R;
+  }
+  out[7] = 0;
+  return PNP_OK;
+}
 
-int pnp_dsg_groups(int Hg, int W, int R, int P) {
+int pnp_dsg_groups(int Hg, int W, int R, int P, int box) {
   if (check_geometry(1, Hg, W, R, P, 1.0)) return -1;
-  return groups_for(Hg, W, R, P);
+  return groups_for(Hg, W, R, P, box != 0);
 }
 
-int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int C, int ntr) {
+int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int box, int C, int ntr) {
   if (check_geometry(1, Hg, W, R, P, 1.0) || C < 1 || C > 2 || ntr < 0) return -1;
-  const int TH = tile_height(P);
-  const int64_t blk = (int64_t)C * (TH + R) * (kTW + 2 * R);
-  const int ng = groups_for(Hg, W, R, P);  // partial groups: NG / cluster size
-  return (int64_t)ntr * (ng / cluster_size(ng)) * ((W + kTW - 1) / kTW) * blk;
+  int kind = 0, TH = 0;
+  if (choose_path(R, P, box != 0, kind, TH)) return -1;
+  const int Rb = kind == PATH_GEN_NEAR ? 0 : R;
+  const int64_t blk = (int64_t)C * (TH + Rb) * (kTW + 2 * Rb);
+  return (int64_t)ntr * groups_for(Hg, W, R, P, box != 0) * ((W + kTW - 1) / kTW) * blk;
 }
 
-int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int ntr) {
+int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int box, int ntr) {
   if (check_geometry(1, Hg, W, R, P, 1.0) || ntr < 0) return -1;
-  return (int64_t)half_window(R) * ntr * tile_height(P) * (((W + kTW - 1) / kTW) * kTW);
+  int kind = 0, TH = 0;
+  if (choose_path(R, P, box != 0, kind, TH)) return -1;
+  if (kind != PATH_FAST) return 0;  // the general sweep recomputes its weights
+  return (int64_t)half_window(R) * ntr * TH * (((W + kTW - 1) / kTW) * kTW);
 }
 
 int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float* x,
@@ -1442,7 +1683,7 @@ int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float*
   if (ntr < 0 || part_off < 0 || part_off + ntr > part_ntr) return fail(PNP_EINVAL, "bad tiles");
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, 1, Hg, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, 1, Hg, W, R, P, taps_box(taps, P), g))) return rc;
   if (tr0 < 0 || tr0 + ntr > g.tiles_y) return fail(PNP_EINVAL, "tile rows out of range");
   Window w{buf_r0, buf_rows, tr0, ntr, 0, part_off, part_ntr, 0, 0};
   const int use = kcache ? MODE_CACHED : MODE_RECOMPUTE;
@@ -1468,7 +1709,7 @@ int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float*
 }
 
 int pnp_dsg_strip_fixup(pnp_ctx* ctx, int mode, const float* partial, int part_tr0,
-                        int part_ntr, int Hg, int W, int R, int P, int y0, int y1, int buf_r0,
+                        int part_ntr, int Hg, int W, int R, int P, int box, int y0, int y1, int buf_r0,
                         int buf_rows, float* rs, float* kx, float* d, unsigned* mbits,
                         const float* inv_m, const float* x, float* out) {
   if (!ctx || !partial) return fail(PNP_EINVAL, "null argument");
@@ -1477,7 +1718,7 @@ int pnp_dsg_strip_fixup(pnp_ctx* ctx, int mode, const float* partial, int part_t
   if (y0 < buf_r0 || y1 > buf_r0 + buf_rows || y0 > y1) return fail(PNP_EINVAL, "bad rows");
   PNP_CUDA(cudaSetDevice(ctx->device));
   Geom g;
-  if ((rc = make_geom(ctx, 1, Hg, W, R, P, g))) return rc;
+  if ((rc = make_geom(ctx, 1, Hg, W, R, P, box != 0, g))) return rc;
   Window w{buf_r0, buf_rows, 0, 0, part_tr0, 0, part_ntr, y0, y1 - y0};
   FixIO io{};
   io.rs = rs;

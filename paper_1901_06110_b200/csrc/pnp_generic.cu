@@ -1,0 +1,36 @@
+// Instantiations + launcher of the general DSG sweep (dsg_generic.cuh).
+#include <atomic>
+
+#include "dsg_generic.cuh"
+
+namespace pnp {
+
+template <int C, bool BOX, bool SYM>
+static cudaError_t launch_gen_t(const GenArgs& a, dim3 grid, cudaStream_t st) {
+  const size_t smem = (size_t)gen_smem(a.TH, a.P, a.R, C, SYM).total * sizeof(float);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  // opt in to the largest dynamic shared memory once per device
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(dsg_generic_kernel<C, BOX, SYM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  return launch_pdl(dsg_generic_kernel<C, BOX, SYM>, grid, dim3(kGenThreads), smem, st, a);
+}
+
+cudaError_t launch_generic(const GenArgs& a, int C, bool box, bool sym, dim3 grid,
+                           cudaStream_t st) {
+  if (C == 1) {
+    if (box) return sym ? launch_gen_t<1, true, true>(a, grid, st) : launch_gen_t<1, true, false>(a, grid, st);
+    return sym ? launch_gen_t<1, false, true>(a, grid, st) : launch_gen_t<1, false, false>(a, grid, st);
+  }
+  if (box) return sym ? launch_gen_t<2, true, true>(a, grid, st) : launch_gen_t<2, true, false>(a, grid, st);
+  return sym ? launch_gen_t<2, false, true>(a, grid, st) : launch_gen_t<2, false, false>(a, grid, st);
+}
+
+}  // namespace pnp

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>
@@ -61,17 +62,26 @@ struct pnp_ctx {
   int sms = 148;
   cudaStream_t stream = 0;
   pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
-  pnp::DevBuf kcache;              // pair weights of the last adaptive denoise
+  // adaptive-denoise k cache: a caller-bound buffer (pnp_ctx_bind_kcache; the
+  // Python layer binds torch-allocated memory per call), else allocated from
+  // the stream-ordered pool at the start of the call and freed at its end
+  void* kc_ext = nullptr;
+  size_t kc_ext_bytes = 0;
+  float* kc_call = nullptr;        // the current call's cache (banded calls)
+  bool kc_call_pooled = false;
   pnp::DevBuf cg;                  // conjugate-gradients work vectors + state
   pnp::DevBuf counter;             // last-CTA reduction counter (kept at zero)
   size_t cache_limit = (size_t)-1;  // bytes; 0 disables the k cache
-  // offset tables keyed by (R, NG): host blobs of Chunk (hat, no-hat) + NG+1
-  // group starts; they reach the kernels through the launch parameters
+  // offset tables keyed by (R, NG, sweep path): host blobs of Chunk (hat,
+  // no-hat) + NG+1 group starts, which reach the kernels through the launch
+  // parameters; the general kernel's dy-group starts + a device table of
+  // log2 hat per offset
   struct Tables {
     std::vector<char> hat, nohat;
     std::vector<int> grp;
+    pnp::DevBuf ltab;
   };
-  std::map<std::pair<int, int>, Tables> tables;
+  std::map<std::tuple<int, int, int>, Tables> tables;
   // per-iteration timing events of the native ADMM loop (pnp_admm_run)
   std::vector<cudaEvent_t> iter_events;
   // its side stream (the next iteration's SR residual overlaps the denoiser),
@@ -126,7 +136,7 @@ int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, con
 struct pnp_frozen {
   int device = 0;
   int B = 0, H = 0, W = 0, R = 0, P = 0;
-  float taps[16] = {0};
+  float taps[64] = {0};
   double bw = 0;
   float* guide = nullptr;  // B*H*W
   float* rs = nullptr;     // B*H*W

@@ -6,42 +6,11 @@
 #include <cstring>
 
 #include "dsg_sweep.cuh"
-#include "dsg_sweep_ws.cuh"
-
-#ifndef PNP_WS
-#define PNP_WS 0  // warp-specialized sweep A (dsg_sweep_ws.cuh)
-#endif
 
 namespace pnp {
 
-template <int P, int RB, int MODE>
-cudaError_t launch_sweep_ws(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st) {
-  constexpr size_t smem = (size_t)CfgWs<P, RB, MODE>::TOTAL * sizeof(float);
-  static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
-  static std::atomic<unsigned long long> attr_set{0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(dsg_sweep_ws_kernel<P, RB, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set.fetch_or(bit, std::memory_order_acq_rel);
-  }
-  ChunkTab<RB> tab;
-  memset(&tab, 0, sizeof(tab));
-  memcpy(tab.c, t.ch, sizeof(Chunk) * t.nch);
-  memcpy(tab.grp, t.grp, sizeof(int) * (t.ng + 1));
-  dsg_sweep_ws_kernel<P, RB, MODE><<<grid, kWsThreads, smem, st>>>(a, tab);
-  return cudaGetLastError();
-}
-
 template <int P, int RB, int C, int MODE>
 cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st) {
-  if constexpr (PNP_WS && C == 1 && MODE != MODE_CACHED) {
-    if (a.cg <= 1 && t.nch <= max_chunks(RB) && t.ng <= kMaxGroups)
-      return launch_sweep_ws<P, RB, MODE>(a, t, grid, st);
-  }
   constexpr size_t smem = (size_t)Cfg<P, RB, C, MODE>::TOTAL * sizeof(float);
   static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
   // the opt-in shared-memory size is a per-device function attribute
@@ -60,27 +29,8 @@ cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaSt
   memset(&tab, 0, sizeof(tab));
   memcpy(tab.c, t.ch, sizeof(Chunk) * t.nch);
   memcpy(tab.grp, t.grp, sizeof(int) * (t.ng + 1));
-  if (a.cg <= 1) {
-    return launch_pdl(dsg_sweep_kernel<P, RB, C, MODE>, grid, dim3(kThreads), smem, st, a, tab);
-  }
-  // a tile's offset groups as one thread-block cluster (grid.y = NG, a
-  // multiple of cg): they reduce their planes on chip (dsg_sweep.cuh)
-  if (a.cg > kMaxCluster || grid.y % a.cg) return cudaErrorInvalidValue;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = (unsigned)a.cg;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, dsg_sweep_kernel<P, RB, C, MODE>, a, tab);
+  return launch_pdl(dsg_sweep_kernel<P, RB, C, MODE>, grid, dim3(kThreads), smem, st, a, tab);
 }
-
 
 #define PNP_INSTANTIATE_P(P) \
   template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \

@@ -14,6 +14,7 @@ BASELINE.json configs); ``None`` keeps the reference's box patch distance.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 from dataclasses import dataclass
@@ -63,6 +64,12 @@ class PatchParams:
         a = np.arange(P, dtype=np.float64) - (P - 1) // 2
         w = np.exp(-(a * a) / (2.0 * self.patch_sigma ** 2))
         return w / w.sum()
+
+    @property
+    def is_box(self) -> bool:
+        """The reference's box patch distance (equal taps): the library runs
+        it with running-sum box filters, cost flat in P."""
+        return self.patch_sigma is None or self.patch_side == 1
 
     def _ctaps(self):
         return (C.c_float * self.patch_side)(*[float(v) for v in self.taps()])
@@ -143,6 +150,54 @@ def build_dense_weights(guide, params: PatchParams):
     return A.from_device64(out, kind)
 
 
+_KC_HEADROOM = 4 << 30
+
+
+def _kcache_bytes(dev: int, B: int, H: int, W: int, params: PatchParams) -> int:
+    """Bytes of the adaptive k cache to bind: all tile rows when they fit in
+    what torch can hand out (free HBM + its idle cache, less 4 GiB), else as
+    many as fit (the rest recompute, same bits), 0 below 1/8 of them."""
+    limit = L.cache_limits.get(dev, None)
+    if limit == 0:
+        return 0
+    row = int(L.lib.pnp_dsg_kcache_floats(H, W, params.window_radius, params.patch_side,
+                                          int(params.is_box), 1)) * 4 * B
+    if row <= 0:
+        return 0
+    tiles = -(-H // L.dsg_geometry(H, W, params.window_radius, params.patch_side,
+                                   params.is_box)[0])
+    free, _ = torch.cuda.mem_get_info(dev)
+    idle = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    budget = free + idle - _KC_HEADROOM
+    if limit is not None:
+        budget = min(budget, limit)
+    rows = min(tiles, max(0, budget) // row)
+    return rows * row if rows * 8 >= tiles else 0
+
+
+@contextlib.contextmanager
+def kcache_scope(dev: int, B: int, H: int, W: int, params: PatchParams):
+    """Bind a k cache from torch's caching allocator to this thread's native
+    context for one adaptive call (or one DenoiseStream run): torch owns the
+    memory, sees it, and recycles it when the scope ends (allocated on the
+    current stream, which the context is bound to)."""
+    buf = None
+    if not torch.cuda.is_current_stream_capturing():
+        n = _kcache_bytes(dev, B, H, W, params)
+        if n:
+            try:
+                buf = torch.empty(n, dtype=torch.uint8, device=torch.device("cuda", dev))
+            except torch.cuda.OutOfMemoryError:
+                buf = None
+    ctx = L.context(dev)
+    L.call("pnp_ctx_bind_kcache", ctx, L.ptr(buf), 0 if buf is None else buf.numel())
+    try:
+        yield
+    finally:
+        L.call("pnp_ctx_bind_kcache", ctx, None, 0)
+        del buf
+
+
 def _pair(image, guide):
     """_check_pair (denoise.py:244-251) -> device tensors + result kind."""
     image, kind = A.validate(image, "image", batch_ok=True)
@@ -184,10 +239,10 @@ def dsg_nlm_denoise(image, params: PatchParams, guide=None, distances: str = "in
     out = torch.empty_like(x)
     d = torch.empty_like(x) if return_aux else None
     alpha = torch.empty(B, dtype=torch.float32, device=x.device) if return_aux else None
-    ctx = L.context(dev)
-    L.call("pnp_dsg_denoise", ctx, L.ptr(x), L.ptr(g), L.ptr(out), B, H, W,
-           params.window_radius, params.patch_side, params._ctaps(), float(params.bandwidth),
-           L.ptr(d), L.ptr(alpha))
+    with kcache_scope(dev, B, H, W, params):
+        L.call("pnp_dsg_denoise", L.context(dev), L.ptr(x), L.ptr(g), L.ptr(out), B, H, W,
+               params.window_radius, params.patch_side, params._ctaps(), float(params.bandwidth),
+               L.ptr(d), L.ptr(alpha))
     res = A.from_device(out, kind)
     if return_aux:
         return res, A.from_device(d, kind), (alpha if kind == A.TORCH else alpha.cpu().numpy().astype(np.float64))
@@ -202,19 +257,24 @@ _NP_BANDS = 8
 
 def _numpy_bands(image, params: PatchParams):
     """Input rows [0, need[j]) of each band when the banded numpy path
-    applies (a large finite-typed 2-D numpy image, guide = image), else None."""
+    applies (a large 2-D numpy image of a native-endian float / integer type,
+    guide = image, the P-templated sweep), else None: everything else takes
+    the validated one-shot path."""
     if isinstance(image, torch.Tensor):
         return None
     a = np.asarray(image)
-    if a.ndim != 2 or a.size < A._BIG or a.dtype.kind not in "fiu":
+    if (a.ndim != 2 or a.size < A._BIG or a.dtype.kind not in "fiu" or a.dtype.itemsize > 8
+            or not a.dtype.isnative):
         return None
     H, W = a.shape
-    TH = 32 - (params.patch_side - 1)
-    if -(-H // TH) < 2 * _NP_BANDS or params.pad_margin > min(H, W):
+    if params.pad_margin > min(H, W):
+        return None
+    geom = L.dsg_geometry(H, W, params.window_radius, params.patch_side, params.is_box)
+    if geom[3] != 0 or -(-H // geom[0]) < 2 * _NP_BANDS:
         return None
     te, need = (C.c_int * _NP_BANDS)(), (C.c_int * _NP_BANDS)()
-    L.call("pnp_dsg_band_rows", H, W, params.window_radius, params.patch_side, _NP_BANDS, te,
-           need)
+    L.call("pnp_dsg_band_rows", H, W, params.window_radius, params.patch_side,
+           int(params.is_box), _NP_BANDS, te, need)
     return list(need)
 
 
@@ -235,7 +295,7 @@ def _dsg_numpy_banded(image, params: PatchParams, bands):
     h2d.wait_stream(cur)
     ctx = L.context(dev)
     taps, R, P, bw = params._ctaps(), params.window_radius, params.patch_side, float(params.bandwidth)
-    with A.staging() as st:
+    with A.staging() as st, kcache_scope(dev, 1, H, W, params):
         stage = st.f32("in", H * W).view(H, W)
         r0 = 0
         for j, r1 in enumerate(bands):
@@ -245,6 +305,7 @@ def _dsg_numpy_banded(image, params: PatchParams, bands):
                 with torch.cuda.stream(h2d):
                     x[r0:r1].copy_(stage[r0:r1], non_blocking=True)
                     ev.record(h2d)
+                x.record_stream(h2d)  # x stays allocated until the uploads land
                 cur.wait_event(ev)
                 r0 = r1
             L.call("pnp_dsg_band_sweep", ctx, L.ptr(x), H, W, R, P, taps, bw, len(bands), j)

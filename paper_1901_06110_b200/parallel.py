@@ -4,11 +4,12 @@ A large image (config 4: 8192^2) is split into row strips of whole tiles,
 one per rank (one process per GPU, ``torch.distributed`` over NCCL for the
 plumbing).  One adaptive denoise is
 
-    halo rows of the input (p above, R + max(p, KY) below)   [P2P exchange]
+    halo rows of the input (pnp_dsg_geometry: p above,
+      R + max(p, KY) below for the P-templated sweep)        [P2P exchange]
     sweep A (mass g) on own tile rows (+ the strip's k cache when it fits)
     the last ceil(R/TH) tile rows of partial blocks -> next rank
     fixup: rs = g^-1/2 on own rows
-    R + KY rows of rs -> previous rank                         [P2P exchange]
+    the rs rows the sweep reads below -> previous rank       [P2P exchange]
     sweep B (K x and d) on own tile rows (streams the k cache if present)
     partial blocks -> next rank                                [P2P exchange]
     fixup: K x, d, local max d
@@ -34,12 +35,12 @@ import torch
 from . import _lib as L
 from .denoise import PatchParams
 
-KY = 4  # offsets per chunk in the sweep (csrc/dsg_sweep.cuh kKY)
-
-
 @dataclass(frozen=True)
 class StripLayout:
-    """Which rows / tile rows rank ``rank`` of ``nranks`` owns and reads."""
+    """Which rows / tile rows rank ``rank`` of ``nranks`` owns and reads.
+    Tile height, block band and halos come from the library
+    (``pnp_dsg_geometry``): they depend on the sweep path, i.e. on (R, P)
+    and whether the patch taps are the reference's box taps."""
 
     Hg: int
     W: int
@@ -47,10 +48,25 @@ class StripLayout:
     P: int
     nranks: int
     rank: int
+    box: bool = False
+
+    @property
+    def geom(self) -> tuple:
+        return L.dsg_geometry(self.Hg, self.W, self.R, self.P, self.box)
 
     @property
     def TH(self) -> int:
-        return 32 - (self.P - 1)
+        return self.geom[0]
+
+    @property
+    def Rb(self) -> int:
+        """Far band of a partial block (0: blocks cover the tile only)."""
+        return self.geom[2]
+
+    @property
+    def rs_below(self) -> int:
+        """Rows of the channel planes a tile row's sweep reads below it."""
+        return self.geom[6]
 
     @property
     def tiles_y(self) -> int:
@@ -69,12 +85,12 @@ class StripLayout:
     @property
     def dti(self) -> int:
         """Tile rows of the rank above whose partial blocks reach our rows."""
-        return -(-self.R // self.TH)
+        return -(-self.Rb // self.TH)
 
     @property
     def halo(self) -> tuple[int, int]:
-        p = (self.P - 1) // 2
-        return p, self.R + max(p, KY)
+        g = self.geom
+        return g[4], g[5]
 
     @property
     def window(self) -> tuple[int, int]:
@@ -111,11 +127,13 @@ class _RankState:
         self.d = torch.zeros_like(self.buf)
         self.out = torch.zeros_like(self.buf)
         self.mbits = torch.zeros(1, dtype=torch.int32, device=device)
-        pf = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, 2, lay.part[2]))
+        box = int(lay.box)
+        pf = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, box, 2, lay.part[2]))
         if pf < 0:
             raise ValueError(L.lib.pnp_last_error().decode())
         self.partial = torch.zeros(pf, dtype=torch.float32, device=device)
-        self.block_floats_c1 = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, 1, 1))
+        self.block_floats_c1 = int(L.lib.pnp_dsg_partial_floats(lay.Hg, lay.W, lay.R, lay.P, box,
+                                                                1, 1))
         self.block_floats_c2 = 2 * self.block_floats_c1
         self.kcache = None
         self.kc_per_tile_row = 0
@@ -125,7 +143,7 @@ class _RankState:
         streams them: bitwise neutral) when they fit with ``headroom`` spare."""
         lay = self.lay
         t0, t1 = lay.tile_rows
-        n = int(L.lib.pnp_dsg_kcache_floats(lay.Hg, lay.W, lay.R, lay.P, t1 - t0))
+        n = int(L.lib.pnp_dsg_kcache_floats(lay.Hg, lay.W, lay.R, lay.P, int(lay.box), t1 - t0))
         free, _ = torch.cuda.mem_get_info(self.buf.device)
         if n <= 0 or 4 * n + headroom > free:
             return False
@@ -283,7 +301,11 @@ class ShardedDSG:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.states = []
         for r in ranks:
-            lay = StripLayout(Hg, W, params.window_radius, params.patch_side, nranks, r)
+            lay = StripLayout(Hg, W, params.window_radius, params.patch_side, nranks, r,
+                              params.is_box)
+            if lay.geom[3] == 2:
+                raise ValueError("row-strip sharding needs the half-window sweep; this search "
+                                 "radius / patch side only runs on one GPU")
             lay.validate()
             self.states.append(_RankState(lay, self.device))
             if kcache:
@@ -333,7 +355,8 @@ class ShardedDSG:
         part0, off, nslot = lay.part
         p = self.params
         L.call("pnp_dsg_strip_fixup", L.context(self.device.index), mode, L.ptr(st.partial),
-               part0, nslot, lay.Hg, lay.W, p.window_radius, p.patch_side, y0, y1, b0, b1 - b0,
+               part0, nslot, lay.Hg, lay.W, p.window_radius, p.patch_side, int(lay.box), y0, y1,
+               b0, b1 - b0,
                L.ptr(st.rs), L.ptr(st.kx), L.ptr(st.d), L.ptr(st.mbits), L.ptr(inv_m), L.ptr(x),
                L.ptr(out))
 
@@ -342,20 +365,20 @@ class ShardedDSG:
         """Own rows that need the partial blocks received from the rank above
         (the first R rows) and the rest: ((y0, ya), (ya, y1))."""
         y0, y1 = st.lay.rows
-        ya = min(y1, y0 + (st.lay.R if st.lay.rank > 0 else 0))
+        ya = min(y1, y0 + (st.lay.Rb if st.lay.rank > 0 else 0))
         return (y0, ya), (ya, y1)
 
     @staticmethod
     def _split_tiles(st):
         """Tile rows whose sweep reads the rs halo from the rank below (rows
-        past y1 within R + KY - 1 of the tile) and the rest: (early, late)."""
+        past y1 within rs_below rows of the tile) and the rest: (early, late)."""
         lay = st.lay
         t0, t1 = lay.tile_rows
         _, y1 = lay.rows
         if lay.rank == lay.nranks - 1:
             return (t0, t1), (t1, t1)
         tb = t0
-        while tb < t1 and (tb + 1) * lay.TH + lay.R + KY - 1 <= y1:
+        while tb < t1 and (tb + 1) * lay.TH + lay.rs_below <= y1:
             tb += 1
         return (t0, tb), (tb, t1)
 
@@ -469,7 +492,7 @@ class ShardedSRADMM:
         blocks -> next rank, fixup with the global 1/m [P2P]
         u-update + primal / dual / PSNR partial sums   [all-reduce]
 
-    Strip boundaries are DSG tile rows (multiples of TH = 32 - 2p, which the
+    Strip boundaries are DSG tile rows (multiples of TH, pnp_dsg_geometry; the
     decimation factor must divide), every operator reads global rows through
     halos, so x, z, v, u are bit-identical to the single-GPU solver; the
     records' float64 sums differ only in summation order.  ``ranks`` /

@@ -29,6 +29,7 @@ def read(device: int | None = None) -> dict:
 def set_cache_limit(nbytes: int | None, device: int | None = None) -> None:
     """k-cache budget in bytes (None: unlimited, 0: disabled)."""
     dev = torch.cuda.current_device() if device is None else device
+    L.cache_limits[dev] = None if nbytes is None else int(nbytes)
     L.call("pnp_ctx_set_cache_limit", L.context(dev), -1 if nbytes is None else int(nbytes))
 
 

@@ -37,7 +37,7 @@ import torch
 
 from . import _arrays as A
 from . import _lib as L
-from .denoise import PatchParams, freeze_guide
+from .denoise import PatchParams, freeze_guide, kcache_scope
 from .forward import (QIS_FLOOR, QisCounts, QisModel, SuperResOp, power_iteration_lipschitz,
                       qis_grad_device, qis_grad_xupdate_device, qis_initial_estimate, sr_adjoint)
 from .image import UNCONSTRAINED, Constraint, bounds
@@ -287,9 +287,11 @@ def _dsg_device(img: torch.Tensor, params: PatchParams) -> torch.Tensor:
     """Unchecked device DSG-NLM (inputs already validated by the solver)."""
     B, H, W = A.dims(img)
     out = torch.empty_like(img)
-    L.call("pnp_dsg_denoise", L.context(img.device.index), L.ptr(img), L.ptr(img), L.ptr(out),
-           B, H, W, params.window_radius, params.patch_side, params._ctaps(),
-           float(params.bandwidth), None, None)
+    dev = img.device.index
+    with kcache_scope(dev, B, H, W, params):
+        L.call("pnp_dsg_denoise", L.context(dev), L.ptr(img), L.ptr(img), L.ptr(out),
+               B, H, W, params.window_radius, params.patch_side, params._ctaps(),
+               float(params.bandwidth), None, None)
     return out
 
 

@@ -19,7 +19,7 @@ import torch
 
 from . import _arrays as A
 from . import _lib as L
-from .denoise import PatchParams, _check_margin
+from .denoise import PatchParams, _check_margin, kcache_scope
 
 
 class DenoiseStream:
@@ -42,17 +42,17 @@ class DenoiseStream:
         self.s_h2d, self.s_comp, self.s_d2h = (torch.cuda.Stream(d) for _ in range(3))
         self._taps = params._ctaps()
         L.call("pnp_ctx_reserve", L.context(self.dev), B, H, W, params.window_radius,
-               params.patch_side)
+               params.patch_side, int(params.is_box))
         # the first image of a run has no earlier image to hide its upload
         # behind: it goes up in row bands and its sweep A starts band by band
         # (pnp_dsg_denoise_banded); later images overlap the previous denoise
         self._bands = None
         nb = 4
-        TH = 32 - (params.patch_side - 1)
-        if B == 1 and -(-H // TH) >= 4 * nb:
+        geom = L.dsg_geometry(H, W, params.window_radius, params.patch_side, params.is_box)
+        if B == 1 and geom[3] == 0 and -(-H // geom[0]) >= 4 * nb:
             te, need = (C.c_int * nb)(), (C.c_int * nb)()
-            L.call("pnp_dsg_band_rows", H, W, params.window_radius, params.patch_side, nb, te,
-                   need)
+            L.call("pnp_dsg_band_rows", H, W, params.window_radius, params.patch_side,
+                   int(params.is_box), nb, te, need)
             self._bands = list(need)
 
     def run(self, host_images, host_outs=None):
@@ -68,6 +68,16 @@ class DenoiseStream:
         cur = torch.cuda.current_stream(d)
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             s.wait_stream(cur)
+        with torch.cuda.stream(self.s_comp):  # the k cache lives on the compute stream
+            scope = kcache_scope(self.dev, self.B, self.H, self.W, self.params)
+            scope.__enter__()
+        try:
+            return self._run(host_images, host_outs, n, d, flags, cur)
+        finally:
+            with torch.cuda.stream(self.s_comp):
+                scope.__exit__(None, None, None)
+
+    def _run(self, host_images, host_outs, n, d, flags, cur):
         up = [torch.cuda.Event() for _ in range(n)]
         done = [torch.cuda.Event() for _ in range(n)]
         down = [torch.cuda.Event() for _ in range(n)]

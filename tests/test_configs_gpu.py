@@ -1,0 +1,159 @@
+"""Parity at BASELINE.json's stated sizes against goldens produced by the REAL
+reference (tests/golden/make_golden_configs.py: pnprestore's own
+linearized_pnp_admm / dsg_nlm_denoise, Gaussian engine swap for the configs'
+patch weights).  North-star bar: max |dv| <= 1e-4 on [0, 1] intensities and
+final ADMM PSNR within 0.02 dB.
+
+* config 2: 512^2 SR, 30 iterations, frozen bicubic guide (the golden's guide)
+* config 3: 512^2 QIS, 50 iterations, dsg-fixed frozen at 15
+* config 4: the bench's own 8192^2 image (synth scene 4 + noise seed 5): d and
+  K x on six windows (interior / edges / corners) from reference crops
+* config 5: images 0 and 63 of the 64 x 1024^2 batch, 20 iterations, run as
+  one batched solve (per-image alpha)
+* the reference's Table-1 timing shape: 256^2, R = 21, box P in
+  {11, 17, 23, 29} -- out and d against the unmodified dsg_nlm_denoise
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+TOL_V = 1e-4      # max |v_gpu - v_ref| (fp32 device vs float64 reference)
+TOL_PSNR = 0.02   # dB, every iteration
+
+
+@pytest.fixture(scope="module")
+def pnp():
+    import paper_1901_06110_b200 as pnp
+    return pnp
+
+
+def _rec(recs):
+    return np.array([[r.index, r.primal, r.dual, r.psnr, r.objective] for r in recs])
+
+
+def _bicubic_x2(y32):
+    """The golden's guide recipe (make_golden_configs.bicubic_x2)."""
+    import torch.nn.functional as F
+    t = torch.from_numpy(y32.astype(np.float64))
+    g = F.interpolate(t[None, None], scale_factor=2, mode="bicubic", align_corners=False)[0, 0]
+    return g.clamp(0, 1).numpy().astype(np.float32)
+
+
+def test_config2_sr_512(pnp):
+    from paper_1901_06110_b200 import synth
+    gd = load_golden("cfg2.npz")
+    truth = synth.scene(512, 512, 2).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    prob = pnp.make_sr_problem(op, torch.from_numpy(gd["y"]).to(dev),
+                               ground_truth=torch.from_numpy(truth).to(dev))
+    fz = pnp.freeze_guide(torch.from_numpy(gd["guide"]).to(dev),
+                          pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0))
+    assert abs(float(fz.alpha[0]) - float(gd["m"])) < 1e-5
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=30, constraint=pnp.UNIT_BOX)
+    v, recs = pnp.linearized_pnp_admm(prob, cfg, denoiser=fz.as_denoiser())
+    got, ref = _rec(recs), gd["rec"]
+    dv = float((v.double().cpu() - torch.from_numpy(gd["v"]).double()).abs().max())
+    assert dv <= TOL_V, dv
+    assert np.abs(got[:, 3] - ref[:, 3]).max() < TOL_PSNR
+    assert np.allclose(got[:, 4], ref[:, 4], rtol=1e-4)
+
+
+def test_config3_qis_512(pnp):
+    from paper_1901_06110_b200 import synth
+    gd = load_golden("cfg3.npz")
+    truth = synth.scene(512, 512, 3).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    model = pnp.QisModel(128, 64.0)
+    counts = pnp.QisCounts(gd["ones"].astype(np.float64), gd["zeros"].astype(np.float64))
+    prob = pnp.make_qis_problem(counts, model, ground_truth=torch.from_numpy(truth).to(dev))
+    prob.x0 = torch.from_numpy(np.asarray(prob.x0, dtype=np.float32)).to(dev)
+    alpha = pnp.default_qis_alpha(counts, model)
+    assert alpha == float(gd["alpha"])
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=alpha, max_iters=50, freeze_at=15,
+                           constraint=pnp.UNIT_BOX, denoiser="dsg-fixed", patch_side=7,
+                           window_radius=10, bandwidth=(10 / 255) / math.sqrt(2.0),
+                           patch_sigma=2.0)
+    v, recs = pnp.linearized_pnp_admm(prob, cfg)
+    got, ref = _rec(recs), gd["rec"]
+    dv = float((v.double().cpu() - torch.from_numpy(gd["v"]).double()).abs().max())
+    assert dv <= TOL_V, dv
+    assert np.abs(got[:, 3] - ref[:, 3]).max() < TOL_PSNR
+    assert np.allclose(got[:, 4], ref[:, 4], rtol=1e-4)
+
+
+def test_config4_windows_bench_image(pnp):
+    """The 8192^2 image bench.py denoises (make_image_rows: scene 4 + noise
+    seed 5, float32), full-size denoise, compared on six windows with the
+    reference run on crops (d exactly local; W x with the GPU's global m)."""
+    from paper_1901_06110_b200 import synth
+    gd = load_golden("cfg4_windows.npz")
+    n, S = 8192, int(gd["S"])
+    img = synth.noisy(synth.scene(n, n, 4), 25 / 255, 5).astype(np.float32)
+    x = torch.from_numpy(img).cuda()
+    p = pnp.PatchParams.from_h(7, 10, 12 / 255, 2.0)
+    out, d, alpha = pnp.dsg_nlm_denoise(x, p, return_aux=True)
+    m = float(alpha[0])
+    assert m == float(d.max())
+    for i, (r0, c0) in enumerate(gd["windows"]):
+        a0, b0 = gd[f"w{i}_origin"]
+        crop = gd[f"w{i}_crop"]
+        assert np.array_equal(img[a0:a0 + crop.shape[0], b0:b0 + crop.shape[1]], crop)
+        sl = (slice(r0, r0 + S), slice(c0, c0 + S))
+        d_gpu = d[sl].double().cpu().numpy()
+        o_gpu = out[sl].double().cpu().numpy()
+        xw = img[sl].astype(np.float64)
+        wx_ref = gd[f"w{i}_kx"] / m + (1.0 - gd[f"w{i}_d"] / m) * xw
+        assert np.abs(d_gpu - gd[f"w{i}_d"]).max() <= 1e-5
+        assert np.abs(o_gpu - wx_ref).max() <= TOL_V
+
+
+def test_config5_images_0_and_63(pnp):
+    """Images 0 and 63 of the config-5 batch in one batched solve."""
+    from paper_1901_06110_b200 import synth
+    gds = [load_golden("cfg5_img0.npz"), load_golden("cfg5_img63.npz")]
+    dev = torch.device("cuda", 0)
+    truths = [synth.scene(1024, 1024, 1000 + i).astype(np.float32) for i in (0, 63)]
+    guides = []
+    for gd in gds:
+        g = _bicubic_x2(gd["y"])
+        assert hashlib.sha256(g.tobytes()).hexdigest() == str(gd["guide_sha256"])
+        guides.append(g)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    yb = torch.from_numpy(np.stack([gd["y"] for gd in gds])).to(dev)
+    prob = pnp.make_sr_problem(op, yb, ground_truth=torch.from_numpy(np.stack(truths)).to(dev))
+    fz = pnp.freeze_guide(torch.from_numpy(np.stack(guides)).to(dev),
+                          pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0))
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=20, constraint=pnp.UNIT_BOX)
+    v, recs = pnp.linearized_pnp_admm(prob, cfg, denoiser=fz.as_denoiser())
+    for j, gd in enumerate(gds):
+        assert abs(float(fz.alpha[j]) - float(gd["m"])) < 1e-5
+        dv = float((v[j].double().cpu() - torch.from_numpy(gd["v"]).double()).abs().max())
+        assert dv <= TOL_V, dv
+        psnr = np.array([np.atleast_1d(r.psnr)[j] for r in recs])
+        assert np.abs(psnr - gd["rec"][:, 3]).max() < TOL_PSNR
+
+
+@pytest.mark.parametrize("P", [11, 17, 23, 29])
+def test_table1_shape_box_matches_reference(pnp, P):
+    """256^2, R = 21, box patches (the reference's own distance), P beyond the
+    P-templated kernel: the running-sum general sweep vs pnprestore."""
+    gd = load_golden("table1.npz")
+    x = torch.from_numpy(gd["image"]).float().cuda()
+    p = pnp.PatchParams(P, 21, 0.15)
+    out, d, alpha = pnp.dsg_nlm_denoise(x, p, return_aux=True)
+    assert abs(float(alpha[0]) - float(gd[f"p{P}_m"])) <= 1e-5
+    assert float((d.cpu() - torch.from_numpy(gd[f"p{P}_d"])).abs().max()) <= 1e-5
+    assert float((out.cpu() - torch.from_numpy(gd[f"p{P}_out"])).abs().max()) <= TOL_V
+    # numpy drop-in (float64 in / out) and the frozen guide give the same bits
+    o64 = pnp.dsg_nlm_denoise(gd["image"], p)
+    assert np.array_equal(o64, out.double().cpu().numpy())
+    assert torch.equal(pnp.freeze_guide(x, p).apply(x), out)

@@ -1,0 +1,122 @@
+"""The general sweep (csrc/dsg_generic.cuh): box patch distances by running
+sums at any odd P <= 63, Gaussian taps beyond the P-templated kernel, search
+radii beyond 32 (incl. the full-window variant when the far plane exceeds
+shared memory) -- against the float64 oracle (a restatement of
+pnprestore/denoise.py pinned to the reference's goldens), plus the bitwise
+invariants the reference's tests hold (frozen == adaptive,
+tests/test_denoise.py:256-268; batch == single; reruns)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1901_06110_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def pnp():
+    import paper_1901_06110_b200 as pnp
+    return pnp
+
+
+def _path(pnp, H, W, p):
+    return L.dsg_geometry(H, W, p.window_radius, p.patch_side, p.is_box)[3]
+
+
+CASES = [
+    # H, W, R, P, bw, sigma, seed
+    (40, 52, 3, 1, 0.2, None, 1),
+    (37, 45, 2, 3, 0.25, None, 2),
+    (48, 70, 5, 7, 0.2, None, 3),      # box at a small P: general kernel too
+    (64, 64, 8, 17, 0.15, None, 4),
+    (50, 71, 6, 31, 0.3, None, 5),
+    (70, 90, 4, 45, 0.4, None, 6),
+    (80, 80, 5, 63, 0.5, None, 7),
+    (66, 130, 21, 23, 0.15, None, 8),  # Table-1 radius, W not a multiple of 64
+    (90, 75, 40, 5, 0.2, None, 9),     # R > 32, half window (shared far plane)
+    (45, 60, 4, 17, 0.2, 3.0, 10),     # Gaussian taps beyond P = 15
+    (40, 50, 36, 3, 0.2, 1.0, 11),     # Gaussian, R > 32
+]
+
+
+@pytest.mark.parametrize("H,W,R,P,bw,sigma,seed", CASES)
+def test_general_sweep_vs_oracle(pnp, H, W, R, P, bw, sigma, seed):
+    rng = np.random.default_rng(seed)
+    img = rng.random((H, W))
+    p = pnp.PatchParams(P, R, bw, sigma)
+    assert _path(pnp, H, W, p) in (1, 2)
+    out, d, alpha = pnp.dsg_nlm_denoise(img, p, return_aux=True)
+    ref, dref, mref = oracle.dsg_nlm_denoise(img, P, R, bw, patch_sigma=sigma, return_aux=True)
+    assert np.abs(out - ref).max() <= TOL
+    assert np.abs(d - dref).max() <= 1e-5
+    assert abs(float(alpha[0]) - mref) <= 1e-5
+
+
+def test_full_window_variant_vs_oracle(pnp):
+    """A radius whose half-window far plane exceeds shared memory runs the
+    full-window (near-only) variant of the general kernel."""
+    rng = np.random.default_rng(12)
+    H, W, R, P, bw = 104, 110, 100, 1, 0.3
+    img = rng.random((H, W))
+    p = pnp.PatchParams(P, R, bw)
+    assert _path(pnp, H, W, p) == 2
+    out, d, alpha = pnp.dsg_nlm_denoise(img, p, return_aux=True)
+    ref, dref, mref = oracle.dsg_nlm_denoise(img, P, R, bw, return_aux=True)
+    assert np.abs(out - ref).max() <= TOL
+    assert np.abs(d - dref).max() <= 1e-5
+    fz = pnp.freeze_guide(img, p)
+    assert np.array_equal(fz.apply(img), out)
+
+
+@pytest.mark.parametrize("P,R,sigma", [(17, 21, None), (5, 40, None), (19, 6, 2.5)])
+def test_general_bitwise_invariants(pnp, P, R, sigma):
+    g = torch.Generator(device="cuda").manual_seed(P * 100 + R)
+    x = torch.rand(3, 96, 130, device="cuda", generator=g)
+    p = pnp.PatchParams(P, R, 0.2, sigma)
+    out, d, a = pnp.dsg_nlm_denoise(x, p, return_aux=True)
+    again = pnp.dsg_nlm_denoise(x, p)
+    assert torch.equal(out, again)                               # reruns
+    fz = pnp.freeze_guide(x, p)
+    assert torch.equal(fz.apply(x), out)                         # frozen == adaptive
+    for i in range(3):                                           # batch == single
+        o, di, ai = pnp.dsg_nlm_denoise(x[i].contiguous(), p, return_aux=True)
+        assert torch.equal(o, out[i]) and torch.equal(di, d[i]) and float(ai[0]) == float(a[i])
+
+
+def test_general_linearity_and_fixed_point(pnp):
+    rng = np.random.default_rng(13)
+    guide = rng.random((60, 80))
+    p = pnp.PatchParams(21, 12, 0.25)
+    fz = pnp.freeze_guide(guide, p)
+    a, b = rng.random((60, 80)), rng.random((60, 80))
+    lhs = fz.apply(2.0 * a - 0.5 * b)
+    rhs = 2.0 * fz.apply(a) - 0.5 * fz.apply(b)
+    assert np.abs(lhs - rhs).max() < 1e-5
+    c = np.full((60, 80), 0.42)
+    assert np.abs(fz.apply(c) - c).max() < 1e-6                  # W 1 = 1
+    y = fz.apply(a)
+    assert abs(float(y.mean()) - float(a.mean())) < 1e-6         # mean preserved
+
+
+def test_general_nlm_vs_oracle(pnp):
+    rng = np.random.default_rng(14)
+    img = rng.random((50, 66))
+    p = pnp.PatchParams(19, 7, 0.2)
+    out = pnp.nlm_denoise(img, p)
+    ref = oracle.nlm_denoise(img, 19, 7, 0.2)
+    assert np.abs(out - ref).max() <= TOL
+
+
+def test_general_sharded_equals_single(pnp):
+    """Row strips over the general kernel (virtual ranks): same bits."""
+    from paper_1901_06110_b200.parallel import sharded_dsg_nlm_denoise
+    g = torch.Generator(device="cuda").manual_seed(15)
+    x = torch.rand(256, 200, device="cuda", generator=g)
+    p = pnp.PatchParams(17, 21, 0.15)
+    ref = pnp.dsg_nlm_denoise(x, p)
+    for n in (2, 3):
+        assert torch.equal(sharded_dsg_nlm_denoise(x, p, n), ref)
