@@ -151,19 +151,30 @@ def build_dense_weights(guide, params: PatchParams):
 
 
 _KC_HEADROOM = 4 << 30
+# (device, B, H, W, R, P, box, limit) -> bytes granted last time (the
+# free-memory query is paid only when a shape is new, the grant was partial,
+# or torch could not hand the bytes out again)
+_KC_GRANT: dict = {}
 
 
-def _kcache_bytes(dev: int, B: int, H: int, W: int, params: PatchParams) -> int:
-    """Bytes of the adaptive k cache to bind: all tile rows when they fit in
-    what torch can hand out (free HBM + its idle cache, less 4 GiB), else as
-    many as fit (the rest recompute, same bits), 0 below 1/8 of them."""
+def _kcache_bytes(dev: int, B: int, H: int, W: int, params: PatchParams,
+                  fresh: bool = False) -> tuple[int, int]:
+    """(bytes to bind, bytes of the whole cache).  All tile rows when they fit
+    in what torch can hand out (free HBM + its idle cache, less 4 GiB for the
+    library's own scratch), else as many as fit (the rest recompute, same
+    bits), 0 below 1/8 of them."""
     limit = L.cache_limits.get(dev, None)
     if limit == 0:
-        return 0
+        return 0, 0
+    key = (dev, B, H, W, params.window_radius, params.patch_side, params.is_box, limit)
+    hit = _KC_GRANT.get(key)
+    if hit is not None and not fresh and hit[0] == hit[1]:
+        return hit
     row = int(L.lib.pnp_dsg_kcache_floats(H, W, params.window_radius, params.patch_side,
                                           int(params.is_box), 1)) * 4 * B
     if row <= 0:
-        return 0
+        _KC_GRANT[key] = (0, 0)
+        return 0, 0
     tiles = -(-H // L.dsg_geometry(H, W, params.window_radius, params.patch_side,
                                    params.is_box)[0])
     free, _ = torch.cuda.mem_get_info(dev)
@@ -172,7 +183,9 @@ def _kcache_bytes(dev: int, B: int, H: int, W: int, params: PatchParams) -> int:
     if limit is not None:
         budget = min(budget, limit)
     rows = min(tiles, max(0, budget) // row)
-    return rows * row if rows * 8 >= tiles else 0
+    n = rows * row if rows * 8 >= tiles else 0
+    _KC_GRANT[key] = (n, tiles * row)
+    return n, tiles * row
 
 
 @contextlib.contextmanager
@@ -183,12 +196,17 @@ def kcache_scope(dev: int, B: int, H: int, W: int, params: PatchParams):
     current stream, which the context is bound to)."""
     buf = None
     if not torch.cuda.is_current_stream_capturing():
-        n = _kcache_bytes(dev, B, H, W, params)
+        n, _ = _kcache_bytes(dev, B, H, W, params)
         if n:
             try:
                 buf = torch.empty(n, dtype=torch.uint8, device=torch.device("cuda", dev))
             except torch.cuda.OutOfMemoryError:
-                buf = None
+                n, _ = _kcache_bytes(dev, B, H, W, params, fresh=True)
+                try:
+                    buf = torch.empty(n, dtype=torch.uint8,
+                                      device=torch.device("cuda", dev)) if n else None
+                except torch.cuda.OutOfMemoryError:
+                    buf = None
     ctx = L.context(dev)
     L.call("pnp_ctx_bind_kcache", ctx, L.ptr(buf), 0 if buf is None else buf.numel())
     try:

@@ -286,6 +286,61 @@ class TorchComm:
             recv(self.rank).copy_(tmp)
 
 
+class HostStagedComm(TorchComm):
+    """TorchComm over a CPU backend (gloo) for device-resident strips: every
+    message is staged through host memory (device -> host copy, gloo
+    send/recv, host -> device copy).  Used to run the sharded algorithm in
+    several processes where NCCL between them is not available (e.g. ranks
+    sharing one GPU in a test); the exchanges complete before the call
+    returns, so no rank's kernels ever wait on another's."""
+
+    def start_shift(self, states, send, recv, direction):
+        (st,) = states
+        to = self.rank + direction
+        frm = self.rank - direction
+        ops, host_in, dst = [], None, None
+        if 0 <= to < self.size:
+            t = send(st).detach().to("cpu").contiguous()
+            ops.append(self.dist.P2POp(self.dist.isend, t, self._peer(to), self.group))
+        if 0 <= frm < self.size:
+            dst = recv(st)
+            host_in = torch.empty(tuple(dst.shape), dtype=dst.dtype)
+            ops.append(self.dist.P2POp(self.dist.irecv, host_in, self._peer(frm), self.group))
+        for req in (self.dist.batch_isend_irecv(ops) if ops else []):
+            req.wait()
+        if host_in is not None:
+            dst.copy_(host_in)
+        return lambda: None
+
+    def allreduce_max(self, states):
+        (st,) = states
+        h = st.mbits.to("cpu")
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.MAX, group=self.group)
+        st.mbits.copy_(h)
+
+    def allreduce_sum(self, tensors):
+        (t,) = tensors
+        h = t.to("cpu")
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
+        t.copy_(h)
+
+    def shift(self, n, send, recv, direction):
+        ops = []
+        to, frm = self.rank + direction, self.rank - direction
+        if 0 <= to < self.size:
+            ops.append(self.dist.P2POp(self.dist.isend, send(self.rank).detach().to("cpu")
+                                       .contiguous(), self._peer(to), self.group))
+        host_in = None
+        if 0 <= frm < self.size:
+            dst = recv(self.rank)
+            host_in = torch.empty(tuple(dst.shape), dtype=dst.dtype)
+            ops.append(self.dist.P2POp(self.dist.irecv, host_in, self._peer(frm), self.group))
+        for req in (self.dist.batch_isend_irecv(ops) if ops else []):
+            req.wait()
+        if host_in is not None:
+            recv(self.rank).copy_(host_in)
+
+
 class ShardedDSG:
     """Adaptive DSG-NLM of a Hg x W image split in row strips.
 

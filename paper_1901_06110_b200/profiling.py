@@ -33,6 +33,13 @@ def set_cache_limit(nbytes: int | None, device: int | None = None) -> None:
     L.call("pnp_ctx_set_cache_limit", L.context(dev), -1 if nbytes is None else int(nbytes))
 
 
+def trim(device: int | None = None) -> None:
+    """Return the idle memory of the device's stream-ordered pool (frozen
+    guides' buffers after their handles died) to the device."""
+    dev = torch.cuda.current_device() if device is None else device
+    L.call("pnp_ctx_trim", L.context(dev))
+
+
 def peak_rates(device: int | None = None) -> tuple[float, float]:
     """Measured (FFMA/s, MUFU.EX2/s) of the whole GPU."""
     dev = torch.cuda.current_device() if device is None else device

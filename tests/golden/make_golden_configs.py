@@ -19,7 +19,10 @@ QIS counts) is stored, so the GPU tests feed the identical arrays.
       guide, P=7 Gaussian sigma_p=2, R=10, h=8/255.
 * c3  config 3: 512^2 QIS, K = 4x4x8 = 128 jots, gain 64 (alpha_s = 8),
       seed 103, 50 iterations, dsg-fixed frozen at iteration 15, P=7
-      Gaussian sigma_p=2, R=10, h=10/255, alpha = default_qis_alpha.
+      Gaussian sigma_p=2, R=10, h=10/255, alpha = default_qis_alpha; v at
+      iterations 5 and 10, and the reference's own sensitivity: the same run
+      from x0 perturbed by 1e-7 (relative) -- its final max |dv| and
+      per-iteration PSNR differences.
 * c4  config 4: windows of the 8192^2 bench image (seed 4 + noise 25/255,
       seed 5): the row sums d and K x on 48x48 windows, from crops with a
       2R+p margin (d and K x at a pixel depend on the guide within 2R+p).
@@ -135,10 +138,26 @@ def c3():
     cfg = ref.SolverConfig(rho=1.0, lam=0.01, alpha=alpha, max_iters=50, freeze_at=freeze_at,
                            constraint=ref.UNIT_BOX, denoiser="dsg-fixed", patch_side=7,
                            window_radius=10, bandwidth=params.bandwidth)
-    v, recs = ref.linearized_pnp_admm(prob, cfg, denoiser=fixed)
+    early = {}
+
+    def keep(k, x, v, u):
+        if k in (5, 10):
+            early[k] = v.astype(np.float32)
+
+    v, recs = ref.linearized_pnp_admm(prob, cfg, denoiser=fixed, callback=keep)
+    # The iteration amplifies perturbations (alpha = default_qis_alpha = 128):
+    # the same float64 run from x0 * (1 + 1e-7 N(0,1)) ends far from it.  Its
+    # deviation is the envelope any non-bit-identical implementation lives in.
+    state.clear()
+    rng = np.random.default_rng(1)
+    prob.x0 = prob.x0 * (1 + 1e-7 * rng.standard_normal(prob.x0.shape))
+    v_p, recs_p = ref.linearized_pnp_admm(prob, cfg, denoiser=fixed)
+    dpsnr = np.array([a.psnr - b.psnr for a, b in zip(recs_p, recs)])
     np.savez_compressed(HERE / "cfg3.npz", ones=counts.ones.astype(np.uint8),
                         zeros=counts.zeros.astype(np.uint8), alpha=np.array(alpha),
-                        v=v.astype(np.float32), rec=records(recs))
+                        v=v.astype(np.float32), rec=records(recs), v5=early[5], v10=early[10],
+                        pert_max_dv=np.array(np.abs(v_p - v).max()),
+                        pert_dpsnr=dpsnr)
 
 
 C4_WINDOWS = [(4000, 4100), (0, 0), (0, 6000), (8192 - 48, 8192 - 48), (5000, 8192 - 48),

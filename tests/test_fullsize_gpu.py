@@ -97,6 +97,26 @@ def test_k_cache_neutral_full_size(pnp, big):
     assert torch.equal(ref, out)
 
 
+def test_kcache_memory_is_torchs(pnp, big):
+    """The adaptive k cache of an 8192^2 denoise (59 GB) comes from torch's
+    caching allocator and goes back to it when the call returns: nothing
+    large stays hidden in the library, and torch can hand 100 GB out
+    right after the call."""
+    from paper_1901_06110_b200 import profiling
+    x, p, out, _, _ = big
+    profiling.trim()
+    torch.cuda.synchronize()
+    assert torch.equal(pnp.dsg_nlm_denoise(x, p), out)
+    torch.cuda.synchronize()
+    free, total = torch.cuda.mem_get_info()
+    hidden = (total - free) - torch.cuda.memory_reserved()
+    assert hidden < (4 << 30), hidden / 2 ** 30          # context + small scratch only
+    t = torch.empty(100 << 30, dtype=torch.uint8, device="cuda")
+    t[-1] = 1
+    del t
+    torch.cuda.empty_cache()
+
+
 def test_config5_batch_equals_single(pnp):
     """Config-5 shape: a batch of 1024^2 images denoised in one call (per-image
     alpha) == each image on its own, bitwise; frozen batch apply too."""
