@@ -3,17 +3,21 @@
 
 Workload (one "step"): one adaptive DSG-NLM denoise of the config-4 image —
 8192 x 8192 float32 seeded scene + noise 25/255, search 21x21 (R=10), patch
-7x7 Gaussian sigma_p=2, h=12/255 (bandwidth h/sqrt(2)); the full
-dsg_nlm_denoise pipeline (sweep A, rs, sweep B, fixups, max, finalize).
-With --gpus N > 1 (launched by torchrun) the image is sharded in row strips
-across the N ranks (parallel.ShardedDSG: NCCL halo/partial-block exchange,
-max all-reduce); the problem size is fixed ("strong" scaling).
+7x7 Gaussian sigma_p=2, h=12/255 (bandwidth h/sqrt(2)); the full pipeline
+(sweep A, rs, sweep B, fixups, max, finalize).  Every N runs the row-strip
+algorithm (parallel.ShardedDSG): N = 1 is one strip (exchanges are no-ops;
+the product call dsg_nlm_denoise on the same image is timed beside it as
+"single_call"), N > 1 (torchrun) shards the rows across the ranks (NCCL
+halo / partial-block exchange, max all-reduce); the problem size is fixed
+("strong" scaling).
 
 value    = 8192^2 * 441 pixel-offsets / device time per step (max over
            ranks), in Gpixel*offset/s, inputs resident in HBM (268 MB > L2,
            so every step streams from HBM; no flush needed);
-e2e      = the same through the public API with pinned host buffers: H2D of
-           the image, denoise, D2H of the result inside the timed region;
+e2e      = the same through the public API with host buffers, transfers in
+           the timed region: the headline is the reference's own call shape,
+           dsg_nlm_denoise(float64 numpy) -> float64 numpy; the pipelined
+           DenoiseStream and the synchronous pinned-tensor call beside it;
 roofline = the dominant kernel of the step (CUDA events on the library
            stream): the fused sweep A (FP32-bound: SURVEY.md §8(d)'s algorithmic
            ops per pixel-offset / its launch time vs the FFMA rate measured on
@@ -21,13 +25,17 @@ roofline = the dominant kernel of the step (CUDA events on the library
            (HBM-bound: 4 B per half-window pair vs MEASURED_PEAKS hbm_gbs); plus
            "denoise": the whole step vs the FP32 roofline of the algorithm
            (20.95 ops per pixel-offset);
-cpu_baseline = the float64 CPU oracle port (oracle/, restating pnprestore)
-           on a bounded sample of the same workload.
-Extras: ADMM iterations/s for configs 2 and 3 (512^2 SR / QIS) and image
-iterations/s for config 5 (64 x 1024^2 SR batched in one solver call).
+cpu_baseline = the reference itself (pnprestore installed unmodified into
+           oracle/_ref) on one uncached crop of the same image, 1 core.
+Extras: config 5 (64 x 1024^2 SR ADMM, 20 iterations) split image-per-GPU
+at every N; at N = 1 also config 1 (256^2 denoise) and ADMM iterations/s for
+configs 2 and 3, each with the reference's final PSNR beside ours
+(tests/golden).
 
-``--impl reference`` times the reference's CPU algorithm (oracle port) with
-all host cores on bounded samples of the same workload.
+``--impl reference`` times the reference's own dsg_nlm_denoise (oracle/_ref)
+with all host cores, one process per core, on uncached crops of the same
+image.  ``--dist-backend gloo`` runs N > 1 with host-staged messages (ranks
+may share a GPU: tests the N > 1 path on one device).
 """
 
 from __future__ import annotations
@@ -64,6 +72,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu / ADMM extras")
     ap.add_argument("--no-cache", action="store_true",
                     help="disable the k cache (recompute the patch filter in sweep B)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N > 1: NCCL between GPUs, or gloo with host-staged messages "
+                         "(several ranks sharing one GPU, for testing the N > 1 path)")
     return ap.parse_args()
 
 
@@ -248,6 +259,8 @@ def run_gpu(args, rank, world, local_rank):
     import paper_1901_06110_b200 as pnp
     from paper_1901_06110_b200 import profiling
 
+    # (--dist-backend gloo may put several ranks on one GPU)
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if args.no_cache:
@@ -260,21 +273,24 @@ def run_gpu(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    # every N (1 included) runs the row-strip algorithm (parallel.ShardedDSG):
+    # the scaling curve compares one code path; at N = 1 there is one strip
+    # and the exchanges are no-ops (same kernels as dsg_nlm_denoise, which is
+    # timed beside it as "single_call")
+    from paper_1901_06110_b200.parallel import HostStagedComm, LocalComm, ShardedDSG, TorchComm
     if world == 1:
-        x = torch.from_numpy(make_image_rows(n, 0, n)).to(dev)
-        out = torch.empty_like(x)
-
-        def step():
-            pnp.dsg_nlm_denoise(x, params)
+        comm = LocalComm()
+    elif args.dist_backend == "gloo":
+        comm = HostStagedComm()
     else:
-        from paper_1901_06110_b200.parallel import ShardedDSG, TorchComm
-        sh = ShardedDSG(params, n, n, world, [rank], TorchComm(), device=dev)
-        st = sh.states[0]
-        y0, y1 = st.lay.rows
-        st.own(st.buf).copy_(torch.from_numpy(make_image_rows(n, y0, y1)))
+        comm = TorchComm()
+    sh = ShardedDSG(params, n, n, world, [rank], comm, device=dev, kcache=not args.no_cache)
+    st = sh.states[0]
+    y0, y1 = st.lay.rows
+    st.own(st.buf).copy_(torch.from_numpy(make_image_rows(n, y0, y1)))
 
-        def step():
-            sh.denoise()
+    def step():
+        sh.denoise()
 
     for _ in range(args.warmup):
         step()
@@ -369,6 +385,24 @@ def run_gpu(args, rank, world, local_rank):
     }
     clocks = clk.summary()
     line["clocks"] = clocks
+    if world == 1:
+        # the product call on the same image, timed beside the strip path
+        x = st.own(st.buf).clone()
+        del sh, st
+        torch.cuda.empty_cache()
+        for _ in range(2):
+            pnp.dsg_nlm_denoise(x, params)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            pnp.dsg_nlm_denoise(x, params)
+        e1.record()
+        torch.cuda.synchronize()
+        ms1 = e0.elapsed_time(e1) / args.steps
+        line["single_call"] = {"value": units / (ms1 * 1e-3) / 1e9, "ms_per_step": ms1,
+                               "api": "paper_1901_06110_b200.dsg_nlm_denoise(device tensor)"}
+        del x
+        torch.cuda.empty_cache()
 
     if not args.no_extras:
         # e2e through the public API with pinned host buffers: every step
@@ -450,8 +484,11 @@ def run_gpu(args, rank, world, local_rank):
                            "h2d_bytes_per_step": nbytes * world,
                            "d2h_bytes_per_step": nbytes * world, "ms_per_step": float(t[0]),
                            "api": "parallel.ShardedDSG.denoise"}
+        if world > 1:
+            del sh, st
+        torch.cuda.empty_cache()  # the k caches (59 GB at 8192^2) sit in torch's cache
+        line["config5"] = config5(pnp, dev, rank, world, True)
         if rank == 0 and world == 1:
-            torch.cuda.empty_cache()  # the adaptive k cache (59 GB) sits in torch's cache
             line["admm"] = admm_extras(pnp, dev)
             from oracle import refcpu  # the checker / baseline, timed on the host only
             side = refcpu.uncached_side(R_C4)
@@ -591,11 +628,25 @@ def admm_extras(pnp, dev):
                               "psnr_db": recs[-1].psnr,
                               **golden_check("cfg3.npz", v, recs),
                               "timing": "median of 9 solves incl. the freeze at iteration 15"}
-    # config 5: 64 independent 1024^2 SR problems batched in one solver call
-    # (blockIdx.z), per-image alpha, frozen bicubic guides, 20 iterations
+    res["reference_cpu_note"] = "survey: pnprestore config-2 shape 0.79 iters/s on 1 CPU core"
+    return res
+
+
+def config5(pnp, dev, rank, world, dist_ok):
+    """Config 5: 64 independent 1024^2 SR problems, 20 iterations, frozen
+    bicubic guides, per-image alpha; split image-per-GPU (rank r solves images
+    [64 r / N, 64 (r+1) / N) as one batched call: blockIdx.z).  Solve time per
+    rank from CUDA events (median of 3 after one untimed), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    synth = _synth()
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    p2 = pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0)
     nb, side = 64, 1024
+    i0, i1 = nb * rank // world, nb * (rank + 1) // world
+    mine = list(range(i0, i1))
     truths, ys = [], []
-    for i in range(nb):  # the golden's recipe: float64 simulation, float32 observation
+    for i in mine:  # the golden's recipe: float64 simulation, float32 observation
         t_i = synth.scene(side, side, 1000 + i).astype(np.float32)
         truths.append(t_i)
         ys.append(pnp.sr_simulate(t_i.astype(np.float64), op, 5 / 255,
@@ -605,35 +656,44 @@ def admm_extras(pnp, dev):
     guides = torch.from_numpy(np.stack([bicubic_x2(y_i) for y_i in ys])).to(dev)
     cfg5 = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=20, constraint=pnp.UNIT_BOX)
     prob5 = pnp.make_sr_problem(op, yb, ground_truth=gtb)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     fz5 = None
     for _ in range(2):  # the second freeze is timed (the first warms the pool)
         fz5 = None
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        e0.record()
         fz5 = pnp.freeze_guide(guides, p2)
+        e1.record()
         torch.cuda.synchronize()
-        t_freeze = time.perf_counter() - t0
+        t_freeze = e0.elapsed_time(e1) / 1e3
     runs = []
     for i in range(4):
         torch.cuda.synchronize()
-        t1 = time.perf_counter()
+        e0.record()
         v5, recs5 = pnp.linearized_pnp_admm(prob5, cfg5, denoiser=fz5.as_denoiser())
+        e1.record()
         torch.cuda.synchronize()
         if i:
-            runs.append(time.perf_counter() - t1)
-    t_solve = float(np.median(runs))
+            runs.append(e0.elapsed_time(e1) / 1e3)
+    t = torch.tensor([float(np.median(runs)), t_freeze], device=dev, dtype=torch.float64)
+    if world > 1 and dist_ok:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_solve, t_freeze = float(t[0]), float(t[1])
     kc5 = fz5.cache_info()
     fz5 = None
-    res["config5_sr_64x1024"] = {
-        "images": nb, "iters": 20, "image_iters_per_s": nb * 20 / t_solve,
+    res = {
+        "images": nb, "iters": 20, "n_gpus": world, "images_per_gpu": len(mine),
+        "image_iters_per_s": nb * 20 / t_solve,
         "pixel_offsets_per_s_in_applies": nb * side * side * 441 * 20 / t_solve,
         "freeze_ms": t_freeze * 1e3, "end_to_end_ms": (t_freeze + t_solve) * 1e3,
         "kcache_rows_cached": f"{kc5['rows_cached']}/{kc5['tile_rows']}",
-        "psnr_db_mean": float(np.mean(recs5[-1].psnr)),
-        "oracle_images": {f"img{i}": golden_check(f"cfg5_img{i}.npz", v5[i], recs5, y=ys[i],
-                                                  image=i) for i in (0, 63)},
-        "timing": "median of 3 solves (wall) after one untimed; freeze timed separately"}
-    res["reference_cpu_note"] = "survey: pnprestore config-2 shape 0.79 iters/s on 1 CPU core"
+        "psnr_db_mean_rank0": float(np.mean(recs5[-1].psnr)),
+        "scaling": "strong (64 images split image-per-GPU, no collective on the data path)",
+        "timing": "per-rank CUDA events: median of 3 solves after one untimed, max over ranks; "
+                  "freeze timed separately"}
+    res["oracle_images"] = {f"img{i}": golden_check(f"cfg5_img{i}.npz", v5[j], recs5, y=ys[j],
+                                                    image=j)
+                            for j, i in enumerate(mine) if i in (0, 63)}
     return res
 
 
@@ -647,7 +707,7 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        if args.impl == "pnp":
+        if args.impl == "pnp" and args.dist_backend == "nccl":
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
