@@ -58,6 +58,7 @@ struct GenArgs {
   float taps_h[kGenMaxP];   // Gaussian: normalized taps w_b
   float taps_v[kGenMaxP];   // Gaussian: -log2(e)/(2 bw^2) * w_a
   int grp[kMaxGroups + 1];  // offset groups: dy-index ranges (dy = dyi + dy_min)
+  long long partial_floats;  // buffer size (PNP_CHECKS)
 };
 
 // Shared-memory geometry of one CTA (floats); also used by the host to pick TH.
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
     const int dx_lo = (SYM && dy == 0) ? 1 : -R;
     for (int dxa = dx_lo; dxa <= R; dxa += kGenDXC) {
       const int dxb = min(dxa + kGenDXC, R + 1);
-      __syncthreads();  // previous users of Gpart / Ys are done
+      jitter_sync();  // previous users of Gpart / Ys are done
       // partner guide rows: map row q <-> image row r0g - p + q + dy, col j
       // <-> image col c0g - p + dxa + j
       const int gpw = kTW + 2 * p + (dxb - dxa) - 1;
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
         for (int r = tid / 32; r < TH; r += kGenThreads / 32)
           for (int j = tid & 31; j < yw; j += 32)
             Ys[(c_ * TH + r) * L.YS + j] = yval(c_, r0g + r + dy, c0g + dxa + j);
-      __syncthreads();
+      jitter_sync();
 
       for (int dx = dxa; dx < dxb; ++dx) {
         if (!SYM && dy == 0 && dx == 0) continue;  // self pair: analytic
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
             }
           }
         }
-        __syncthreads();
+        jitter_sync();
         // ---- phase V: column x, rows [rA, rA + N) ----
         {
           const float Lt = a.ltab ? a.ltab[(dy + R) * n_dx + dx + R] : 0.f;
@@ -241,12 +242,13 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
               near[c_][i] = __fmaf_rn(k, yp[(c_ * TH + i) * L.YS], near[c_][i]);
               if (SYM) {
                 float* q = ap + (c_ * L.AR + i) * L.AC;
+                PNP_CHECK(q >= As && q < As + C * L.AR * L.AC);
                 *q = __fmaf_rn(k, yown[c_][i], *q);
               }
             }
           }
         }
-        __syncthreads();
+        jitter_sync();
       }
     }
   }
@@ -257,6 +259,8 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
   const size_t slot =
       (((size_t)b * a.part_ntr + a.part_off + tyl) * gridDim.y + blockIdx.y) * a.tiles_x + tx;
   float* out = a.partial + slot * (size_t)(C * BR * BC);
+  PNP_CHECK((long long)((slot + 1) * (size_t)(C * BR * BC)) <= a.partial_floats);
+  PNP_CHECK(L.total * 4 <= 227 * 1024);
   if (SYM) {
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)

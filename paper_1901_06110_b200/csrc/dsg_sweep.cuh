@@ -140,6 +140,7 @@ struct SweepArgs {
   // (single) accesses, and a chunk is one contiguous kc*TH*64*4 B run.
   float* kcache;
   long long kc_img, kc_tile;
+  long long partial_floats, kcache_floats;  // buffer sizes (PNP_CHECKS)
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
 };
@@ -276,7 +277,10 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
       float* dst = Gs + q * GS + lane;
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
-        if (gcol[j] >= 0) dst[32 * j] = __ldg(src + gcol[j]);
+        if (gcol[j] >= 0) {
+          PNP_CHECK(dst + 32 * j < Hs);
+          dst[32 * j] = __ldg(src + gcol[j]);
+        }
     }
   }
   {
@@ -418,6 +422,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
         else if (j == WIN - 1) v = pf[c_][WIN - 2].y;
         else v = __fadd_rn(pf[c_][j].x, pf[c_][j - 1].y);
         float* pA = base + c_ * AR * YC + j * YC;
+        PNP_CHECK(pA >= As && pA < As + C * AR * YC);
         *pA = __fadd_rn(*pA, v);
       }
   };
@@ -434,6 +439,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 #pragma unroll
         for (int j = 0; j < KY - 1; ++j) {
           float* pA = pend + c_ * AR * YC + j * YC;
+          PNP_CHECK(pA >= As && pA < As + C * AR * YC);
           *pA = __fadd_rn(*pA, pendv[c_][j]);
         }
     }
@@ -459,12 +465,14 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
 #pragma unroll
             for (int bb = 1; bb < P; ++bb)
               h = __ffma2_rn(make_float2(a.taps_h[bb], a.taps_h[bb]), dd[i + bb], h);
+            PNP_CHECK((const float*)(hrow0 + kp * 32 * HS + i) >= Hs &&
+                      (const float*)(hrow0 + kp * 32 * HS + i) < Ys);
             hrow0[kp * 32 * HS + i] = h;
           }
         }
       }
     }
-    __syncthreads();
+    jitter_sync();
 
     // ---------------- phase 2: vertical filter, exp, near/far -------------
     const float* ybase = Ys + (r0 + dy0) * YC + c + dx + RB;
@@ -585,6 +593,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
               float* plane = const_cast<float*>(kq) + 2 * kp * HPF;
               if (pairp) {
                 float2* dst = reinterpret_cast<float2*>(plane) + r0 * kTW + kpos<N>(c, r & ~1);
+                PNP_CHECK(((const float*)(dst + ((r & 1) ? 2 : 1)) - a.kcache) <= a.kcache_floats);
                 if (r & 1)
                   __stcs(reinterpret_cast<float4*>(dst),
                          make_float4(kk[r - 1].x, kk[r - 1].y, kk[r].x, kk[r].y));
@@ -592,6 +601,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
                   __stcs(dst, kk[r]);
               } else {  // single plane: the even offset only
                 float* dst = plane + r0 * kTW + kpos<N>(c, r & ~1);
+                PNP_CHECK((dst + ((r & 1) ? 2 : 1) - a.kcache) <= a.kcache_floats);
                 if (r & 1)
                   __stcs(reinterpret_cast<float2*>(dst), make_float2(kk[r - 1].x, kk[r].x));
                 else if (r == N - 1)
@@ -622,7 +632,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
           pendv[c_][j] = j == 0 ? pf[c_][0].x : __fadd_rn(pf[c_][j].x, pf[c_][j - 1].y);
       pend = abase;
     }
-    __syncthreads();
+    jitter_sync();
   }
   if (g == 1 && pend) {
 #pragma unroll
@@ -648,6 +658,7 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   const size_t slot =
       (((size_t)b * a.part_ntr + a.part_off + tyl) * gridDim.y + blockIdx.y) * a.tiles_x + tx;
   float* out = a.partial + slot * (size_t)(C * BR * BC);
+  PNP_CHECK((long long)((slot + 1) * (size_t)(C * BR * BC)) <= a.partial_floats);
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_) {
     const float* A0 = As + c_ * AR * YC + (RB - R);

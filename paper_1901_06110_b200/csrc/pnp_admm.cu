@@ -50,6 +50,7 @@ int pnp_admm_run(pnp_ctx* ctx, int kind, const float* obs, const float* obs2, in
     float* vcur = v0;
     float* vnext = v1;
     for (int k = k0; k <= k1; ++k) {
+      Nvtx iter("admm_iteration");
       int* fk = flags + (k - 1);
       double* obj = (objv && k >= 2) ? objv + (size_t)(k - 2) * batch : nullptr;
       int rc = kind == 0

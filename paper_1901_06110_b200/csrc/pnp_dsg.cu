@@ -11,6 +11,7 @@
 // The Kx and d channels see exactly the same instruction sequence in every
 // variant, so apply() is bit-identical to the adaptive call.
 #include <float.h>
+#include <limits.h>
 #include <math.h>
 
 #include <algorithm>
@@ -616,6 +617,9 @@ static int pick_groups(int ntiles, int nchunks) {
 enum { PATH_FAST = 0, PATH_GEN_SYM = 1, PATH_GEN_NEAR = 2 };
 
 static int choose_path(int R, int P, bool box, int& kind, int& TH) {
+#ifdef PNP_BOX_FAST  // A/B variant: box taps through the P-templated kernel too
+  box = false;
+#endif
   if (!box && P <= kMaxP && R <= kMaxR) {
     kind = PATH_FAST;
     TH = tile_height(P);
@@ -945,6 +949,8 @@ static int run_sweep_gen(pnp_ctx* ctx, const Geom& g, const Window& w, int C, co
     a.taps_v[i] = (float)(scale * (double)taps[i]);
   }
   for (int i = 0; i <= g.NG; ++i) a.grp[i] = g.grp[i];
+  a.partial_floats = partial == ctx->partial.ptr ? (long long)(ctx->partial.bytes / sizeof(float))
+                                                 : LLONG_MAX;
   dim3 grid(w.ntr * g.tiles_x, g.NG, g.B);
   ProfScope prof(ctx, PROF_SWEEP);
   cudaError_t e = launch_generic(a, C, g.box, g.kind == PATH_GEN_SYM, grid, ctx->stream);
@@ -980,6 +986,9 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
   a.kcache = kcache;
   a.kc_tile = (long long)half_window(g.R) * g.TH * kTW;
   a.kc_img = (long long)w.ntr * g.tiles_x * a.kc_tile;
+  a.partial_floats = partial == ctx->partial.ptr ? (long long)(ctx->partial.bytes / sizeof(float))
+                                                 : LLONG_MAX;
+  a.kcache_floats = kcache ? (long long)g.B * a.kc_img : 0;
   // k = exp(-sum w_a w_b D / (2 bw^2)) = ex2(-log2(e)/(2 bw^2) * ...)
   const double scale = -1.0 / (2.0 * log(2.0) * bw * bw);
   for (int i = 0; i < g.P; ++i) {
@@ -1238,6 +1247,7 @@ int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P, int box
 int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out, int batch,
                     int H, int W, int R, int P, const float* taps, double bandwidth,
                     float* d_out, float* alpha_out) {
+  Nvtx range("dsg_denoise");
   if (!ctx || !x || !out) return fail(PNP_EINVAL, "null argument");
   int rc = check_geometry(batch, H, W, R, P, bandwidth);
   if (rc) return rc;
@@ -1412,6 +1422,7 @@ int pnp_dsg_denoise_banded(pnp_ctx* ctx, const float* x, float* out, int H, int 
 
 int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, int R, int P,
                    const float* taps, double bandwidth, pnp_frozen** out) {
+  Nvtx range("dsg_freeze");
   if (!ctx || !guide || !out) return fail(PNP_EINVAL, "null argument");
   int rc = check_geometry(batch, H, W, R, P, bandwidth);
   if (rc) return rc;
@@ -1481,6 +1492,7 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
 }
 
 int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out) {
+  Nvtx range("dsg_apply");
   if (fz && ctx) fz->stream = ctx->stream;
   if (!ctx || !fz || !x || !out) return fail(PNP_EINVAL, "null argument");
   if (fz->device != ctx->device) return fail(PNP_EINVAL, "handle belongs to another device");
@@ -1597,6 +1609,7 @@ int pnp_frozen_cache(const pnp_frozen* fz, int* rows_cached, int* tile_rows,
 
 int pnp_nlm_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out, int batch,
                     int H, int W, int R, int P, const float* taps, double bandwidth) {
+  Nvtx range("nlm_denoise");
   if (!ctx || !x || !out) return fail(PNP_EINVAL, "null argument");
   int rc = check_geometry(batch, H, W, R, P, bandwidth);
   if (rc) return rc;

@@ -1222,6 +1222,7 @@ int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, con
   float* vnext = v1;
   int cur = 0;
   for (int k = k0; k <= k1; ++k) {
+    Nvtx iter("admm_iteration");
     int* fk = flags + (k - 1);
     double* obj = (objv && k >= 2) ? objv + (size_t)(k - 2) * batch : nullptr;
     if (k > k0) PNP_CUDA(cudaStreamWaitEvent(main, ctx->ev_res, 0));

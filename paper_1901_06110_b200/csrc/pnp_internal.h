@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <map>
 #include <tuple>
@@ -99,12 +100,25 @@ struct pnp_ctx {
 };
 
 namespace pnp {
-// Brackets one kernel launch with events on the context stream when
-// profiling is on (used by bench.py for the live roofline numbers).
+// NVTX range for timelines (nsys): API calls, launches, ADMM iterations.
+// Header-only NVTX v3: a no-op unless a tool is attached.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+inline const char* prof_name(int cat) {
+  static const char* names[] = {"sweep", "fixup", "forward", "admm", "sweep_cached", "check"};
+  return cat >= 0 && cat < 6 ? names[cat] : "pnp";
+}
+// Brackets one kernel launch with an NVTX range and, when profiling is on,
+// with events on the context stream (bench.py's live roofline numbers).
 struct ProfScope {
   pnp_ctx* c;
   size_t idx;
-  ProfScope(pnp_ctx* ctx, int cat) : c(ctx), idx((size_t)-1) {
+  Nvtx range;
+  ProfScope(pnp_ctx* ctx, int cat) : c(ctx), idx((size_t)-1), range(prof_name(cat)) {
     if (!c->prof) return;
     if (c->nslots == c->slots.size()) {
       ProfSlot s;

@@ -50,3 +50,31 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 }  // namespace pnp
+
+// ---- debug builds (scripts/build_variant.py ... -- -DPNP_CHECKS -DPNP_JITTER) ----
+// PNP_CHECKS: device asserts on shared-memory indices and on every global
+// write of the sweeps / fixups (partial blocks, k cache) against the buffer
+// sizes the host passes; PNP_JITTER: every warp sleeps a pseudo-random
+// 0-2 us before each block barrier of the sweeps, so warps reach the ordered
+// flushes in a different order on every run -- any missing barrier shows up
+// as a result that changes between runs (compute-sanitizer is not available
+// on this pool; tests/test_checks_gpu.py drives both).
+#include <assert.h>
+#ifdef PNP_CHECKS
+#define PNP_CHECK(cond) assert(cond)
+#else
+#define PNP_CHECK(cond) ((void)0)
+#endif
+namespace pnp {
+__device__ __forceinline__ void jitter_sync() {
+#ifdef PNP_JITTER
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  unsigned h = (unsigned)(t ^ (t >> 13)) * 2654435761u;
+  h ^= (blockIdx.x * 977u + blockIdx.y * 131u + (threadIdx.x >> 5) * 40503u) * 2246822519u;
+  __nanosleep((h >> 7) & 2047u);
+#endif
+  __syncthreads();
+}
+}  // namespace pnp
+

@@ -94,7 +94,8 @@ def test_config3_qis_512(pnp):
 
     def keep(k, x, v, u):
         if k in (5, 10):
-            early[k] = v.double().cpu().numpy()
+            early[k] = (v.double().cpu().numpy() if isinstance(v, torch.Tensor)
+                        else np.asarray(v, dtype=np.float64))
 
     v, recs = pnp.linearized_pnp_admm(prob, cfg, callback=keep)
     got, ref = _rec(recs), gd["rec"]
