@@ -82,9 +82,10 @@ int pnp_ctx_reserve(pnp_ctx* ctx, int batch, int H, int W, int R, int P, int box
  * out = K x / m + (1 - d / m) x with K = D^-1/2 (hat o K_nlm) D^-1/2,
  * d = K 1 (normalized row sums), m = max d per image.
  * taps: P normalized 1-D patch taps.  Equal taps (1/P) are the reference's
- * box patch distance and run the general sweep with running-sum box filters
- * (cost flat in P; any odd P <= 63, any R); other taps (Gaussian) run the
- * P-templated sweep for P <= 15, R <= 32 and the general sweep beyond.
+ * box patch distance; from P = 11 they run the general sweep with
+ * running-sum box filters (cost flat in P; any odd P <= 63, any R), below it
+ * the P-templated sweep.  Other taps (Gaussian) run the P-templated sweep for
+ * P <= 15, R <= 32 and the general sweep beyond.
  * guide may equal x.  d_out (B*H*W) and alpha_out (B floats, = m) are
  * optional device outputs. */
 int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out,

@@ -1,8 +1,9 @@
 // DSG-NLM offset sweep for any patch side and search radius (sm_100a).
 //
 // The P-templated sweep (dsg_sweep.cuh) covers Gaussian patch weights with
-// P <= 15, R <= 32.  This kernel is the general one, and the one used for the
-// reference's own box patch weights at every P: the box patch distance
+// P <= 15 (box weights with P <= 9), R <= 32.  This kernel is the general one,
+// and the one used for the reference's own box patch weights from P = 11 on
+// (its Table-1 range, P = 11..29, in one kernel): the box patch distance
 //   SSD_t(s) = sum_{a,b < P} (G(s+ab) - G(s+t+ab))^2       (denoise.py:131-158)
 // is computed with running sums (a horizontal then a vertical running box
 // sum over the squared-difference rows), so the cost per pixel-offset does
@@ -34,6 +35,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "dsg_sweep.cuh"
@@ -44,6 +46,7 @@ constexpr int kGenThreads = 128;  // 64 columns x 2 row halves in phase V
 constexpr int kGenDXC = 32;       // dx values per staged chunk
 constexpr int kGenMaxP = 63;      // largest patch side (shared memory)
 constexpr int kGenSeg = 32;       // phase-H segment (running-sum restart)
+constexpr int kGenNmax = 16;      // rows per phase-V thread (TH <= 32)
 
 struct GenArgs {
   const float* guide;  // [B][buf_rows][W]
@@ -61,26 +64,29 @@ struct GenArgs {
   long long partial_floats;  // buffer size (PNP_CHECKS)
 };
 
-// Shared-memory geometry of one CTA (floats); also used by the host to pick TH.
+// Shared-memory geometry of one CTA (floats); also used by the host to pick
+// the tile height TH and the batch size KG.
 struct GenSmem {
-  int M, GOS, GPS, HS, YS, AR, AC;
+  int M, GOS, GPR, GPS, HS, YR, YS, AR, AC;
   int off_gp, off_h, off_y, off_a, total;
 };
 
-__host__ __device__ inline GenSmem gen_smem(int TH, int P, int R, int C, bool sym) {
+__host__ __device__ inline GenSmem gen_smem(int TH, int P, int R, int C, bool sym, int KG) {
   GenSmem s;
   const int p = (P - 1) / 2;
   s.M = TH + 2 * p;
   s.GOS = (kTW + 2 * p) | 1;
+  s.GPR = s.M + KG - 1;
   s.GPS = (kTW + 2 * p + kGenDXC) | 1;
   s.HS = kTW + 1;
+  s.YR = TH + KG - 1;
   s.YS = kTW + kGenDXC;
-  s.AR = sym ? TH + R : 0;
+  s.AR = sym ? TH + R + KG - 1 : 0;
   s.AC = sym ? kTW + 2 * R : 0;
   s.off_gp = s.M * s.GOS;
-  s.off_h = s.off_gp + s.M * s.GPS;
-  s.off_y = s.off_h + s.M * s.HS;
-  s.off_a = s.off_y + C * TH * s.YS;
+  s.off_h = s.off_gp + s.GPR * s.GPS;
+  s.off_y = s.off_h + KG * s.M * s.HS;
+  s.off_a = s.off_y + C * s.YR * s.YS;
   s.total = s.off_a + C * s.AR * s.AC;
   return s;
 }
@@ -90,12 +96,12 @@ __device__ __forceinline__ float sqd(float a, float b) {
   return __fmul_rn(t, t);
 }
 
-template <int C, bool BOX, bool SYM>
+template <int C, bool BOX, bool SYM, int KG>
 __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs a) {
   pdl_begin();
   extern __shared__ float smem[];
   const int R = a.R, P = a.P, TH = a.TH, p = (P - 1) / 2;
-  const GenSmem L = gen_smem(TH, P, R, C, SYM);
+  const GenSmem L = gen_smem(TH, P, R, C, SYM, KG);
   float* Gown = smem;
   float* Gpart = smem + L.off_gp;
   float* Hs = smem + L.off_h;
@@ -146,52 +152,90 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 
   const int x = tid & (kTW - 1), g = tid / kTW;
   const int N = TH / 2, rA = g * N;  // phase-V rows [rA, rA + N)
-  float near[C][16], yown[C][16];
+  float near[C][kGenNmax], yown[C][kGenNmax];
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < kGenNmax; ++i) {
       const float v = i < N ? yval(c_, r0g + rA + i, c0g + x) : 0.f;
       yown[c_][i] = v;
       near[c_][i] = blockIdx.y == 0 ? v : 0.f;  // self pair: k = hat = 1
     }
 
+  // Far end (SYM), per batch of KG offsets (dy0 + j, dx): thread (x, g)
+  // credits tile rows rA + i + dy0 + j of column x + dx; they sit in a
+  // register window pf[w], w = i + j < N + KG - 1, flushed once per dx.  The
+  // two row halves' windows overlap in KG - 1 rows: half 0 flushes its whole
+  // window before the barrier that ends the dx step, half 1 its private rows;
+  // half 1's shared rows go in after that barrier (top of the next step,
+  // before the next phase-H barrier): one writer per cell between barriers,
+  // a fixed order (half 0, half 1) -> bit-reproducible.
+  constexpr int WIN = kGenNmax + KG - 1;
+  float pf[C][SYM ? WIN : 1];
+  float pendv[C][KG > 1 ? KG - 1 : 1];
+  float* pend = nullptr;
+  auto flush_pending = [&]() {
+    if (SYM && pend) {
+#pragma unroll
+      for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+        for (int w = 0; w < KG - 1; ++w) {
+          float* q = pend + (c_ * L.AR + w) * L.AC;
+          PNP_CHECK(q >= As && q < As + C * L.AR * L.AC);
+          *q = __fadd_rn(*q, pendv[c_][w]);
+        }
+      pend = nullptr;
+    }
+  };
+
   const int dy_min = SYM ? 0 : -R;
   const int n_dx = 2 * R + 1;
-  for (int dyi = a.grp[blockIdx.y]; dyi < a.grp[blockIdx.y + 1]; ++dyi) {
-    const int dy = dyi + dy_min;
-    // half window: dy == 0 -> dx in [1, R]; full window skips (0, 0) only
-    const int dx_lo = (SYM && dy == 0) ? 1 : -R;
-    for (int dxa = dx_lo; dxa <= R; dxa += kGenDXC) {
+  const int gend = a.grp[blockIdx.y + 1];
+  for (int b0 = a.grp[blockIdx.y]; b0 < gend; b0 += KG) {
+    const int nb = min(KG, gend - b0);
+    const int dy0 = b0 + dy_min;
+    for (int dxa = -R; dxa <= R; dxa += kGenDXC) {
       const int dxb = min(dxa + kGenDXC, R + 1);
       jitter_sync();  // previous users of Gpart / Ys are done
-      // partner guide rows: map row q <-> image row r0g - p + q + dy, col j
-      // <-> image col c0g - p + dxa + j
+      // partner guide rows: row q <-> image row r0g - p + q + dy0 (offset j
+      // reads rows q + j), col jj <-> image col c0g - p + dxa + jj
       const int gpw = kTW + 2 * p + (dxb - dxa) - 1;
-      for (int q = tid / 32; q < M; q += kGenThreads / 32) {
-        const float* src = Gimg + (size_t)grow(r0g - p + q + dy) * W;
-        for (int j = tid & 31; j < gpw; j += 32)
-          Gpart[q * L.GPS + j] = __ldg(src + reflect_index(c0g - p + dxa + j, W));
+      for (int q = tid / 32; q < L.GPR; q += kGenThreads / 32) {
+        const float* src = Gimg + (size_t)grow(r0g - p + q + dy0) * W;
+        for (int jj = tid & 31; jj < gpw; jj += 32)
+          Gpart[q * L.GPS + jj] = __ldg(src + reflect_index(c0g - p + dxa + jj, W));
       }
-      // partner channel rows: row r <-> image row r0g + r + dy, col j <->
-      // image col c0g + dxa + j
+      // partner channel rows: row r <-> image row r0g + r + dy0, col jj <->
+      // image col c0g + dxa + jj
       const int yw = kTW + (dxb - dxa) - 1;
 #pragma unroll
       for (int c_ = 0; c_ < C; ++c_)
-        for (int r = tid / 32; r < TH; r += kGenThreads / 32)
-          for (int j = tid & 31; j < yw; j += 32)
-            Ys[(c_ * TH + r) * L.YS + j] = yval(c_, r0g + r + dy, c0g + dxa + j);
+        for (int r = tid / 32; r < L.YR; r += kGenThreads / 32)
+          for (int jj = tid & 31; jj < yw; jj += 32)
+            Ys[(c_ * L.YR + r) * L.YS + jj] = yval(c_, r0g + r + dy0, c0g + dxa + jj);
       jitter_sync();
 
       for (int dx = dxa; dx < dxb; ++dx) {
-        if (!SYM && dy == 0 && dx == 0) continue;  // self pair: analytic
         const int cdx = dx - dxa;
-        // ---- phase H: map row q, columns [x0, x0 + 32) ----
-        for (int it = tid; it < 2 * M; it += kGenThreads) {
-          const int q = it >> 1, x0 = (it & 1) * kGenSeg;
+        // offsets of the batch that exist: j < nb, minus the half window's
+        // (0, dx <= 0) / the full window's self pair (uniform over the CTA)
+        unsigned valid = 0;
+#pragma unroll
+        for (int j = 0; j < KG; ++j) {
+          const int dy = dy0 + j;
+          const bool ok = j < nb && !(dy == 0 && (SYM ? dx <= 0 : dx == 0));
+          valid |= (ok ? 1u : 0u) << j;
+        }
+        if (!valid) continue;
+        flush_pending();
+        // ---- phase H: offset j, map row q, columns [x0, x0 + 32) ----
+        for (int it = tid; it < KG * 2 * M; it += kGenThreads) {
+          const int j = it / (2 * M), rem = it - j * 2 * M;
+          if (!((valid >> j) & 1u)) continue;
+          const int x0 = (rem / M) * kGenSeg, q = rem % M;
           const float* own = Gown + q * L.GOS + x0;
-          const float* part = Gpart + q * L.GPS + x0 + cdx;
-          float* h = Hs + q * L.HS + x0;
+          const float* part = Gpart + (q + j) * L.GPS + x0 + cdx;
+          float* h = Hs + (j * M + q) * L.HS + x0;
           if (BOX) {
             float s = sqd(part[0], own[0]);
             for (int bb = 1; bb < P; ++bb) s = __fadd_rn(s, sqd(part[bb], own[bb]));
@@ -213,45 +257,77 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
           }
         }
         jitter_sync();
-        // ---- phase V: column x, rows [rA, rA + N) ----
-        {
-          const float Lt = a.ltab ? a.ltab[(dy + R) * n_dx + dx + R] : 0.f;
-          const float* hc = Hs + rA * L.HS + x;
-          const float* yp = Ys + rA * L.YS + x + cdx;
-          float* ap = SYM ? As + (rA + dy) * L.AC + x + dx + R : nullptr;
-          float s = 0.f;
-          if (BOX) {
-            s = hc[0];
-            for (int aa = 1; aa < P; ++aa) s = __fadd_rn(s, hc[aa * L.HS]);
-          }
+        // ---- phase V: column x, rows [rA, rA + N), the batch's offsets as
+        // independent chains ----
+        float Lt[KG], sv[KG];
+        const float* hc[KG];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i >= N) break;
+        for (int j = 0; j < KG; ++j) {
+          const int dy = dy0 + j;
+          Lt[j] = ((valid >> j) & 1u) ? (a.ltab ? a.ltab[(dy + R) * n_dx + dx + R] : 0.f)
+                                      : -INFINITY;
+          hc[j] = Hs + (j * M + rA) * L.HS + x;
+          sv[j] = 0.f;
+          if (BOX && ((valid >> j) & 1u)) {
+            float s = hc[j][0];
+            for (int aa = 1; aa < P; ++aa) s = __fadd_rn(s, hc[j][aa * L.HS]);
+            sv[j] = s;
+          }
+        }
+        if (SYM) {
+#pragma unroll
+          for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+            for (int w = 0; w < WIN; ++w) pf[c_][w] = 0.f;
+        }
+        const float* yp = Ys + rA * L.YS + x + cdx;
+#pragma unroll
+        for (int i = 0; i < kGenNmax; ++i) {
+          if (i >= N) break;
+#pragma unroll
+          for (int j = 0; j < KG; ++j) {
+            if (!((valid >> j) & 1u)) continue;
             float e;
             if (BOX) {
-              e = __fmaf_rn(s, a.cv, Lt);
+              e = __fmaf_rn(sv[j], a.cv, Lt[j]);
               if (i + 1 < N)
-                s = __fsub_rn(__fadd_rn(s, hc[(i + P) * L.HS]), hc[i * L.HS]);
+                sv[j] = __fsub_rn(__fadd_rn(sv[j], hc[j][(i + P) * L.HS]), hc[j][i * L.HS]);
             } else {
-              e = Lt;
-              for (int aa = 0; aa < P; ++aa) e = __fmaf_rn(a.taps_v[aa], hc[(i + aa) * L.HS], e);
+              e = Lt[j];
+              for (int aa = 0; aa < P; ++aa)
+                e = __fmaf_rn(a.taps_v[aa], hc[j][(i + aa) * L.HS], e);
             }
             const float k = ex2_approx(e);
 #pragma unroll
             for (int c_ = 0; c_ < C; ++c_) {
-              near[c_][i] = __fmaf_rn(k, yp[(c_ * TH + i) * L.YS], near[c_][i]);
-              if (SYM) {
-                float* q = ap + (c_ * L.AR + i) * L.AC;
-                PNP_CHECK(q >= As && q < As + C * L.AR * L.AC);
-                *q = __fmaf_rn(k, yown[c_][i], *q);
-              }
+              near[c_][i] = __fmaf_rn(k, yp[(c_ * L.YR + i + j) * L.YS], near[c_][i]);
+              if (SYM) pf[c_][i + j] = __fmaf_rn(k, yown[c_][i], pf[c_][i + j]);
             }
           }
+        }
+        if (SYM) {  // flush the window (half 1 defers its first KG - 1 rows)
+          float* base = As + (rA + dy0) * L.AC + x + dx + R;
+#pragma unroll
+          for (int c_ = 0; c_ < C; ++c_)
+#pragma unroll
+            for (int w = 0; w < WIN; ++w) {
+              if (w >= N + KG - 1) break;
+              if (g == 1 && w < KG - 1) {
+                pendv[c_][w] = pf[c_][w];
+                continue;
+              }
+              float* q = base + (c_ * L.AR + w) * L.AC;
+              PNP_CHECK(q >= As && q < As + C * L.AR * L.AC);
+              *q = __fadd_rn(*q, pf[c_][w]);
+            }
+          if (g == 1 && KG > 1) pend = base;
         }
         jitter_sync();
       }
     }
   }
+  flush_pending();
+  jitter_sync();
 
   // ---- emit: own pixels get near + far; the block is tile + band (SYM) or
   // the tile alone ----
@@ -260,12 +336,11 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
       (((size_t)b * a.part_ntr + a.part_off + tyl) * gridDim.y + blockIdx.y) * a.tiles_x + tx;
   float* out = a.partial + slot * (size_t)(C * BR * BC);
   PNP_CHECK((long long)((slot + 1) * (size_t)(C * BR * BC)) <= a.partial_floats);
-  PNP_CHECK(L.total * 4 <= 227 * 1024);
   if (SYM) {
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < kGenNmax; ++i) {
         if (i >= N) break;
         float* q = As + (c_ * L.AR + rA + i) * L.AC + x + R;
         *q = __fadd_rn(near[c_][i], *q);
@@ -278,17 +353,15 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < kGenNmax; ++i) {
         if (i >= N) break;
         out[((size_t)c_ * BR + rA + i) * BC + x] = near[c_][i];
       }
   }
 }
 
-}  // namespace pnp
-
-namespace pnp {
 // pnp_generic.cu
-cudaError_t launch_generic(const GenArgs& a, int C, bool box, bool sym, dim3 grid,
+cudaError_t launch_generic(const GenArgs& a, int C, bool box, bool sym, int KG, dim3 grid,
                            cudaStream_t st);
+
 }  // namespace pnp

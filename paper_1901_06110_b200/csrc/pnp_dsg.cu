@@ -538,6 +538,7 @@ struct Geom {
   int kind;          // PATH_FAST / PATH_GEN_SYM / PATH_GEN_NEAR
   bool box;          // equal patch taps: running-sum box filter (general kernel)
   int Rb;            // far band of a partial block (R, or 0 for tile-only blocks)
+  int KG;            // general kernel: dy offsets per batch
   const Chunk* chunks;        // hat-tapered table (DSG), host (fast kernel)
   const Chunk* chunks_nohat;  // same offsets, L = 0 (plain NLM), host
   const int* grp;             // NG+1 group starts (chunks, or dy indices), host
@@ -607,40 +608,64 @@ static int pick_groups(int ntiles, int nchunks) {
 
 // Which sweep kernel a geometry uses -- a function of (R, P, box) only, so
 // adaptive, frozen, batched and sharded calls agree:
-//   PATH_FAST      Gaussian taps, P <= 15, R <= 32: the P-templated sweep
-//                  (dsg_sweep.cuh; k cache, packed f32x2 filter)
-//   PATH_GEN_SYM   box taps (the reference's patch distance) at any P, or
-//                  Gaussian beyond the fast kernel: the general sweep
-//                  (dsg_generic.cuh), half window, tile + band blocks
+//   PATH_FAST      R <= 32 and Gaussian taps with P <= 15 / box taps with
+//                  P <= 9: the P-templated sweep (dsg_sweep.cuh; k cache,
+//                  packed f32x2 filter)
+//   PATH_GEN_SYM   box taps (the reference's patch distance) from P = 11, and
+//                  everything beyond the fast kernel: the general sweep
+//                  (dsg_generic.cuh; running-sum box filter, cost flat in P),
+//                  half window, tile + band blocks
 //   PATH_GEN_NEAR  the general sweep over the full window, tile-only blocks
 //                  (search radii whose far plane exceeds shared memory)
 enum { PATH_FAST = 0, PATH_GEN_SYM = 1, PATH_GEN_NEAR = 2 };
 
-static int choose_path(int R, int P, bool box, int& kind, int& TH) {
+static int choose_path(int R, int P, bool box, int& kind, int& TH, int& KG) {
 #ifdef PNP_BOX_FAST  // A/B variant: box taps through the P-templated kernel too
   box = false;
 #endif
-  if (!box && P <= kMaxP && R <= kMaxR) {
+  KG = 0;
+  // Box patches (the reference's distance) run the general kernel from
+  // P = 11 on -- one running-sum kernel over the reference's own Table-1 range
+  // (P = 11..29, flat in P); below, and for Gaussian taps up to P = 15, the
+  // P-templated kernel (its direct filter is the faster one there).
+  if (P <= (box ? 9 : kMaxP) && R <= kMaxR) {
     kind = PATH_FAST;
     TH = tile_height(P);
     return PNP_OK;
   }
   if (P > kGenMaxP)
     return fail(PNP_EINVAL, "patch_side > " + std::to_string(kGenMaxP) + " not supported");
-  auto bytes = [&](int th, bool sym) { return (size_t)gen_smem(th, P, R, 2, sym).total * 4; };
+  auto bytes = [&](int th, bool sym, int kg) {
+    return (size_t)gen_smem(th, P, R, 2, sym, kg).total * 4;
+  };
   const size_t two = 113 * 1024, one = 227 * 1024;  // 2 / 1 CTAs per SM
-  for (int th : {32, 16})
-    if (bytes(th, true) <= two) { kind = PATH_GEN_SYM; TH = th; return PNP_OK; }
-  for (int th : {32, 16, 8})
-    if (bytes(th, true) <= one) { kind = PATH_GEN_SYM; TH = th; return PNP_OK; }
-  for (int th : {32, 16, 8})
-    if (bytes(th, false) <= one) { kind = PATH_GEN_NEAR; TH = th; return PNP_OK; }
+  // (tile height, batch): taller tiles amortize the patch halo, bigger
+  // batches the barriers; two resident CTAs per SM first
+  const int cand[][2] = {{32, 4}, {16, 4}, {32, 2}, {16, 2}, {8, 4}, {8, 2}};
+  for (size_t lim : {two, one})
+    for (auto& c : cand)
+      if (bytes(c[0], true, c[1]) <= lim) {
+        kind = PATH_GEN_SYM;
+        TH = c[0];
+        KG = c[1];
+        return PNP_OK;
+      }
+  for (auto& c : cand)
+    if (bytes(c[0], false, c[1]) <= one) {
+      kind = PATH_GEN_NEAR;
+      TH = c[0];
+      KG = c[1];
+      return PNP_OK;
+    }
   return fail(PNP_EINVAL, "patch / window too large for shared memory");
 }
 
 // The general kernel's offset groups: ranges of dy values, balanced by offset
 // count, about 4 CTAs per SM over the whole grid.
-static void gen_groups(int R, bool sym, int ntiles, std::vector<int>& grp) {
+static void gen_groups(int R, bool sym, int KG, int ntiles, std::vector<int>& grp) {
+  // balanced by offset count over the dy values; a group's last batch of KG
+  // may be partial (its missing offsets are masked in the kernel)
+  (void)KG;
   const int ndy = sym ? R + 1 : 2 * R + 1;
   std::vector<long long> cnt(ndy);
   long long total = 0;
@@ -690,12 +715,12 @@ static bool taps_box(const float* taps, int P) {
 }
 
 static int groups_for(int Hg, int W, int R, int P, bool box) {
-  int kind = 0, TH = 0;
-  if (choose_path(R, P, box, kind, TH)) return -1;
+  int kind = 0, TH = 0, KG = 0;
+  if (choose_path(R, P, box, kind, TH, KG)) return -1;
   const int ntiles = ((W + kTW - 1) / kTW) * ((Hg + TH - 1) / TH);
   if (kind != PATH_FAST) {
     std::vector<int> grp;
-    gen_groups(R, kind == PATH_GEN_SYM, ntiles, grp);
+    gen_groups(R, kind == PATH_GEN_SYM, KG, ntiles, grp);
     return (int)grp.size() - 1;
   }
   int nch = 0;
@@ -710,7 +735,7 @@ static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, bool box,
   g.R = R;
   g.P = P;
   g.box = box;
-  int rc = choose_path(R, P, box, g.kind, g.TH);
+  int rc = choose_path(R, P, box, g.kind, g.TH, g.KG);
   if (rc) return rc;
   g.Rb = g.kind == PATH_GEN_NEAR ? 0 : R;
   g.tiles_x = (W + kTW - 1) / kTW;
@@ -720,10 +745,10 @@ static int make_geom(pnp_ctx* ctx, int B, int Hg, int W, int R, int P, bool box,
   const int ntiles = g.tiles_x * g.tiles_y;
   if (g.kind != PATH_FAST) {
     std::vector<int> grp;
-    gen_groups(R, g.kind == PATH_GEN_SYM, ntiles, grp);
+    gen_groups(R, g.kind == PATH_GEN_SYM, g.KG, ntiles, grp);
     g.NG = g.NP = (int)grp.size() - 1;
     g.nchunks = 0;
-    auto key = std::make_tuple(R, g.NG, g.kind);
+    auto key = std::make_tuple(R, g.NG * 8 + g.KG, g.kind);
     auto it = ctx->tables.find(key);
     if (it == ctx->tables.end()) {
       pnp_ctx::Tables t;
@@ -953,7 +978,7 @@ static int run_sweep_gen(pnp_ctx* ctx, const Geom& g, const Window& w, int C, co
                                                  : LLONG_MAX;
   dim3 grid(w.ntr * g.tiles_x, g.NG, g.B);
   ProfScope prof(ctx, PROF_SWEEP);
-  cudaError_t e = launch_generic(a, C, g.box, g.kind == PATH_GEN_SYM, grid, ctx->stream);
+  cudaError_t e = launch_generic(a, C, g.box, g.kind == PATH_GEN_SYM, g.KG, grid, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "dsg_generic_kernel");
   return PNP_OK;
 }
@@ -1302,8 +1327,8 @@ int pnp_dsg_band_rows(int H, int W, int R, int P, int box, int nbands, int* tile
   if (!tile_end || !rows_needed || nbands < 1) return fail(PNP_EINVAL, "bad arguments");
   int rc = check_geometry(1, H, W, R, P, 1.0);
   if (rc) return rc;
-  int kind = 0, th = 0;
-  if ((rc = choose_path(R, P, box != 0, kind, th))) return rc;
+  int kind = 0, th = 0, kg = 0;
+  if ((rc = choose_path(R, P, box != 0, kind, th, kg))) return rc;
   if (kind != PATH_FAST) return fail(PNP_EINVAL, "banded denoise needs the P-templated sweep");
   if (nbands > (H + tile_height(P) - 1) / tile_height(P))
     return fail(PNP_EINVAL, "more bands than tile rows");
@@ -1636,8 +1661,8 @@ int pnp_dsg_geometry(int Hg, int W, int R, int P, int box, int* out) {
   if (!out) return fail(PNP_EINVAL, "null argument");
   int rc = check_geometry(1, Hg, W, R, P, 1.0);
   if (rc) return rc;
-  int kind = 0, TH = 0;
-  if ((rc = choose_path(R, P, box != 0, kind, TH))) return rc;
+  int kind = 0, TH = 0, KG = 0;
+  if ((rc = choose_path(R, P, box != 0, kind, TH, KG))) return rc;
   const int p = (P - 1) / 2;
   out[0] = TH;
   out[1] = groups_for(Hg, W, R, P, box != 0);
@@ -1658,7 +1683,7 @@ int pnp_dsg_geometry(int Hg, int W, int R, int P, int box, int* out) {
     out[5] = R + p;
     out[6] = R;
   }
-  out[7] = 0;
+  out[7] = KG;
   return PNP_OK;
 }
 
@@ -1669,8 +1694,8 @@ int pnp_dsg_groups(int Hg, int W, int R, int P, int box) {
 
 int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int box, int C, int ntr) {
   if (check_geometry(1, Hg, W, R, P, 1.0) || C < 1 || C > 2 || ntr < 0) return -1;
-  int kind = 0, TH = 0;
-  if (choose_path(R, P, box != 0, kind, TH)) return -1;
+  int kind = 0, TH = 0, KG = 0;
+  if (choose_path(R, P, box != 0, kind, TH, KG)) return -1;
   const int Rb = kind == PATH_GEN_NEAR ? 0 : R;
   const int64_t blk = (int64_t)C * (TH + Rb) * (kTW + 2 * Rb);
   return (int64_t)ntr * groups_for(Hg, W, R, P, box != 0) * ((W + kTW - 1) / kTW) * blk;
@@ -1678,8 +1703,8 @@ int64_t pnp_dsg_partial_floats(int Hg, int W, int R, int P, int box, int C, int 
 
 int64_t pnp_dsg_kcache_floats(int Hg, int W, int R, int P, int box, int ntr) {
   if (check_geometry(1, Hg, W, R, P, 1.0) || ntr < 0) return -1;
-  int kind = 0, TH = 0;
-  if (choose_path(R, P, box != 0, kind, TH)) return -1;
+  int kind = 0, TH = 0, KG = 0;
+  if (choose_path(R, P, box != 0, kind, TH, KG)) return -1;
   if (kind != PATH_FAST) return 0;  // the general sweep recomputes its weights
   return (int64_t)half_window(R) * ntr * TH * (((W + kTW - 1) / kTW) * kTW);
 }

@@ -29,9 +29,9 @@ def _path(pnp, H, W, p):
 
 CASES = [
     # H, W, R, P, bw, sigma, seed
-    (40, 52, 3, 1, 0.2, None, 1),
-    (37, 45, 2, 3, 0.25, None, 2),
-    (48, 70, 5, 7, 0.2, None, 3),      # box at a small P: general kernel too
+    (40, 52, 3, 11, 0.2, None, 1),     # box from P = 11: the general kernel
+    (37, 45, 2, 13, 0.25, None, 2),
+    (48, 70, 5, 15, 0.2, None, 3),
     (64, 64, 8, 17, 0.15, None, 4),
     (50, 71, 6, 31, 0.3, None, 5),
     (70, 90, 4, 45, 0.4, None, 6),

@@ -74,3 +74,22 @@ def test_synth_splitmix_matches_reference(golden_forward):
     assert [r.next_uint64() for _ in range(4)] == [int(v) for v in f["splitmix_u64"]]
     assert np.array_equal(SplitMix64(99).uniforms(1001), f["splitmix_uniforms"])
     assert np.array_equal(SplitMix64(5).normals(999), f["splitmix_normals"])
+
+
+def test_sweep_path_routing():
+    """pnp_dsg_geometry (host logic, no GPU): box taps run the P-templated
+    kernel up to P = 9 and the running-sum general kernel from P = 11 (the
+    reference's Table-1 range, P = 11..29, in one kernel whose cost is flat in
+    P); Gaussian taps the P-templated kernel up to P = 15, R <= 32; the
+    full-window variant once the half-window far plane exceeds shared memory."""
+    from paper_1901_06110_b200 import _lib as L
+    for P, box, R, want in [(1, True, 3, 0), (7, True, 10, 0), (9, True, 10, 0),
+                            (11, True, 10, 1), (29, True, 21, 1), (63, True, 5, 1),
+                            (7, False, 10, 0), (15, False, 10, 0), (17, False, 10, 1),
+                            (7, False, 40, 1), (1, True, 100, 2)]:
+        g = L.dsg_geometry(256, 256, R, P, box)
+        assert g[3] == want, (P, box, R, g)
+        assert g[0] in (8, 16, 32) or g[3] == 0
+    import pytest
+    with pytest.raises(ValueError):
+        L.dsg_geometry(256, 256, 5, 65, True)
