@@ -582,30 +582,51 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
           float2 hcol[N + 2 * p];
 #pragma unroll
           for (int i = 0; i < N + 2 * p; ++i) hcol[i] = hcol0[(kp * 32 + i) * HS];
+          // rows in pairs: the four weights of rows (r, r+1) are produced in
+          // one 128-bit register quad, which is also the k-cache store operand
+          // (the pair plane interleaves rows 2i, 2i+1; kpos)
 #pragma unroll
-          for (int r = 0; r < N; ++r) {
-            float2 v = L;
+          for (int r = 0; r < N; r += 2) {
+            float* plane = STORE ? const_cast<float*>(kq) + 2 * kp * HPF : nullptr;
+            if (r + 1 < N) {
+              float2 v0 = L, v1 = L;
 #pragma unroll
-            for (int aa = 0; aa < P; ++aa)
-              v = __ffma2_rn(make_float2(a.taps_v[aa], a.taps_v[aa]), hcol[r + aa], v);
-            kk[r] = make_float2(ex2_approx(v.x), ex2_approx(v.y));
-            if (STORE) {
-              float* plane = const_cast<float*>(kq) + 2 * kp * HPF;
-              if (pairp) {
-                float2* dst = reinterpret_cast<float2*>(plane) + r0 * kTW + kpos<N>(c, r & ~1);
-                PNP_CHECK(((const float*)(dst + ((r & 1) ? 2 : 1)) - a.kcache) <= a.kcache_floats);
-                if (r & 1)
-                  __stcs(reinterpret_cast<float4*>(dst),
-                         make_float4(kk[r - 1].x, kk[r - 1].y, kk[r].x, kk[r].y));
-                else if (r == N - 1)
+              for (int aa = 0; aa < P; ++aa) {
+                const float2 t = make_float2(a.taps_v[aa], a.taps_v[aa]);
+                v0 = __ffma2_rn(t, hcol[r + aa], v0);
+                v1 = __ffma2_rn(t, hcol[r + 1 + aa], v1);
+              }
+              const float4 q4 = make_float4(ex2_approx(v0.x), ex2_approx(v0.y),
+                                            ex2_approx(v1.x), ex2_approx(v1.y));
+              kk[r] = make_float2(q4.x, q4.y);
+              kk[r + 1] = make_float2(q4.z, q4.w);
+              if (STORE) {
+                if (pairp) {
+                  float2* dst = reinterpret_cast<float2*>(plane) + r0 * kTW + kpos<N>(c, r);
+                  PNP_CHECK(((const float*)(dst + 2) - a.kcache) <= a.kcache_floats);
+                  __stcs(reinterpret_cast<float4*>(dst), q4);
+                } else {  // single plane: the even offset only
+                  float* dst = plane + r0 * kTW + kpos<N>(c, r);
+                  PNP_CHECK((dst + 2 - a.kcache) <= a.kcache_floats);
+                  __stcs(reinterpret_cast<float2*>(dst), make_float2(q4.x, q4.z));
+                }
+              }
+            } else {  // N odd: the last row alone
+              float2 v = L;
+#pragma unroll
+              for (int aa = 0; aa < P; ++aa)
+                v = __ffma2_rn(make_float2(a.taps_v[aa], a.taps_v[aa]), hcol[r + aa], v);
+              kk[r] = make_float2(ex2_approx(v.x), ex2_approx(v.y));
+              if (STORE) {
+                if (pairp) {
+                  float2* dst = reinterpret_cast<float2*>(plane) + r0 * kTW + kpos<N>(c, r);
+                  PNP_CHECK(((const float*)(dst + 1) - a.kcache) <= a.kcache_floats);
                   __stcs(dst, kk[r]);
-              } else {  // single plane: the even offset only
-                float* dst = plane + r0 * kTW + kpos<N>(c, r & ~1);
-                PNP_CHECK((dst + ((r & 1) ? 2 : 1) - a.kcache) <= a.kcache_floats);
-                if (r & 1)
-                  __stcs(reinterpret_cast<float2*>(dst), make_float2(kk[r - 1].x, kk[r].x));
-                else if (r == N - 1)
+                } else {
+                  float* dst = plane + r0 * kTW + kpos<N>(c, r);
+                  PNP_CHECK((dst + 1 - a.kcache) <= a.kcache_floats);
                   __stcs(dst, kk[r].x);
+                }
               }
             }
           }

@@ -70,3 +70,22 @@ def test_denoise_oracle_flag(tmp_path, capsys):
     assert cli.main(["denoise", str(ini), "--oracle", "--denoiser", "nlm"]) == 2
     ini.write_text(ini.read_text().replace("small.pfm", "big.pfm"))
     assert cli.main(["denoise", str(ini), "--oracle"]) == 2
+
+
+def test_bench_denoiser_default_shape(tmp_path):
+    """bench-denoiser with the reference's default bench section (256^2,
+    R = 21, P in {11, 17, 23, 29}, bandwidth 0.15; cli.py:115-120): all four
+    rows written, GPU times within the reference's criterion-4 ratio (< 2,
+    tests/test_acceptance.py:131-153); the brute-force columns the GPU does not
+    time are nan."""
+    from paper_1901_06110_b200 import cli
+    ini = tmp_path / "b.ini"
+    ini.write_text(f"[run]\noutput_dir = {tmp_path}/runs\n[bench]\nrepeats = 5\n")
+    assert cli.main(["bench-denoiser", str(ini)]) == 0
+    (d,) = list((tmp_path / "runs").iterdir())
+    rows = (d / "bench.csv").read_text().splitlines()
+    assert rows[0] == "np,fast_s,brute_s,speedup"
+    vals = [r.split(",") for r in rows[1:]]
+    assert [int(v[0]) for v in vals] == [11, 17, 23, 29]
+    t = [float(v[1]) for v in vals]
+    assert max(t) / min(t) < 2.0, t
