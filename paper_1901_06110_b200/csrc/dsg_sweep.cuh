@@ -45,6 +45,7 @@
 // blocks of every pixel in a fixed order.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (the driver entry point is resolved at run time)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -141,6 +142,9 @@ struct SweepArgs {
   float* kcache;
   long long kc_img, kc_tile;
   long long partial_floats, kcache_floats;  // buffer sizes (PNP_CHECKS)
+  // the launch's guide tensor map (3-D: W x buf_rows x B fp32, box GCB x GR x
+  // 1) is valid: interior tiles stage their guide tile with one TMA load
+  int tma;
   float taps_h[kMaxP];  // normalized patch taps w_b (phase 1)
   float taps_v[kMaxP];  // -log2(e)/(2 bw^2) * w_a (phase 2)
 };
@@ -173,7 +177,16 @@ struct Cfg {
   static constexpr int KCH = KY * TH * kTW;  // floats per chunk (KY offset planes)
   static constexpr int OFF_K = (OFF_A + C * AR * YC + 3) & ~3;
   static constexpr int OFF_MB = OFF_K + (TMAK ? 2 * KCH : 0);
-  static constexpr int TOTAL = OFF_MB + (TMAK ? 4 : 0);  // floats
+  // guide staging by TMA (recompute / store sweeps): a dense GCB-pitch box
+  // landed in the H-map / channel / far area (128-byte aligned; all staged
+  // after it), then re-laid out with the odd pitch GS; one mbarrier
+  // box width: the tile's GC columns from a 16-byte-aligned start column (the
+  // TMA box's inner start must be 16-byte aligned: up to 3 leading columns)
+  static constexpr int GCB = (GC + 3 + 3) & ~3;
+  static constexpr int OFF_TB = (OFF_MB + (TMAK ? 4 : 0) + 1) & ~1;
+  static constexpr int TOTAL = OFF_TB + (CACHED ? 0 : 2);  // floats
+  static_assert(CACHED || OFF_TB - OFF_H >= GCB * GR + 32,
+                "TMA box fits the H-map / channel / far area");
 };
 
 __device__ __forceinline__ int reflect_index(int i, int n) {
@@ -229,9 +242,22 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// One TMA load of a 3-D box (fp32) into shared memory, completing on `bar`.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 template <int P, int RB, int C, int MODE>
 __global__ void __launch_bounds__(kThreads)
-dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
+dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab, const __grid_constant__ CUtensorMap gmap) {
   using K = Cfg<P, RB, C, MODE>;
   constexpr bool CACHED = K::CACHED, STORE = MODE == MODE_STORE;
   constexpr int p = K::p, TH = K::TH, N = K::N, SEG = K::SEG, SEGW = K::SEGW, KY = K::KY;
@@ -262,25 +288,48 @@ dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab) {
   // warps walk rows, lanes walk columns: index math once per row / column.
   // G col cc <-> image col c0g - RB - p + cc ; row q <-> r0g - p + q
   if (!CACHED) {
-    constexpr int NJ = (GC + 31) / 32;
-    int gcol[NJ];
+    // interior tiles (no reflection anywhere in the guide tile, all its rows
+    // in the buffer): one TMA load of the tile, then re-laid out with the odd
+    // pitch GS (conflict-free phase-1 loads); border tiles gather with the
+    // half-sample reflection (image.py:97-113).  Same floats either way.
+    const int gx0 = c0g - RB - p, gy0 = r0g - p, ly0 = gy0 - br0;
+    const int gxa = gx0 & ~3, sx = gx0 - gxa;  // 16-byte-aligned box start
+    const bool tma = a.tma && gx0 >= 0 && gxa + K::GCB <= W && gy0 >= 0 && gy0 + GR <= Hg &&
+                     ly0 >= 0 && ly0 + GR <= brows;
+    if (tma) {
+      float* tbuf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Hs) + 127) & ~uintptr_t(127));
+      uint64_t* tbar = reinterpret_cast<uint64_t*>(smem + K::OFF_TB);
+      if (tid == 0) {
+        mbar_init(tbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tma_load_3d(tbuf, &gmap, gxa, ly0, b, (unsigned)(K::GCB * GR * 4), tbar);
+      }
+      __syncthreads();
+      mbar_wait(tbar, 0);
+      for (int q = warp; q < GR; q += kThreads / 32)
+        for (int j = lane; j < GC; j += 32) Gs[q * GS + j] = tbuf[q * K::GCB + sx + j];
+      __syncthreads();  // tbuf (the H-map / channel / far area) is free again
+    } else {
+      constexpr int NJ = (GC + 31) / 32;
+      int gcol[NJ];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const int cc = lane + 32 * j;
-      gcol[j] = cc < GC ? reflect_index(c0g - RB - p + cc, W) : -1;
-    }
+      for (int j = 0; j < NJ; ++j) {
+        const int cc = lane + 32 * j;
+        gcol[j] = cc < GC ? reflect_index(c0g - RB - p + cc, W) : -1;
+      }
 #pragma unroll 2
-    for (int q = warp; q < GR; q += kThreads / 32) {
-      int lr = reflect_index(r0g - p + q, Hg) - br0;
-      lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
-      const float* src = Gimg + (size_t)lr * W;
-      float* dst = Gs + q * GS + lane;
+      for (int q = warp; q < GR; q += kThreads / 32) {
+        int lr = reflect_index(r0g - p + q, Hg) - br0;
+        lr = lr < 0 ? 0 : (lr >= brows ? brows - 1 : lr);
+        const float* src = Gimg + (size_t)lr * W;
+        float* dst = Gs + q * GS + lane;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
-        if (gcol[j] >= 0) {
-          PNP_CHECK(dst + 32 * j < Hs);
-          dst[32 * j] = __ldg(src + gcol[j]);
-        }
+        for (int j = 0; j < NJ; ++j)
+          if (gcol[j] >= 0) {
+            PNP_CHECK(dst + 32 * j < Hs);
+            dst[32 * j] = __ldg(src + gcol[j]);
+          }
+      }
     }
   }
   {

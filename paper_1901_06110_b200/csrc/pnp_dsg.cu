@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -845,29 +846,65 @@ static bool fixup_px(const Geom& g) {
 }
 
 template <int RB, int C, int MODE>
-static cudaError_t launch_sweep_rc(const SweepArgs& a, const HostTab& t, int P, dim3 grid, cudaStream_t st) {
+static cudaError_t launch_sweep_rc(const SweepArgs& a, const HostTab& t, int P, dim3 grid,
+                                   cudaStream_t st, const CUtensorMap& m) {
   switch (P) {
-    case 1: return launch_sweep<1, RB, C, MODE>(a, t, grid, st);
-    case 3: return launch_sweep<3, RB, C, MODE>(a, t, grid, st);
-    case 5: return launch_sweep<5, RB, C, MODE>(a, t, grid, st);
-    case 7: return launch_sweep<7, RB, C, MODE>(a, t, grid, st);
-    case 9: return launch_sweep<9, RB, C, MODE>(a, t, grid, st);
-    case 11: return launch_sweep<11, RB, C, MODE>(a, t, grid, st);
-    case 13: return launch_sweep<13, RB, C, MODE>(a, t, grid, st);
-    case 15: return launch_sweep<15, RB, C, MODE>(a, t, grid, st);
+    case 1: return launch_sweep<1, RB, C, MODE>(a, t, grid, st, m);
+    case 3: return launch_sweep<3, RB, C, MODE>(a, t, grid, st, m);
+    case 5: return launch_sweep<5, RB, C, MODE>(a, t, grid, st, m);
+    case 7: return launch_sweep<7, RB, C, MODE>(a, t, grid, st, m);
+    case 9: return launch_sweep<9, RB, C, MODE>(a, t, grid, st, m);
+    case 11: return launch_sweep<11, RB, C, MODE>(a, t, grid, st, m);
+    case 13: return launch_sweep<13, RB, C, MODE>(a, t, grid, st, m);
+    case 15: return launch_sweep<15, RB, C, MODE>(a, t, grid, st, m);
   }
   return cudaErrorInvalidValue;
 }
 
 template <int C, int MODE>
 static cudaError_t launch_sweep_cm(const SweepArgs& a, const HostTab& t, const Geom& g, dim3 grid,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, const CUtensorMap& m) {
   switch (r_bucket(g.R)) {
-    case 5: return launch_sweep_rc<5, C, MODE>(a, t, g.P, grid, st);
-    case 10: return launch_sweep_rc<10, C, MODE>(a, t, g.P, grid, st);
-    case 16: return launch_sweep_rc<16, C, MODE>(a, t, g.P, grid, st);
-    default: return launch_sweep_rc<32, C, MODE>(a, t, g.P, grid, st);
+    case 5: return launch_sweep_rc<5, C, MODE>(a, t, g.P, grid, st, m);
+    case 10: return launch_sweep_rc<10, C, MODE>(a, t, g.P, grid, st, m);
+    case 16: return launch_sweep_rc<16, C, MODE>(a, t, g.P, grid, st, m);
+    default: return launch_sweep_rc<32, C, MODE>(a, t, g.P, grid, st, m);
   }
+}
+
+// The guide as a 3-D TMA tensor (W x buf_rows x B fp32) with the sweep
+// tile's box (GCB x GR x 1) for the recompute / store sweeps' staging; false
+// (no TMA: every tile gathers) when the layout does not allow it (row pitch
+// not a multiple of 16 bytes, unaligned base) or the driver entry point is
+// unavailable.
+static bool guide_tmap(const Geom& g, const Window& w, const float* guide, CUtensorMap* m) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (EncodeFn) nullptr;
+    }
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
+  if (!encode || g.W % 4 || ((uintptr_t)guide & 15)) return false;
+  const int p = (g.P - 1) / 2, RB = r_bucket(g.R);
+  const int GC = kTW + 2 * (RB + p), GCB = (GC + 6) & ~3, GR = 33 + RB;  // Cfg::GCB
+  if (GCB > 256 || GR > 256 || GCB > g.W || GR > w.buf_rows) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)w.buf_rows, (cuuint64_t)g.B};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.W * 4, (cuuint64_t)w.buf_rows * g.W * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)GCB, (cuuint32_t)GR, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(guide), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Half-window offsets (one k-cache plane of TH x 64 floats each per tile).
@@ -1021,16 +1058,21 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
     a.taps_v[i] = (float)(scale * (double)taps[i]);
   }
   dim3 grid(w.ntr * g.tiles_x, g.NG, g.B);
+  CUtensorMap gm;
+  memset(&gm, 0, sizeof(gm));
+  static const bool no_tma = getenv("PNP_NO_TMA") != nullptr;  // A/B switch
+  a.tma = (!no_tma && mode != MODE_CACHED && guide_tmap(g, w, guide, &gm)) ? 1 : 0;
   ProfScope prof(ctx, mode == MODE_CACHED ? PROF_SWEEP_CACHED : PROF_SWEEP);
   cudaError_t e = cudaErrorInvalidValue;
   if (mode != MODE_RECOMPUTE && !kcache) return fail(PNP_EINVAL, "k cache missing");
+  cudaStream_t st = ctx->stream;
   if (C == 1) {
-    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<1, MODE_RECOMPUTE>(a, tab, g, grid, ctx->stream);
-    else if (mode == MODE_STORE) e = launch_sweep_cm<1, MODE_STORE>(a, tab, g, grid, ctx->stream);
-    else e = launch_sweep_cm<1, MODE_CACHED>(a, tab, g, grid, ctx->stream);
+    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<1, MODE_RECOMPUTE>(a, tab, g, grid, st, gm);
+    else if (mode == MODE_STORE) e = launch_sweep_cm<1, MODE_STORE>(a, tab, g, grid, st, gm);
+    else e = launch_sweep_cm<1, MODE_CACHED>(a, tab, g, grid, st, gm);
   } else {
-    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<2, MODE_RECOMPUTE>(a, tab, g, grid, ctx->stream);
-    else if (mode == MODE_CACHED) e = launch_sweep_cm<2, MODE_CACHED>(a, tab, g, grid, ctx->stream);
+    if (mode == MODE_RECOMPUTE) e = launch_sweep_cm<2, MODE_RECOMPUTE>(a, tab, g, grid, st, gm);
+    else if (mode == MODE_CACHED) e = launch_sweep_cm<2, MODE_CACHED>(a, tab, g, grid, st, gm);
   }
   if (e != cudaSuccess) return cuda_fail(e, "dsg_sweep_kernel");
   return PNP_OK;

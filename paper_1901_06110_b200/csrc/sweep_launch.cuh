@@ -10,7 +10,8 @@
 namespace pnp {
 
 template <int P, int RB, int C, int MODE>
-cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st) {
+cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaStream_t st,
+                         const CUtensorMap& gmap) {
   constexpr size_t smem = (size_t)Cfg<P, RB, C, MODE>::TOTAL * sizeof(float);
   static_assert(smem <= 227 * 1024, "sweep tile exceeds shared memory");
   // the opt-in shared-memory size is a per-device function attribute
@@ -29,52 +30,53 @@ cudaError_t launch_sweep(const SweepArgs& a, const HostTab& t, dim3 grid, cudaSt
   memset(&tab, 0, sizeof(tab));
   memcpy(tab.c, t.ch, sizeof(Chunk) * t.nch);
   memcpy(tab.grp, t.grp, sizeof(int) * (t.ng + 1));
-  return launch_pdl(dsg_sweep_kernel<P, RB, C, MODE>, grid, dim3(kThreads), smem, st, a, tab);
+  return launch_pdl(dsg_sweep_kernel<P, RB, C, MODE>, grid, dim3(kThreads), smem, st, a, tab,
+                    gmap);
 }
 
 #define PNP_INSTANTIATE_P(P) \
-  template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t);
+  template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&);
 
 #define PNP_DECLARE_P(P) \
-  extern template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t); \
-  extern template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t);
+  extern template cudaError_t launch_sweep<P, 5, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 5, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 5, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 5, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 5, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 10, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 10, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 10, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 16, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 16, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 16, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 1>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 32, 1, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 32, 2, 0>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&); \
+  extern template cudaError_t launch_sweep<P, 32, 2, 2>(const SweepArgs&, const HostTab&, dim3, cudaStream_t, const CUtensorMap&);
 
 PNP_DECLARE_P(1)
 PNP_DECLARE_P(3)
