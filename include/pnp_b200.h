@@ -92,6 +92,15 @@ int pnp_dsg_denoise(pnp_ctx* ctx, const float* x, const float* guide, float* out
                     int batch, int H, int W, int R, int P, const float* taps,
                     double bandwidth, float* d_out, float* alpha_out);
 
+/* dsg_nlm_denoise(..., distances="direct") — the reference's brute-force
+ * per-pixel path (denoise.py:291-355): three passes with the patch distance
+ * summed directly over the P x P patch (cost window area x patch area); the
+ * bench-denoiser timing baseline.  Same result as pnp_dsg_denoise within fp32
+ * rounding (P <= 63). */
+int pnp_dsg_denoise_direct(pnp_ctx* ctx, const float* x, const float* guide, float* out,
+                           int batch, int H, int W, int R, int P, const float* taps,
+                           double bandwidth);
+
 /* freeze_guide(guide, params) -> FrozenGuide — denoise.py:358-386.  The
  * library-owned handle copies the guide and keeps rs = g^-1/2, d and m. */
 int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, int R,

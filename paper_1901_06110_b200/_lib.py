@@ -47,6 +47,7 @@ _SIGS = {
     "pnp_ctx_profile_read": (i32, [vp, C.POINTER(f64), C.POINTER(i32)]),
     "pnp_peak_rates": (i32, [i32, C.POINTER(f64), C.POINTER(f64)]),
     "pnp_dsg_denoise": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64, vp, vp]),
+    "pnp_dsg_denoise_direct": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, fptr, f64]),
     "pnp_dsg_freeze": (i32, [vp, vp, i32, i32, i32, i32, i32, fptr, f64, C.POINTER(vp)]),
     "pnp_dsg_apply": (i32, [vp, vp, vp, vp]),
     "pnp_frozen_destroy": (i32, [vp]),

@@ -239,14 +239,26 @@ def dsg_nlm_denoise(image, params: PatchParams, guide=None, distances: str = "in
                     *, return_aux: bool = False):
     """Doubly stochastic NLM, W x = K x / m + (1 - d/m) x (denoise.py:272-288).
 
-    ``distances`` is accepted for drop-in compatibility ("integral" or
-    "direct" give identical results by the reference's contract,
-    tests/test_denoise.py:244-249); the GPU always uses its direct separable
-    patch filter.  ``return_aux=True`` also returns the normalized row sums d
-    and the max row sum m (north-star "alpha") as device tensors.
+    ``distances="integral"`` (default) runs the fast sweeps; ``"direct"`` the
+    brute-force per-pixel path, as in the reference (denoise.py:291-355: patch
+    distances summed over every patch element, cost window area x patch area;
+    the bench-denoiser baseline).  Both give the same result within fp32
+    rounding (the reference pins them to 1e-9 in float64,
+    tests/test_denoise.py:244-249).  ``return_aux=True`` also returns the
+    normalized row sums d and the max row sum m (north-star "alpha") as
+    device tensors (fast path).
     """
     if distances not in ("integral", "direct"):
         raise ValueError(f"unknown distance method {distances!r}")
+    if distances == "direct" and not return_aux:
+        x, g, kind, dev = _pair(image, guide)
+        B, H, W = A.dims(x)
+        _check_margin(params, H, W)
+        out = torch.empty_like(x)
+        L.call("pnp_dsg_denoise_direct", L.context(dev), L.ptr(x), L.ptr(g), L.ptr(out), B, H,
+               W, params.window_radius, params.patch_side, params._ctaps(),
+               float(params.bandwidth))
+        return A.from_device(out, kind)
     if guide is None and not return_aux:
         bands = _numpy_bands(image, params)
         if bands:

@@ -89,3 +89,6 @@ def test_bench_denoiser_default_shape(tmp_path):
     assert [int(v[0]) for v in vals] == [11, 17, 23, 29]
     t = [float(v[1]) for v in vals]
     assert max(t) / min(t) < 2.0, t
+    brute = [float(v[2]) for v in vals]
+    speed = [float(v[3]) for v in vals]
+    assert all(b > f for b, f in zip(brute, t)) and speed[-1] > speed[0] > 1.0

@@ -120,3 +120,17 @@ def test_general_sharded_equals_single(pnp):
     ref = pnp.dsg_nlm_denoise(x, p)
     for n in (2, 3):
         assert torch.equal(sharded_dsg_nlm_denoise(x, p, n), ref)
+
+
+@pytest.mark.parametrize("P,R,sigma", [(29, 21, None), (7, 10, 2.0), (3, 2, None)])
+def test_direct_distances_match(pnp, P, R, sigma):
+    """distances="direct": the brute-force per-pixel path (reference
+    denoise.py:291-355) gives the fast path's result (and the oracle's)."""
+    rng = np.random.default_rng(P + R)
+    img = rng.random((50, 61))
+    p = pnp.PatchParams(P, R, 0.2, sigma)
+    fast = pnp.dsg_nlm_denoise(img, p)
+    brute = pnp.dsg_nlm_denoise(img, p, distances="direct")
+    ref = oracle.dsg_nlm_denoise(img, P, R, 0.2, patch_sigma=sigma)
+    assert np.abs(brute - fast).max() <= 1e-5
+    assert np.abs(brute - ref).max() <= TOL
