@@ -134,3 +134,51 @@ def test_direct_distances_match(pnp, P, R, sigma):
     ref = oracle.dsg_nlm_denoise(img, P, R, 0.2, patch_sigma=sigma)
     assert np.abs(brute - fast).max() <= 1e-5
     assert np.abs(brute - ref).max() <= TOL
+
+
+def test_general_sweep_in_admm_vs_oracle(pnp):
+    """Linearized ADMM with the reference's own box weights at P = 11 (the
+    general sweep: adaptive iterations, then a frozen guide, dsg-fixed)
+    against the float64 oracle."""
+    import math
+
+    from oracle import admm as oadmm
+    from oracle import forward as ofw
+    from paper_1901_06110_b200 import synth
+    truth = synth.scene(96, 96, 2)
+    k = ofw.gaussian_kernel(1.0, 4)
+    y = ofw.sr_simulate(truth, k, 2, "symmetric", 5 / 255, 102)
+    P, R, bw = 11, 6, 0.12
+    den = oadmm.make_denoiser("dsg-fixed", P, R, bw, freeze_at=4)
+    x0 = 4 * ofw.sr_adjoint(k, 2, "symmetric", y)
+    v_ref, rec_ref = oadmm.linearized_pnp_admm(
+        x0, lambda x: ofw.sr_gradient(k, 2, "symmetric", x, y), den, rho=1.0, alpha=1.0,
+        max_iters=8, lo=0.0, hi=1.0, ground_truth=truth)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=8, freeze_at=4,
+                           constraint=pnp.UNIT_BOX, denoiser="dsg-fixed", patch_side=P,
+                           window_radius=R, bandwidth=bw)
+    v, recs = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, y, ground_truth=truth), cfg)
+    assert np.abs(v - v_ref).max() < 1e-4
+    assert abs(recs[-1].psnr - rec_ref[-1][3]) < 0.02
+    assert not math.isnan(recs[-1].psnr)
+
+
+def test_general_sweep_sharded_sr_admm_bitwise(pnp):
+    """Row-strip SR ADMM over the general sweep (box P = 13, virtual ranks)
+    equals the single-GPU solver bit for bit."""
+    from paper_1901_06110_b200.parallel import sharded_linearized_pnp_admm_sr
+    g = torch.Generator(device="cuda").manual_seed(41)
+    H, W = 256, 130
+    truth = torch.rand(H, W, device="cuda", generator=g)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
+    y = (op.apply_device(truth) + 0.02 * torch.randn(H // 2, W // 2, device="cuda",
+                                                       generator=g)).contiguous()
+    guide = (truth + 0.05 * torch.randn(H, W, device="cuda", generator=g)).clamp(0, 1)
+    params = pnp.PatchParams(13, 8, 0.15)
+    cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=4, constraint=pnp.UNIT_BOX)
+    prob = pnp.make_sr_problem(op, y, ground_truth=truth)
+    v1, _ = pnp.linearized_pnp_admm(prob, cfg,
+                                    denoiser=pnp.freeze_guide(guide, params).as_denoiser())
+    v2, _ = sharded_linearized_pnp_admm_sr(op, y, guide, params, cfg, 2, ground_truth=truth)
+    assert torch.equal(v1, v2)
