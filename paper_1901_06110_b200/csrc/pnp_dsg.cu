@@ -1225,6 +1225,7 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   for (cudaEvent_t e : ctx->iter_events) cudaEventDestroy(e);
   if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
   if (ctx->ev_res) cudaEventDestroy(ctx->ev_res);
+  if (ctx->ev_switch) cudaEventDestroy(ctx->ev_switch);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   ctx->admm_r.release();
   ctx->admm_part.release();
@@ -1234,7 +1235,26 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
 
 int pnp_ctx_set_stream(pnp_ctx* ctx, void* stream) {
   if (!ctx) return fail(PNP_EINVAL, "ctx is null");
-  ctx->stream = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (s != ctx->stream) {
+    // Calls are stream-ordered and share the context's scratch: a call issued
+    // on the new stream must not start before the context's work queued on
+    // the old one (two host streams driving one context would race on it).
+    // Skipped when either stream is being captured into a graph: the capture
+    // orders its own work, and an event from outside it cannot be joined.
+    cudaStreamCaptureStatus c0 = cudaStreamCaptureStatusNone, c1 = cudaStreamCaptureStatusNone;
+    const bool ok = cudaStreamIsCapturing(ctx->stream, &c0) == cudaSuccess &&
+                    cudaStreamIsCapturing(s, &c1) == cudaSuccess;
+    if (!ok) (void)cudaGetLastError();
+    if (ok && c0 == cudaStreamCaptureStatusNone && c1 == cudaStreamCaptureStatusNone) {
+      PNP_CUDA(cudaSetDevice(ctx->device));
+      if (!ctx->ev_switch)
+        PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_switch, cudaEventDisableTiming));
+      PNP_CUDA(cudaEventRecord(ctx->ev_switch, ctx->stream));
+      PNP_CUDA(cudaStreamWaitEvent(s, ctx->ev_switch, 0));
+    }
+    ctx->stream = s;
+  }
   return PNP_OK;
 }
 

@@ -62,6 +62,9 @@ struct pnp_ctx {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = 0;
+  // orders a call on a new stream after the context's work on the previous
+  // one (the scratch buffers below are shared by every call on the context)
+  cudaEvent_t ev_switch = nullptr;
   pnp::DevBuf partial, rs, kx, d, mbits, stats, flags;
   // adaptive-denoise k cache: a caller-bound buffer (pnp_ctx_bind_kcache; the
   // Python layer binds torch-allocated memory per call), else allocated from

@@ -390,3 +390,33 @@ def test_helpers_match_reference_goldens(pnp):
         assert got == pytest.approx(float(want), abs=1e-14)
     W = pnp.build_dense_weights(h["gw"], pnp.PatchParams(3, 2, 0.25))
     assert np.abs(W - h["W"]).max() < 1e-12
+
+
+def test_two_streams_share_a_context_safely(pnp, rng):
+    """One thread issuing denoises / frozen applies on two torch streams uses
+    one native context (per thread and device) whose scratch every call
+    shares: switching streams orders the new call after the context's work on
+    the old stream, so the results equal the serial ones bit for bit."""
+    p = pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0)
+    xs = [torch.from_numpy(rng.random((1024, 1536)).astype(np.float32)).cuda() for _ in range(4)]
+    fz = [pnp.freeze_guide(x, p) for x in xs[:2]]
+    ser_d = [pnp.dsg_nlm_denoise(x, p) for x in xs]
+    ser_f = [f.apply(x) for f, x in zip(fz, xs[2:])]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    cur = torch.cuda.current_stream()
+    for _ in range(3):
+        outs = []
+        for s in streams:
+            s.wait_stream(cur)
+        for i, x in enumerate(xs):
+            with torch.cuda.stream(streams[i % 2]):
+                outs.append(pnp.dsg_nlm_denoise(x, p))
+        for i, (f, x) in enumerate(zip(fz, xs[2:])):
+            with torch.cuda.stream(streams[i % 2]):
+                outs.append(f.apply(x))
+        for s in streams:
+            cur.wait_stream(s)
+        torch.cuda.synchronize()
+        for a, b in zip(outs, ser_d + ser_f):
+            assert torch.equal(a, b)
