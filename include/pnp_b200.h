@@ -52,8 +52,11 @@ int pnp_ctx_synchronize(pnp_ctx* ctx);
  * identical either way.  bytes = 0 disables, < 0 = no limit (default).  When
  * the whole cache does not fit (the budget or free HBM less 4 GiB), the tile
  * rows that fit are cached and the rest recomputed (at least 1/8 of them, else
- * none).  Frozen guides allocate theirs from the device's stream-ordered pool
- * (cudaMallocAsync) and free it on the stream of their last use.  An adaptive
+ * none).  A frozen guide uses the buffer bound with pnp_ctx_bind_kcache when
+ * it is created (the buffer must then outlive the handle; the Python layer
+ * binds torch memory and keeps it with the FrozenGuide), else allocates its
+ * cache from the device's stream-ordered pool (cudaMallocAsync) and frees it
+ * on the stream of its last use.  An adaptive
  * denoise holds its cache only for the duration of the call: a buffer the
  * caller bound with pnp_ctx_bind_kcache (the Python layer binds memory from
  * torch's caching allocator, so torch sees and reuses it), else a

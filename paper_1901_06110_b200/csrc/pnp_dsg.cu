@@ -1545,7 +1545,22 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   e = cudaMemcpyAsync(fz->guide, guide, n * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemcpyAsync(guide)"));
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return bail(rc);
-  const int kc_rows = kcache_rows(ctx, g, 0);
+  fz->kc_stream = ctx->stream;
+  if (ctx->kc_ext && ctx->cache_limit != 0 && g.kind == PATH_FAST) {
+    // caller-bound cache (torch memory on the Python side): as many tile
+    // rows as it holds, none below 1/8 of them
+    const size_t row_b = kcache_floats(g, 1) * sizeof(float);
+    size_t budget = ctx->kc_ext_bytes < ctx->cache_limit ? ctx->kc_ext_bytes : ctx->cache_limit;
+    int r = (int)std::min<size_t>(budget / row_b, (size_t)g.tiles_y);
+    if (r * 8 < g.tiles_y) r = 0;
+    if (r > 0) {
+      fz->kcache = static_cast<float*>(ctx->kc_ext);
+      fz->kc_ext = true;
+      fz->kc_rows = r;
+      fz->kc_bytes = (size_t)r * row_b;
+    }
+  }
+  const int kc_rows = fz->kc_ext ? 0 : kcache_rows(ctx, g, 0);
   if (kc_rows > 0) {
     e = pool_alloc(ctx, (void**)&fz->kcache, kcache_floats(g, kc_rows) * sizeof(float));
     if (e != cudaSuccess) {
@@ -1644,8 +1659,24 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
 int pnp_frozen_destroy(pnp_frozen* fz) {
   if (!fz) return PNP_OK;
   cudaSetDevice(fz->device);
+  if (fz->kc_ext && fz->kcache && fz->stream != fz->kc_stream) {
+    // the caller frees the bound cache on the stream it was handed out on:
+    // order that stream after the handle's last use
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+      if (cudaEventRecord(ev, fz->stream) != cudaSuccess ||
+          cudaStreamWaitEvent(fz->kc_stream, ev, 0) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamSynchronize(fz->stream);
+      }
+      cudaEventDestroy(ev);
+    } else {
+      cudaGetLastError();
+      cudaStreamSynchronize(fz->stream);
+    }
+  }
   for (void* p : {(void*)fz->guide, (void*)fz->rs, (void*)fz->d, (void*)fz->mv,
-                  (void*)fz->kcache})
+                  fz->kc_ext ? nullptr : (void*)fz->kcache})
     if (p && cudaFreeAsync(p, fz->stream) != cudaSuccess) {
       cudaGetLastError();
       cudaFree(p);  // stream gone: synchronous free

@@ -162,7 +162,11 @@ struct pnp_frozen {
   float* kcache = nullptr; // pair weights (null: recompute on apply)
   int kc_rows = 0;
   int tiles_y = 0;         // tile rows per image (kc_rows == tiles_y: fully cached)
-  size_t kc_bytes = 0;         // tile rows (per image, from the top) the k cache covers
+  size_t kc_bytes = 0;     // bytes of the k cache
+  bool kc_ext = false;     // the k cache is a caller-bound buffer (not freed here)
+  // the stream current at the freeze (a caller-bound k cache was handed out
+  // on it): destroy orders it after the handle's last use
+  cudaStream_t kc_stream = 0;
   // buffers come from the device's stream-ordered pool (cudaMallocAsync) and
   // go back to it on the stream of the handle's last use: no device-wide
   // synchronization and no page-mapping cost when ADMM runs re-freeze

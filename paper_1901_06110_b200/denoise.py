@@ -210,7 +210,7 @@ def kcache_scope(dev: int, B: int, H: int, W: int, params: PatchParams):
     ctx = L.context(dev)
     L.call("pnp_ctx_bind_kcache", ctx, L.ptr(buf), 0 if buf is None else buf.numel())
     try:
-        yield
+        yield buf
     finally:
         L.call("pnp_ctx_bind_kcache", ctx, None, 0)
         del buf
@@ -386,15 +386,22 @@ class FrozenGuide:
         else:
             self.guide = g.clone()
         self._h = C.c_void_p()
-        ctx = L.context(self._dev)
-        L.call("pnp_dsg_freeze", ctx, L.ptr(g), B, H, W, params.window_radius,
-               params.patch_side, params._ctaps(), float(params.bandwidth), C.byref(self._h))
+        # the pair-weight cache comes from torch's caching allocator (torch
+        # sees it; re-freezing reuses the freed block instead of mapping new
+        # pages) and lives as long as the handle
+        with kcache_scope(self._dev, B, H, W, params) as kc:
+            ctx = L.context(self._dev)
+            L.call("pnp_dsg_freeze", ctx, L.ptr(g), B, H, W, params.window_radius,
+                   params.patch_side, params._ctaps(), float(params.bandwidth), C.byref(self._h))
+            self._kc = kc if self.cache_info()["rows_cached"] else None
         self._B = B
 
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
             try:
+                # orders the cache's allocation stream after the last apply;
+                # torch recycles self._kc once this object is gone
                 L.lib.pnp_frozen_destroy(h)
             except Exception:  # interpreter shutdown
                 pass

@@ -420,3 +420,30 @@ def test_two_streams_share_a_context_safely(pnp, rng):
         torch.cuda.synchronize()
         for a, b in zip(outs, ser_d + ser_f):
             assert torch.equal(a, b)
+
+
+def test_frozen_kcache_is_torch_memory(pnp, rng):
+    """A frozen guide's pair-weight cache is torch memory held by the
+    FrozenGuide: torch counts it while the handle lives, takes it back when
+    the handle goes, and re-freezing (old handle alive during the new freeze,
+    as in an ADMM loop) recycles blocks instead of growing."""
+    p = pnp.PatchParams.from_h(7, 10, 8 / 255, 2.0)
+    x = torch.from_numpy(rng.random((1024, 1024)).astype(np.float32)).cuda()
+    ref = pnp.dsg_nlm_denoise(x, p)
+    torch.cuda.synchronize()
+    a0 = torch.cuda.memory_allocated()
+    fz = pnp.freeze_guide(x, p)
+    info = fz.cache_info()
+    assert info["rows_cached"] == info["tile_rows"] and info["bytes"] > 0
+    assert torch.cuda.memory_allocated() - a0 >= info["bytes"]
+    assert torch.equal(fz.apply(x), ref)
+    for _ in range(2):
+        fz = pnp.freeze_guide(x, p)
+    r1 = torch.cuda.memory_reserved()
+    for _ in range(4):
+        fz = pnp.freeze_guide(x, p)
+        assert torch.equal(fz.apply(x), ref)
+    assert torch.cuda.memory_reserved() <= r1 + (64 << 20)  # no new cache-sized blocks
+    del fz
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() - a0 < info["bytes"]
