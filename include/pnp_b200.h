@@ -329,6 +329,17 @@ int pnp_project(pnp_ctx* ctx, const float* x, float* y, int64_t n, double lo, do
  * element of x (n floats, device, 16 B aligned) is NaN/Inf, else 0.  One
  * pass on the ctx stream, then a synchronizing 4-byte read-back. */
 int pnp_check_finite(pnp_ctx* ctx, const float* x, int64_t n, int* all_finite);
+
+/* Host casts of the numpy drop-in path (float64 numpy in / out around the
+ * fp32 device compute; the reference's call shape, denoise.py:272-288):
+ * AVX2 conversions with non-temporal stores on a persistent worker pool
+ * (nthreads <= 0: all of it), round-to-nearest-even = a C cast, bit for bit.
+ * Host pointers; no device work. */
+int pnp_host_cast_f32_f64(const float* src, double* dst, int64_t n, int nthreads);
+int pnp_host_cast_f64_f32(const double* src, float* dst, int64_t n, int nthreads);
+/* Zero-fill (first touch) of a fresh float64 result on the same pool: the
+ * numpy path faults the result's pages in while the device computes. */
+int pnp_host_zero_f64(double* dst, int64_t n, int nthreads);
 /* Stream-ordered variant for pipelines: *flag (device int) |= 1 when x holds
  * a NaN/Inf; no synchronization. */
 int pnp_flag_nonfinite(pnp_ctx* ctx, const float* x, int64_t n, int* flag);

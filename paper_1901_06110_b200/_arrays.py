@@ -90,7 +90,7 @@ def to_device(a, dev: int | None = None) -> torch.Tensor:
         # multi-threaded cast into pinned staging, then a DMA copy (the caching
         # host allocator keeps the staging block until the copy completes)
         stage = torch.empty(arr.shape, dtype=torch.float32, pin_memory=True)
-        stage.copy_(_host_tensor(arr))
+        cast_into(stage, _host_tensor(arr))
         return stage.to(torch.device("cuda", dev), non_blocking=True)
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
     return torch.from_numpy(arr).to(torch.device("cuda", dev), non_blocking=False)
@@ -124,6 +124,23 @@ def _pinned_f32(n: int) -> torch.Tensor:
     return buf[:n]
 
 
+def cast_into(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst[...] = src between host tensors: the library's streaming AVX2
+    casts for contiguous float32 <-> float64 (the numpy path's casts are host
+    memory bound and on the call's critical path), torch's copy otherwise.
+    Same bits either way (round to nearest even)."""
+    from . import _lib as L
+
+    pair = (src.dtype, dst.dtype)
+    if (pair in ((torch.float32, torch.float64), (torch.float64, torch.float32))
+            and src.is_contiguous() and dst.is_contiguous() and src.numel() == dst.numel()
+            and not src.is_cuda and not dst.is_cuda):
+        fn = "pnp_host_cast_f32_f64" if pair[0] == torch.float32 else "pnp_host_cast_f64_f32"
+        L.call(fn, src.data_ptr(), dst.data_ptr(), src.numel(), 0)
+    else:
+        dst.copy_(src)
+
+
 def from_device(t: torch.Tensor, kind: str):
     if kind == TORCH:
         return t
@@ -133,7 +150,7 @@ def from_device(t: torch.Tensor, kind: str):
         with _stage_lock:
             stage = _pinned_f32(src.numel())
             stage.copy_(src)
-            torch.from_numpy(out).view(-1).copy_(stage)
+            cast_into(torch.from_numpy(out).view(-1), stage)
         return out
     return t.detach().to("cpu").numpy().astype(np.float64)
 
@@ -202,7 +219,7 @@ def download64_banded(t: torch.Tensor, st: _Staging, nbands: int, res=None) -> n
     t.record_stream(d2h)
     for (r0, r1), ev in zip(rows, evs):
         ev.synchronize()
-        dst[r0:r1].copy_(stage[r0:r1])  # multi-threaded cast
+        cast_into(dst[r0:r1], stage[r0:r1])  # multi-threaded streaming cast
     return res
 
 

@@ -89,6 +89,9 @@ _SIGS = {
     "pnp_sr_cg": (i32, [vp, vp, vp, i32, i32, i32, fptr, i32, i32, i32, f64, f64, i32, i32,
                         C.POINTER(i32), C.POINTER(f64), C.POINTER(i32)]),
     "pnp_check_finite": (i32, [vp, vp, i64, C.POINTER(i32)]),
+    "pnp_host_cast_f32_f64": (i32, [vp, vp, i64, i32]),
+    "pnp_host_cast_f64_f32": (i32, [vp, vp, i64, i32]),
+    "pnp_host_zero_f64": (i32, [vp, i64, i32]),
     "pnp_flag_nonfinite": (i32, [vp, vp, i64, vp]),
     "pnp_splitmix_uniforms": (i32, [vp, C.c_uint64, i64, vp]),
     "pnp_pad_symmetric_f64": (i32, [vp, vp, i32, i32, i32, vp]),

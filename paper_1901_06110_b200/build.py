@@ -33,7 +33,7 @@ def needs_build() -> bool:
 
 
 def sources():
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def build(force: bool = False, verbose: bool = False, extra=()) -> Path:
@@ -49,7 +49,11 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> Path:
 
     def one(src: Path):
         obj = build_dir / (src.stem + ".o")
-        cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + common
+        if src.suffix == ".cpp":  # host-only code (runtime dispatch to AVX2 inside)
+            cmd = [os.environ.get("CXX", "g++"), "-c", str(src), "-o", str(obj), "-O3", "-g",
+                   "-std=c++17", "-fPIC", "-pthread", "-I", str(ROOT / "include")]
+        else:
+            cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + common
         r = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, r
 

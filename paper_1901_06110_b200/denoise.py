@@ -330,7 +330,7 @@ def _dsg_numpy_banded(image, params: PatchParams, bands):
         r0 = 0
         for j, r1 in enumerate(bands):
             if r1 > r0:
-                stage[r0:r1].copy_(src[r0:r1])  # multi-threaded cast
+                A.cast_into(stage[r0:r1], src[r0:r1])  # multi-threaded cast
                 ev = torch.cuda.Event()
                 with torch.cuda.stream(h2d):
                     x[r0:r1].copy_(stage[r0:r1], non_blocking=True)
@@ -343,8 +343,8 @@ def _dsg_numpy_banded(image, params: PatchParams, bands):
         L.call("pnp_dsg_band_finish", ctx, L.ptr(x), L.ptr(out), H, W, R, P, taps, bw)
         # fault the result's pages in (threaded) while the device denoises
         res = np.empty((H, W), dtype=np.float64)
-        torch.from_numpy(res).zero_()
-        res = A.download64_banded(out, st, 2 * _NP_BANDS, res)
+        L.call("pnp_host_zero_f64", res.ctypes.data, res.size, 0)
+        res = A.download64_banded(out, st, _NP_BANDS, res)
     if int(flag.item()):
         a = np.asarray(image, dtype=np.float64)
         if not np.all(np.isfinite(a)):

@@ -93,3 +93,29 @@ def test_sweep_path_routing():
     import pytest
     with pytest.raises(ValueError):
         L.dsg_geometry(256, 256, 5, 65, True)
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 31, 1000, (1 << 20) + 5])
+def test_host_casts_are_c_casts(n):
+    """The numpy path's streaming host casts (pnp_host_cast_*) give numpy's
+    astype bits: misaligned ends, overflow to inf, nan, denormals."""
+    import torch
+
+    from paper_1901_06110_b200 import _arrays as A
+
+    rng = np.random.default_rng(n)
+    s64 = rng.standard_normal(n) * 10.0 ** rng.integers(-45, 45, n)
+    if n > 4:
+        s64[:4] = [np.inf, -np.nan, 1e300, -1e-320]
+    buf32 = np.full(n + 3, -7.0, dtype=np.float32)
+    o32 = buf32[3:]                     # 12-byte offset: scalar head + vector body
+    A.cast_into(torch.from_numpy(o32), torch.from_numpy(s64))
+    with np.errstate(over="ignore"):
+        want = s64.astype(np.float32)
+    assert np.array_equal(o32.view(np.uint32), want.view(np.uint32))
+    assert np.all(buf32[:3] == -7.0)
+    buf64 = np.full(n + 1, -7.0)
+    o64 = buf64[1:]
+    A.cast_into(torch.from_numpy(o64), torch.from_numpy(want))
+    assert np.array_equal(o64.view(np.uint64), want.astype(np.float64).view(np.uint64))
+    assert buf64[0] == -7.0
