@@ -534,7 +534,11 @@ def golden_check(name, v, recs, y=None, image=None):
            "max_abs_dv_vs_oracle": float(np.abs(vv - gd["v"]).max()),
            "oracle": f"tests/golden/{name} (pnprestore linearized_pnp_admm, float64)"}
     if y is not None:
-        out["inputs_match_golden"] = bool(np.array_equal(np.asarray(y), gd["y"]))
+        # the observation is simulated here on the device (fp32 blur, float64
+        # noise), the golden's by the reference in float64: same seeds, equal
+        # to fp32 rounding (not bitwise)
+        yy = y.double().cpu().numpy() if hasattr(y, "cpu") else np.asarray(y, np.float64)
+        out["inputs_max_abs_diff_vs_golden"] = float(np.abs(yy - gd["y"].astype(np.float64)).max())
     return out
 
 

@@ -37,6 +37,11 @@ for cu in sorted(csrc.glob("*.cu")):
     obj = out / (cu.stem + ".o")
     objs.append(str(obj))
     procs.append(subprocess.Popen(["nvcc", "-c", str(cu), "-o", str(obj)] + flags))
+for cpp in sorted(csrc.glob("*.cpp")):  # host-only sources (as in build.py)
+    obj = out / (cpp.stem + ".o")
+    objs.append(str(obj))
+    procs.append(subprocess.Popen(["g++", "-c", str(cpp), "-o", str(obj), "-O3", "-g",
+                                   "-std=c++17", "-fPIC", "-pthread", "-I", str(inc)]))
 if any(p.wait() for p in procs):
     sys.exit("compile failed")
 subprocess.run(["nvcc", "-shared", "-o", str(out / "libpnpb200.so")] + objs + arch +
