@@ -11,6 +11,7 @@
 // C cast / torch's copy_.
 #include <immintrin.h>
 #include <stdint.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <condition_variable>
@@ -25,7 +26,7 @@ namespace {
 
 class Pool {
  public:
-  explicit Pool(int n) {
+  explicit Pool(int n) : pid_(getpid()) {
     for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
   }
   ~Pool() {
@@ -39,6 +40,10 @@ class Pool {
   int size() const { return (int)workers_.size() + 1; }
   // run fn(part) for part in [0, parts) on the caller + workers; returns when all are done
   void run(int parts, const std::function<void(int)>& fn) {
+    if (getpid() != pid_) {  // a forked child has no workers: run inline
+      for (int p = 0; p < parts; ++p) fn(p);
+      return;
+    }
     std::unique_lock<std::mutex> call(call_m_);  // one job at a time
     {
       std::lock_guard<std::mutex> lk(m_);
@@ -74,6 +79,7 @@ class Pool {
       if (--pending_ == 0) done_cv_.notify_one();
     }
   }
+  const pid_t pid_;
   std::vector<std::thread> workers_;
   std::mutex m_, call_m_;
   std::condition_variable cv_, done_cv_;

@@ -119,3 +119,28 @@ def test_host_casts_are_c_casts(n):
     A.cast_into(torch.from_numpy(o64), torch.from_numpy(want))
     assert np.array_equal(o64.view(np.uint64), want.astype(np.float64).view(np.uint64))
     assert buf64[0] == -7.0
+
+
+@pytest.mark.filterwarnings("ignore::DeprecationWarning")
+def test_host_casts_in_a_forked_child():
+    """The cast pool's workers do not survive fork(): a child process runs
+    the casts inline instead of waiting for them."""
+    import os
+
+    import torch
+
+    from paper_1901_06110_b200 import _arrays as A
+
+    s = np.arange(1 << 20, dtype=np.float32)
+    d = np.empty(1 << 20)
+    A.cast_into(torch.from_numpy(d), torch.from_numpy(s))   # pool started in the parent
+    pid = os.fork()
+    if pid == 0:
+        try:
+            d2 = np.empty(1 << 20)
+            A.cast_into(torch.from_numpy(d2), torch.from_numpy(s))
+            os._exit(0 if np.array_equal(d2, s) else 1)
+        except BaseException:
+            os._exit(2)
+    _, status = os.waitpid(pid, 0)
+    assert os.WIFEXITED(status) and os.WEXITSTATUS(status) == 0
