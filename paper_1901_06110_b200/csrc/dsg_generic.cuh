@@ -62,6 +62,11 @@ struct GenArgs {
   float taps_v[kGenMaxP];   // Gaussian: -log2(e)/(2 bw^2) * w_a
   int grp[kMaxGroups + 1];  // offset groups: dy-index ranges (dy = dyi + dy_min)
   long long partial_floats;  // buffer size (PNP_CHECKS)
+  // k cache (SYM, MODE STORE / CACHED): one TH x 64 plane per tile and
+  // half-window offset, offsets in the sweep's walk order, tiles
+  // (b, tile row of the launch, tile col) in raster order
+  float* kcache;
+  long long kcache_floats;  // buffer size (PNP_CHECKS)
 };
 
 // Shared-memory geometry of one CTA (floats); also used by the host to pick
@@ -71,7 +76,9 @@ struct GenSmem {
   int off_gp, off_h, off_y, off_a, total;
 };
 
-__host__ __device__ inline GenSmem gen_smem(int TH, int P, int R, int C, bool sym, int KG) {
+// cached: the k-cache sweep stages no guide and keeps no H map
+__host__ __device__ inline GenSmem gen_smem(int TH, int P, int R, int C, bool sym, int KG,
+                                            bool cached = false) {
   GenSmem s;
   const int p = (P - 1) / 2;
   s.M = TH + 2 * p;
@@ -83,9 +90,9 @@ __host__ __device__ inline GenSmem gen_smem(int TH, int P, int R, int C, bool sy
   s.YS = kTW + kGenDXC;
   s.AR = sym ? TH + R + KG - 1 : 0;
   s.AC = sym ? kTW + 2 * R : 0;
-  s.off_gp = s.M * s.GOS;
-  s.off_h = s.off_gp + s.GPR * s.GPS;
-  s.off_y = s.off_h + KG * s.M * s.HS;
+  s.off_gp = cached ? 0 : s.M * s.GOS;
+  s.off_h = s.off_gp + (cached ? 0 : s.GPR * s.GPS);
+  s.off_y = s.off_h + (cached ? 0 : KG * s.M * s.HS);
   s.off_a = s.off_y + C * s.YR * s.YS;
   s.total = s.off_a + C * s.AR * s.AC;
   return s;
@@ -96,12 +103,14 @@ __device__ __forceinline__ float sqd(float a, float b) {
   return __fmul_rn(t, t);
 }
 
-template <int C, bool BOX, bool SYM, int KG>
+template <int C, bool BOX, bool SYM, int KG, int MODE>
 __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs a) {
+  constexpr bool STORE = MODE == MODE_STORE, CACHED = MODE == MODE_CACHED;
+  static_assert(SYM || MODE == MODE_RECOMPUTE, "the k cache covers the half window");
   pdl_begin();
   extern __shared__ float smem[];
   const int R = a.R, P = a.P, TH = a.TH, p = (P - 1) / 2;
-  const GenSmem L = gen_smem(TH, P, R, C, SYM, KG);
+  const GenSmem L = gen_smem(TH, P, R, C, SYM, KG, CACHED);
   float* Gown = smem;
   float* Gpart = smem + L.off_gp;
   float* Hs = smem + L.off_h;
@@ -142,11 +151,12 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 
   // ---- own guide rows (map rows q <-> image row r0g - p + q, map col j <->
   // image col c0g - p + j), far plane cleared ----
-  for (int q = tid / 32; q < M; q += kGenThreads / 32) {
-    const float* src = Gimg + (size_t)grow(r0g - p + q) * W;
-    for (int j = tid & 31; j < kTW + 2 * p; j += 32)
-      Gown[q * L.GOS + j] = __ldg(src + reflect_index(c0g - p + j, W));
-  }
+  if (!CACHED)
+    for (int q = tid / 32; q < M; q += kGenThreads / 32) {
+      const float* src = Gimg + (size_t)grow(r0g - p + q) * W;
+      for (int j = tid & 31; j < kTW + 2 * p; j += 32)
+        Gown[q * L.GOS + j] = __ldg(src + reflect_index(c0g - p + j, W));
+    }
   if (SYM)
     for (int i = tid; i < C * L.AR * L.AC; i += kGenThreads) As[i] = 0.f;
 
@@ -191,6 +201,17 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
   const int dy_min = SYM ? 0 : -R;
   const int n_dx = 2 * R + 1;
   const int gend = a.grp[blockIdx.y + 1];
+  // k cache: this tile's planes; kplane = planes of the offsets walked before
+  // (dy = 0 has R offsets in the half window, every dy > 0 has 2R + 1)
+  float* ktile = nullptr;
+  int kplane = 0;
+  if (STORE || CACHED) {
+    const int hw = 2 * R * R + 2 * R;
+    ktile = a.kcache + ((((size_t)b * (gridDim.x / a.tiles_x) + tyl) * a.tiles_x + tx) * hw) *
+                           (size_t)(TH * kTW);
+    const int dyf = a.grp[blockIdx.y];
+    kplane = dyf == 0 ? 0 : R + (dyf - 1) * n_dx;
+  }
   for (int b0 = a.grp[blockIdx.y]; b0 < gend; b0 += KG) {
     const int nb = min(KG, gend - b0);
     const int dy0 = b0 + dy_min;
@@ -200,11 +221,12 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
       // partner guide rows: row q <-> image row r0g - p + q + dy0 (offset j
       // reads rows q + j), col jj <-> image col c0g - p + dxa + jj
       const int gpw = kTW + 2 * p + (dxb - dxa) - 1;
-      for (int q = tid / 32; q < L.GPR; q += kGenThreads / 32) {
-        const float* src = Gimg + (size_t)grow(r0g - p + q + dy0) * W;
-        for (int jj = tid & 31; jj < gpw; jj += 32)
-          Gpart[q * L.GPS + jj] = __ldg(src + reflect_index(c0g - p + dxa + jj, W));
-      }
+      if (!CACHED)
+        for (int q = tid / 32; q < L.GPR; q += kGenThreads / 32) {
+          const float* src = Gimg + (size_t)grow(r0g - p + q + dy0) * W;
+          for (int jj = tid & 31; jj < gpw; jj += 32)
+            Gpart[q * L.GPS + jj] = __ldg(src + reflect_index(c0g - p + dxa + jj, W));
+        }
       // partner channel rows: row r <-> image row r0g + r + dy0, col jj <->
       // image col c0g + dxa + jj
       const int yw = kTW + (dxb - dxa) - 1;
@@ -228,8 +250,25 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
         }
         if (!valid) continue;
         flush_pending();
+        // this step's k planes (valid offsets in order): kplane, kplane + 1, ...
+        float kv[CACHED ? KG : 1][CACHED ? kGenNmax : 1];
+        if (CACHED) {  // all the step's loads in flight before the sums
+#pragma unroll
+          for (int j = 0; j < KG; ++j) {
+            const bool vj = (valid >> j) & 1u;
+            const float* kq = ktile +
+                              (size_t)(kplane + __popc(valid & ((1u << j) - 1u))) * (TH * kTW) +
+                              rA * kTW + x;
+#pragma unroll
+            for (int i = 0; i < kGenNmax; ++i) {
+              const bool ok = vj && i < N;
+              PNP_CHECK(!ok || (long long)(kq + i * kTW - a.kcache) < a.kcache_floats);
+              kv[j][i] = ok ? __ldcs(kq + i * kTW) : 0.f;
+            }
+          }
+        }
         // ---- phase H: offset j, map row q, columns [x0, x0 + 32) ----
-        for (int it = tid; it < KG * 2 * M; it += kGenThreads) {
+        for (int it = tid; it < (CACHED ? 0 : KG * 2 * M); it += kGenThreads) {
           const int j = it / (2 * M), rem = it - j * 2 * M;
           if (!((valid >> j) & 1u)) continue;
           const int x0 = (rem / M) * kGenSeg, q = rem % M;
@@ -268,7 +307,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
                                       : -INFINITY;
           hc[j] = Hs + (j * M + rA) * L.HS + x;
           sv[j] = 0.f;
-          if (BOX && ((valid >> j) & 1u)) {
+          if (BOX && !CACHED && ((valid >> j) & 1u)) {
             float s = hc[j][0];
             for (int aa = 1; aa < P; ++aa) s = __fadd_rn(s, hc[j][aa * L.HS]);
             sv[j] = s;
@@ -287,17 +326,29 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 #pragma unroll
           for (int j = 0; j < KG; ++j) {
             if (!((valid >> j) & 1u)) continue;
-            float e;
-            if (BOX) {
-              e = __fmaf_rn(sv[j], a.cv, Lt[j]);
-              if (i + 1 < N)
-                sv[j] = __fsub_rn(__fadd_rn(sv[j], hc[j][(i + P) * L.HS]), hc[j][i * L.HS]);
+            float k;
+            if (CACHED) {
+              k = kv[j][i];
             } else {
-              e = Lt[j];
-              for (int aa = 0; aa < P; ++aa)
-                e = __fmaf_rn(a.taps_v[aa], hc[j][(i + aa) * L.HS], e);
+              float e;
+              if (BOX) {
+                e = __fmaf_rn(sv[j], a.cv, Lt[j]);
+                if (i + 1 < N)
+                  sv[j] = __fsub_rn(__fadd_rn(sv[j], hc[j][(i + P) * L.HS]), hc[j][i * L.HS]);
+              } else {
+                e = Lt[j];
+                for (int aa = 0; aa < P; ++aa)
+                  e = __fmaf_rn(a.taps_v[aa], hc[j][(i + aa) * L.HS], e);
+              }
+              k = ex2_approx(e);
+              if (STORE) {
+                float* kq = ktile +
+                            (size_t)(kplane + __popc(valid & ((1u << j) - 1u))) * (TH * kTW) +
+                            (rA + i) * kTW + x;
+                PNP_CHECK((long long)(kq - a.kcache) < a.kcache_floats);
+                __stcs(kq, k);
+              }
             }
-            const float k = ex2_approx(e);
 #pragma unroll
             for (int c_ = 0; c_ < C; ++c_) {
               near[c_][i] = __fmaf_rn(k, yp[(c_ * L.YR + i + j) * L.YS], near[c_][i]);
@@ -322,6 +373,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
             }
           if (g == 1 && KG > 1) pend = base;
         }
+        if (STORE || CACHED) kplane += __popc(valid);
         jitter_sync();
       }
     }
@@ -361,7 +413,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 }
 
 // pnp_generic.cu
-cudaError_t launch_generic(const GenArgs& a, int C, bool box, bool sym, int KG, dim3 grid,
-                           cudaStream_t st);
+cudaError_t launch_generic(const GenArgs& a, int C, bool box, bool sym, int KG, int mode,
+                           dim3 grid, cudaStream_t st);
 
 }  // namespace pnp

@@ -931,8 +931,9 @@ static bool kcache_fits(pnp_ctx* ctx, size_t floats, size_t already) {
 // them when the whole cache fits, else as many as the budget allows (the
 // rest is recomputed -- same bits either way), 0 below 1/8 of the image.
 static int kcache_rows(pnp_ctx* ctx, const Geom& g, size_t already) {
-  if (ctx->cache_limit == 0 || g.kind != PATH_FAST) return 0;
+  if (ctx->cache_limit == 0 || g.kind == PATH_GEN_NEAR) return 0;
   if (kcache_fits(ctx, kcache_floats(g, g.tiles_y), already)) return g.tiles_y;
+  if (g.kind != PATH_FAST) return 0;  // the general sweep caches all tile rows or none
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
   const size_t head = (size_t)4 << 30, row_b = kcache_floats(g, 1) * sizeof(float);
@@ -950,12 +951,12 @@ static int kcache_acquire(pnp_ctx* ctx, const Geom& g, float** kc, int* rows) {
   *rows = 0;
   ctx->kc_call = nullptr;
   ctx->kc_call_pooled = false;
-  if (ctx->cache_limit == 0 || g.kind != PATH_FAST) return PNP_OK;
+  if (ctx->cache_limit == 0 || g.kind == PATH_GEN_NEAR) return PNP_OK;
   const size_t row_b = kcache_floats(g, 1) * sizeof(float);
   if (ctx->kc_ext) {
     size_t budget = ctx->kc_ext_bytes < ctx->cache_limit ? ctx->kc_ext_bytes : ctx->cache_limit;
     int r = (int)std::min<size_t>(budget / row_b, (size_t)g.tiles_y);
-    if (r * 8 < g.tiles_y) r = 0;
+    if (r * 8 < g.tiles_y || (g.kind != PATH_FAST && r < g.tiles_y)) r = 0;
     *kc = r ? static_cast<float*>(ctx->kc_ext) : nullptr;
     *rows = r;
     ctx->kc_call = *kc;
@@ -983,9 +984,13 @@ static void kcache_release(pnp_ctx* ctx) {
 
 static int run_sweep_gen(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const float* guide,
                          ChanSpec c0, ChanSpec c1, const float* taps, double bw, bool use_hat,
-                         float* partial) {
+                         float* partial, int mode, float* kcache) {
   GenArgs a;
   memset(&a, 0, sizeof(a));
+  if (mode != MODE_RECOMPUTE && (!kcache || g.kind != PATH_GEN_SYM))
+    return fail(PNP_EINVAL, "k cache missing (or full-window general sweep)");
+  a.kcache = mode != MODE_RECOMPUTE ? kcache : nullptr;
+  a.kcache_floats = (long long)kcache_floats(g, w.ntr);
   a.guide = guide;
   a.ch[0] = c0;
   a.ch[1] = c1;
@@ -1014,8 +1019,9 @@ static int run_sweep_gen(pnp_ctx* ctx, const Geom& g, const Window& w, int C, co
   a.partial_floats = partial == ctx->partial.ptr ? (long long)(ctx->partial.bytes / sizeof(float))
                                                  : LLONG_MAX;
   dim3 grid(w.ntr * g.tiles_x, g.NG, g.B);
-  ProfScope prof(ctx, PROF_SWEEP);
-  cudaError_t e = launch_generic(a, C, g.box, g.kind == PATH_GEN_SYM, g.KG, grid, ctx->stream);
+  ProfScope prof(ctx, mode == MODE_CACHED ? PROF_SWEEP_CACHED : PROF_SWEEP);
+  cudaError_t e =
+      launch_generic(a, C, g.box, g.kind == PATH_GEN_SYM, g.KG, mode, grid, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "dsg_generic_kernel");
   return PNP_OK;
 }
@@ -1025,9 +1031,8 @@ static int run_sweep(pnp_ctx* ctx, const Geom& g, const Window& w, int C, const 
                      float* partial, int mode = MODE_RECOMPUTE, float* kcache = nullptr) {
   if (w.ntr <= 0) return PNP_OK;
   if (g.kind != PATH_FAST) {
-    if (mode != MODE_RECOMPUTE && mode != MODE_STORE)
-      return fail(PNP_EINVAL, "the general sweep has no k cache");
-    return run_sweep_gen(ctx, g, w, C, guide, c0, c1, taps, bw, use_hat, partial);
+    if (!kcache) mode = MODE_RECOMPUTE;
+    return run_sweep_gen(ctx, g, w, C, guide, c0, c1, taps, bw, use_hat, partial, mode, kcache);
   }
   SweepArgs a;
   memset(&a, 0, sizeof(a));
@@ -1084,7 +1089,7 @@ static int run_sweep_kc(pnp_ctx* ctx, const Geom& g, int C, const float* guide, 
                         ChanSpec c1, const float* taps, double bw, float* partial, int kmode,
                         float* kc, int kc_rows) {
   const Window w = full_window(g);
-  if (!kc || kc_rows <= 0)
+  if (!kc || kc_rows <= 0 || (g.kind != PATH_FAST && kc_rows < g.tiles_y))
     return run_sweep(ctx, g, w, C, guide, c0, c1, taps, bw, true, partial, MODE_RECOMPUTE);
   if (kc_rows >= g.tiles_y)
     return run_sweep(ctx, g, w, C, guide, c0, c1, taps, bw, true, partial, kmode, kc);
@@ -1560,13 +1565,13 @@ int pnp_dsg_freeze(pnp_ctx* ctx, const float* guide, int batch, int H, int W, in
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemcpyAsync(guide)"));
   if ((rc = ctx->mbits.ensure(batch * sizeof(unsigned)))) return bail(rc);
   fz->kc_stream = ctx->stream;
-  if (ctx->kc_ext && ctx->cache_limit != 0 && g.kind == PATH_FAST) {
+  if (ctx->kc_ext && ctx->cache_limit != 0 && g.kind != PATH_GEN_NEAR) {
     // caller-bound cache (torch memory on the Python side): as many tile
     // rows as it holds, none below 1/8 of them
     const size_t row_b = kcache_floats(g, 1) * sizeof(float);
     size_t budget = ctx->kc_ext_bytes < ctx->cache_limit ? ctx->kc_ext_bytes : ctx->cache_limit;
     int r = (int)std::min<size_t>(budget / row_b, (size_t)g.tiles_y);
-    if (r * 8 < g.tiles_y) r = 0;
+    if (r * 8 < g.tiles_y || (g.kind != PATH_FAST && r < g.tiles_y)) r = 0;
     if (r > 0) {
       fz->kcache = static_cast<float*>(ctx->kc_ext);
       fz->kc_ext = true;
@@ -1830,6 +1835,8 @@ int pnp_dsg_strip_sweep(pnp_ctx* ctx, int pass, const float* guide, const float*
   Geom g;
   if ((rc = make_geom(ctx, 1, Hg, W, R, P, taps_box(taps, P), g))) return rc;
   if (tr0 < 0 || tr0 + ntr > g.tiles_y) return fail(PNP_EINVAL, "tile rows out of range");
+  if (kcache && g.kind != PATH_FAST)
+    return fail(PNP_EINVAL, "strips of the general sweep have no k cache");
   Window w{buf_r0, buf_rows, tr0, ntr, 0, part_off, part_ntr, 0, 0};
   const int use = kcache ? MODE_CACHED : MODE_RECOMPUTE;
   switch (pass) {

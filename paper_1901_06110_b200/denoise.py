@@ -170,20 +170,25 @@ def _kcache_bytes(dev: int, B: int, H: int, W: int, params: PatchParams,
     hit = _KC_GRANT.get(key)
     if hit is not None and not fresh and hit[0] == hit[1]:
         return hit
-    row = int(L.lib.pnp_dsg_kcache_floats(H, W, params.window_radius, params.patch_side,
-                                          int(params.is_box), 1)) * 4 * B
+    R = params.window_radius
+    geom = L.dsg_geometry(H, W, R, params.patch_side, params.is_box)
+    general = geom[3] == 1  # the general half-window sweep: all tile rows or none
+    if general:
+        row = (2 * R * R + 2 * R) * geom[0] * (-(-W // 64) * 64) * 4 * B
+    else:
+        row = int(L.lib.pnp_dsg_kcache_floats(H, W, R, params.patch_side,
+                                              int(params.is_box), 1)) * 4 * B
     if row <= 0:
         _KC_GRANT[key] = (0, 0)
         return 0, 0
-    tiles = -(-H // L.dsg_geometry(H, W, params.window_radius, params.patch_side,
-                                   params.is_box)[0])
+    tiles = -(-H // geom[0])
     free, _ = torch.cuda.mem_get_info(dev)
     idle = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
     budget = free + idle - _KC_HEADROOM
     if limit is not None:
         budget = min(budget, limit)
     rows = min(tiles, max(0, budget) // row)
-    n = rows * row if rows * 8 >= tiles else 0
+    n = rows * row if rows * 8 >= tiles and (rows == tiles or not general) else 0
     _KC_GRANT[key] = (n, tiles * row)
     return n, tiles * row
 

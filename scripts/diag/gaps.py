@@ -12,7 +12,10 @@ sys.path.insert(0, str(ROOT))
 import paper_1901_06110_b200 as pnp  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-p = pnp.PatchParams.from_h(7, 10, 12 / 255, 2.0)
+if len(sys.argv) > 3:  # n R P: box patches (the reference's own), bandwidth 0.15
+    p = pnp.PatchParams(int(sys.argv[3]), int(sys.argv[2]), 0.15)
+else:
+    p = pnp.PatchParams.from_h(7, 10, 12 / 255, 2.0)
 x = torch.rand(n, n, device="cuda")
 for _ in range(3):
     pnp.dsg_nlm_denoise(x, p)

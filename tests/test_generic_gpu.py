@@ -182,3 +182,31 @@ def test_general_sweep_sharded_sr_admm_bitwise(pnp):
                                     denoiser=pnp.freeze_guide(guide, params).as_denoiser())
     v2, _ = sharded_linearized_pnp_admm_sr(op, y, guide, params, cfg, 2, ground_truth=truth)
     assert torch.equal(v1, v2)
+
+
+@pytest.mark.parametrize("P,R,sigma,shape", [(17, 21, None, (2, 90, 140)),
+                                             (11, 21, None, (256, 256)),
+                                             (19, 6, 2.5, (70, 100))])
+def test_general_kcache_is_bitwise_neutral(pnp, P, R, sigma, shape):
+    """The general sweep's pair-weight cache (sweep A stores, sweep B and
+    frozen applies stream it): same bits as recomputing, adaptive and frozen."""
+    from paper_1901_06110_b200 import profiling
+    g = torch.Generator(device="cuda").manual_seed(P + R)
+    x = torch.rand(*shape, device="cuda", generator=g)
+    y = torch.rand(*shape, device="cuda", generator=g)
+    p = pnp.PatchParams(P, R, 0.2, sigma)
+    out, d, a = pnp.dsg_nlm_denoise(x, p, return_aux=True)
+    fz = pnp.freeze_guide(x, p)
+    info = fz.cache_info()
+    assert info["rows_cached"] == info["tile_rows"] and info["bytes"] > 0
+    fy = fz.apply(y)
+    profiling.set_cache_limit(0)
+    try:
+        out0, d0, a0 = pnp.dsg_nlm_denoise(x, p, return_aux=True)
+        fz0 = pnp.freeze_guide(x, p)
+        assert fz0.cache_info()["rows_cached"] == 0
+        fy0 = fz0.apply(y)
+    finally:
+        profiling.set_cache_limit(None)
+    assert torch.equal(out, out0) and torch.equal(d, d0) and torch.equal(a, a0)
+    assert torch.equal(fy, fy0)
