@@ -49,6 +49,12 @@ keep("gen_box_r21", pnp.dsg_nlm_denoise(rand(96, 130), pnp.PatchParams(11, 21, 0
 keep("gen_gauss", pnp.dsg_nlm_denoise(rand(60, 70), pnp.PatchParams(19, 4, 0.2, 3.0)))
 keep("gen_near", pnp.dsg_nlm_denoise(rand(104, 104), pnp.PatchParams(1, 100, 0.3)))
 keep("gen_sharded", sharded_dsg_nlm_denoise(rand(256, 200), pnp.PatchParams(17, 21, 0.15), 2))
+xg = rand(2, 90, 140)
+keep("gen_frozen", pnp.freeze_guide(xg, pnp.PatchParams(13, 9, 0.2)).apply(rand(2, 90, 140)))
+profiling.set_cache_limit(0)
+keep("gen_recompute", pnp.dsg_nlm_denoise(xg, pnp.PatchParams(13, 9, 0.2)))
+profiling.set_cache_limit(None)
+keep("gen_cached", pnp.dsg_nlm_denoise(xg, pnp.PatchParams(13, 9, 0.2)))
 keep("nlm", pnp.nlm_denoise(x, pg))
 op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, "symmetric")
 truth = rand(64, 96)
