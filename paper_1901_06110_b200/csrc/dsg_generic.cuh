@@ -103,8 +103,12 @@ __device__ __forceinline__ float sqd(float a, float b) {
   return __fmul_rn(t, t);
 }
 
-template <int C, bool BOX, bool SYM, int KG, int MODE>
-__global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs a) {
+// NM: rows per phase-V thread the register arrays hold (>= TH / 2); the
+// k-cache sweep is instantiated per tile height (fewer registers -> more
+// resident CTAs for the stream), the others with the maximum
+template <int C, bool BOX, bool SYM, int KG, int MODE, int NM = kGenNmax>
+__global__ void __launch_bounds__(kGenThreads, MODE == MODE_CACHED && NM <= 8 ? 4 : 1)
+    dsg_generic_kernel(const GenArgs a) {
   constexpr bool STORE = MODE == MODE_STORE, CACHED = MODE == MODE_CACHED;
   static_assert(SYM || MODE == MODE_RECOMPUTE, "the k cache covers the half window");
   pdl_begin();
@@ -162,11 +166,11 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 
   const int x = tid & (kTW - 1), g = tid / kTW;
   const int N = TH / 2, rA = g * N;  // phase-V rows [rA, rA + N)
-  float near[C][kGenNmax], yown[C][kGenNmax];
+  float near[C][NM], yown[C][NM];
 #pragma unroll
   for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-    for (int i = 0; i < kGenNmax; ++i) {
+    for (int i = 0; i < NM; ++i) {
       const float v = i < N ? yval(c_, r0g + rA + i, c0g + x) : 0.f;
       yown[c_][i] = v;
       near[c_][i] = blockIdx.y == 0 ? v : 0.f;  // self pair: k = hat = 1
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
   // half 1's shared rows go in after that barrier (top of the next step,
   // before the next phase-H barrier): one writer per cell between barriers,
   // a fixed order (half 0, half 1) -> bit-reproducible.
-  constexpr int WIN = kGenNmax + KG - 1;
+  constexpr int WIN = NM + KG - 1;
   float pf[C][SYM ? WIN : 1];
   float pendv[C][KG > 1 ? KG - 1 : 1];
   float* pend = nullptr;
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
         if (!valid) continue;
         flush_pending();
         // this step's k planes (valid offsets in order): kplane, kplane + 1, ...
-        float kv[CACHED ? KG : 1][CACHED ? kGenNmax : 1];
+        float kv[CACHED ? KG : 1][CACHED ? NM : 1];
         if (CACHED) {  // all the step's loads in flight before the sums
 #pragma unroll
           for (int j = 0; j < KG; ++j) {
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
                               (size_t)(kplane + __popc(valid & ((1u << j) - 1u))) * (TH * kTW) +
                               rA * kTW + x;
 #pragma unroll
-            for (int i = 0; i < kGenNmax; ++i) {
+            for (int i = 0; i < NM; ++i) {
               const bool ok = vj && i < N;
               PNP_CHECK(!ok || (long long)(kq + i * kTW - a.kcache) < a.kcache_floats);
               kv[j][i] = ok ? __ldcs(kq + i * kTW) : 0.f;
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
         }
         const float* yp = Ys + rA * L.YS + x + cdx;
 #pragma unroll
-        for (int i = 0; i < kGenNmax; ++i) {
+        for (int i = 0; i < NM; ++i) {
           if (i >= N) break;
 #pragma unroll
           for (int j = 0; j < KG; ++j) {
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-      for (int i = 0; i < kGenNmax; ++i) {
+      for (int i = 0; i < NM; ++i) {
         if (i >= N) break;
         float* q = As + (c_ * L.AR + rA + i) * L.AC + x + R;
         *q = __fadd_rn(near[c_][i], *q);
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(kGenThreads) dsg_generic_kernel(const GenArgs 
 #pragma unroll
     for (int c_ = 0; c_ < C; ++c_)
 #pragma unroll
-      for (int i = 0; i < kGenNmax; ++i) {
+      for (int i = 0; i < NM; ++i) {
         if (i >= N) break;
         out[((size_t)c_ * BR + rA + i) * BC + x] = near[c_][i];
       }

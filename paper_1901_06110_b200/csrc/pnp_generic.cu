@@ -5,8 +5,9 @@
 
 namespace pnp {
 
-template <int C, bool BOX, bool SYM, int KG, int MODE>
+template <int C, bool BOX, bool SYM, int KG, int MODE, int NM = kGenNmax>
 static cudaError_t launch_gen_t(const GenArgs& a, dim3 grid, cudaStream_t st) {
+  if (a.TH / 2 > NM) return cudaErrorInvalidValue;
   const size_t smem =
       (size_t)gen_smem(a.TH, a.P, a.R, C, SYM, KG, MODE == MODE_CACHED).total * sizeof(float);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
@@ -16,13 +17,13 @@ static cudaError_t launch_gen_t(const GenArgs& a, dim3 grid, cudaStream_t st) {
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(dsg_generic_kernel<C, BOX, SYM, KG, MODE>,
+    cudaError_t e = cudaFuncSetAttribute(dsg_generic_kernel<C, BOX, SYM, KG, MODE, NM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
-  return launch_pdl(dsg_generic_kernel<C, BOX, SYM, KG, MODE>, grid, dim3(kGenThreads), smem, st,
-                    a);
+  return launch_pdl(dsg_generic_kernel<C, BOX, SYM, KG, MODE, NM>, grid, dim3(kGenThreads), smem,
+                    st, a);
 }
 
 template <int KG>
@@ -30,6 +31,12 @@ static cudaError_t launch_gen_kg(const GenArgs& a, int C, bool box, bool sym, in
                                  dim3 grid, cudaStream_t st) {
   if (mode == MODE_CACHED) {  // no patch filter: box or not is the same kernel
     if (!sym) return cudaErrorInvalidValue;
+    if (a.TH <= 8)
+      return C == 1 ? launch_gen_t<1, false, true, KG, MODE_CACHED, 4>(a, grid, st)
+                    : launch_gen_t<2, false, true, KG, MODE_CACHED, 4>(a, grid, st);
+    if (a.TH <= 16)
+      return C == 1 ? launch_gen_t<1, false, true, KG, MODE_CACHED, 8>(a, grid, st)
+                    : launch_gen_t<2, false, true, KG, MODE_CACHED, 8>(a, grid, st);
     return C == 1 ? launch_gen_t<1, false, true, KG, MODE_CACHED>(a, grid, st)
                   : launch_gen_t<2, false, true, KG, MODE_CACHED>(a, grid, st);
   }
