@@ -40,6 +40,7 @@ CASES = [
     (90, 75, 40, 5, 0.2, None, 9),     # R > 32, half window (shared far plane)
     (45, 60, 4, 17, 0.2, 3.0, 10),     # Gaussian taps beyond P = 15
     (40, 50, 36, 3, 0.2, 1.0, 11),     # Gaussian, R > 32
+    (26, 29, 21, 11, 0.15, None, 12),  # margin = min extent: one tile, cached
 ]
 
 
@@ -186,7 +187,9 @@ def test_general_sweep_sharded_sr_admm_bitwise(pnp):
 
 @pytest.mark.parametrize("P,R,sigma,shape", [(17, 21, None, (2, 90, 140)),
                                              (11, 21, None, (256, 256)),
-                                             (19, 6, 2.5, (70, 100))])
+                                             (19, 6, 2.5, (70, 100)),
+                                             (11, 21, None, (26, 29)),
+                                             (29, 21, None, (3, 50, 200))])
 def test_general_kcache_is_bitwise_neutral(pnp, P, R, sigma, shape):
     """The general sweep's pair-weight cache (sweep A stores, sweep B and
     frozen applies stream it): same bits as recomputing, adaptive and frozen."""
