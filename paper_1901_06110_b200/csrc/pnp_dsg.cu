@@ -22,6 +22,7 @@
 #include <string>
 #include <vector>
 
+#include "admm_math.cuh"
 #include "dsg_generic.cuh"
 #include "dsg_sweep.cuh"
 #include "sweep_launch.cuh"
@@ -87,14 +88,35 @@ struct FixIO {
   // when set, the last CTA reduces part3 into stats_out[b][0..2] (stride 4)
   double* stats_out;
   unsigned* counter;   // zero between launches (the last CTA resets it)
+  // FIX_APPLY_U with grad set: the next iteration's x-update fused in
+  // (solver.py:219-221): x = clamp(mu (alpha x + rho (v - u) - grad)) over
+  // xa, z = x + u over the apply input; its finite flags into xflags
+  const float* grad;
+  double mu, alpha;
+  float lo, hi;
+  int* xflags;
 };
+
+// the fused x-update of one pixel (grad set): x_a and the apply input z are
+// rewritten in place (this thread alone reads / writes them at o)
+__device__ __forceinline__ int admm_x_next(const FixIO& io, size_t o, float xa, float v,
+                                           float un) {
+  float xf, zf;
+  const int f = admm_xupdate(io.mu, io.alpha, io.rho, io.lo, io.hi, xa, v, un, io.grad[o], xf, zf);
+  const_cast<float*>(io.xa)[o] = xf;
+  const_cast<float*>(io.x)[o] = zf;
+  return f;
+}
 
 // u-update of one pixel (same arithmetic as admm_uupdate_kernel)
 __device__ __forceinline__ int admm_u_pixel(const FixIO& io, size_t o, float v, double& s0,
-                                            double& s1, double& s2) {
-  const double xv = io.xa[o], vv = v;
+                                            double& s1, double& s2, float& xa_out, float& un_out) {
+  const float xa = io.xa[o];
+  const double xv = xa, vv = v;
   const float un = (float)((double)io.u[o] + (xv - vv));
   io.u[o] = un;
+  xa_out = xa;
+  un_out = un;
   s0 += (xv - vv) * (xv - vv);
   const double dv = io.rho * (vv - (io.vprev ? (double)io.vprev[o] : 0.0));
   s1 += dv * dv;
@@ -108,10 +130,11 @@ __device__ __forceinline__ int admm_u_pixel(const FixIO& io, size_t o, float v, 
 // the same u-update from preloaded values (vprev / gt ignored when null)
 __device__ __forceinline__ int admm_u_values(const FixIO& io, size_t o, float v, float u,
                                              float xa, float vprev, float gt, double& s0,
-                                             double& s1, double& s2) {
+                                             double& s1, double& s2, float& un_out) {
   const double xv = xa, vv = v;
   const float un = (float)((double)u + (xv - vv));
   io.u[o] = un;
+  un_out = un;
   s0 += (xv - vv) * (xv - vv);
   const double dv = io.rho * (vv - (io.vprev ? (double)vprev : 0.0));
   s1 += dv * dv;
@@ -290,14 +313,16 @@ __global__ void __launch_bounds__(256, PNP_FIXLB) dsg_fixup_px_kernel(const FixG
 
   float dmax = 0.f;
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-  int uf = 0;
+  int uf = 0, xf = 0;
   if (own) {
     const float s0 = s[0];
     if (MODE == FIX_APPLY_U) {
       const float kx = __fmul_rn(e_rs, s0);
       const float v = dsg_finish(kx, e_d, io.inv_m[b], e_x);
       io.out[o] = v;
-      uf = admm_u_values(io, o, v, e_u, e_xa, e_vp, e_gt, u0, u1, u2);
+      float un;
+      uf = admm_u_values(io, o, v, e_u, e_xa, e_vp, e_gt, u0, u1, u2, un);
+      if (io.grad) xf = admm_x_next(io, o, e_xa, v, un);
     } else if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
@@ -313,6 +338,10 @@ __global__ void __launch_bounds__(256, PNP_FIXLB) dsg_fixup_px_kernel(const FixG
     } else {  // FIX_NLM: num / den
       io.out[o] = __fdiv_rn(s0, s[C - 1]);
     }
+  }
+  if (MODE == FIX_APPLY_U && io.grad) {
+    xf = __reduce_or_sync(0xffffffffu, xf);
+    if (xf && (threadIdx.x & 31) == 0) atomicOr(io.xflags, xf);
   }
   if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2), admm_stats_last(io);
   if (MODE == FIX_KXD || MODE == FIX_D) {
@@ -424,7 +453,7 @@ __global__ void __launch_bounds__(256, MODE == FIX_NLM ? 3 : 4) dsg_fixup_tile_k
 
   float dmax = 0.f;
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-  int uf = 0;
+  int uf = 0, xf = 0;
 #pragma unroll
   for (int k = 0; k < kFixRows; ++k) {
     const int y = ti * TH + ly0 + 4 * k;
@@ -435,7 +464,9 @@ __global__ void __launch_bounds__(256, MODE == FIX_NLM ? 3 : 4) dsg_fixup_tile_k
       const float kx = __fmul_rn(io.rs[o], s0);
       const float v = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
       io.out[o] = v;
-      uf |= admm_u_pixel(io, o, v, u0, u1, u2);
+      float xa, un;
+      uf |= admm_u_pixel(io, o, v, u0, u1, u2, xa, un);
+      if (io.grad) xf |= admm_x_next(io, o, xa, v, un);
     } else if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
@@ -454,6 +485,10 @@ __global__ void __launch_bounds__(256, MODE == FIX_NLM ? 3 : 4) dsg_fixup_tile_k
     } else {  // FIX_NLM: num / den
       io.out[o] = __fdiv_rn(s0, s[C - 1][k]);
     }
+  }
+  if (MODE == FIX_APPLY_U && io.grad) {
+    xf = __reduce_or_sync(0xffffffffu, xf);
+    if (xf && (threadIdx.x & 31) == 0) atomicOr(io.xflags, xf);
   }
   if (MODE == FIX_APPLY_U) admm_u_block(io, b, uf, u0, u1, u2), admm_stats_last(io);
   if (MODE == FIX_KXD || MODE == FIX_D) {
@@ -1230,10 +1265,12 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   for (cudaEvent_t e : ctx->iter_events) cudaEventDestroy(e);
   if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
   if (ctx->ev_res) cudaEventDestroy(ctx->ev_res);
+  if (ctx->ev_g) cudaEventDestroy(ctx->ev_g);
   if (ctx->ev_switch) cudaEventDestroy(ctx->ev_switch);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   ctx->admm_r.release();
   ctx->admm_part.release();
+  ctx->admm_g.release();
   delete ctx;
   return PNP_OK;
 }
@@ -1639,6 +1676,16 @@ int pnp_dsg_apply(pnp_ctx* ctx, const pnp_frozen* fz, const float* x, float* out
 int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v,
                        float* u, const float* x, const float* v_prev, const float* gt,
                        double rho, double* stats, int* flags) {
+  return pnp::dsg_apply_admm_x(ctx, fz, z, v, u, x, v_prev, gt, rho, stats, flags, nullptr);
+}
+
+}  // extern "C"
+
+namespace pnp {
+
+int dsg_apply_admm_x(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v, float* u,
+                     const float* x, const float* v_prev, const float* gt, double rho,
+                     double* stats, int* flags, const AdmmXNext* xn) {
   if (fz && ctx) fz->stream = ctx->stream;
   if (!ctx || !fz || !z || !v || !u || !x || !stats || !flags)
     return fail(PNP_EINVAL, "null argument");
@@ -1672,8 +1719,22 @@ int pnp_dsg_apply_admm(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float
   if ((rc = ensure_counter(ctx))) return rc;
   io.stats_out = stats;
   io.counter = ctx->counter.as<unsigned>();
+  if (xn) {  // the next x-update fused in, once its gradient is ready
+    if (!xn->grad || !xn->flags) return fail(PNP_EINVAL, "null argument");
+    if (xn->ready) PNP_CUDA(cudaStreamWaitEvent(ctx->stream, xn->ready, 0));
+    io.grad = xn->grad;
+    io.mu = xn->mu;
+    io.alpha = xn->alpha;
+    io.lo = (float)xn->lo;
+    io.hi = (float)xn->hi;
+    io.xflags = xn->flags;
+  }
   return run_fixup<FIX_APPLY_U>(ctx, g, w, 1, part, io);
 }
+
+}  // namespace pnp
+
+extern "C" {
 
 int pnp_frozen_destroy(pnp_frozen* fz) {
   if (!fz) return PNP_OK;

@@ -18,6 +18,7 @@
 #include <mutex>
 #include <vector>
 
+#include "admm_math.cuh"
 #include "pnp_internal.h"
 #include "pnp_pdl.cuh"
 #include "pnp_reduce.cuh"
@@ -93,14 +94,9 @@ struct XUpd {
 };
 
 __device__ __forceinline__ int xupdate_pixel(const XUpd& q, size_t i, float grad) {
-  const double xv = (double)q.x[i];
-  const double uv = (double)q.u[i];
-  const double xn = q.mu * (q.alpha * xv + q.rho * ((double)q.v[i] - uv) - (double)grad);
-  float xf = (float)xn;
-  int f = isfinite(xf) ? 0 : 1;
-  xf = fminf(fmaxf(xf, q.lo), q.hi);
-  const float zf = (float)((double)xf + uv);
-  if (!isfinite(zf)) f |= 2;
+  float xf, zf;
+  const int f = admm_xupdate(q.mu, q.alpha, q.rho, q.lo, q.hi, q.x[i], q.v[i], q.u[i], grad, xf,
+                             zf);
   q.x[i] = xf;
   q.z[i] = zf;
   return f;
@@ -350,14 +346,8 @@ admm_xupdate_kernel(float* __restrict__ x, const float* __restrict__ v, const fl
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
   if (i < n) {
-    const double xv = (double)x[i];
-    const double uv = (double)u[i];
-    const double xn = mu * (alpha * xv + rho * ((double)v[i] - uv) - (double)grad[i]);
-    float xf = (float)xn;
-    if (!isfinite(xf)) f |= 1;
-    xf = fminf(fmaxf(xf, lo), hi);
-    const float zf = (float)((double)xf + uv);
-    if (!isfinite(zf)) f |= 2;
+    float xf, zf;
+    f = admm_xupdate(mu, alpha, rho, lo, hi, x[i], v[i], u[i], grad[i], xf, zf);
     x[i] = xf;
     z[i] = zf;
   }
@@ -1216,30 +1206,46 @@ int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, con
     return launch_pdl(sr_residual_kernel, rg, dim3(256), rsm, st, x, y, r, res_full(H, factor), W,
                       factor, radius, boundary, t, part, (const CgState*)nullptr);
   };
-  // the first iteration's residual on the main stream (x is x_{k0-1})
+  // iteration k0's gradient + x-update on the main stream (x is x_{k0-1})
+  if ((rc = ctx->admm_g.ensure((size_t)batch * H * W * sizeof(float)))) return rc;
+  if (!ctx->ev_g) PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_g, cudaEventDisableTiming));
+  float* grad = ctx->admm_g.as<float>();
   PNP_CUDA(residual(main));
   float* vcur = v0;
   float* vnext = v1;
-  int cur = 0;
-  for (int k = k0; k <= k1; ++k) {
-    Nvtx iter("admm_iteration");
-    int* fk = flags + (k - 1);
-    double* obj = (objv && k >= 2) ? objv + (size_t)(k - 2) * batch : nullptr;
-    if (k > k0) PNP_CUDA(cudaStreamWaitEvent(main, ctx->ev_res, 0));
-    const XUpd q = make_xupd(x, vcur, u, z, mu, alpha, rho, lo, hi, fk);
+  {
+    double* obj = (objv && k0 >= 2) ? objv + (size_t)(k0 - 2) * batch : nullptr;
+    const XUpd q = make_xupd(x, vcur, u, z, mu, alpha, rho, lo, hi, flags + (k0 - 1));
     const RedEpi red{part, obj, 0.5, nblk, batch};
     PNP_CUDA(launch_pdl(sr_adjoint_kernel<ADJ_XUPD>, ag, dim3(256), asm_, main, (const float*)r,
                         (float*)nullptr, adj_full(H, factor), W, factor, radius, boundary, t, q,
                         CgEpi{}, red));
-    if (k < k1) {  // next iteration's residual overlaps this denoise
+  }
+  int cur = 0;
+  for (int k = k0; k <= k1; ++k) {
+    Nvtx iter("admm_iteration");
+    int* fk = flags + (k - 1);
+    if (k < k1) {
+      // the gradient of x_k (residual + adjoint, and the data term f(x_k)) on
+      // the side stream while the main stream denoises; the apply's fixup
+      // then performs iteration k+1's x-update
       PNP_CUDA(cudaEventRecord(ctx->ev_x, main));
       PNP_CUDA(cudaStreamWaitEvent(side, ctx->ev_x, 0));
       PNP_CUDA(residual(side));
-      PNP_CUDA(cudaEventRecord(ctx->ev_res, side));
-    }
-    if ((rc = pnp_dsg_apply_admm(ctx, fz, z, vnext, u, x, vcur, gt, rho,
-                                 stats + (size_t)(k - 1) * batch * 4, fk)))
+      double* obj = objv ? objv + (size_t)(k - 1) * batch : nullptr;
+      const RedEpi red{part, obj, 0.5, nblk, batch};
+      PNP_CUDA(launch_pdl(sr_adjoint_kernel<ADJ_PLAIN>, ag, dim3(256), asm_, side,
+                          (const float*)r, grad, adj_full(H, factor), W, factor, radius, boundary,
+                          t, XUpd{}, CgEpi{}, red));
+      PNP_CUDA(cudaEventRecord(ctx->ev_g, side));
+      const AdmmXNext xn{grad, mu, alpha, lo, hi, flags + k, ctx->ev_g};
+      if ((rc = dsg_apply_admm_x(ctx, fz, z, vnext, u, x, vcur, gt, rho,
+                                 stats + (size_t)(k - 1) * batch * 4, fk, &xn)))
+        return rc;
+    } else if ((rc = pnp_dsg_apply_admm(ctx, fz, z, vnext, u, x, vcur, gt, rho,
+                                        stats + (size_t)(k - 1) * batch * 4, fk))) {
       return rc;
+    }
     float* tmp = vcur;
     vcur = vnext;
     vnext = tmp;

@@ -91,8 +91,8 @@ struct pnp_ctx {
   // its side stream (the next iteration's SR residual overlaps the denoiser),
   // two ordering events, and the residual / partial buffers it owns
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_x = nullptr, ev_res = nullptr;
-  pnp::DevBuf admm_r, admm_part;
+  cudaEvent_t ev_x = nullptr, ev_res = nullptr, ev_g = nullptr;
+  pnp::DevBuf admm_r, admm_part, admm_g;
   // incremental banded denoise (pnp_dsg_band_sweep / _finish): the next band
   // expected (-1: none in progress), the call's band count and cached tile rows
   int band_next = -1, band_count = 0, band_kc_rows = 0;
@@ -141,8 +141,22 @@ struct ProfScope {
 namespace pnp {
 // stats[b*4 + k] = sum_j part[b][j][k] for k < 3 (pnp_forward.cu)
 int reduce_stats3(pnp_ctx* ctx, const double* part, int nblk, int batch, double* stats);
-// pnp_admm_run's SR loop with the next iteration's residual on a side stream
-// (pnp_forward.cu): same launches and arguments as the sequential loop.
+// The next iteration's x-update fused into a frozen apply's u-update fixup
+// (pnp_dsg_apply_admm + pnp_sr_grad_xupdate in one pass over the pixels): x
+// (the apply's `x`) and z (its input) are rewritten in place once `ready`
+// (the gradient's event, nullable) has fired.
+struct AdmmXNext {
+  const float* grad;
+  double mu, alpha, lo, hi;
+  int* flags;
+  cudaEvent_t ready;
+};
+int dsg_apply_admm_x(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* v, float* u,
+                     const float* x, const float* v_prev, const float* gt, double rho,
+                     double* stats, int* flags, const AdmmXNext* xn);
+// pnp_admm_run's SR loop with the gradient of the next iteration (residual +
+// adjoint) on a side stream during the frozen apply, and the x-update fused
+// into the apply's fixup (pnp_forward.cu): bitwise the sequential loop.
 int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, const float* taps,
                       int radius, int factor, int boundary, const pnp_frozen* fz, int k0, int k1,
                       float* x, float* v0, float* v1, float* u, float* z, const float* gt,
