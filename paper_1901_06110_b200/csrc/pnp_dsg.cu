@@ -1264,7 +1264,6 @@ int pnp_ctx_destroy(pnp_ctx* ctx) {
   }
   for (cudaEvent_t e : ctx->iter_events) cudaEventDestroy(e);
   if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
-  if (ctx->ev_res) cudaEventDestroy(ctx->ev_res);
   if (ctx->ev_g) cudaEventDestroy(ctx->ev_g);
   if (ctx->ev_switch) cudaEventDestroy(ctx->ev_switch);
   if (ctx->side) cudaStreamDestroy(ctx->side);

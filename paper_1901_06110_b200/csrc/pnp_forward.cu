@@ -1190,7 +1190,7 @@ int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, con
   if (!ctx->side) {
     PNP_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
-    PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_res, cudaEventDisableTiming));
+    PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_g, cudaEventDisableTiming));
   }
   const int nl = (H / factor) * (W / factor);
   const dim3 rg = sr_res_grid(H, W, factor, batch), ag = sr_adj_grid(H, W, batch);
@@ -1208,7 +1208,6 @@ int sr_admm_pipelined(pnp_ctx* ctx, const float* y, int batch, int H, int W, con
   };
   // iteration k0's gradient + x-update on the main stream (x is x_{k0-1})
   if ((rc = ctx->admm_g.ensure((size_t)batch * H * W * sizeof(float)))) return rc;
-  if (!ctx->ev_g) PNP_CUDA(cudaEventCreateWithFlags(&ctx->ev_g, cudaEventDisableTiming));
   float* grad = ctx->admm_g.as<float>();
   PNP_CUDA(residual(main));
   float* vcur = v0;

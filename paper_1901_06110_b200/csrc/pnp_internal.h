@@ -88,10 +88,11 @@ struct pnp_ctx {
   std::map<std::tuple<int, int, int>, Tables> tables;
   // per-iteration timing events of the native ADMM loop (pnp_admm_run)
   std::vector<cudaEvent_t> iter_events;
-  // its side stream (the next iteration's SR residual overlaps the denoiser),
-  // two ordering events, and the residual / partial buffers it owns
+  // its side stream (the next iteration's SR gradient overlaps the denoiser),
+  // two ordering events (x ready, gradient ready), and the residual /
+  // partial / gradient buffers it owns
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_x = nullptr, ev_res = nullptr, ev_g = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_g = nullptr;
   pnp::DevBuf admm_r, admm_part, admm_g;
   // incremental banded denoise (pnp_dsg_band_sweep / _finish): the next band
   // expected (-1: none in progress), the call's band count and cached tile rows
