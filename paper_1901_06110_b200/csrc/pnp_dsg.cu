@@ -179,12 +179,14 @@ __device__ __forceinline__ void admm_u_block(const FixIO& io, int b, int f, doub
 
 // The per-image sums of FIX_APPLY_U's partials, folded into the fixup: the
 // last CTA to finish reduces them (same arithmetic as reduce_partials_kernel).
+// One counter per image (blockIdx.z): the last CTA of each image reduces that
+// image's sums, so a batch's reductions run in parallel instead of as one
+// CTA's serial tail (config 5: 64 images).
 __device__ __forceinline__ void admm_stats_last(const FixIO& io) {
-  if (!io.stats_out || !cta_is_last(io.counter)) return;
-  __shared__ double red[3][8];
   const int nblk = gridDim.x * gridDim.y;
-  for (int b = 0; b < (int)gridDim.z; ++b)
-    cta_reduce_partials3(io.part3, nblk, b, 1.0, io.stats_out, 4, red);
+  if (!io.stats_out || !cta_is_last_of(io.counter + blockIdx.z, (unsigned)nblk)) return;
+  __shared__ double red[3][8];
+  cta_reduce_partials3(io.part3, nblk, blockIdx.z, 1.0, io.stats_out, 4, red);
 }
 
 __device__ __forceinline__ float dsg_finish(float kx, float d, float inv_m, float x) {
@@ -454,20 +456,56 @@ __global__ void __launch_bounds__(256, MODE == FIX_NLM ? 3 : 4) dsg_fixup_tile_k
   float dmax = 0.f;
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
   int uf = 0, xf = 0;
+  if (MODE == FIX_APPLY_U) {
+    // the fused ADMM epilogue reads 8 planes per pixel: the loads of 4 rows
+    // are issued together before any of their stores (the stores could alias
+    // the next row's loads for the compiler, which would otherwise serialize
+    // one round trip per row); same per-pixel arithmetic, same row order
+    constexpr int KB = 2;
+#pragma unroll
+    for (int k0 = 0; k0 < kFixRows; k0 += KB) {
+      float ers[KB], ed[KB], ez[KB], exa[KB], eu[KB], evp[KB], egt[KB], egr[KB];
+      size_t oo[KB];
+      bool ok[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int k = k0 + j, y = ti * TH + ly0 + 4 * k;
+        ok[j] = ly0 + 4 * k < TH && y >= ylo && y < yhi && x < W;
+        oo[j] = ok[j] ? (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x : 0;
+        ers[j] = ldg_pred(io.rs + oo[j], ok[j]);
+        ed[j] = ldg_pred(io.d + oo[j], ok[j]);
+        ez[j] = ldg_pred(io.x + oo[j], ok[j]);
+        exa[j] = ldg_pred(io.xa + oo[j], ok[j]);
+        eu[j] = ldg_pred(io.u + oo[j], ok[j]);
+        evp[j] = ldg_pred(io.vprev + oo[j], ok[j] && io.vprev);
+        egt[j] = ldg_pred(io.gt + oo[j], ok[j] && io.gt);
+        egr[j] = ldg_pred(io.grad + oo[j], ok[j] && io.grad);
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        if (!ok[j]) continue;
+        const size_t o = oo[j];
+        const float kx = __fmul_rn(ers[j], s[0][k0 + j]);
+        const float v = dsg_finish(kx, ed[j], io.inv_m[b], ez[j]);
+        io.out[o] = v;
+        float un;
+        uf |= admm_u_values(io, o, v, eu[j], exa[j], evp[j], egt[j], u0, u1, u2, un);
+        if (io.grad) {
+          float xn, zn;
+          xf |= admm_xupdate(io.mu, io.alpha, io.rho, io.lo, io.hi, exa[j], v, un, egr[j], xn, zn);
+          const_cast<float*>(io.xa)[o] = xn;
+          const_cast<float*>(io.x)[o] = zn;
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int k = 0; k < kFixRows; ++k) {
     const int y = ti * TH + ly0 + 4 * k;
-    if (ly0 + 4 * k >= TH || y < ylo || y >= yhi || x >= W) continue;
+    if (MODE == FIX_APPLY_U || ly0 + 4 * k >= TH || y < ylo || y >= yhi || x >= W) continue;
     const size_t o = (size_t)b * f.buf_rows * W + (size_t)(y - f.buf_r0) * W + x;
     const float s0 = s[0][k];
-    if (MODE == FIX_APPLY_U) {
-      const float kx = __fmul_rn(io.rs[o], s0);
-      const float v = dsg_finish(kx, io.d[o], io.inv_m[b], io.x[o]);
-      io.out[o] = v;
-      float xa, un;
-      uf |= admm_u_pixel(io, o, v, u0, u1, u2, xa, un);
-      if (io.grad) xf |= admm_x_next(io, o, xa, v, un);
-    } else if (MODE == FIX_RS) {
+    if (MODE == FIX_RS) {
       io.rs[o] = __fdiv_rn(1.f, __fsqrt_rn(fmaxf(s0, FLT_MIN)));
     } else if (MODE == FIX_KXD) {
       const float r = e_rs[k];
@@ -861,11 +899,11 @@ static cudaError_t pool_alloc(pnp_ctx* ctx, void** p, size_t bytes) {
 
 // Device counter of the last-CTA reductions: allocated and zeroed once; every
 // kernel that uses it leaves it at zero.
-static int ensure_counter(pnp_ctx* ctx) {
-  if (ctx->counter.bytes) return PNP_OK;
-  int rc = ctx->counter.ensure(sizeof(unsigned));
+static int ensure_counter(pnp_ctx* ctx, int n = 1) {
+  if (ctx->counter.bytes >= (size_t)n * sizeof(unsigned)) return PNP_OK;
+  int rc = ctx->counter.ensure((size_t)n * sizeof(unsigned));
   if (rc) return rc;
-  PNP_CUDA(cudaMemsetAsync(ctx->counter.ptr, 0, sizeof(unsigned), ctx->stream));
+  PNP_CUDA(cudaMemsetAsync(ctx->counter.ptr, 0, ctx->counter.bytes, ctx->stream));
   return PNP_OK;
 }
 
@@ -1715,7 +1753,7 @@ int dsg_apply_admm_x(pnp_ctx* ctx, const pnp_frozen* fz, const float* z, float* 
   io.rho = rho;
   io.part3 = ctx->stats.as<double>();
   io.flags = flags;
-  if ((rc = ensure_counter(ctx))) return rc;
+  if ((rc = ensure_counter(ctx, g.B))) return rc;
   io.stats_out = stats;
   io.counter = ctx->counter.as<unsigned>();
   if (xn) {  // the next x-update fused in, once its gradient is ready

@@ -74,10 +74,13 @@ struct RedEpi {
   int nblk, batch;
 };
 
+// CTA (0, 0, z) reduces images z, z + gridDim.z, ... (one image per CTA when the
+// grid's z is the batch): a batch's reductions run in parallel.
 __device__ __forceinline__ void red_epilogue(const RedEpi& e) {
-  if (!e.out || blockIdx.x || blockIdx.y || blockIdx.z) return;
+  if (!e.out || blockIdx.x || blockIdx.y) return;
   __shared__ double red[8];
-  for (int b = 0; b < e.batch; ++b) cta_reduce_partials(e.part, e.nblk, 1, b, 0, e.scale, e.out, 1, red);
+  for (int b = blockIdx.z; b < e.batch; b += gridDim.z)
+    cta_reduce_partials(e.part, e.nblk, 1, b, 0, e.scale, e.out, 1, red);
 }
 
 // The linearized-ADMM x-update (solver.py:219-221) fused into a gradient
@@ -145,30 +148,78 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
   const int oy0 = win.out_r0 + blockIdx.y * kSrT, ox0 = blockIdx.x * kSrT;
   const int y0 = k * oy0 - rad, x0 = k * ox0 - rad;
   const float* xb = x + (size_t)b * win.in_rows * W;
-  for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
-    const int yy = i / S, xx = i - yy * S;
-    int sy = map_index(min(y0 + yy, H - 1 + rad), H, sym) - win.in_r0;
-    sy = sy < 0 ? 0 : (sy >= win.in_rows ? win.in_rows - 1 : sy);  // halo rows only: never hit
-    const int sx = map_index(min(x0 + xx, W - 1 + rad), W, sym);
-    X[i] = xb[(size_t)sy * W + sx];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < S * kSrT; i += blockDim.x) {
-    const int yy = i / kSrT, tx = i - yy * kSrT;
-    const float* row = X + yy * S + k * tx;
-    float s = 0.f;
-    for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
-    Hh[i] = s;
-  }
-  __syncthreads();
+  // this thread's output and its observation, loaded before the staging so
+  // the two global round trips overlap
   const int ty = threadIdx.x / kSrT, tx = threadIdx.x - ty * kSrT;
   const int oy = oy0 + ty, ox = ox0 + tx;
+  const bool own = oy < win.out_r0 + win.out_rows && ox < w;
+  const size_t o = own ? (size_t)b * win.out_rows * w + (size_t)(oy - win.out_r0) * w + ox : 0;
+  const float yo = (own && y) ? y[o] : 0.f;
+  // The configs' operator (factor 2, 9x9 kernel) runs with compile-time tile
+  // sizes and unrolled taps; tiles whose staged window needs no boundary map
+  // copy it row by row.  Same products in the same order as the generic
+  // loops below -> the same bits.
+  constexpr int FS = 2 * (kSrT - 1) + 1 + 8;
+  const bool fast = k == 2 && rad == 4;
+  if (fast && y0 >= 0 && y0 + FS <= H && y0 - win.in_r0 >= 0 &&
+      y0 - win.in_r0 + FS <= win.in_rows && x0 >= 0 && x0 + FS <= W) {
+    // thread (warp w, lane l): rows w + 8m, columns l and l + 32; every load
+    // of the thread in flight before its first shared store
+    const int wq = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const float* src = xb + (size_t)(y0 - win.in_r0 + wq) * W + x0 + l;
+    float v[5][2];
+#pragma unroll
+    for (int m = 0; m < 5; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        v[m][h] = (wq + 8 * m < FS && l + 32 * h < FS) ? src[(size_t)8 * m * W + 32 * h] : 0.f;
+#pragma unroll
+    for (int m = 0; m < 5; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (wq + 8 * m < FS && l + 32 * h < FS) X[(wq + 8 * m) * FS + l + 32 * h] = v[m][h];
+  } else {
+    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+      const int yy = i / S, xx = i - yy * S;
+      int sy = map_index(min(y0 + yy, H - 1 + rad), H, sym) - win.in_r0;
+      sy = sy < 0 ? 0 : (sy >= win.in_rows ? win.in_rows - 1 : sy);  // halo rows only: never hit
+      const int sx = map_index(min(x0 + xx, W - 1 + rad), W, sym);
+      X[i] = xb[(size_t)sy * W + sx];
+    }
+  }
+  __syncthreads();
+  if (fast) {  // thread t: filtered row (t >> 4) + 16 m, low-res column t & 15
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int yy = (threadIdx.x >> 4) + 16 * m;
+      if (yy < FS) {
+        const float* row = X + yy * FS + 2 * (threadIdx.x & 15);
+        float s = 0.f;
+#pragma unroll
+        for (int c = 0; c <= 8; ++c) s = fmaf(taps.tx[c], row[c], s);
+        Hh[yy * kSrT + (threadIdx.x & 15)] = s;
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < S * kSrT; i += blockDim.x) {
+      const int yy = i / kSrT, tx = i - yy * kSrT;
+      const float* row = X + yy * S + k * tx;
+      float s = 0.f;
+      for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
+      Hh[i] = s;
+    }
+  }
+  __syncthreads();
   double sq = 0.0;
-  if (oy < win.out_r0 + win.out_rows && ox < w) {
+  if (own) {
     float acc = 0.f;
-    for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(k * ty + a) * kSrT + tx], acc);
-    const size_t o = (size_t)b * win.out_rows * w + (size_t)(oy - win.out_r0) * w + ox;
-    if (y) acc -= y[o];
+    if (fast) {
+#pragma unroll
+      for (int a = 0; a <= 8; ++a) acc = fmaf(taps.ty[a], Hh[(2 * ty + a) * kSrT + tx], acc);
+    } else {
+      for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(k * ty + a) * kSrT + tx], acc);
+    }
+    if (y) acc -= yo;
     r[o] = acc;
     sq = (double)acc * (double)acc;
   }
@@ -213,32 +264,85 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
   float* Hh = sm + S * S;    // [S][kSrTA]
   const int py0 = win.out_r0 + blockIdx.y * kSrTA, px0 = blockIdx.x * kSrTA;
   const float* rb = r + (size_t)b * win.in_rows * w;
-  for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
-    const int yy = i / S, xx = i - yy * S;
-    const int uy = map_index(min(py0 - rad + yy, H - 1 + rad), H, sym);
-    const int ux = map_index(min(px0 - rad + xx, W - 1 + rad), W, sym);
-    const int qy = uy / k, qx = ux / k;
-    int ly = qy - win.in_r0;
-    ly = ly < 0 ? 0 : (ly >= win.in_rows ? win.in_rows - 1 : ly);  // halo rows only: never hit
-    U[i] = (uy == qy * k && ux == qx * k) ? rb[(size_t)ly * w + qx] : 0.f;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < S * kSrTA; i += blockDim.x) {
-    const int yy = i / kSrTA, xx = i - yy * kSrTA;
-    const float* row = U + yy * S + xx;
-    float s = 0.f;
-    for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
-    Hh[i] = s;
+  // The configs' operator (factor 2, 9x9 kernel) on tiles whose staged window
+  // needs no boundary map: the zero-filled upsampled tile is never built.
+  // Only even high-res rows / columns hold samples, so the horizontal pass
+  // runs over the 20 x 20 low-res samples with the 5 (even output column) or
+  // 4 (odd) taps that meet a sample, and the vertical pass over the 20
+  // filtered sample rows with 5 or 4 taps.  The generic loops add exact
+  // zeros for the skipped taps, in the same order -> the same bits.
+  constexpr int FL = kSrTA / 2 + 4;  // low-res rows / columns staged
+  const bool fast = k == 2 && rad == 4 && ((py0 | px0) & 1) == 0 && py0 - 4 >= 0 &&
+                    py0 + kSrTA + 4 <= H && px0 - 4 >= 0 && px0 + kSrTA + 4 <= W &&
+                    py0 / 2 - 2 - win.in_r0 >= 0 && py0 / 2 - 2 - win.in_r0 + FL <= win.in_rows;
+  // per-thread tap sets: output column / row parity picks the even (5) or
+  // odd (4) taps; a thread's column (lane) and row parity (warp) are fixed
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  if (fast) {
+    const float* src = rb + (size_t)(py0 / 2 - 2 - win.in_r0 + wq) * w + px0 / 2 - 2 + lane;
+    float v[3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) v[m] = (wq + 8 * m < FL && lane < FL) ? src[(size_t)8 * m * w] : 0.f;
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+      if (wq + 8 * m < FL && lane < FL) U[(wq + 8 * m) * FL + lane] = v[m];
+    __syncthreads();
+    const int odd = lane & 1;
+    float t5[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) t5[j] = odd ? (j < 4 ? taps.tx[2 * j + 1] : 0.f) : taps.tx[2 * j];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int i = wq + 8 * m;
+      if (i < FL) {
+        const float* row = U + i * FL + ((lane + 1) >> 1);
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s = fmaf(t5[j], row[j], s);
+        if (!odd) s = fmaf(t5[4], row[4], s);
+        Hh[i * kSrTA + lane] = s;
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+      const int yy = i / S, xx = i - yy * S;
+      const int uy = map_index(min(py0 - rad + yy, H - 1 + rad), H, sym);
+      const int ux = map_index(min(px0 - rad + xx, W - 1 + rad), W, sym);
+      const int qy = uy / k, qx = ux / k;
+      int ly = qy - win.in_r0;
+      ly = ly < 0 ? 0 : (ly >= win.in_rows ? win.in_rows - 1 : ly);  // halo rows only: never hit
+      U[i] = (uy == qy * k && ux == qx * k) ? rb[(size_t)ly * w + qx] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < S * kSrTA; i += blockDim.x) {
+      const int yy = i / kSrTA, xx = i - yy * kSrTA;
+      const float* row = U + yy * S + xx;
+      float s = 0.f;
+      for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
+      Hh[i] = s;
+    }
   }
   __syncthreads();
   int f = 0;
   double dot = 0.0;
+  float ty5[5];  // the rows of thread t have the parity of its warp (yy = wq + 8 m)
+#pragma unroll
+  for (int j = 0; j < 5; ++j)
+    ty5[j] = (wq & 1) ? (j < 4 ? taps.ty[2 * j + 1] : 0.f) : taps.ty[2 * j];
+#pragma unroll 4
   for (int i = threadIdx.x; i < kSrTA * kSrTA; i += blockDim.x) {
     const int yy = i / kSrTA, xx = i - yy * kSrTA;
     const int py = py0 + yy, px = px0 + xx;
     if (py >= win.out_r0 + win.out_rows || px >= W) continue;
     float acc = 0.f;
-    for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
+    if (fast) {  // yy is warp-uniform: a warp is one output row
+      const float* col = Hh + ((yy + 1) >> 1) * kSrTA + xx;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc = fmaf(ty5[j], col[j * kSrTA], acc);
+      if (!(yy & 1)) acc = fmaf(ty5[4], col[4 * kSrTA], acc);
+    } else {
+      for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
+    }
     const size_t o = (size_t)b * win.out_rows * W + (size_t)(py - win.out_r0) * W + px;
     if (XU) {
       f |= xupdate_pixel(q, o, acc);

@@ -65,15 +65,14 @@ __device__ __forceinline__ void cta_reduce_partials3(const double* partial, int 
   __syncthreads();
 }
 
-// Called by every CTA of a grid after it wrote its partials: the last CTA to
-// arrive (device-scope counter, reset by it for the next launch) reduces all
-// `batch` x `nvec` sums.  Returns true in that CTA.
-__device__ __forceinline__ bool cta_is_last(unsigned* counter) {
+// Called by every CTA of a group of `total` CTAs after it wrote its partials:
+// the last CTA to arrive (device-scope counter, reset by it for the next
+// launch) reduces the group's sums.  Returns true in that CTA.
+__device__ __forceinline__ bool cta_is_last_of(unsigned* counter, unsigned total) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
     last = atomicAdd(counter, 1u) == total - 1;
   }
   __syncthreads();
@@ -82,6 +81,11 @@ __device__ __forceinline__ bool cta_is_last(unsigned* counter) {
     if (threadIdx.x == 0) *counter = 0u;
   }
   return last;
+}
+
+// The whole grid as one group: the last CTA reduces all `batch` x `nvec` sums.
+__device__ __forceinline__ bool cta_is_last(unsigned* counter) {
+  return cta_is_last_of(counter, gridDim.x * gridDim.y * gridDim.z);
 }
 
 }  // namespace pnp

@@ -25,7 +25,7 @@ guides = F.interpolate(yb.double()[:, None], scale_factor=2, mode="bicubic",
 cfg = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=20, constraint=pnp.UNIT_BOX)
 prob = pnp.make_sr_problem(op, yb, ground_truth=gtb)
 fz = pnp.freeze_guide(guides, p2)
-for i in range(5):
+for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 5):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     v, recs = pnp.linearized_pnp_admm(prob, cfg, denoiser=fz.as_denoiser())
