@@ -179,12 +179,18 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
       for (int h = 0; h < 2; ++h)
         if (wq + 8 * m < FS && l + 32 * h < FS) X[(wq + 8 * m) * FS + l + 32 * h] = v[m][h];
   } else {
-    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
-      const int yy = i / S, xx = i - yy * S;
-      int sy = map_index(min(y0 + yy, H - 1 + rad), H, sym) - win.in_r0;
-      sy = sy < 0 ? 0 : (sy >= win.in_rows ? win.in_rows - 1 : sy);  // halo rows only: never hit
-      const int sx = map_index(min(x0 + xx, W - 1 + rad), W, sym);
-      X[i] = xb[(size_t)sy * W + sx];
+    // boundary tiles: the (separable) index maps once per staged row / column
+    int* rmap = reinterpret_cast<int*>(Hh + S * kSrT);
+    int* cmap = rmap + S;
+    for (int t = threadIdx.x; t < S; t += blockDim.x) {
+      int sy = map_index(min(y0 + t, H - 1 + rad), H, sym) - win.in_r0;
+      rmap[t] = sy < 0 ? 0 : (sy >= win.in_rows ? win.in_rows - 1 : sy);  // halo rows only: never hit
+      cmap[t] = map_index(min(x0 + t, W - 1 + rad), W, sym);
+    }
+    __syncthreads();
+    for (int yy = threadIdx.x >> 5; yy < S; yy += blockDim.x >> 5) {
+      const float* src = xb + (size_t)rmap[yy] * W;
+      for (int xx = threadIdx.x & 31; xx < S; xx += 32) X[yy * S + xx] = src[cmap[xx]];
     }
   }
   __syncthreads();
@@ -304,45 +310,45 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
       }
     }
   } else {
-    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
-      const int yy = i / S, xx = i - yy * S;
-      const int uy = map_index(min(py0 - rad + yy, H - 1 + rad), H, sym);
-      const int ux = map_index(min(px0 - rad + xx, W - 1 + rad), W, sym);
+    // boundary tiles: the (separable) index maps once per staged row / column,
+    // -1 where the mapped high-res row / column holds no low-res sample
+    int* rmap = reinterpret_cast<int*>(Hh + S * kSrTA);
+    int* cmap = rmap + S;
+    for (int t = threadIdx.x; t < S; t += blockDim.x) {
+      const int uy = map_index(min(py0 - rad + t, H - 1 + rad), H, sym);
+      const int ux = map_index(min(px0 - rad + t, W - 1 + rad), W, sym);
       const int qy = uy / k, qx = ux / k;
       int ly = qy - win.in_r0;
       ly = ly < 0 ? 0 : (ly >= win.in_rows ? win.in_rows - 1 : ly);  // halo rows only: never hit
-      U[i] = (uy == qy * k && ux == qx * k) ? rb[(size_t)ly * w + qx] : 0.f;
+      rmap[t] = uy == qy * k ? ly : -1;
+      cmap[t] = ux == qx * k ? qx : -1;
+    }
+    __syncthreads();
+    for (int yy = threadIdx.x >> 5; yy < S; yy += blockDim.x >> 5) {
+      const int ly = rmap[yy];
+      for (int xx = threadIdx.x & 31; xx < S; xx += 32) {
+        const int qx = cmap[xx];
+        U[yy * S + xx] = (ly >= 0 && qx >= 0) ? rb[(size_t)ly * w + qx] : 0.f;
+      }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < S * kSrTA; i += blockDim.x) {
       const int yy = i / kSrTA, xx = i - yy * kSrTA;
       const float* row = U + yy * S + xx;
       float s = 0.f;
-      for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
+      if (rad == 4) {
+#pragma unroll
+        for (int c = 0; c <= 8; ++c) s = fmaf(taps.tx[c], row[c], s);
+      } else {
+        for (int c = 0; c <= 2 * rad; ++c) s = fmaf(taps.tx[c], row[c], s);
+      }
       Hh[i] = s;
     }
   }
   __syncthreads();
   int f = 0;
   double dot = 0.0;
-  float ty5[5];  // the rows of thread t have the parity of its warp (yy = wq + 8 m)
-#pragma unroll
-  for (int j = 0; j < 5; ++j)
-    ty5[j] = (wq & 1) ? (j < 4 ? taps.ty[2 * j + 1] : 0.f) : taps.ty[2 * j];
-#pragma unroll 4
-  for (int i = threadIdx.x; i < kSrTA * kSrTA; i += blockDim.x) {
-    const int yy = i / kSrTA, xx = i - yy * kSrTA;
-    const int py = py0 + yy, px = px0 + xx;
-    if (py >= win.out_r0 + win.out_rows || px >= W) continue;
-    float acc = 0.f;
-    if (fast) {  // yy is warp-uniform: a warp is one output row
-      const float* col = Hh + ((yy + 1) >> 1) * kSrTA + xx;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc = fmaf(ty5[j], col[j * kSrTA], acc);
-      if (!(yy & 1)) acc = fmaf(ty5[4], col[4 * kSrTA], acc);
-    } else {
-      for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
-    }
+  auto emit = [&](int py, int px, float acc) {
     const size_t o = (size_t)b * win.out_rows * W + (size_t)(py - win.out_r0) * W + px;
     if (XU) {
       f |= xupdate_pixel(q, o, acc);
@@ -353,6 +359,63 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
       dot += (double)pv * (double)ap;
     } else {
       out[o] = acc;
+    }
+  };
+  if (fast && MODE != ADJ_CG) {
+    // thread (warp wq, lane): output rows 4 wq .. 4 wq + 3 of column lane from
+    // filtered sample rows 2 wq .. 2 wq + 5 (even rows: 5 taps, odd rows: 4)
+    const float* col = Hh + 2 * wq * kSrTA + lane;
+    float h6[6];
+#pragma unroll
+    for (int j6 = 0; j6 < 6; ++j6) h6[j6] = col[j6 * kSrTA];
+    const int px = px0 + lane, py = py0 + 4 * wq;
+    const size_t o0 = (size_t)b * win.out_rows * W + (size_t)(py - win.out_r0) * W + px;
+#pragma unroll
+    for (int r4 = 0; r4 < 4; ++r4) {
+      const int base = (r4 + 1) >> 1, odd = r4 & 1;
+      float acc = 0.f;
+#pragma unroll
+      for (int j5 = 0; j5 < 4; ++j5) acc = fmaf(taps.ty[2 * j5 + odd], h6[base + j5], acc);
+      if (!odd) acc = fmaf(taps.ty[8], h6[base + 4], acc);
+      if (py + r4 < win.out_r0 + win.out_rows) {
+        const size_t o = o0 + (size_t)r4 * W;
+        if (XU) f |= xupdate_pixel(q, o, acc);
+        else out[o] = acc;
+      }
+    }
+  } else if (fast) {
+    // (conjugate gradients: the generic loop's thread / output order, so the
+    // per-thread dot partials sum in the same order) thread (warp wq, lane):
+    // output rows wq + 8 m, column lane; the rows' parity is the warp's
+    float ty5[5];
+#pragma unroll
+    for (int j5 = 0; j5 < 5; ++j5)
+      ty5[j5] = (wq & 1) ? (j5 < 4 ? taps.ty[2 * j5 + 1] : 0.f) : taps.ty[2 * j5];
+    const int px = px0 + lane;
+#pragma unroll
+    for (int m = 0; m < kSrTA * kSrTA / 256; ++m) {
+      const int yy = wq + 8 * m, py = py0 + yy;
+      if (py >= win.out_r0 + win.out_rows || px >= W) continue;
+      const float* col = Hh + ((yy + 1) >> 1) * kSrTA + lane;
+      float acc = 0.f;
+#pragma unroll
+      for (int j5 = 0; j5 < 4; ++j5) acc = fmaf(ty5[j5], col[j5 * kSrTA], acc);
+      if (!(wq & 1)) acc = fmaf(ty5[4], col[4 * kSrTA], acc);
+      emit(py, px, acc);
+    }
+  } else {
+    for (int i = threadIdx.x; i < kSrTA * kSrTA; i += blockDim.x) {
+      const int yy = i / kSrTA, xx = i - yy * kSrTA;
+      const int py = py0 + yy, px = px0 + xx;
+      if (py >= win.out_r0 + win.out_rows || px >= W) continue;
+      float acc = 0.f;
+      if (rad == 4) {
+#pragma unroll
+        for (int a = 0; a <= 8; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
+      } else {
+        for (int a = 0; a <= 2 * rad; ++a) acc = fmaf(taps.ty[a], Hh[(yy + a) * kSrTA + xx], acc);
+      }
+      emit(py, px, acc);
     }
   }
   if (XU) flags_or(q.flags, f);
@@ -370,13 +433,13 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
   if (MODE != ADJ_CG) red_epilogue(red);  // data term of the residual kernel
 }
 
-static size_t sr_res_smem(int k, int rad) {
+static size_t sr_res_smem(int k, int rad) {  // + the row / column index maps
   const int S = k * (kSrT - 1) + 1 + 2 * rad;
-  return (size_t)(S * S + S * kSrT) * sizeof(float);
+  return (size_t)(S * S + S * kSrT + 2 * S) * sizeof(float);
 }
 static size_t sr_adj_smem(int rad) {
   const int S = kSrTA + 2 * rad;
-  return (size_t)(S * S + S * kSrTA) * sizeof(float);
+  return (size_t)(S * S + S * kSrTA + 2 * S) * sizeof(float);
 }
 static dim3 sr_res_grid(int H, int W, int k, int batch) {  // H: output HR rows of the window
   return dim3((W / k + kSrT - 1) / kSrT, (H / k + kSrT - 1) / kSrT, batch);
