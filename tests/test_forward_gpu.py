@@ -146,3 +146,34 @@ def test_device_sr_noise_matches_host_box_muller(pnp, shape):
     assert np.all(np.abs(got - ref32) <= ulp)
     assert np.mean(got == ref32) > 0.999
     assert np.array_equal(pnp.sr_simulate(x, op, 0.0, seed=77), clean)
+
+
+@pytest.mark.parametrize("boundary", ["periodic", "symmetric"])
+def test_sr_fast_tiles_bitwise_equal_generic(pnp, rng, boundary):
+    """The configs' operator (factor 2, 9x9) takes a compile-time fast path on
+    tiles whose staged window needs no boundary map (the adjoint filters only
+    the low-res samples); border tiles take the generic path.  Shifting the
+    image inside a larger one moves every interior pixel to another tile (and
+    tile kind): the interior outputs must be the same bits either way, and
+    match the float64 oracle."""
+    k = ofw.gaussian_kernel(1.0, 4)
+    op = pnp.SuperResOp(pnp.gaussian_kernel(1.0, 4), 2, boundary)
+    H, W, s = 192, 224, 20  # s: shift in low-res pixels (40 high-res)
+    y = rng.random((3, H // 2, W // 2)).astype(np.float32)
+    big = rng.random((3, H // 2 + 2 * s, W // 2 + 2 * s)).astype(np.float32)
+    big[:, s:s + H // 2, s:s + W // 2] = y
+    a = pnp.sr_adjoint(op, y)
+    b = pnp.sr_adjoint(op, big)[:, 2 * s:2 * s + H, 2 * s:2 * s + W]
+    m = 8  # high-res rows / columns reached by the boundary from either side
+    assert np.array_equal(a[:, m:-m, m:-m], b[:, m:-m, m:-m])
+    for i in range(3):
+        assert np.abs(a[i] - ofw.sr_adjoint(k, 2, boundary, y[i])).max() < 2e-6
+    x = rng.random((3, H, W)).astype(np.float32)
+    xb = rng.random((3, H + 4 * s, W + 4 * s)).astype(np.float32)
+    xb[:, 2 * s:2 * s + H, 2 * s:2 * s + W] = x
+    ra = pnp.sr_apply(op, x)
+    rb = pnp.sr_apply(op, xb)[:, s:s + H // 2, s:s + W // 2]
+    ml = 4
+    assert np.array_equal(ra[:, ml:-ml, ml:-ml], rb[:, ml:-ml, ml:-ml])
+    for i in range(3):
+        assert np.abs(ra[i] - ofw.sr_apply(k, 2, boundary, x[i])).max() < 2e-6
