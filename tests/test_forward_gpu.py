@@ -162,8 +162,10 @@ def test_sr_fast_tiles_bitwise_equal_generic(pnp, rng, boundary):
     y = rng.random((3, H // 2, W // 2)).astype(np.float32)
     big = rng.random((3, H // 2 + 2 * s, W // 2 + 2 * s)).astype(np.float32)
     big[:, s:s + H // 2, s:s + W // 2] = y
-    a = pnp.sr_adjoint(op, y)
-    b = pnp.sr_adjoint(op, big)[:, 2 * s:2 * s + H, 2 * s:2 * s + W]
+    import torch
+    dev = lambda t: torch.from_numpy(t).cuda()  # noqa: E731 (batched device path)
+    a = pnp.sr_adjoint(op, dev(y)).cpu().numpy()
+    b = pnp.sr_adjoint(op, dev(big)).cpu().numpy()[:, 2 * s:2 * s + H, 2 * s:2 * s + W]
     m = 8  # high-res rows / columns reached by the boundary from either side
     assert np.array_equal(a[:, m:-m, m:-m], b[:, m:-m, m:-m])
     for i in range(3):
@@ -171,8 +173,8 @@ def test_sr_fast_tiles_bitwise_equal_generic(pnp, rng, boundary):
     x = rng.random((3, H, W)).astype(np.float32)
     xb = rng.random((3, H + 4 * s, W + 4 * s)).astype(np.float32)
     xb[:, 2 * s:2 * s + H, 2 * s:2 * s + W] = x
-    ra = pnp.sr_apply(op, x)
-    rb = pnp.sr_apply(op, xb)[:, s:s + H // 2, s:s + W // 2]
+    ra = pnp.sr_apply(op, dev(x)).cpu().numpy()
+    rb = pnp.sr_apply(op, dev(xb)).cpu().numpy()[:, s:s + H // 2, s:s + W // 2]
     ml = 4
     assert np.array_equal(ra[:, ml:-ml, ml:-ml], rb[:, ml:-ml, ml:-ml])
     for i in range(3):
