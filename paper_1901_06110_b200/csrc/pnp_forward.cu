@@ -171,8 +171,12 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
 #pragma unroll
     for (int m = 0; m < 5; ++m)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        v[m][h] = (wq + 8 * m < FS && l + 32 * h < FS) ? src[(size_t)8 * m * W + 32 * h] : 0.f;
+      for (int h = 0; h < 2; ++h) {
+        const bool in = wq + 8 * m < FS && l + 32 * h < FS;
+        PNP_CHECK(!in || (y0 - win.in_r0 + wq + 8 * m < win.in_rows && x0 + l + 32 * h < W &&
+                          x0 + l + 32 * h >= 0 && S == FS));
+        v[m][h] = in ? src[(size_t)8 * m * W + 32 * h] : 0.f;
+      }
 #pragma unroll
     for (int m = 0; m < 5; ++m)
 #pragma unroll
@@ -190,7 +194,10 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
     __syncthreads();
     for (int yy = threadIdx.x >> 5; yy < S; yy += blockDim.x >> 5) {
       const float* src = xb + (size_t)rmap[yy] * W;
-      for (int xx = threadIdx.x & 31; xx < S; xx += 32) X[yy * S + xx] = src[cmap[xx]];
+      for (int xx = threadIdx.x & 31; xx < S; xx += 32) {
+        PNP_CHECK(rmap[yy] >= 0 && rmap[yy] < win.in_rows && cmap[xx] >= 0 && cmap[xx] < W);
+        X[yy * S + xx] = src[cmap[xx]];
+      }
     }
   }
   __syncthreads();
@@ -200,6 +207,7 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
       const int yy = (threadIdx.x >> 4) + 16 * m;
       if (yy < FS) {
         const float* row = X + yy * FS + 2 * (threadIdx.x & 15);
+        PNP_CHECK(row + 8 < X + S * S);
         float s = 0.f;
 #pragma unroll
         for (int c = 0; c <= 8; ++c) s = fmaf(taps.tx[c], row[c], s);
@@ -220,6 +228,7 @@ sr_residual_kernel(const float* __restrict__ x, const float* __restrict__ y, flo
   if (own) {
     float acc = 0.f;
     if (fast) {
+      PNP_CHECK((2 * ty + 8) * kSrT + tx < S * kSrT);
 #pragma unroll
       for (int a = 0; a <= 8; ++a) acc = fmaf(taps.ty[a], Hh[(2 * ty + a) * kSrT + tx], acc);
     } else {
@@ -288,7 +297,12 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
     const float* src = rb + (size_t)(py0 / 2 - 2 - win.in_r0 + wq) * w + px0 / 2 - 2 + lane;
     float v[3];
 #pragma unroll
-    for (int m = 0; m < 3; ++m) v[m] = (wq + 8 * m < FL && lane < FL) ? src[(size_t)8 * m * w] : 0.f;
+    for (int m = 0; m < 3; ++m) {
+      const bool in = wq + 8 * m < FL && lane < FL;
+      PNP_CHECK(!in || (py0 / 2 - 2 - win.in_r0 + wq + 8 * m < win.in_rows &&
+                        px0 / 2 - 2 + lane < w && px0 / 2 - 2 + lane >= 0 && FL * FL <= S * S));
+      v[m] = in ? src[(size_t)8 * m * w] : 0.f;
+    }
 #pragma unroll
     for (int m = 0; m < 3; ++m)
       if (wq + 8 * m < FL && lane < FL) U[(wq + 8 * m) * FL + lane] = v[m];
@@ -302,6 +316,7 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
       const int i = wq + 8 * m;
       if (i < FL) {
         const float* row = U + i * FL + ((lane + 1) >> 1);
+        PNP_CHECK(row + (odd ? 3 : 4) < U + FL * FL);
         float s = 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) s = fmaf(t5[j], row[j], s);
@@ -328,6 +343,7 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
       const int ly = rmap[yy];
       for (int xx = threadIdx.x & 31; xx < S; xx += 32) {
         const int qx = cmap[xx];
+        PNP_CHECK(ly < win.in_rows && qx < w);
         U[yy * S + xx] = (ly >= 0 && qx >= 0) ? rb[(size_t)ly * w + qx] : 0.f;
       }
     }
@@ -365,6 +381,7 @@ sr_adjoint_kernel(const float* __restrict__ r, float* __restrict__ out, const Sr
     // thread (warp wq, lane): output rows 4 wq .. 4 wq + 3 of column lane from
     // filtered sample rows 2 wq .. 2 wq + 5 (even rows: 5 taps, odd rows: 4)
     const float* col = Hh + 2 * wq * kSrTA + lane;
+    PNP_CHECK(col + 5 * kSrTA < Hh + FL * kSrTA);
     float h6[6];
 #pragma unroll
     for (int j6 = 0; j6 < 6; ++j6) h6[j6] = col[j6 * kSrTA];

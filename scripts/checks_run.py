@@ -68,6 +68,17 @@ cfgs = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=2, constraint=pn
                         cg_tol=1e-6, cg_max_iters=20)
 v, _ = pnp.standard_pnp_admm_cg(prob, cfgs, denoiser=pnp.freeze_guide(truth, pg).as_denoiser())
 keep("admm_cg", v)
+# SR fast tiles (factor 2, 9x9: interior tiles of a 192 x 224 batch) + boundary
+# tiles; a frozen-guide ADMM run at that size (pipelined loop, fused x-update)
+ys, xs = rand(2, 96, 112), rand(2, 192, 224)
+keep("sr_adjoint_batch", op.adjoint_device(ys))
+keep("sr_apply_batch", op.apply_device(xs))
+keep("sr_grad_batch", pnp.sr_gradient(op, xs, ys))
+prob2 = pnp.make_sr_problem(op, ys, ground_truth=xs)
+cfg2 = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=3, constraint=pnp.UNIT_BOX)
+v, recs = pnp.linearized_pnp_admm(prob2, cfg2, denoiser=pnp.freeze_guide(xs, pg).as_denoiser())
+keep("admm_sr_batch", v)
+keep("admm_sr_batch_rec", np.array([[r.primal, r.dual, r.psnr, r.objective] for r in recs]))
 torch.cuda.synchronize()
 np.savez(sys.argv[1], **out)
 print("checks run ok:", len(out), "outputs")

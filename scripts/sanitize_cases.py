@@ -55,5 +55,12 @@ pnp.linearized_pnp_admm(pnp.make_qis_problem(counts, pnp.QisModel(16, 16.0)), cf
 cfgs = pnp.SolverConfig(rho=1.0, lam=0.01, alpha=1.0, max_iters=2, constraint=pnp.UNIT_BOX,
                         cg_tol=1e-6, cg_max_iters=20)
 pnp.standard_pnp_admm_cg(prob, cfgs, denoiser=pnp.freeze_guide(truth, pg).as_denoiser())
+# SR fast tiles (factor 2, 9x9: interior tiles of a 192 x 224 batch) and
+# their boundary tiles, residual + adjoint + fused x-update
+ys = rand(2, 96, 112)
+xs = rand(2, 192, 224)
+op.adjoint_device(ys)
+op.apply_device(xs)
+pnp.sr_gradient(op, xs, ys)
 torch.cuda.synchronize()
 print("sanitize cases ok")
