@@ -255,17 +255,8 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// The single-channel recompute / store sweeps ask ptxas for 3 resident CTAs
-// per SM explicitly: the same 168 registers as its own choice, scheduled for
-// that budget (sweep A + store 15.09 -> 14.57 ms at 8192², same-box A/B,
-// profiles/sweep_history.md); the two-channel and k-cache variants keep
-// ptxas's choice (forcing 3 CTAs spills the C = 2 sweeps).
-__host__ __device__ constexpr int sweep_min_blocks(int C, int MODE) {
-  return (C == 1 && MODE != MODE_CACHED) ? 3 : 1;
-}
-
 template <int P, int RB, int C, int MODE>
-__global__ void __launch_bounds__(kThreads, sweep_min_blocks(C, MODE))
+__global__ void __launch_bounds__(kThreads)
 dsg_sweep_kernel(const SweepArgs a, const ChunkTab<RB> tab, const __grid_constant__ CUtensorMap gmap) {
   using K = Cfg<P, RB, C, MODE>;
   constexpr bool CACHED = K::CACHED, STORE = MODE == MODE_STORE;
