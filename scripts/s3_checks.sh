@@ -1,3 +1,4 @@
+# session-3 hygiene check: debug-build comparison + forward/ADMM/checks GPU tests
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/$1
 timeout 900 bash scripts/checks_compare.sh > gpurun_out/$1/checks.log 2>&1; echo "checks rc $?" >> gpurun_out/$1/checks.log

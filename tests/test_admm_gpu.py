@@ -189,13 +189,21 @@ def test_batched_admm_matches_single(pnp):
     Y = torch.tensor(np.stack(ys), dtype=torch.float32, device="cuda")
     G = torch.clamp(torch.nn.functional.interpolate(Y[:, None], scale_factor=2, mode="bicubic",
                                                     align_corners=False)[:, 0], 0, 1).contiguous()
+    T = torch.tensor(np.stack(truths), dtype=torch.float32, device="cuda")
     fzb = pnp.freeze_guide(G, p)
-    vb, rb = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, Y), cfg, denoiser=fzb.as_denoiser())
+    vb, rb = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, Y, ground_truth=T), cfg,
+                                     denoiser=fzb.as_denoiser())
     for i in range(3):
         fz = pnp.freeze_guide(G[i].contiguous(), p)
-        vi, ri = pnp.linearized_pnp_admm(pnp.make_sr_problem(op, Y[i].contiguous()), cfg,
-                                         denoiser=fz.as_denoiser())
+        vi, ri = pnp.linearized_pnp_admm(
+            pnp.make_sr_problem(op, Y[i].contiguous(), ground_truth=T[i].contiguous()), cfg,
+            denoiser=fz.as_denoiser())
         assert torch.equal(vb[i], vi)
+        # per-image statistics (each image's partials reduced by its own last
+        # CTA in the batched fixup): the same doubles as the single solve
+        for k in range(len(ri)):
+            for f in ("primal", "dual", "psnr", "objective"):
+                assert np.asarray(getattr(rb[k], f))[i] == getattr(ri[k], f), (k, f)
 
 
 @pytest.mark.parametrize("schedule", ["frozen-plugin", "dsg-fixed", "dsg-adaptive", "nlm"])
